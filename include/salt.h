@@ -1,0 +1,148 @@
+/*
+ * salt.h — C ABI of libsalt.so, the B200 (sm_100a) evaluator for fused
+ * BLAS-1 expression trees (the hot path of SALT, arXiv 1109.1264).
+ *
+ * The reference (`lanevec`, pure Python + NumPy) has no native boundary:
+ * its hot path is the pair of engine entry points
+ *
+ *     execute_assign(root, plan=None, *, backend, unroll, packages, stepped)
+ *         pkg/src/lanevec/engine.py:295-311  -> _run_block_assign :243-264
+ *     execute_reduce(root, plan=None, *, backend, unroll, packages, stepped)
+ *         pkg/src/lanevec/engine.py:314-329  -> _run_block_reduce :267-292
+ *
+ * This header is the boundary that replaces those loops.  The Python host
+ * layer (paper_1109_1264_b200/engine.py) keeps the reference signatures,
+ * performs every validation the reference performs (and raises the same
+ * exceptions) BEFORE calling in here, lowers the tree to a postfix
+ * signature and calls one of the functions below through ctypes.
+ *
+ * Conventions
+ *  - POD arguments only; no torch types.  Device pointers are BORROWED
+ *    (never freed).  Element counts are int64 (config 5 has 2^31 elements).
+ *  - `sig` is the canonical postfix tree signature, tokens separated by one
+ *    space:  L<k> leaf k, S<k> scalar k, D (the value just assigned, only in
+ *    the reduce tree of salt_assign_reduce), and the binary operators
+ *    + - * (left operand first).  Examples:
+ *        axpy  y + a*x              "L0 S0 L1 * +"        (L0 = y = dst)
+ *        d = a + (b - c)            "L0 L1 L2 - +"
+ *        d = al*a + be*(b - c)      "S0 L0 * S1 L1 L2 - * +"
+ *        dot(x, y)                  "L0 L1 *"
+ *  - scalars are passed as doubles that already hold the element-typed
+ *    value (the Python side coerces them first, expressions.py:282).
+ *  - `stream` is a cudaStream_t (NULL = legacy default stream).
+ *  - Every function returns 0 on success and a negative SALT_E* code on
+ *    failure; salt_last_error() returns a thread-local message.
+ *  - Re-entrant: mutable state is limited to a once-initialised kernel
+ *    table (mutex protected), per-device attribute caches and a
+ *    thread-local error string.  Reduction scratch is caller-owned.
+ */
+#ifndef SALT_H
+#define SALT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SALT_ABI_VERSION 1
+
+/* element types (lanes.py:31-43 accepts exactly f32 / f64) */
+#define SALT_F32 0
+#define SALT_F64 1
+
+/* reduction flags */
+#define SALT_SQRT    1 /* finish with sqrt in the element type (ops.norm2, ops.py:53-55) */
+#define SALT_PARTIAL 2 /* write the per-device double-double partial {hi, lo} instead of
+                          the rounded scalar (multi-GPU: all-gather then salt_reduce_finish) */
+
+/* error codes */
+#define SALT_OK          0
+#define SALT_EINVAL     -1 /* bad signature / argument */
+#define SALT_ECUDA      -2 /* CUDA runtime or driver failure */
+#define SALT_EJIT       -3 /* NVRTC unavailable or compile failure */
+#define SALT_EWORKSPACE -4 /* reduction workspace too small */
+
+/* Elementwise assignment dst[i] = tree(leaves[.][i], scalars), i in [0, n).
+ * Replaces engine.execute_assign (engine.py:295-311): one fused kernel, no
+ * intermediate vector (AssignNode.block_commit, expressions.py:392-395).
+ * dst may be identical to one of the leaves (exact aliasing, expressions.py
+ * :326-333); shifted overlap is unsupported, as in the reference. */
+int salt_assign(int dtype, const char* sig, void* dst,
+                const void* const* leaves, int nleaves,
+                const double* scalars, int nscalars,
+                int64_t n, void* stream);
+
+/* Reduction sum_i tree(leaves[.][i], scalars).  Replaces
+ * engine.execute_reduce (engine.py:314-329) + SumNode.block_accumulate /
+ * combine_partials (expressions.py:457-480).  Deterministic: fixed grid,
+ * compensated (double-double) per-CTA partials combined in fixed order by
+ * the last CTA.  out_dev receives one element of `dtype` (or, with
+ * SALT_PARTIAL, one {double hi, double lo} pair).  If out_host is non-NULL
+ * the result is also copied there and the stream is synchronised.
+ * workspace must be >= salt_reduce_workspace_bytes() bytes of device memory,
+ * zero-filled once before first use, and not shared by concurrent calls. */
+int salt_reduce(int dtype, const char* sig,
+                const void* const* leaves, int nleaves,
+                const double* scalars, int nscalars,
+                int64_t n, int flags,
+                void* workspace, size_t workspace_bytes,
+                void* out_dev, void* out_host, void* stream);
+
+/* Fused assignment + reduction in ONE pass (BASELINE config 5, axpy -> dot):
+ * dst[i] = assign_sig(...);  result = sum_i reduce_sig(..., D = dst[i]).
+ * Replaces ops.axpy (ops.py:32-36) followed by ops.dot (ops.py:18-20),
+ * which the reference runs as two traversals. */
+int salt_assign_reduce(int dtype, const char* assign_sig, const char* reduce_sig,
+                       void* dst, const void* const* leaves, int nleaves,
+                       const double* scalars, int nscalars,
+                       int64_t n, int flags,
+                       void* workspace, size_t workspace_bytes,
+                       void* out_dev, void* out_host, void* stream);
+
+/* Combine `count` {hi, lo} partials (e.g. all-gathered from the ranks, in
+ * rank order) in fixed order, round to dtype, optional SALT_SQRT. */
+int salt_reduce_finish(int dtype, const void* partials_dev, int count, int flags,
+                       void* out_dev, void* out_host, void* stream);
+
+/* Host-buffer (end-to-end) variants: leaves / dst are HOST pointers (pinned
+ * memory for full speed).  Chunks are streamed H2D -> fused kernel -> D2H
+ * through `staging` (device memory, caller-owned) on three caller streams
+ * so PCIe traffic in both directions overlaps the kernels.  Blocking. */
+int salt_assign_host(int dtype, const char* sig, void* host_dst,
+                     const void* const* host_leaves, int nleaves,
+                     const double* scalars, int nscalars, int64_t n,
+                     void* staging, size_t staging_bytes,
+                     void* const* streams3);
+
+int salt_reduce_host(int dtype, const char* sig,
+                     const void* const* host_leaves, int nleaves,
+                     const double* scalars, int nscalars, int64_t n, int flags,
+                     void* staging, size_t staging_bytes,
+                     void* const* streams3, void* out_host);
+
+/* Bytes of device scratch salt_reduce / salt_assign_reduce need. */
+size_t salt_reduce_workspace_bytes(void);
+
+/* 0 = invalid signature, 1 = compiled-in (AOT) kernel, 2 = needs the NVRTC
+ * JIT.  kind: 0 assign, 1 reduce, 2 assign+reduce (reduce_sig used). */
+int salt_signature_kind(int dtype, const char* sig, const char* reduce_sig, int kind);
+
+/* Force (1) or forbid (0) the JIT for signatures that also have an AOT
+ * kernel; default 0.  Used by tests to prove AOT == JIT bit for bit. */
+void salt_set_force_jit(int on);
+
+/* Number of kernels this library has launched since load (all devices). */
+uint64_t salt_launch_count(void);
+
+/* Thread-local description of the last failure on this thread. */
+const char* salt_last_error(void);
+
+int salt_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SALT_H */

@@ -1,0 +1,125 @@
+"""ctypes binding of libsalt.so (the C ABI declared in include/salt.h).
+
+This module is the only place Python talks to native code.  There is no CPU
+fallback: if the library is missing or a CUDA call fails, the error is raised
+here (RuntimeError with the library's thread-local message), mirroring how the
+reference surfaces failures as exceptions (error
+conventions).
+"""
+
+import ctypes
+import os
+import threading
+from pathlib import Path
+
+__all__ = [
+    "lib",
+    "check",
+    "SALT_F32",
+    "SALT_F64",
+    "SALT_SQRT",
+    "SALT_PARTIAL",
+    "LIB_PATH",
+    "HEADER_SYMBOLS",
+]
+
+SALT_F32 = 0
+SALT_F64 = 1
+SALT_SQRT = 1
+SALT_PARTIAL = 2
+
+LIB_PATH = Path(os.environ.get("SALT_LIB", Path(__file__).with_name("libsalt.so")))
+
+# Every function include/salt.h declares (tests check the .so exports them all).
+HEADER_SYMBOLS = (
+    "salt_assign",
+    "salt_reduce",
+    "salt_assign_reduce",
+    "salt_reduce_finish",
+    "salt_assign_host",
+    "salt_reduce_host",
+    "salt_reduce_workspace_bytes",
+    "salt_signature_kind",
+    "salt_set_force_jit",
+    "salt_launch_count",
+    "salt_last_error",
+    "salt_abi_version",
+)
+
+_c_int = ctypes.c_int
+_c_i64 = ctypes.c_int64
+_c_size = ctypes.c_size_t
+_c_vp = ctypes.c_void_p
+_c_str = ctypes.c_char_p
+_c_vpp = ctypes.POINTER(ctypes.c_void_p)
+_c_dp = ctypes.POINTER(ctypes.c_double)
+
+_SIGNATURES = {
+    "salt_assign": (_c_int, [_c_int, _c_str, _c_vp, _c_vpp, _c_int, _c_dp, _c_int, _c_i64, _c_vp]),
+    "salt_reduce": (
+        _c_int,
+        [_c_int, _c_str, _c_vpp, _c_int, _c_dp, _c_int, _c_i64, _c_int, _c_vp, _c_size, _c_vp, _c_vp, _c_vp],
+    ),
+    "salt_assign_reduce": (
+        _c_int,
+        [_c_int, _c_str, _c_str, _c_vp, _c_vpp, _c_int, _c_dp, _c_int, _c_i64, _c_int, _c_vp, _c_size,
+         _c_vp, _c_vp, _c_vp],
+    ),
+    "salt_reduce_finish": (_c_int, [_c_int, _c_vp, _c_int, _c_int, _c_vp, _c_vp, _c_vp]),
+    "salt_assign_host": (
+        _c_int, [_c_int, _c_str, _c_vp, _c_vpp, _c_int, _c_dp, _c_int, _c_i64, _c_vp, _c_size, _c_vpp]
+    ),
+    "salt_reduce_host": (
+        _c_int,
+        [_c_int, _c_str, _c_vpp, _c_int, _c_dp, _c_int, _c_i64, _c_int, _c_vp, _c_size, _c_vpp, _c_vp],
+    ),
+    "salt_reduce_workspace_bytes": (_c_size, []),
+    "salt_signature_kind": (_c_int, [_c_int, _c_str, _c_str, _c_int]),
+    "salt_set_force_jit": (None, [_c_int]),
+    "salt_launch_count": (ctypes.c_uint64, []),
+    "salt_last_error": (_c_str, []),
+    "salt_abi_version": (_c_int, []),
+}
+
+_lock = threading.Lock()
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libsalt.so once; raise loudly if it has not been built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is None:
+            if not LIB_PATH.exists():
+                raise RuntimeError(
+                    f"libsalt.so not found at {LIB_PATH}; build it with "
+                    "`python -c 'import __graft_entry__ as g; g.build()'` "
+                    "(there is no CPU fallback)"
+                )
+            handle = ctypes.CDLL(str(LIB_PATH))
+            for name, (res, args) in _SIGNATURES.items():
+                fn = getattr(handle, name)
+                fn.restype = res
+                fn.argtypes = args
+            if handle.salt_abi_version() != 1:
+                raise RuntimeError("libsalt.so ABI version mismatch; rebuild it")
+            _lib = handle
+    return _lib
+
+
+def check(rc: int) -> None:
+    if rc != 0:
+        msg = lib().salt_last_error()
+        raise RuntimeError(f"libsalt error {rc}: {msg.decode() if msg else 'unknown'}")
+
+
+def ptr_array(ptrs):
+    arr = (ctypes.c_void_p * max(1, len(ptrs)))(*[ctypes.c_void_p(p) for p in ptrs])
+    return ctypes.cast(arr, _c_vpp), arr
+
+
+def double_array(values):
+    arr = (ctypes.c_double * max(1, len(values)))(*values)
+    return ctypes.cast(arr, _c_dp), arr

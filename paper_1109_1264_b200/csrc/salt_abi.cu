@@ -1,0 +1,752 @@
+// salt_abi.cu — libsalt.so: the C ABI declared in include/salt.h.
+//
+// Host runtime around the fused kernels of salt_expr.cuh:
+//   * signature parsing / validation (postfix, see salt.h),
+//   * the kernel table: compiled-in (AOT, sm_100a) instantiations for the
+//     trees the reference's named ops and the BASELINE configs use, plus an
+//     NVRTC JIT that instantiates the SAME template for any other tree and
+//     caches the cubin per signature and the module per device,
+//   * launch geometry (persistent grid = SMs x resident CTAs),
+//   * deterministic reductions (per-CTA double-double partials, last-CTA
+//     combine) and the multi-device finish,
+//   * the host-buffer streaming path (H2D / kernel / D2H pipelined over
+//     three streams) used for end-to-end evaluation of host vectors.
+//
+// Reference anchors (pkg/src/lanevec/): engine.py:243-264 (assign loop),
+// :267-292 (reduce loop), expressions.py:392-395 (commit), :457-480 (sum).
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/salt.h"
+#include "salt_expr.cuh"
+
+namespace {
+
+using salt::i64;
+
+constexpr int kBlock = 256;
+constexpr int kUnrollVec = 2;     // 256-bit vectors in flight per leaf per thread
+constexpr int kUnrollScalar = 4;  // V == 1 fallback (misaligned operands)
+constexpr int kMaxGrid = 4096;    // reduction partial slots in the workspace
+constexpr size_t kWsHeader = 256; // ticket lives in the first 256 bytes
+constexpr int kMaxDevices = 64;
+
+thread_local std::string g_err;
+std::atomic<uint64_t> g_launches{0};
+std::atomic<int> g_force_jit{0};
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+int cuda_fail(cudaError_t e, const char* what) {
+  return fail(SALT_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define SALT_CUDA(call)                                  \
+  do {                                                   \
+    cudaError_t e_ = (call);                             \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #call);  \
+  } while (0)
+
+// ------------------------------------------------------------------ signatures
+struct Sig {
+  std::string canon;  // tokens joined by single spaces
+  std::string type;   // C++ type of the tree, e.g. salt::Add<salt::L<0>,salt::L<1>>
+  int nl = 0, ns = 0;
+  bool uses_d = false;
+};
+
+bool parse_index(const std::string& t, int& k) {
+  if (t.size() < 2 || t.size() > 3) return false;
+  k = 0;
+  for (size_t i = 1; i < t.size(); ++i) {
+    if (t[i] < '0' || t[i] > '9') return false;
+    k = k * 10 + (t[i] - '0');
+  }
+  return true;
+}
+
+// Returns "" on success, else an error message.
+std::string parse_sig(const char* s, bool allow_d, Sig& out) {
+  if (!s) return "signature is NULL";
+  std::vector<std::string> toks;
+  std::string cur;
+  for (const char* p = s;; ++p) {
+    if (*p == ' ' || *p == '\t' || *p == '\0') {
+      if (!cur.empty()) toks.push_back(cur), cur.clear();
+      if (*p == '\0') break;
+    } else {
+      cur.push_back(*p);
+    }
+  }
+  if (toks.empty()) return "empty signature";
+  if (toks.size() > 256) return "signature too long";
+  std::vector<std::string> st;
+  out = Sig();
+  for (const auto& t : toks) {
+    int k = 0;
+    if (t == "+" || t == "-" || t == "*") {
+      if (st.size() < 2) return "operator '" + t + "' needs two operands in '" + s + "'";
+      std::string b = st.back(); st.pop_back();
+      std::string a = st.back(); st.pop_back();
+      const char* node = t == "+" ? "salt::Add<" : t == "-" ? "salt::Sub<" : "salt::Mul<";
+      st.push_back(std::string(node) + a + "," + b + ">");
+    } else if (t[0] == 'L' && parse_index(t, k)) {
+      if (k >= salt::MAX_LEAVES) return "leaf index out of range: " + t;
+      out.nl = std::max(out.nl, k + 1);
+      st.push_back("salt::L<" + std::to_string(k) + ">");
+    } else if (t[0] == 'S' && parse_index(t, k)) {
+      if (k >= salt::MAX_SCALARS) return "scalar index out of range: " + t;
+      out.ns = std::max(out.ns, k + 1);
+      st.push_back("salt::S<" + std::to_string(k) + ">");
+    } else if (t == "D" && allow_d) {
+      out.uses_d = true;
+      st.push_back("salt::D");
+    } else {
+      return "bad token '" + t + "' in signature '" + s + "'";
+    }
+    if (!out.canon.empty()) out.canon.push_back(' ');
+    out.canon += t;
+  }
+  if (st.size() != 1) return std::string("signature leaves ") + std::to_string(st.size()) +
+                            " values on the stack: '" + s + "'";
+  out.type = st.back();
+  return "";
+}
+
+// ------------------------------------------------------------------ driver / NVRTC
+struct Driver {
+  bool ok = false;
+  std::string why;
+  CUresult (*ModuleLoadData)(CUmodule*, const void*) = nullptr;
+  CUresult (*ModuleGetFunction)(CUfunction*, CUmodule, const char*) = nullptr;
+  CUresult (*LaunchKernel)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned,
+                           unsigned, CUstream, void**, void**) = nullptr;
+  CUresult (*OccupancyMaxActiveBlocksPerMultiprocessor)(int*, CUfunction, int, size_t) = nullptr;
+  CUresult (*GetErrorString)(CUresult, const char**) = nullptr;
+};
+
+template <class F> bool entry(const char* name, F& fp, std::string& why) {
+  void* p = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess || !p) {
+    why = std::string("driver entry point missing: ") + name;
+    return false;
+  }
+  fp = reinterpret_cast<F>(p);
+  return true;
+}
+
+Driver& driver() {
+  static Driver d;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    d.ok = entry("cuModuleLoadData", d.ModuleLoadData, d.why) &&
+           entry("cuModuleGetFunction", d.ModuleGetFunction, d.why) &&
+           entry("cuLaunchKernel", d.LaunchKernel, d.why) &&
+           entry("cuOccupancyMaxActiveBlocksPerMultiprocessor",
+                 d.OccupancyMaxActiveBlocksPerMultiprocessor, d.why) &&
+           entry("cuGetErrorString", d.GetErrorString, d.why);
+  });
+  return d;
+}
+
+typedef int nvrtcResult_t;
+struct Nvrtc {
+  bool ok = false;
+  std::string why;
+  void* h = nullptr;
+  nvrtcResult_t (*CreateProgram)(void**, const char*, const char*, int, const char* const*,
+                                 const char* const*) = nullptr;
+  nvrtcResult_t (*AddNameExpression)(void*, const char*) = nullptr;
+  nvrtcResult_t (*CompileProgram)(void*, int, const char* const*) = nullptr;
+  nvrtcResult_t (*GetProgramLogSize)(void*, size_t*) = nullptr;
+  nvrtcResult_t (*GetProgramLog)(void*, char*) = nullptr;
+  nvrtcResult_t (*GetCUBINSize)(void*, size_t*) = nullptr;
+  nvrtcResult_t (*GetCUBIN)(void*, char*) = nullptr;
+  nvrtcResult_t (*GetLoweredName)(void*, const char*, const char**) = nullptr;
+  nvrtcResult_t (*DestroyProgram)(void**) = nullptr;
+};
+
+Nvrtc& nvrtc() {
+  static Nvrtc n;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    const char* env = getenv("SALT_NVRTC_LIB");
+    const char* cands[] = {env, "libnvrtc.so.12", "/usr/local/cuda/lib64/libnvrtc.so.12",
+                           "libnvrtc.so"};
+    for (const char* c : cands) {
+      if (!c) continue;
+      n.h = dlopen(c, RTLD_NOW | RTLD_LOCAL);
+      if (n.h) break;
+    }
+    if (!n.h) {
+      n.why = "libnvrtc.so.12 not found (set SALT_NVRTC_LIB)";
+      return;
+    }
+#define SYM(F, NAME)                                               \
+  n.F = reinterpret_cast<decltype(n.F)>(dlsym(n.h, NAME));         \
+  if (!n.F) { n.why = std::string("nvrtc symbol missing: ") + NAME; return; }
+    SYM(CreateProgram, "nvrtcCreateProgram");
+    SYM(AddNameExpression, "nvrtcAddNameExpression");
+    SYM(CompileProgram, "nvrtcCompileProgram");
+    SYM(GetProgramLogSize, "nvrtcGetProgramLogSize");
+    SYM(GetProgramLog, "nvrtcGetProgramLog");
+    SYM(GetCUBINSize, "nvrtcGetCUBINSize");
+    SYM(GetCUBIN, "nvrtcGetCUBIN");
+    SYM(GetLoweredName, "nvrtcGetLoweredName");
+    SYM(DestroyProgram, "nvrtcDestroyProgram");
+#undef SYM
+    n.ok = true;
+  });
+  return n;
+}
+
+const char* kExprSource =
+#include "salt_expr_src.inc"
+    ;
+
+// ------------------------------------------------------------------ kernel table
+struct Kernel {
+  const void* aot = nullptr;                 // compiled-in kernel
+  std::string cubin, lowered;                // JIT kernel (device independent)
+  CUfunction jit_fn[kMaxDevices] = {};       // JIT module per device
+  int occ[kMaxDevices] = {};                 // resident CTAs per SM, per device
+  int vec = 1;                               // lanes per vector access
+  int unroll = 1;
+};
+
+std::string key_of(int dtype, int mode, int vec, const std::string& ta, const std::string& tr) {
+  return std::to_string(dtype) + "|" + std::to_string(mode) + "|" + std::to_string(vec) + "|" +
+         ta + "|" + tr;
+}
+
+std::mutex g_table_mu;
+std::unordered_map<std::string, std::unique_ptr<Kernel>>& table() {
+  static std::unordered_map<std::string, std::unique_ptr<Kernel>> t;
+  return t;
+}
+std::unordered_map<std::string, std::unique_ptr<Kernel>>& jit_table() {
+  static std::unordered_map<std::string, std::unique_ptr<Kernel>> t;
+  return t;
+}
+
+template <class T> constexpr int dtype_of();
+template <> constexpr int dtype_of<float>() { return SALT_F32; }
+template <> constexpr int dtype_of<double>() { return SALT_F64; }
+template <class T> constexpr int vec_of() { return 32 / (int)sizeof(T); }
+
+template <class T, class EA, class ER, int MODE>
+void reg_one(const char* asig, const char* rsig) {
+  Sig sa, sr;
+  std::string ta = "salt::None", tr = "salt::None";
+  if (asig) { parse_sig(asig, false, sa); ta = sa.type; }
+  if (rsig) { parse_sig(rsig, MODE == salt::MODE_ASSIGN_REDUCE, sr); tr = sr.type; }
+  constexpr int V = vec_of<T>();
+  auto k1 = std::make_unique<Kernel>();
+  k1->aot = (const void*)&salt::fused_kernel<T, EA, ER, MODE, V, kUnrollVec, kBlock>;
+  k1->vec = V; k1->unroll = kUnrollVec;
+  table()[key_of(dtype_of<T>(), MODE, V, ta, tr)] = std::move(k1);
+  auto k2 = std::make_unique<Kernel>();
+  k2->aot = (const void*)&salt::fused_kernel<T, EA, ER, MODE, 1, kUnrollScalar, kBlock>;
+  k2->vec = 1; k2->unroll = kUnrollScalar;
+  table()[key_of(dtype_of<T>(), MODE, 1, ta, tr)] = std::move(k2);
+}
+
+template <class EA, class ER, int MODE> void reg(const char* asig, const char* rsig) {
+  reg_one<float, EA, ER, MODE>(asig, rsig);
+  reg_one<double, EA, ER, MODE>(asig, rsig);
+}
+
+using namespace salt;
+// Trees of the reference's named ops (ops.py:18-55) and of BASELINE.json's
+// configs.  The sig string and the C++ type on each line must agree; the GPU
+// tests prove it by comparing every entry against the JIT build of its sig.
+void register_aot() {
+  constexpr int A = MODE_ASSIGN, R = MODE_REDUCE, AR = MODE_ASSIGN_REDUCE;
+  // --- assignments
+  reg<L<0>, None, A>("L0", nullptr);                                      // copy
+  reg<Mul<S<0>, L<0>>, None, A>("S0 L0 *", nullptr);                      // scal / scaled_copy
+  reg<Add<L<0>, Mul<S<0>, L<1>>>, None, A>("L0 S0 L1 * +", nullptr);      // axpy  y + a*x
+  reg<Add<Mul<S<0>, L<0>>, L<1>>, None, A>("S0 L0 * L1 +", nullptr);      // a*x + y
+  reg<Add<L<0>, L<1>>, None, A>("L0 L1 +", nullptr);
+  reg<Sub<L<0>, L<1>>, None, A>("L0 L1 -", nullptr);
+  reg<Mul<L<0>, L<1>>, None, A>("L0 L1 *", nullptr);
+  reg<Add<L<0>, Sub<L<1>, L<2>>>, None, A>("L0 L1 L2 - +", nullptr);      // C2 T1
+  reg<Add<Mul<S<0>, L<0>>, Mul<S<1>, Sub<L<1>, L<2>>>>, None, A>(         // C2 T2
+      "S0 L0 * S1 L1 L2 - * +", nullptr);
+  reg<Add<Sub<Mul<S<0>, Add<L<0>, L<1>>>, Mul<S<1>, Sub<L<2>, L<3>>>>, Mul<S<2>, L<0>>>, None,
+      A>("S0 L0 L1 + * S1 L2 L3 - * - S2 L0 * +", nullptr);               // C4 e-tree
+  // --- reductions
+  reg<None, L<0>, R>(nullptr, "L0");                                      // sum
+  reg<None, Mul<L<0>, L<1>>, R>(nullptr, "L0 L1 *");                      // dot
+  reg<None, Mul<L<0>, L<0>>, R>(nullptr, "L0 L0 *");                      // dot(x,x) / nrm2
+  // --- fused assign + reduce (C5: y = y + a*x ; r = dot(y, z))
+  reg<Add<L<0>, Mul<S<0>, L<1>>>, Mul<D, L<2>>, AR>("L0 S0 L1 * +", "D L2 *");
+  reg<Add<L<0>, Mul<S<0>, L<1>>>, Mul<D, D>, AR>("L0 S0 L1 * +", "D D *");
+}
+
+void ensure_table() {
+  static std::once_flag once;
+  std::call_once(once, [] { register_aot(); });
+}
+
+// Compile the tree with NVRTC; returns nullptr + g_err on failure.
+Kernel* jit_compile(int dtype, int mode, int vec, const std::string& ta, const std::string& tr,
+                    const std::string& key) {
+  Nvrtc& nv = nvrtc();
+  if (!nv.ok) { g_err = "NVRTC unavailable: " + nv.why; return nullptr; }
+  const char* tname = dtype == SALT_F32 ? "float" : "double";
+  const int unroll = vec == 1 ? kUnrollScalar : kUnrollVec;
+  std::string expr = std::string("salt::fused_kernel<") + tname + "," + ta + "," + tr + "," +
+                     std::to_string(mode) + "," + std::to_string(vec) + "," +
+                     std::to_string(unroll) + "," + std::to_string(kBlock) + ">";
+  void* prog = nullptr;
+  if (nv.CreateProgram(&prog, kExprSource, "salt_expr_jit.cu", 0, nullptr, nullptr) != 0) {
+    g_err = "nvrtcCreateProgram failed";
+    return nullptr;
+  }
+  nv.AddNameExpression(prog, expr.c_str());
+  const char* opts[] = {"--gpu-architecture=sm_100a", "-fmad=false", "--std=c++17",
+                        "-lineinfo", "-default-device"};
+  int rc = nv.CompileProgram(prog, 5, opts);
+  if (rc != 0) {
+    size_t ls = 0;
+    nv.GetProgramLogSize(prog, &ls);
+    std::string log(ls, '\0');
+    nv.GetProgramLog(prog, &log[0]);
+    nv.DestroyProgram(&prog);
+    g_err = "NVRTC compile failed for " + expr + ":\n" + log;
+    return nullptr;
+  }
+  auto k = std::make_unique<Kernel>();
+  size_t cs = 0;
+  nv.GetCUBINSize(prog, &cs);
+  k->cubin.resize(cs);
+  nv.GetCUBIN(prog, &k->cubin[0]);
+  const char* low = nullptr;
+  nv.GetLoweredName(prog, expr.c_str(), &low);
+  k->lowered = low ? low : "";
+  nv.DestroyProgram(&prog);
+  k->vec = vec;
+  k->unroll = unroll;
+  Kernel* raw = k.get();
+  jit_table()[key] = std::move(k);
+  return raw;
+}
+
+// Look up (or JIT) the kernel; nullptr + g_err on failure.
+Kernel* get_kernel(int dtype, int mode, int vec, const std::string& ta, const std::string& tr) {
+  ensure_table();
+  const std::string key = key_of(dtype, mode, vec, ta, tr);
+  std::lock_guard<std::mutex> lk(g_table_mu);
+  if (!g_force_jit.load()) {
+    auto it = table().find(key);
+    if (it != table().end()) return it->second.get();
+  }
+  auto jt = jit_table().find(key);
+  if (jt != jit_table().end()) return jt->second.get();
+  return jit_compile(dtype, mode, vec, ta, tr, key);
+}
+
+struct DevInfo { int sms = 0; };
+DevInfo g_dev[kMaxDevices];
+std::mutex g_dev_mu;
+
+int current_device(int& dev) {
+  SALT_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= kMaxDevices) return fail(SALT_EINVAL, "device ordinal out of range");
+  return 0;
+}
+
+// Resolve per-device state (SM count, occupancy, JIT module) for a kernel.
+int prepare(Kernel* k, int dev, int& sms, int& occ) {
+  std::lock_guard<std::mutex> lk(g_dev_mu);
+  if (g_dev[dev].sms == 0) {
+    int v = 0;
+    SALT_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev));
+    g_dev[dev].sms = v;
+  }
+  sms = g_dev[dev].sms;
+  if (!k->aot && !k->jit_fn[dev]) {
+    Driver& d = driver();
+    if (!d.ok) return fail(SALT_EJIT, "driver API unavailable: " + d.why);
+    CUmodule mod;
+    CUresult r = d.ModuleLoadData(&mod, k->cubin.data());
+    if (r != CUDA_SUCCESS) {
+      const char* s = "?";
+      d.GetErrorString(r, &s);
+      return fail(SALT_EJIT, std::string("cuModuleLoadData: ") + s);
+    }
+    r = d.ModuleGetFunction(&k->jit_fn[dev], mod, k->lowered.c_str());
+    if (r != CUDA_SUCCESS) return fail(SALT_EJIT, "cuModuleGetFunction failed for " + k->lowered);
+  }
+  if (k->occ[dev] == 0) {
+    int o = 0;
+    if (k->aot) {
+      SALT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k->aot, kBlock, 0));
+    } else {
+      if (driver().OccupancyMaxActiveBlocksPerMultiprocessor(&o, k->jit_fn[dev], kBlock, 0) !=
+          CUDA_SUCCESS)
+        return fail(SALT_EJIT, "occupancy query failed");
+    }
+    k->occ[dev] = o > 0 ? o : 1;
+  }
+  occ = k->occ[dev];
+  return 0;
+}
+
+template <class T> int launch(Kernel* k, int dev, int grid, salt::Args<T>& args, cudaStream_t st) {
+  void* params[] = {&args};
+  if (k->aot) {
+    cudaError_t e = cudaLaunchKernel(k->aot, dim3(grid), dim3(kBlock), params, 0, st);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaLaunchKernel");
+  } else {
+    CUresult r = driver().LaunchKernel(k->jit_fn[dev], grid, 1, 1, kBlock, 1, 1, 0,
+                                       (CUstream)st, params, nullptr);
+    if (r != CUDA_SUCCESS) {
+      const char* s = "?";
+      driver().GetErrorString(r, &s);
+      return fail(SALT_ECUDA, std::string("cuLaunchKernel: ") + s);
+    }
+  }
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return 0;
+}
+
+// Common 32-byte misalignment of all operands -> (vec, head, nvec).
+template <class T>
+void geometry(void* dst, const void* const* leaves, int nl, i64 n, int& vec, i64& head,
+              i64& nvec) {
+  constexpr int V = vec_of<T>();
+  uintptr_t mis = (uintptr_t)-1;
+  bool same = true;
+  auto check = [&](const void* p) {
+    uintptr_t m = (uintptr_t)p % 32;
+    if (mis == (uintptr_t)-1) mis = m;
+    else if (m != mis) same = false;
+    if (m % sizeof(T)) same = false;
+  };
+  if (dst) check(dst);
+  for (int l = 0; l < nl; ++l) check(leaves[l]);
+  if (mis == (uintptr_t)-1) mis = 0;
+  if (same) {
+    i64 h = (i64)(((32 - mis) % 32) / sizeof(T));
+    if (h > n) h = n;
+    vec = V;
+    head = h;
+    nvec = (n - h) / V;
+  } else {
+    vec = 1;
+    head = 0;
+    nvec = n;
+  }
+}
+
+struct Plan {
+  Sig sa, sr;
+  int mode;
+  int nl, ns;
+};
+
+int make_plan(int dtype, const char* asig, const char* rsig, int mode, int nleaves, int nscalars,
+              Plan& p) {
+  if (dtype != SALT_F32 && dtype != SALT_F64) return fail(SALT_EINVAL, "dtype must be SALT_F32 or SALT_F64");
+  p.mode = mode;
+  std::string err;
+  p.sa.type = p.sr.type = "salt::None";
+  if (mode != salt::MODE_REDUCE) {
+    err = parse_sig(asig, false, p.sa);
+    if (!err.empty()) return fail(SALT_EINVAL, err);
+  }
+  if (mode != salt::MODE_ASSIGN) {
+    err = parse_sig(rsig, mode == salt::MODE_ASSIGN_REDUCE, p.sr);
+    if (!err.empty()) return fail(SALT_EINVAL, err);
+  }
+  p.nl = std::max(p.sa.nl, p.sr.nl);
+  p.ns = std::max(p.sa.ns, p.sr.ns);
+  if (nleaves < p.nl || nleaves > salt::MAX_LEAVES)
+    return fail(SALT_EINVAL, "signature references " + std::to_string(p.nl) + " leaves but " +
+                                 std::to_string(nleaves) + " were passed");
+  if (nscalars < p.ns || nscalars > salt::MAX_SCALARS)
+    return fail(SALT_EINVAL, "signature references " + std::to_string(p.ns) + " scalars but " +
+                                 std::to_string(nscalars) + " were passed");
+  return 0;
+}
+
+template <class T>
+int run_fused(const Plan& p, void* dst, const void* const* leaves, int nleaves,
+              const double* scalars, int nscalars, i64 n, int flags, void* ws, size_t ws_bytes,
+              void* out_dev, void* out_host, cudaStream_t st) {
+  if (n < 0) return fail(SALT_EINVAL, "negative length");
+  const bool reduce = p.mode != salt::MODE_ASSIGN;
+  if (!reduce && n == 0) return 0;  // zero length assign is a no-op (test_engine.py:147-153)
+  if (p.mode != salt::MODE_REDUCE && !dst) return fail(SALT_EINVAL, "NULL destination");
+  for (int l = 0; l < p.nl; ++l)
+    if (!leaves || !leaves[l]) return fail(SALT_EINVAL, "NULL leaf pointer");
+  if (reduce) {
+    if (!out_dev) return fail(SALT_EINVAL, "NULL reduction output");
+    if (!ws || ws_bytes < salt_reduce_workspace_bytes())
+      return fail(SALT_EWORKSPACE, "reduction workspace smaller than salt_reduce_workspace_bytes()");
+  }
+  salt::Args<T> a;
+  memset(&a, 0, sizeof(a));
+  a.dst = (T*)dst;
+  for (int l = 0; l < p.nl; ++l) a.leaf[l] = (const T*)leaves[l];
+  for (int s = 0; s < p.ns; ++s) a.sc[s] = (T)scalars[s];
+  a.n = n;
+  a.flags = flags;
+  int vec;
+  geometry<T>(p.mode == salt::MODE_REDUCE ? nullptr : dst, leaves, p.nl, n, vec, a.head, a.nvec);
+  Kernel* k = get_kernel(dtype_of<T>(), p.mode, vec, p.sa.type, p.sr.type);
+  if (!k) return SALT_EJIT;
+  int dev, sms, occ;
+  int rc = current_device(dev);
+  if (rc) return rc;
+  rc = prepare(k, dev, sms, occ);
+  if (rc) return rc;
+  const i64 per_cta = (i64)kBlock * k->unroll;
+  i64 want = (a.nvec + per_cta - 1) / per_cta;
+  if (want < 1) want = 1;
+  i64 cap = (i64)sms * occ;
+  if (reduce && cap > kMaxGrid) cap = kMaxGrid;
+  int grid = (int)(want < cap ? want : cap);
+  if (reduce) {
+    a.ticket = (unsigned int*)ws;
+    a.partials = (salt::DD*)((char*)ws + kWsHeader);
+    a.out = out_dev;
+  }
+  rc = launch<T>(k, dev, grid, a, st);
+  if (rc) return rc;
+  if (reduce && out_host) {
+    size_t bytes = (flags & SALT_PARTIAL) ? sizeof(salt::DD) : sizeof(T);
+    SALT_CUDA(cudaMemcpyAsync(out_host, out_dev, bytes, cudaMemcpyDeviceToHost, st));
+    SALT_CUDA(cudaStreamSynchronize(st));
+  }
+  return 0;
+}
+
+int dispatch(int dtype, const Plan& p, void* dst, const void* const* leaves, int nleaves,
+             const double* scalars, int nscalars, i64 n, int flags, void* ws, size_t ws_bytes,
+             void* out_dev, void* out_host, cudaStream_t st) {
+  if (dtype == SALT_F32)
+    return run_fused<float>(p, dst, leaves, nleaves, scalars, nscalars, n, flags, ws, ws_bytes,
+                            out_dev, out_host, st);
+  return run_fused<double>(p, dst, leaves, nleaves, scalars, nscalars, n, flags, ws, ws_bytes,
+                           out_dev, out_host, st);
+}
+
+template <class T>
+int finish(const void* parts, int count, int flags, void* out_dev, void* out_host,
+           cudaStream_t st) {
+  if (count < 0 || (count > 0 && !parts) || !out_dev) return fail(SALT_EINVAL, "bad finish arguments");
+  void* params[] = {(void*)&parts, &count, &flags, &out_dev};
+  SALT_CUDA(cudaLaunchKernel((const void*)&salt::finish_kernel<T, kBlock>, dim3(1), dim3(kBlock),
+                             params, 0, st));
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  if (out_host) {
+    size_t bytes = (flags & SALT_PARTIAL) ? sizeof(salt::DD) : sizeof(T);
+    SALT_CUDA(cudaMemcpyAsync(out_host, out_dev, bytes, cudaMemcpyDeviceToHost, st));
+    SALT_CUDA(cudaStreamSynchronize(st));
+  }
+  return 0;
+}
+
+// ------------------------------------------------------------------ host streaming
+struct Events {
+  std::vector<cudaEvent_t> ev;
+  ~Events() { for (auto e : ev) cudaEventDestroy(e); }
+  int make(int count) {
+    ev.resize(count, nullptr);
+    for (auto& e : ev) SALT_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    return 0;
+  }
+};
+
+constexpr int kNBuf = 3;
+constexpr i64 kMaxChunk = i64(1) << 23;
+
+// Shared by assign (reduce == false) and reduce: stream chunk c of every
+// operand through buffer c % 3; the fused kernel runs on streams[1].
+int host_pipeline(int dtype, const Plan& p, void* host_dst, const void* const* host_leaves,
+                  int nleaves, const double* scalars, int nscalars, i64 n, int flags,
+                  void* staging, size_t staging_bytes, void* const* streams3, void* out_host) {
+  const bool reduce = p.mode == salt::MODE_REDUCE;
+  const size_t esz = dtype == SALT_F32 ? 4 : 8;
+  if (n < 0) return fail(SALT_EINVAL, "negative length");
+  if (!streams3 || !staging) return fail(SALT_EINVAL, "NULL staging or streams");
+  if (!reduce && n == 0) return 0;
+  cudaStream_t sh = (cudaStream_t)streams3[0], sc = (cudaStream_t)streams3[1],
+               sd = (cudaStream_t)streams3[2];
+  const int nl = p.nl;
+  const int nbufs_per_set = nl + (reduce ? 0 : 1);
+  // staging: [reduce workspace][chunk partials][result 256B][kNBuf x (nl leaves + dst)]
+  size_t ws = reduce ? salt_reduce_workspace_bytes() : 0;
+  size_t fixed = ws + (reduce ? 256 * 1024 : 0) + 256;
+  if (staging_bytes <= fixed + 256) return fail(SALT_EWORKSPACE, "staging too small");
+  i64 chunk = (i64)((staging_bytes - fixed) / (kNBuf * nbufs_per_set * esz));
+  chunk = chunk / 64 * 64;
+  if (chunk > kMaxChunk) chunk = kMaxChunk;
+  if (chunk < 64) return fail(SALT_EWORKSPACE, "staging too small for one chunk");
+  const i64 nchunks = (n + chunk - 1) / chunk;
+  if (reduce && nchunks * (i64)sizeof(salt::DD) > 256 * 1024)
+    return fail(SALT_EWORKSPACE, "too many chunks for the partial buffer; enlarge staging");
+  char* base = (char*)staging;
+  void* wsp = base;
+  salt::DD* parts = (salt::DD*)(base + ws);
+  void* result = base + ws + (reduce ? 256 * 1024 : 0);
+  char* bufs = base + fixed;
+  auto buf = [&](int b, int i) -> void* {
+    return bufs + ((size_t)b * nbufs_per_set + i) * chunk * esz;
+  };
+  if (reduce) SALT_CUDA(cudaMemsetAsync(wsp, 0, kWsHeader, sc));
+  Events h2d, comp, d2h;
+  int rc = h2d.make(kNBuf);
+  if (!rc) rc = comp.make(kNBuf);
+  if (!rc) rc = d2h.make(kNBuf);
+  if (rc) return rc;
+  for (i64 c = 0; c < nchunks; ++c) {
+    const int b = (int)(c % kNBuf);
+    const i64 off = c * chunk;
+    const i64 m = std::min(chunk, n - off);
+    if (c >= kNBuf) SALT_CUDA(cudaStreamWaitEvent(sh, comp.ev[b], 0));
+    const void* dleaves[salt::MAX_LEAVES];
+    for (int l = 0; l < nl; ++l) {
+      SALT_CUDA(cudaMemcpyAsync(buf(b, l), (const char*)host_leaves[l] + off * esz, m * esz,
+                                cudaMemcpyHostToDevice, sh));
+      dleaves[l] = buf(b, l);
+    }
+    SALT_CUDA(cudaEventRecord(h2d.ev[b], sh));
+    SALT_CUDA(cudaStreamWaitEvent(sc, h2d.ev[b], 0));
+    if (!reduce && c >= kNBuf) SALT_CUDA(cudaStreamWaitEvent(sc, d2h.ev[b], 0));
+    void* ddst = reduce ? nullptr : buf(b, nl);
+    rc = dispatch(dtype, p, ddst, dleaves, nleaves, scalars, nscalars, m,
+                  reduce ? SALT_PARTIAL : 0, wsp, ws, reduce ? (void*)(parts + c) : nullptr,
+                  nullptr, sc);
+    if (rc) return rc;
+    SALT_CUDA(cudaEventRecord(comp.ev[b], sc));
+    if (!reduce) {
+      SALT_CUDA(cudaStreamWaitEvent(sd, comp.ev[b], 0));
+      SALT_CUDA(cudaMemcpyAsync((char*)host_dst + off * esz, ddst, m * esz,
+                                cudaMemcpyDeviceToHost, sd));
+      SALT_CUDA(cudaEventRecord(d2h.ev[b], sd));
+    }
+  }
+  if (reduce) {
+    if (nchunks == 0) {
+      // zero length: the sum is dtype(0) (test_engine.py:147-153)
+      rc = dispatch(dtype, p, nullptr, host_leaves, nleaves, scalars, nscalars, 0, flags, wsp, ws,
+                    result, out_host, sc);
+      if (rc) return rc;
+    } else {
+      rc = dtype == SALT_F32 ? finish<float>(parts, (int)nchunks, flags, result, out_host, sc)
+                             : finish<double>(parts, (int)nchunks, flags, result, out_host, sc);
+      if (rc) return rc;
+    }
+  }
+  SALT_CUDA(cudaStreamSynchronize(sh));
+  SALT_CUDA(cudaStreamSynchronize(sc));
+  SALT_CUDA(cudaStreamSynchronize(sd));
+  return 0;
+}
+
+}  // namespace
+
+// ====================================================================== C ABI
+extern "C" {
+
+int salt_abi_version(void) { return SALT_ABI_VERSION; }
+
+const char* salt_last_error(void) { return g_err.c_str(); }
+
+uint64_t salt_launch_count(void) { return g_launches.load(); }
+
+void salt_set_force_jit(int on) { g_force_jit.store(on ? 1 : 0); }
+
+size_t salt_reduce_workspace_bytes(void) { return kWsHeader + (size_t)kMaxGrid * sizeof(salt::DD); }
+
+int salt_signature_kind(int dtype, const char* sig, const char* reduce_sig, int kind) {
+  if (kind < 0 || kind > 2) return 0;
+  Plan p;
+  const char* a = kind == 1 ? nullptr : sig;
+  const char* r = kind == 0 ? nullptr : (kind == 1 ? sig : reduce_sig);
+  if (make_plan(dtype, a, r, kind, salt::MAX_LEAVES, salt::MAX_SCALARS, p)) return 0;
+  ensure_table();
+  const int V = dtype == SALT_F32 ? 8 : 4;
+  std::lock_guard<std::mutex> lk(g_table_mu);
+  return table().count(key_of(dtype, kind, V, p.sa.type, p.sr.type)) ? 1 : 2;
+}
+
+int salt_assign(int dtype, const char* sig, void* dst, const void* const* leaves, int nleaves,
+                const double* scalars, int nscalars, int64_t n, void* stream) {
+  Plan p;
+  int rc = make_plan(dtype, sig, nullptr, salt::MODE_ASSIGN, nleaves, nscalars, p);
+  if (rc) return rc;
+  return dispatch(dtype, p, dst, leaves, nleaves, scalars, nscalars, n, 0, nullptr, 0, nullptr,
+                  nullptr, (cudaStream_t)stream);
+}
+
+int salt_reduce(int dtype, const char* sig, const void* const* leaves, int nleaves,
+                const double* scalars, int nscalars, int64_t n, int flags, void* workspace,
+                size_t workspace_bytes, void* out_dev, void* out_host, void* stream) {
+  Plan p;
+  int rc = make_plan(dtype, nullptr, sig, salt::MODE_REDUCE, nleaves, nscalars, p);
+  if (rc) return rc;
+  return dispatch(dtype, p, nullptr, leaves, nleaves, scalars, nscalars, n, flags, workspace,
+                  workspace_bytes, out_dev, out_host, (cudaStream_t)stream);
+}
+
+int salt_assign_reduce(int dtype, const char* assign_sig, const char* reduce_sig, void* dst,
+                       const void* const* leaves, int nleaves, const double* scalars,
+                       int nscalars, int64_t n, int flags, void* workspace,
+                       size_t workspace_bytes, void* out_dev, void* out_host, void* stream) {
+  Plan p;
+  int rc = make_plan(dtype, assign_sig, reduce_sig, salt::MODE_ASSIGN_REDUCE, nleaves, nscalars, p);
+  if (rc) return rc;
+  return dispatch(dtype, p, dst, leaves, nleaves, scalars, nscalars, n, flags, workspace,
+                  workspace_bytes, out_dev, out_host, (cudaStream_t)stream);
+}
+
+int salt_reduce_finish(int dtype, const void* partials_dev, int count, int flags, void* out_dev,
+                       void* out_host, void* stream) {
+  if (dtype == SALT_F32)
+    return finish<float>(partials_dev, count, flags, out_dev, out_host, (cudaStream_t)stream);
+  if (dtype == SALT_F64)
+    return finish<double>(partials_dev, count, flags, out_dev, out_host, (cudaStream_t)stream);
+  return fail(SALT_EINVAL, "dtype must be SALT_F32 or SALT_F64");
+}
+
+int salt_assign_host(int dtype, const char* sig, void* host_dst, const void* const* host_leaves,
+                     int nleaves, const double* scalars, int nscalars, int64_t n, void* staging,
+                     size_t staging_bytes, void* const* streams3) {
+  Plan p;
+  int rc = make_plan(dtype, sig, nullptr, salt::MODE_ASSIGN, nleaves, nscalars, p);
+  if (rc) return rc;
+  if (!host_dst) return fail(SALT_EINVAL, "NULL destination");
+  return host_pipeline(dtype, p, host_dst, host_leaves, nleaves, scalars, nscalars, n, 0, staging,
+                       staging_bytes, streams3, nullptr);
+}
+
+int salt_reduce_host(int dtype, const char* sig, const void* const* host_leaves, int nleaves,
+                     const double* scalars, int nscalars, int64_t n, int flags, void* staging,
+                     size_t staging_bytes, void* const* streams3, void* out_host) {
+  Plan p;
+  int rc = make_plan(dtype, nullptr, sig, salt::MODE_REDUCE, nleaves, nscalars, p);
+  if (rc) return rc;
+  if (!out_host) return fail(SALT_EINVAL, "NULL out_host");
+  return host_pipeline(dtype, p, nullptr, host_leaves, nleaves, scalars, nscalars, n, flags,
+                       staging, staging_bytes, streams3, out_host);
+}
+
+}  // extern "C"

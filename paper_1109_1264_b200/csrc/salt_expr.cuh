@@ -1,0 +1,338 @@
+// salt_expr.cuh — device-side expression templates and the fused kernel.
+//
+// This is SALT's idea (arXiv 1109.1264, Fig. 1 / Listing 2) moved to
+// the GPU: an expression tree is a TYPE (Add<L<0>, Sub<L<1>, L<2>>>), the
+// kernel is instantiated per tree shape, and the whole tree is evaluated in
+// registers between one vectorised load burst and one store burst, so no
+// intermediate vector ever reaches HBM.
+//
+// Reference semantics reproduced bit for bit (pkg/src/lanevec/...):
+//   * every binary node is ONE IEEE op in the element type, left operand
+//     first (expressions.py:239-249, operator.add/sub/mul :255-270);
+//   * ScaleNode is alpha * child with alpha already coerced to the element
+//     type (expressions.py:282, :319-320);
+//   * no FMA contraction, no flush-to-zero: the __{d,f}{add,sub,mul}_rn
+//     intrinsics pin round-to-nearest and forbid contraction;
+//   * AssignNode computes the full value before the store, so exact
+//     aliasing dst == leaf is safe (expressions.py:392-395).
+//
+// Reductions (SumNode, expressions.py:401-467) are NOT order-reproduced: the
+// reference's order depends on its CPU unroll plan and its contract is a
+// tolerance.  Here they are compensated (double-double) and
+// deterministic, i.e. more accurate than the reference's own engine.
+//
+// The header is self-contained (no #include) so NVRTC can compile it verbatim
+// for signatures that are not in the compiled-in table.
+#pragma once
+
+namespace salt {
+
+typedef long long i64;
+
+// ---------------------------------------------------------------- arithmetic
+template <class T> struct Arith;
+template <> struct Arith<double> {
+  static __device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
+  static __device__ __forceinline__ double sub(double a, double b) { return __dsub_rn(a, b); }
+  static __device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
+  static __device__ __forceinline__ double sqrt_rn(double a) { return __dsqrt_rn(a); }
+};
+template <> struct Arith<float> {
+  static __device__ __forceinline__ float add(float a, float b) { return __fadd_rn(a, b); }
+  static __device__ __forceinline__ float sub(float a, float b) { return __fsub_rn(a, b); }
+  static __device__ __forceinline__ float mul(float a, float b) { return __fmul_rn(a, b); }
+  static __device__ __forceinline__ float sqrt_rn(float a) { return __fsqrt_rn(a); }
+};
+
+__host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
+
+// ---------------------------------------------------------------- tree nodes
+// Each node exposes: NL (leaves referenced = max index + 1), NS (scalars),
+// USES_D (reads the just-assigned value) and ev(env, k) for lane k.
+template <int I> struct L {
+  enum { NL = I + 1, NS = 0, USES_D = 0 };
+  template <class Env> static __device__ __forceinline__ typename Env::T ev(const Env& e, int k) {
+    return e.x[I][k];
+  }
+};
+template <int I> struct S {
+  enum { NL = 0, NS = I + 1, USES_D = 0 };
+  template <class Env> static __device__ __forceinline__ typename Env::T ev(const Env& e, int) {
+    return e.s[I];
+  }
+};
+struct D {
+  enum { NL = 0, NS = 0, USES_D = 1 };
+  template <class Env> static __device__ __forceinline__ typename Env::T ev(const Env& e, int k) {
+    return e.d[k];
+  }
+};
+// Placeholder for "no tree" (reduce-only kernels have no assign tree and
+// vice versa).
+struct None {
+  enum { NL = 0, NS = 0, USES_D = 0 };
+  template <class Env> static __device__ __forceinline__ typename Env::T ev(const Env&, int) {
+    return typename Env::T(0);
+  }
+};
+
+#define SALT_BINARY_NODE(NAME, FN)                                                       \
+  template <class A, class B> struct NAME {                                              \
+    enum { NL = cmax(A::NL, B::NL), NS = cmax(A::NS, B::NS), USES_D = A::USES_D | B::USES_D }; \
+    template <class Env> static __device__ __forceinline__ typename Env::T ev(const Env& e, int k) { \
+      return Arith<typename Env::T>::FN(A::ev(e, k), B::ev(e, k));                      \
+    }                                                                                    \
+  };
+SALT_BINARY_NODE(Add, add)
+SALT_BINARY_NODE(Sub, sub)
+SALT_BINARY_NODE(Mul, mul)
+#undef SALT_BINARY_NODE
+
+// ---------------------------------------------------------------- kernel ABI
+enum { MAX_LEAVES = 8, MAX_SCALARS = 8, MODE_ASSIGN = 0, MODE_REDUCE = 1, MODE_ASSIGN_REDUCE = 2 };
+enum { FLAG_SQRT = 1, FLAG_PARTIAL = 2 };
+
+struct DD { double hi, lo; };  // double-double partial (same layout as double2)
+
+// One by-value parameter block shared by AOT and JIT kernels.
+template <class T> struct Args {
+  T* dst;                         // assign modes
+  const T* leaf[MAX_LEAVES];
+  T sc[MAX_SCALARS];
+  i64 n;                          // elements
+  i64 head;                       // scalar elements before the first aligned vector
+  i64 nvec;                       // aligned vectors of V elements after `head`
+  DD* partials;                   // reduce modes: per-CTA partials (workspace)
+  unsigned int* ticket;           // reduce modes: last-CTA counter (workspace, zeroed)
+  void* out;                      // reduce modes: T result or DD partial
+  int flags;
+};
+
+// 32-byte (256-bit) vector access: LDG.E.ENL2.256 / STG.E.ENL2.256 on sm_100a.
+// Plain (coherent) loads: a leaf may alias the destination (axpy, scal).
+template <class T, int V> struct VecIO;
+template <> struct VecIO<double, 4> {
+  static __device__ __forceinline__ void load(double (&r)[4], const double* p) {
+    asm volatile("ld.global.L1::no_allocate.v4.f64 {%0,%1,%2,%3}, [%4];"
+                 : "=d"(r[0]), "=d"(r[1]), "=d"(r[2]), "=d"(r[3]) : "l"(p));
+  }
+  static __device__ __forceinline__ void store(double* p, const double (&r)[4]) {
+    asm volatile("st.global.L1::no_allocate.v4.f64 [%0], {%1,%2,%3,%4};"
+                 :: "l"(p), "d"(r[0]), "d"(r[1]), "d"(r[2]), "d"(r[3]) : "memory");
+  }
+};
+template <> struct VecIO<float, 8> {
+  static __device__ __forceinline__ void load(float (&r)[8], const float* p) {
+    asm volatile("ld.global.L1::no_allocate.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]),
+                   "=f"(r[4]), "=f"(r[5]), "=f"(r[6]), "=f"(r[7]) : "l"(p));
+  }
+  static __device__ __forceinline__ void store(float* p, const float (&r)[8]) {
+    asm volatile("st.global.L1::no_allocate.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
+                 :: "l"(p), "f"(r[0]), "f"(r[1]), "f"(r[2]), "f"(r[3]),
+                    "f"(r[4]), "f"(r[5]), "f"(r[6]), "f"(r[7]) : "memory");
+  }
+};
+template <class T> struct VecIO<T, 1> {
+  static __device__ __forceinline__ void load(T (&r)[1], const T* p) { r[0] = *p; }
+  static __device__ __forceinline__ void store(T* p, const T (&r)[1]) { *p = r[0]; }
+};
+
+// Registers of one unroll slot: V lanes of every leaf, the scalars, and the
+// assigned value (read back by D in fused assign+reduce trees).
+template <class T_, int NL, int NS, int V> struct Env {
+  typedef T_ T;
+  T x[NL > 0 ? NL : 1][V];
+  T s[NS > 0 ? NS : 1];
+  T d[V];
+};
+
+// ---------------------------------------------------------------- reductions
+// Knuth TwoSum: s + e == a + b exactly.
+__device__ __forceinline__ void two_sum(double a, double b, double& s, double& e) {
+  s = __dadd_rn(a, b);
+  double bp = __dsub_rn(s, a);
+  double ap = __dsub_rn(s, bp);
+  e = __dadd_rn(__dsub_rn(a, ap), __dsub_rn(b, bp));
+}
+__device__ __forceinline__ DD dd_add(DD a, DD b) {
+  double s, e;
+  two_sum(a.hi, b.hi, s, e);
+  e = __dadd_rn(e, __dadd_rn(a.lo, b.lo));
+  DD r;
+  two_sum(s, e, r.hi, r.lo);
+  return r;
+}
+
+// Per-thread accumulator.  f64 terms: compensated (TwoSum per term).
+// f32 terms: exact conversion to double and a plain double sum — a thread
+// sums O(10^3) terms, so its error (~1e-13 relative) is far below f32 eps.
+template <class T> struct Acc;
+template <> struct Acc<double> {
+  double hi = 0.0, lo = 0.0;
+  __device__ __forceinline__ void add(double v) {
+    double s, e;
+    two_sum(hi, v, s, e);
+    hi = s;
+    lo = __dadd_rn(lo, e);
+  }
+  __device__ __forceinline__ DD get() const { DD r; two_sum(hi, lo, r.hi, r.lo); return r; }
+};
+template <> struct Acc<float> {
+  double hi = 0.0;
+  __device__ __forceinline__ void add(float v) { hi = __dadd_rn(hi, (double)v); }
+  __device__ __forceinline__ DD get() const { DD r; r.hi = hi; r.lo = 0.0; return r; }
+};
+
+template <int BLOCK> __device__ __forceinline__ DD block_reduce_dd(DD v, DD* smem) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    DD o;
+    o.hi = __shfl_xor_sync(0xffffffffu, v.hi, off);
+    o.lo = __shfl_xor_sync(0xffffffffu, v.lo, off);
+    v = dd_add(v, o);
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) smem[warp] = v;
+  __syncthreads();
+  if (warp == 0) {
+    DD z; z.hi = 0.0; z.lo = 0.0;
+    v = lane < BLOCK / 32 ? smem[lane] : z;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      DD o;
+      o.hi = __shfl_xor_sync(0xffffffffu, v.hi, off);
+      o.lo = __shfl_xor_sync(0xffffffffu, v.lo, off);
+      v = dd_add(v, o);
+    }
+  }
+  return v;  // valid in thread 0
+}
+
+// Round a double-double total to the element type, optional sqrt, store.
+template <class T> __device__ __forceinline__ void finish_store(DD tot, int flags, void* out) {
+  if (flags & FLAG_PARTIAL) {
+    *(DD*)out = tot;
+    return;
+  }
+  T r = (T)__dadd_rn(tot.hi, tot.lo);
+  if (flags & FLAG_SQRT) r = Arith<T>::sqrt_rn(r);
+  *(T*)out = r;
+}
+
+// ---------------------------------------------------------------- the kernel
+// MODE_ASSIGN:        dst[i] = EA(i)
+// MODE_REDUCE:        out    = sum_i ER(i)
+// MODE_ASSIGN_REDUCE: dst[i] = EA(i); out = sum_i ER(i, D = dst[i])   (one pass)
+//
+// Layout of the index space: [0, head) scalar, then nvec aligned vectors of
+// V lanes, then the scalar tail.  Each CTA walks the vectors in chunks of
+// BLOCK*UNR (grid-stride), issuing all UNR x NL 256-bit loads of a chunk
+// before any arithmetic: the GPU form of the reference's load burst /
+// vector_op burst / store burst (engine.py:209-225).
+template <class T, class EA, class ER, int MODE, int V, int UNR, int BLOCK>
+__global__ void __launch_bounds__(BLOCK) fused_kernel(Args<T> a) {
+  constexpr int NL = cmax(EA::NL, ER::NL);
+  constexpr int NS = cmax(EA::NS, ER::NS);
+  constexpr bool ASSIGN = MODE != MODE_REDUCE;
+  constexpr bool REDUCE = MODE != MODE_ASSIGN;
+  typedef Env<T, NL, NS, V> E1;
+  typedef Env<T, NL, NS, 1> ES;
+
+  Acc<T> acc;
+  const i64 nthreads = (i64)gridDim.x * BLOCK;
+  const i64 gtid = (i64)blockIdx.x * BLOCK + threadIdx.x;
+
+  // ---- scalar head + tail (at most 2*(V-1) elements, or all of them if V == 1)
+  {
+    const i64 tail0 = a.head + a.nvec * V;
+    const i64 nscalar = a.head + (a.n - tail0);
+    for (i64 t = gtid; t < nscalar; t += nthreads) {
+      const i64 i = t < a.head ? t : tail0 + (t - a.head);
+      ES e;
+#pragma unroll
+      for (int l = 0; l < NL; ++l) e.x[l][0] = a.leaf[l][i];
+#pragma unroll
+      for (int s = 0; s < NS; ++s) e.s[s] = a.sc[s];
+      if (ASSIGN) {
+        e.d[0] = EA::ev(e, 0);
+        a.dst[i] = e.d[0];
+      }
+      if (REDUCE) acc.add(ER::ev(e, 0));
+    }
+  }
+
+  // ---- vector body
+  for (i64 base = (i64)blockIdx.x * BLOCK * UNR + threadIdx.x; base < a.nvec;
+       base += nthreads * UNR) {
+    E1 e[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const i64 j = base + (i64)u * BLOCK;
+      if (j < a.nvec) {
+        const i64 off = a.head + j * V;
+#pragma unroll
+        for (int l = 0; l < NL; ++l) VecIO<T, V>::load(e[u].x[l], a.leaf[l] + off);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const i64 j = base + (i64)u * BLOCK;
+      if (j < a.nvec) {
+#pragma unroll
+        for (int s = 0; s < NS; ++s) e[u].s[s] = a.sc[s];
+        if (ASSIGN) {
+#pragma unroll
+          for (int k = 0; k < V; ++k) e[u].d[k] = EA::ev(e[u], k);
+          VecIO<T, V>::store(a.dst + a.head + j * V, e[u].d);
+        }
+        if (REDUCE) {
+#pragma unroll
+          for (int k = 0; k < V; ++k) acc.add(ER::ev(e[u], k));
+        }
+      }
+    }
+  }
+
+  if (REDUCE) {
+    __shared__ DD smem[BLOCK / 32];
+    __shared__ bool is_last;
+    DD part = block_reduce_dd<BLOCK>(acc.get(), smem);
+    if (threadIdx.x == 0) {
+      a.partials[blockIdx.x] = part;
+      __threadfence();
+      unsigned int t = atomicAdd(a.ticket, 1u);
+      is_last = (t == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (is_last) {
+      __threadfence();
+      // Fixed-order combine of all CTA partials: thread t folds t, t+BLOCK, ...
+      DD v; v.hi = 0.0; v.lo = 0.0;
+      for (int b = threadIdx.x; b < (int)gridDim.x; b += BLOCK) {
+        DD p;  // L2 loads: other CTAs wrote these during this launch
+        p.hi = __ldcg(&a.partials[b].hi);
+        p.lo = __ldcg(&a.partials[b].lo);
+        v = dd_add(v, p);
+      }
+      __syncthreads();
+      DD tot = block_reduce_dd<BLOCK>(v, smem);
+      if (threadIdx.x == 0) {
+        finish_store<T>(tot, a.flags, a.out);
+        *a.ticket = 0u;  // ready for the next launch on this workspace
+      }
+    }
+  }
+}
+
+// Combine `count` partials (all-gathered per-device DD values, rank order).
+template <class T, int BLOCK>
+__global__ void __launch_bounds__(BLOCK) finish_kernel(const DD* parts, int count, int flags, void* out) {
+  __shared__ DD smem[BLOCK / 32];
+  DD v; v.hi = 0.0; v.lo = 0.0;
+  for (int b = threadIdx.x; b < count; b += BLOCK) v = dd_add(v, parts[b]);
+  DD tot = block_reduce_dd<BLOCK>(v, smem);
+  if (threadIdx.x == 0) finish_store<T>(tot, flags, out);
+}
+
+}  // namespace salt

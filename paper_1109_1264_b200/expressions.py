@@ -1,0 +1,362 @@
+"""Lazy expression nodes built by operator overloading.
+
+Same classes, constructors, checks and operator sugar as the reference
+(pkg/src/lanevec/expressions.py): building a tree touches no element
+(test_acceptance.py:246-254); dtype mismatches are TypeErrors
+at construction (:196-203, :340-343); ScaleNode coerces alpha to the element
+type (:282); AssignNode's destination must be a Leaf (:338-339); lengths are
+checked before any access (`common_length`, :483-497).
+
+What differs is evaluation.  The reference nodes implement a per-block CPU
+contract (init / load / vector_op / store / single_op ..., :3-15) that its
+Python loop engine drives.  Here every node instead knows how to emit itself
+in postfix (`_postfix`), so the engine can lower the whole tree to one
+signature string — e.g. `S0 L0 * S1 L1 L2 - * +` for alpha*a + beta*(b - c)
+— and hand it to libsalt.so, which runs the tree as ONE fused sm_100a kernel.
+"""
+
+import numbers
+
+import numpy as np
+
+from .lanes import LaneVector, horizontal_sum
+
+__all__ = [
+    "Expression",
+    "Leaf",
+    "AddNode",
+    "SubNode",
+    "MulNode",
+    "ScaleNode",
+    "AssignNode",
+    "SumNode",
+    "AssignReduceNode",
+    "LengthMismatchError",
+    "as_node",
+    "common_length",
+    "combine_partials",
+]
+
+
+class LengthMismatchError(ValueError):
+    """Leaves of one expression tree disagree on length."""
+
+
+def _is_vector(obj) -> bool:
+    # The reference's duck-typed vector test (expressions.py:68-69).
+    return hasattr(obj, "read_block") and hasattr(obj, "dtype")
+
+
+def as_node(obj) -> "Expression":
+    """Wrap a vector in a Leaf; pass expressions through."""
+    if isinstance(obj, Expression):
+        return obj
+    if _is_vector(obj):
+        return Leaf(obj)
+    raise TypeError(f"cannot use {type(obj).__name__} in a vector expression")
+
+
+def add_nodes(a, b):
+    return AddNode(as_node(a), as_node(b))
+
+
+def sub_nodes(a, b):
+    return SubNode(as_node(a), as_node(b))
+
+
+def mul_nodes(a, b):
+    if isinstance(b, numbers.Real):
+        return ScaleNode(b, as_node(a))
+    return MulNode(as_node(a), as_node(b))
+
+
+def scale_node(alpha, x):
+    return ScaleNode(alpha, as_node(x))
+
+
+def negate_node(x):
+    return ScaleNode(-1, as_node(x))
+
+
+class _Lowering:
+    """Collects leaves (deduplicated by vector identity, numbered by first
+    appearance in postfix order) and scalars (numbered by appearance)."""
+
+    __slots__ = ("tokens", "vectors", "_ids", "scalars", "occurrences", "dest_id")
+
+    def __init__(self, parent: "_Lowering" = None, dest=None):
+        # A child lowering (the reduce tree of a fused assign+reduce root)
+        # shares the parent's leaf table and scalar list; its references to
+        # the destination become `D`, the value just assigned.
+        self.tokens = []
+        self.vectors = parent.vectors if parent else []
+        self._ids = parent._ids if parent else {}
+        self.scalars = parent.scalars if parent else []
+        self.occurrences = parent.occurrences if parent else []
+        self.dest_id = id(dest) if dest is not None else None
+
+    def leaf(self, vector):
+        if self.dest_id is not None and id(vector) == self.dest_id:
+            self.tokens.append("D")
+            return
+        k = self._ids.get(id(vector))
+        if k is None:
+            k = len(self.vectors)
+            self._ids[id(vector)] = k
+            self.vectors.append(vector)
+            self.occurrences.append(0)
+        self.occurrences[k] += 1
+        self.tokens.append(f"L{k}")
+
+    def scalar(self, value):
+        self.tokens.append(f"S{len(self.scalars)}")
+        self.scalars.append(float(value))
+
+
+class Expression:
+    """Base class: operator sugar (reference expressions.py:103-132)."""
+
+    __slots__ = ()
+
+    __array_ufunc__ = None
+
+    def __add__(self, other):
+        return add_nodes(self, other)
+
+    def __radd__(self, other):
+        return add_nodes(other, self)
+
+    def __sub__(self, other):
+        return sub_nodes(self, other)
+
+    def __rsub__(self, other):
+        return sub_nodes(other, self)
+
+    def __mul__(self, other):
+        return mul_nodes(self, other)
+
+    def __rmul__(self, other):
+        if isinstance(other, numbers.Real):
+            return ScaleNode(other, self)
+        return mul_nodes(other, self)
+
+    def __neg__(self):
+        return negate_node(self)
+
+
+class Leaf(Expression):
+    """Direct view of a vector."""
+
+    __slots__ = ("vector", "dtype")
+
+    def __init__(self, vector):
+        self.vector = vector
+        self.dtype = vector.dtype
+
+    @property
+    def register_footprint(self) -> int:
+        return 1
+
+    def leaves(self):
+        yield self
+
+    def _postfix(self, lw: _Lowering):
+        lw.leaf(self.vector)
+
+    def __repr__(self):
+        return f"Leaf({self.vector!r})"
+
+
+class _BinaryNode(Expression):
+    """left (op) right, one IEEE op in the element type, left operand first."""
+
+    __slots__ = ("left", "right", "dtype")
+
+    _symbol = "?"
+
+    def __init__(self, left: Expression, right: Expression):
+        if left.dtype != right.dtype:
+            raise TypeError(f"mixed element types in expression: {left.dtype} vs {right.dtype}")
+        self.left = left
+        self.right = right
+        self.dtype = left.dtype
+
+    @property
+    def register_footprint(self) -> int:
+        return self.left.register_footprint + self.right.register_footprint
+
+    def leaves(self):
+        yield from self.left.leaves()
+        yield from self.right.leaves()
+
+    def _postfix(self, lw: _Lowering):
+        self.left._postfix(lw)
+        self.right._postfix(lw)
+        lw.tokens.append(self._symbol)
+
+    def __repr__(self):
+        return f"({self.left!r} {self._symbol} {self.right!r})"
+
+
+class AddNode(_BinaryNode):
+    __slots__ = ()
+    _symbol = "+"
+
+
+class SubNode(_BinaryNode):
+    __slots__ = ()
+    _symbol = "-"
+
+
+class MulNode(_BinaryNode):
+    __slots__ = ()
+    _symbol = "*"
+
+
+class ScaleNode(Expression):
+    """alpha * child; alpha coerced to the element type at construction."""
+
+    __slots__ = ("alpha", "child", "dtype")
+
+    def __init__(self, alpha, child: Expression):
+        self.child = child
+        self.dtype = child.dtype
+        self.alpha = self.dtype.type(alpha)
+
+    @property
+    def register_footprint(self) -> int:
+        return 1 + self.child.register_footprint
+
+    def leaves(self):
+        yield from self.child.leaves()
+
+    def _postfix(self, lw: _Lowering):
+        # alpha is the LEFT operand, as in the reference (expressions.py:320)
+        lw.scalar(self.alpha)
+        self.child._postfix(lw)
+        lw.tokens.append("*")
+
+    def __repr__(self):
+        return f"({float(self.alpha)!r} * {self.child!r})"
+
+
+class AssignNode(Expression):
+    """Evaluation root writing an elementwise expression into `dest`.
+
+    The destination is written once per element and never read unless it
+    is also a source leaf; exact aliasing (dest is a source leaf, e.g. scal
+    and axpy) is safe because each thread computes its whole vector of
+    results before storing it.  Overlap at a shifted offset is unsupported
+    and unchecked, as in the reference (expressions.py:326-333).
+    """
+
+    __slots__ = ("dest", "source", "dtype")
+
+    def __init__(self, dest: Leaf, source: Expression):
+        if not isinstance(dest, Leaf):
+            raise TypeError("assignment destination must be a vector leaf")
+        if dest.dtype != source.dtype:
+            raise TypeError(f"mixed element types in assignment: {dest.dtype} vs {source.dtype}")
+        self.dest = dest
+        self.source = source
+        self.dtype = dest.dtype
+
+    @property
+    def register_footprint(self) -> int:
+        # +1 lane for the result held between op burst and store burst
+        # (reference expressions.py:350-354; only plan selection uses it).
+        return 1 + self.source.register_footprint
+
+    def leaves(self):
+        yield self.dest
+        yield from self.source.leaves()
+
+    def __repr__(self):
+        return f"Assign({self.dest!r} <- {self.source!r})"
+
+
+class SumNode(Expression):
+    """Reduction root: sum of the child over all indices."""
+
+    __slots__ = ("child", "dtype")
+
+    def __init__(self, child: Expression):
+        self.child = child
+        self.dtype = child.dtype
+
+    @property
+    def register_footprint(self) -> int:
+        return 1 + self.child.register_footprint
+
+    def leaves(self):
+        yield from self.child.leaves()
+
+    def __repr__(self):
+        return f"Sum({self.child!r})"
+
+
+def combine_partials(rows, remainder):
+    """The reference's fixed fold of lane accumulators (expressions.py:470-480):
+    rows in order, each folded left to right, remainder last.  Kept for API
+    parity; GPU reductions combine double-double partials instead."""
+    total = None
+    for row in rows:
+        h = horizontal_sum(LaneVector(np.asarray(row)))
+        total = h if total is None else total + h
+    return remainder if total is None else total + remainder
+
+
+def common_length(root: Expression) -> int:
+    """Length shared by every leaf (the destination included); checked before
+    any element is touched."""
+    length = None
+    for leaf in root.leaves():
+        n = len(leaf.vector)
+        if length is None:
+            length = n
+        elif n != length:
+            raise LengthMismatchError(f"expression mixes vectors of length {length} and {n}")
+    if length is None:
+        raise TypeError("expression has no vector leaves")
+    return length
+
+
+class AssignReduceNode(Expression):
+    """Fused root: run `assign`, then reduce `total` over the NEW values of
+    the destination, in one pass over memory (no reference counterpart: the
+    reference needs two traversals, ops.axpy then ops.dot, ops.py:18-36).
+
+    Inside `total`, leaves that are the destination vector read the value
+    just assigned; every other leaf reads its (unchanged) input.
+    """
+
+    __slots__ = ("assign", "total", "dtype")
+
+    def __init__(self, assign: AssignNode, total: SumNode):
+        if not isinstance(assign, AssignNode):
+            raise TypeError("AssignReduceNode needs an AssignNode")
+        if not isinstance(total, SumNode):
+            raise TypeError("AssignReduceNode needs a SumNode")
+        if assign.dtype != total.dtype:
+            raise TypeError(f"mixed element types: {assign.dtype} vs {total.dtype}")
+        self.assign = assign
+        self.total = total
+        self.dtype = assign.dtype
+
+    @property
+    def register_footprint(self) -> int:
+        return self.assign.register_footprint + self.total.register_footprint
+
+    def leaves(self):
+        yield from self.assign.leaves()
+        yield from self.total.leaves()
+
+    def __repr__(self):
+        return f"AssignReduce({self.assign!r}; {self.total!r})"
+
+
+def lower(expr: Expression, parent: _Lowering = None, dest=None) -> _Lowering:
+    """Postfix signature of an elementwise tree (leaves + scalars collected)."""
+    lw = _Lowering(parent, dest)
+    expr._postfix(lw)
+    return lw

@@ -1,0 +1,66 @@
+"""Named level-1 operations (reference pkg/src/lanevec/ops.py:18-55).
+
+Same names, arguments, tree shapes and return types.  Each call is one fused
+kernel launch.  Two B200 additions:
+
+  * `norm2` finishes with the square root inside the reduction kernel
+    (SALT_SQRT) instead of a separate host np.sqrt — same value: the sum is
+    rounded to the element type first, then sqrt'ed in the element type,
+    exactly as np.sqrt(dot(x, x)) does (ops.py:53-55);
+  * `axpy_dot` fuses y = y + alpha*x with dot(y, z) into ONE pass (the
+    building block of BASELINE config 5); the reference composes two
+    traversals.
+
+Reductions accept `lazy=True` to return a DeviceScalar without a host
+synchronisation (for solver loops).
+"""
+
+from . import _native
+from .engine import execute_assign, execute_assign_reduce, execute_reduce
+from .expressions import AssignNode, AssignReduceNode, MulNode, ScaleNode, SumNode, as_node
+
+__all__ = ["dot", "scal", "axpy", "scaled_copy", "sum", "norm2", "axpy_dot"]
+
+
+def dot(x, y, **options):
+    """Sum of elementwise products of two equal-length vectors."""
+    return execute_reduce(SumNode(MulNode(as_node(x), as_node(y))), **options)
+
+
+def scal(alpha, x, **options) -> None:
+    """In-place x = alpha * x (exact aliasing of source and destination)."""
+    execute_assign(AssignNode(as_node(x), ScaleNode(alpha, as_node(x))), **options)
+
+
+def axpy(alpha, x, y, **options) -> None:
+    """In-place y = y + alpha * x."""
+    execute_assign(AssignNode(as_node(y), as_node(y) + ScaleNode(alpha, as_node(x))), **options)
+
+
+def scaled_copy(alpha, x, out, **options) -> None:
+    """out = alpha * x in one traversal (n reads + n writes); out must not
+    overlap x."""
+    execute_assign(AssignNode(as_node(out), ScaleNode(alpha, as_node(x))), **options)
+
+
+def sum(x, **options):  # noqa: A001 - reference name
+    """Sum of all elements."""
+    return execute_reduce(SumNode(as_node(x)), **options)
+
+
+def norm2(x, **options):
+    """Euclidean norm sqrt(dot(x, x)), no overflow scaling (as the reference)."""
+    return execute_reduce(
+        SumNode(MulNode(as_node(x), as_node(x))), _flags=_native.SALT_SQRT, **options
+    )
+
+
+def axpy_dot(alpha, x, y, z, **options):
+    """y = y + alpha*x, then return dot(y_new, z) — one fused pass reading
+    x, y, z once and writing y once."""
+    yl = as_node(y)
+    root = AssignReduceNode(
+        AssignNode(yl, yl + ScaleNode(alpha, as_node(x))),
+        SumNode(MulNode(as_node(y), as_node(z))),
+    )
+    return execute_assign_reduce(root, **options)

@@ -1,0 +1,162 @@
+"""Block-sharded vectors across GPUs (one process per GPU, torch.distributed).
+
+The reference is single-process; the paper only sketches data-parallel
+evaluation.  Here a global vector of length n is split
+into contiguous blocks, one per rank:
+
+    rank r owns [r*B, min(n, (r+1)*B)),  B = ceil(n / world) rounded up to a
+    multiple of 64 elements, so every block base stays 256-byte aligned.
+
+Elementwise trees over ShardedVectors run on each rank's block with no
+communication.  Reductions compute one double-double partial per rank
+(SALT_PARTIAL), all-gather the partials (a 16-byte NCCL all-gather over
+NVLink/NVSwitch, or gloo on CPU), and every rank combines them in rank order
+(salt_reduce_finish) — deterministic and identical on all ranks.
+"""
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from .lanes import as_dtype
+from .vectors import DenseVector
+
+__all__ = ["shard_bounds", "ShardedVector", "SHARD_ALIGN"]
+
+SHARD_ALIGN = 64
+
+
+def shard_bounds(n: int, world: int, rank: int, align: int = SHARD_ALIGN):
+    """[lo, hi) of `rank`'s block of a length-n vector split over `world`."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError(f"bad rank {rank} for world size {world}")
+    if n < 0:
+        raise ValueError(f"length must be >= 0, got {n}")
+    per = -(-n // world) if n else 0
+    per = -(-per // align) * align
+    lo = min(n, rank * per)
+    hi = min(n, lo + per)
+    return lo, hi
+
+
+def _world(group):
+    if dist.is_available() and dist.is_initialized():
+        return dist.get_world_size(group), dist.get_rank(group)
+    return 1, 0
+
+
+class ShardedVector:
+    """A global vector of `global_len` elements; this rank holds `local`."""
+
+    __slots__ = ("local", "global_len", "lo", "hi", "group", "world", "rank")
+
+    __array_ufunc__ = None
+
+    def __init__(self, local: DenseVector, global_len: int, group=None):
+        self.group = group
+        self.world, self.rank = _world(group)
+        self.global_len = int(global_len)
+        self.lo, self.hi = shard_bounds(self.global_len, self.world, self.rank)
+        if len(local) != self.hi - self.lo:
+            raise ValueError(
+                f"rank {self.rank} block must hold {self.hi - self.lo} elements, got {len(local)}"
+            )
+        self.local = local
+
+    @classmethod
+    def zeros(cls, n: int, dtype="f32", group=None, device=None):
+        world, rank = _world(group)
+        lo, hi = shard_bounds(n, world, rank)
+        return cls(DenseVector.zeros(hi - lo, dtype, device=device), n, group)
+
+    @classmethod
+    def from_global(cls, values, dtype="f32", group=None, device=None):
+        """Take this rank's block of a host array holding the global vector."""
+        arr = np.asarray(values).reshape(-1)
+        world, rank = _world(group)
+        lo, hi = shard_bounds(arr.shape[0], world, rank)
+        return cls(DenseVector.from_values(arr[lo:hi], dtype, device=device), arr.shape[0], group)
+
+    @classmethod
+    def from_blocks(cls, n: int, dtype, make_block, group=None, device=None):
+        """Build from `make_block(lo, hi) -> array` for this rank's block only
+        (each rank generates just its own data)."""
+        world, rank = _world(group)
+        lo, hi = shard_bounds(n, world, rank)
+        return cls(DenseVector.from_values(make_block(lo, hi), dtype, device=device), n, group)
+
+    @property
+    def dtype(self):
+        return self.local.dtype
+
+    def __len__(self) -> int:
+        return self.global_len
+
+    def same_partition(self, other) -> bool:
+        return (
+            isinstance(other, ShardedVector)
+            and other.global_len == self.global_len
+            and other.world == self.world
+            and other.group is self.group
+        )
+
+    def gather_partials(self, part: torch.Tensor) -> torch.Tensor:
+        """All-gather one {hi, lo} float64 pair per rank, in rank order."""
+        if self.world == 1:
+            return part.reshape(-1)
+        out = [torch.empty_like(part) for _ in range(self.world)]
+        dist.all_gather(out, part, group=self.group)
+        return torch.cat(out)
+
+    # ---- inspection (collective: every rank must call) ----
+    def to_array(self) -> np.ndarray:
+        if self.world == 1:
+            return self.local.to_array()
+        per = shard_bounds(self.global_len, self.world, 0)[1]
+        dt = as_dtype(self.dtype)
+        buf = torch.zeros(per, dtype=self.local.tensor.dtype, device=self.local.device)
+        buf[: len(self.local)] = self.local.tensor
+        parts = [torch.empty_like(buf) for _ in range(self.world)]
+        dist.all_gather(parts, buf, group=self.group)
+        full = torch.cat(parts)[: self.global_len]
+        return full.cpu().numpy().astype(dt, copy=False)
+
+    def read_block(self, lo: int, hi: int):
+        return self.to_array()[lo:hi]
+
+    def assign(self, expression, **options) -> None:
+        from .engine import execute_assign
+        from .expressions import AssignNode, Leaf, as_node
+
+        execute_assign(AssignNode(Leaf(self), as_node(expression)), **options)
+
+    def __add__(self, other):
+        from .expressions import add_nodes
+
+        return add_nodes(self, other)
+
+    def __sub__(self, other):
+        from .expressions import sub_nodes
+
+        return sub_nodes(self, other)
+
+    def __mul__(self, other):
+        from .expressions import mul_nodes
+
+        return mul_nodes(self, other)
+
+    def __rmul__(self, other):
+        from .expressions import scale_node
+
+        return scale_node(other, self)
+
+    def __neg__(self):
+        from .expressions import negate_node
+
+        return negate_node(self)
+
+    def __repr__(self):
+        return (
+            f"ShardedVector(len={self.global_len}, rank={self.rank}/{self.world}, "
+            f"block=[{self.lo},{self.hi}), dtype={self.dtype})"
+        )

@@ -1,0 +1,244 @@
+"""DenseVector: the leaves and destinations of expressions, resident in HBM.
+
+Reference: pkg/src/lanevec/vectors.py:1-144 (a 64-byte aligned NumPy buffer).
+Here the storage is a 1-D torch tensor — torch is only the allocator — that
+lives either
+
+  * on a CUDA device (the normal case: trees over device vectors run as one
+    fused sm_100a kernel on that device), or
+  * in pinned host memory (`device="cpu"`): trees over host vectors are
+    streamed through the GPU in chunks (H2D -> fused kernel -> D2H, three
+    overlapped streams, `salt_assign_host`).  This is the end-to-end path
+    and also lets vectors larger than HBM be evaluated.
+
+Storage is aligned to DEVICE_ALIGNMENT (256 B), which satisfies the
+reference's CONTAINER_ALIGNMENT (64 B) and the kernels' 256-bit accesses.
+Element access (get/set/read_block/...) keeps the reference's duck-typed
+vector protocol (expressions.py:68-69) and copies across PCIe when the
+storage is on the device; it is for inspection, not for the hot path.
+"""
+
+import numpy as np
+import torch
+
+from .lanes import DEVICE_ALIGNMENT, as_dtype
+
+__all__ = ["DenseVector", "DeviceScalar", "default_device", "torch_dtype"]
+
+_TORCH_DTYPES = {np.dtype(np.float32): torch.float32, np.dtype(np.float64): torch.float64}
+_NP_DTYPES = {torch.float32: np.dtype(np.float32), torch.float64: np.dtype(np.float64)}
+
+
+def torch_dtype(dt: np.dtype) -> torch.dtype:
+    return _TORCH_DTYPES[as_dtype(dt)]
+
+
+def default_device() -> torch.device:
+    """The current CUDA device, or the host when this process has no GPU
+    (vectors can then be built and inspected, but evaluating a tree raises:
+    there is no CPU evaluation path)."""
+    if torch.cuda.is_available():
+        return torch.device("cuda", torch.cuda.current_device())
+    return torch.device("cpu")
+
+
+def _as_device(device) -> torch.device:
+    if device is None:
+        return default_device()
+    if isinstance(device, int):
+        return torch.device("cuda", device)
+    dev = torch.device(device)
+    if dev.type == "cuda" and dev.index is None:
+        dev = torch.device("cuda", torch.cuda.current_device())
+    if dev.type not in ("cuda", "cpu"):
+        raise ValueError(f"unsupported device {device!r}")
+    return dev
+
+
+def _aligned_empty(n: int, dt: np.dtype, device: torch.device) -> torch.Tensor:
+    """Uninitialised length-n storage whose base address is 256-B aligned."""
+    tdt = _TORCH_DTYPES[dt]
+    pad = DEVICE_ALIGNMENT // dt.itemsize
+    if device.type == "cpu":
+        raw = torch.empty(n + pad, dtype=tdt, pin_memory=torch.cuda.is_available())
+    else:
+        raw = torch.empty(n + pad, dtype=tdt, device=device)
+    start = ((-raw.data_ptr()) % DEVICE_ALIGNMENT) // dt.itemsize
+    return raw[start : start + n]
+
+
+class DenseVector:
+    """Fixed-length contiguous f32/f64 vector (reference vectors.py:18-31)."""
+
+    __slots__ = ("_data", "_dtype")
+
+    def __init__(self, data: torch.Tensor, dtype):
+        self._data = data
+        self._dtype = as_dtype(dtype)
+
+    # ------------------------------------------------------------ creation
+    @classmethod
+    def zeros(cls, n: int, dtype="f32", device=None) -> "DenseVector":
+        if n < 0:
+            raise ValueError(f"length must be >= 0, got {n}")
+        dt = as_dtype(dtype)
+        buf = _aligned_empty(int(n), dt, _as_device(device))
+        buf.zero_()
+        return cls(buf, dt)
+
+    @classmethod
+    def empty(cls, n: int, dtype="f32", device=None) -> "DenseVector":
+        """Uninitialised vector (a destination that will be fully assigned)."""
+        if n < 0:
+            raise ValueError(f"length must be >= 0, got {n}")
+        dt = as_dtype(dtype)
+        return cls(_aligned_empty(int(n), dt, _as_device(device)), dt)
+
+    @classmethod
+    def from_values(cls, values, dtype="f32", device=None) -> "DenseVector":
+        dt = as_dtype(dtype)
+        src = np.ascontiguousarray(np.asarray(values, dtype=dt).reshape(-1))
+        buf = _aligned_empty(src.shape[0], dt, _as_device(device))
+        if src.shape[0]:
+            buf.copy_(torch.from_numpy(src))
+        return cls(buf, dt)
+
+    @classmethod
+    def from_tensor(cls, tensor: torch.Tensor) -> "DenseVector":
+        """Wrap an existing 1-D contiguous f32/f64 tensor without copying."""
+        if tensor.dim() != 1 or not tensor.is_contiguous():
+            raise ValueError("from_tensor needs a 1-D contiguous tensor")
+        if tensor.dtype not in _NP_DTYPES:
+            raise TypeError(f"unsupported element type {tensor.dtype}; use float32 or float64")
+        return cls(tensor, _NP_DTYPES[tensor.dtype])
+
+    # ------------------------------------------------------------ properties
+    @property
+    def dtype(self) -> np.dtype:
+        return self._dtype
+
+    @property
+    def device(self) -> torch.device:
+        return self._data.device
+
+    @property
+    def tensor(self) -> torch.Tensor:
+        """The backing storage (borrowed; do not resize)."""
+        return self._data
+
+    @property
+    def address(self) -> int:
+        """Base address of the storage (device or pinned host)."""
+        return self._data.data_ptr()
+
+    def __len__(self) -> int:
+        return int(self._data.shape[0])
+
+    # ------------------------------------------------------------ elements
+    def _check_index(self, i: int) -> None:
+        if not 0 <= i < self._data.shape[0]:
+            raise IndexError(f"index {i} out of range for length {len(self)}")
+
+    def get(self, i: int):
+        self._check_index(i)
+        return self._dtype.type(self._data[i].item())
+
+    def set(self, i: int, value) -> None:
+        self._check_index(i)
+        self._data[i] = float(self._dtype.type(value))
+
+    def __getitem__(self, i: int):
+        return self.get(i)
+
+    def __setitem__(self, i: int, value) -> None:
+        self.set(i, value)
+
+    def to_array(self) -> np.ndarray:
+        """Copy of the contents as a host NumPy array."""
+        return self._data.detach().to("cpu").numpy().copy()
+
+    def to_values(self) -> list:
+        """Elements as a list of element-typed NumPy scalars."""
+        return list(self.to_array())
+
+    # Duck-typed vector protocol (reference vectors.py:88-100).  Block reads
+    # return host copies.
+    def read_block(self, lo: int, hi: int) -> np.ndarray:
+        return self._data[lo:hi].detach().to("cpu").numpy()
+
+    def write_block(self, lo: int, hi: int, values) -> None:
+        src = torch.from_numpy(np.ascontiguousarray(np.asarray(values, dtype=self._dtype)))
+        self._data[lo:hi].copy_(src)
+
+    def read_element(self, i: int):
+        return self._dtype.type(self._data[i].item())
+
+    def write_element(self, i: int, value) -> None:
+        self._data[i] = float(self._dtype.type(value))
+
+    # ------------------------------------------------------------ evaluation
+    def assign(self, expression, **plan_kwargs) -> None:
+        """Evaluate a lazy expression into this vector in one fused pass."""
+        from .engine import execute_assign
+        from .expressions import AssignNode, Leaf, as_node
+
+        execute_assign(AssignNode(Leaf(self), as_node(expression)), **plan_kwargs)
+
+    # Arithmetic builds lazy nodes (reference vectors.py:109-138).
+    def __add__(self, other):
+        from .expressions import add_nodes
+
+        return add_nodes(self, other)
+
+    def __sub__(self, other):
+        from .expressions import sub_nodes
+
+        return sub_nodes(self, other)
+
+    def __mul__(self, other):
+        from .expressions import mul_nodes
+
+        return mul_nodes(self, other)
+
+    def __rmul__(self, other):
+        from .expressions import scale_node
+
+        return scale_node(other, self)
+
+    def __neg__(self):
+        from .expressions import negate_node
+
+        return negate_node(self)
+
+    __array_ufunc__ = None
+
+    def __repr__(self):
+        n = len(self)
+        head = self._data[:6].detach().to("cpu").tolist() if n else []
+        shown = ", ".join(repr(float(v)) for v in head)
+        tail = ", ..." if n > 6 else ""
+        return f"DenseVector([{shown}{tail}], len={n}, dtype={self._dtype}, device={self.device})"
+
+
+class DeviceScalar:
+    """A reduction result left in device memory (no host synchronisation).
+
+    Returned by reductions called with `lazy=True`; `.item()` (or float())
+    copies it to the host and returns the element-typed NumPy scalar the
+    reference returns (test_ops.py:29-31).
+    """
+
+    __slots__ = ("tensor", "dtype")
+
+    def __init__(self, tensor: torch.Tensor, dtype):
+        self.tensor = tensor
+        self.dtype = as_dtype(dtype)
+
+    def item(self):
+        return self.dtype.type(self.tensor.item())
+
+    def __float__(self):
+        return float(self.item())
+
+    def __repr__(self):
+        return f"DeviceScalar({self.item()!r})"
