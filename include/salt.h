@@ -129,6 +129,11 @@ size_t salt_reduce_workspace_bytes(void);
  * JIT.  kind: 0 assign, 1 reduce, 2 assign+reduce (reduce_sig used). */
 int salt_signature_kind(int dtype, const char* sig, const char* reduce_sig, int kind);
 
+/* Compile (without launching) the kernels for a signature: the AOT table
+ * entry if there is one, else NVRTC for both the vector and the scalar-lane
+ * variant, and cache them.  Needs no GPU.  Same `kind` as above. */
+int salt_prepare(int dtype, const char* sig, const char* reduce_sig, int kind);
+
 /* Force (1) or forbid (0) the JIT for signatures that also have an AOT
  * kernel; default 0.  Used by tests to prove AOT == JIT bit for bit. */
 void salt_set_force_jit(int on);

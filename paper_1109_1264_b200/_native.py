@@ -40,6 +40,7 @@ HEADER_SYMBOLS = (
     "salt_reduce_host",
     "salt_reduce_workspace_bytes",
     "salt_signature_kind",
+    "salt_prepare",
     "salt_set_force_jit",
     "salt_launch_count",
     "salt_last_error",
@@ -75,6 +76,7 @@ _SIGNATURES = {
     ),
     "salt_reduce_workspace_bytes": (_c_size, []),
     "salt_signature_kind": (_c_int, [_c_int, _c_str, _c_str, _c_int]),
+    "salt_prepare": (_c_int, [_c_int, _c_str, _c_str, _c_int]),
     "salt_set_force_jit": (None, [_c_int]),
     "salt_launch_count": (ctypes.c_uint64, []),
     "salt_last_error": (_c_str, []),

@@ -177,14 +177,18 @@ struct Nvrtc {
   nvrtcResult_t (*GetCUBIN)(void*, char*) = nullptr;
   nvrtcResult_t (*GetLoweredName)(void*, const char*, const char**) = nullptr;
   nvrtcResult_t (*DestroyProgram)(void**) = nullptr;
+  nvrtcResult_t (*Version)(int*, int*) = nullptr;
+  bool has_256bit = false;  // NVRTC >= 12.9 accepts .v8.f32 / .v4.f64
 };
 
 Nvrtc& nvrtc() {
   static Nvrtc n;
   static std::once_flag once;
   std::call_once(once, [] {
+    // Prefer the toolkit's NVRTC (12.9, PTX ISA 8.8: 256-bit ld/st) by full
+    // path: a bare soname would return torch's already-loaded 12.8 copy.
     const char* env = getenv("SALT_NVRTC_LIB");
-    const char* cands[] = {env, "libnvrtc.so.12", "/usr/local/cuda/lib64/libnvrtc.so.12",
+    const char* cands[] = {env, "/usr/local/cuda/lib64/libnvrtc.so.12", "libnvrtc.so.12",
                            "libnvrtc.so"};
     for (const char* c : cands) {
       if (!c) continue;
@@ -207,7 +211,11 @@ Nvrtc& nvrtc() {
     SYM(GetCUBIN, "nvrtcGetCUBIN");
     SYM(GetLoweredName, "nvrtcGetLoweredName");
     SYM(DestroyProgram, "nvrtcDestroyProgram");
+    SYM(Version, "nvrtcVersion");
 #undef SYM
+    int major = 0, minor = 0;
+    n.Version(&major, &minor);
+    n.has_256bit = major > 12 || (major == 12 && minor >= 9);
     n.ok = true;
   });
   return n;
@@ -319,8 +327,8 @@ Kernel* jit_compile(int dtype, int mode, int vec, const std::string& ta, const s
   }
   nv.AddNameExpression(prog, expr.c_str());
   const char* opts[] = {"--gpu-architecture=sm_100a", "-fmad=false", "--std=c++17",
-                        "-lineinfo", "-default-device"};
-  int rc = nv.CompileProgram(prog, 5, opts);
+                        "-lineinfo", "-default-device", "-DSALT_NO_256BIT"};
+  int rc = nv.CompileProgram(prog, nv.has_256bit ? 5 : 6, opts);
   if (rc != 0) {
     size_t ls = 0;
     nv.GetProgramLogSize(prog, &ls);
@@ -686,6 +694,19 @@ int salt_signature_kind(int dtype, const char* sig, const char* reduce_sig, int 
   const int V = dtype == SALT_F32 ? 8 : 4;
   std::lock_guard<std::mutex> lk(g_table_mu);
   return table().count(key_of(dtype, kind, V, p.sa.type, p.sr.type)) ? 1 : 2;
+}
+
+int salt_prepare(int dtype, const char* sig, const char* reduce_sig, int kind) {
+  if (kind < 0 || kind > 2) return fail(SALT_EINVAL, "kind must be 0, 1 or 2");
+  Plan p;
+  const char* a = kind == 1 ? nullptr : sig;
+  const char* r = kind == 0 ? nullptr : (kind == 1 ? sig : reduce_sig);
+  int rc = make_plan(dtype, a, r, kind, salt::MAX_LEAVES, salt::MAX_SCALARS, p);
+  if (rc) return rc;
+  const int V = dtype == SALT_F32 ? 8 : 4;
+  for (int vec : {V, 1})
+    if (!get_kernel(dtype, kind, vec, p.sa.type, p.sr.type)) return SALT_EJIT;
+  return 0;
 }
 
 int salt_assign(int dtype, const char* sig, void* dst, const void* const* leaves, int nleaves,

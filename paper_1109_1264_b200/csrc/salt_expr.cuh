@@ -111,6 +111,7 @@ template <class T> struct Args {
 // 32-byte (256-bit) vector access: LDG.E.ENL2.256 / STG.E.ENL2.256 on sm_100a.
 // Plain (coherent) loads: a leaf may alias the destination (axpy, scal).
 template <class T, int V> struct VecIO;
+#ifndef SALT_NO_256BIT
 template <> struct VecIO<double, 4> {
   static __device__ __forceinline__ void load(double (&r)[4], const double* p) {
     asm volatile("ld.global.L1::no_allocate.v4.f64 {%0,%1,%2,%3}, [%4];"
@@ -133,6 +134,33 @@ template <> struct VecIO<float, 8> {
                     "f"(r[4]), "f"(r[5]), "f"(r[6]), "f"(r[7]) : "memory");
   }
 };
+#else
+// NVRTC < 12.9 (PTX ISA < 8.8) has no 256-bit ld/st: two 128-bit halves.
+template <> struct VecIO<double, 4> {
+  static __device__ __forceinline__ void load(double (&r)[4], const double* p) {
+    asm volatile("ld.global.L1::no_allocate.v2.f64 {%0,%1}, [%2];" : "=d"(r[0]), "=d"(r[1]) : "l"(p));
+    asm volatile("ld.global.L1::no_allocate.v2.f64 {%0,%1}, [%2];" : "=d"(r[2]), "=d"(r[3]) : "l"(p + 2));
+  }
+  static __device__ __forceinline__ void store(double* p, const double (&r)[4]) {
+    asm volatile("st.global.L1::no_allocate.v2.f64 [%0], {%1,%2};" :: "l"(p), "d"(r[0]), "d"(r[1]) : "memory");
+    asm volatile("st.global.L1::no_allocate.v2.f64 [%0], {%1,%2};" :: "l"(p + 2), "d"(r[2]), "d"(r[3]) : "memory");
+  }
+};
+template <> struct VecIO<float, 8> {
+  static __device__ __forceinline__ void load(float (&r)[8], const float* p) {
+    asm volatile("ld.global.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]) : "l"(p));
+    asm volatile("ld.global.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(r[4]), "=f"(r[5]), "=f"(r[6]), "=f"(r[7]) : "l"(p + 4));
+  }
+  static __device__ __forceinline__ void store(float* p, const float (&r)[8]) {
+    asm volatile("st.global.L1::no_allocate.v4.f32 [%0], {%1,%2,%3,%4};"
+                 :: "l"(p), "f"(r[0]), "f"(r[1]), "f"(r[2]), "f"(r[3]) : "memory");
+    asm volatile("st.global.L1::no_allocate.v4.f32 [%0], {%1,%2,%3,%4};"
+                 :: "l"(p + 4), "f"(r[4]), "f"(r[5]), "f"(r[6]), "f"(r[7]) : "memory");
+  }
+};
+#endif
 template <class T> struct VecIO<T, 1> {
   static __device__ __forceinline__ void load(T (&r)[1], const T* p) { r[0] = *p; }
   static __device__ __forceinline__ void store(T* p, const T (&r)[1]) { *p = r[0]; }

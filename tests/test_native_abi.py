@@ -1,0 +1,104 @@
+"""The C-ABI library (CPU): it loads without a GPU, exports every function
+include/salt.h declares, and validates signatures / arguments before any
+CUDA call (so these run with no device)."""
+
+import ctypes
+import re
+import subprocess
+
+import pytest
+
+from conftest import ROOT
+from paper_1109_1264_b200 import _native
+
+HEADER = ROOT / "include" / "salt.h"
+
+
+def header_functions():
+    text = HEADER.read_text()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(salt_[a-z_0-9]+)\s*\(", text)))
+
+
+def test_header_and_binding_agree():
+    assert header_functions() == sorted(_native.HEADER_SYMBOLS)
+
+
+def test_library_exports_every_header_symbol():
+    lib = _native.lib()
+    for name in header_functions():
+        assert hasattr(lib, name), name
+    out = subprocess.run(["nm", "-D", "--defined-only", str(_native.LIB_PATH)],
+                         capture_output=True, text=True, check=True).stdout
+    exported = set(re.findall(r"\bT (salt_\w+)", out))
+    assert set(header_functions()) <= exported
+
+
+def test_abi_constants():
+    lib = _native.lib()
+    assert lib.salt_abi_version() == 1
+    assert lib.salt_reduce_workspace_bytes() >= 256 + 16 * 1024
+
+
+@pytest.mark.parametrize("sig,kind,expect", [
+    ("L0", 0, 1),
+    ("S0 L0 *", 0, 1),
+    ("L0 S0 L1 * +", 0, 1),
+    ("L0 L1 L2 - +", 0, 1),
+    ("S0 L0 * S1 L1 L2 - * +", 0, 1),
+    ("S0 L0 L1 + * S1 L2 L3 - * - S2 L0 * +", 0, 1),
+    ("L0 L1 *", 1, 1),
+    ("L0 L0 *", 1, 1),
+    ("L0", 1, 1),
+    ("L0 L1 * L2 *", 0, 2),          # not in the table: NVRTC instantiates it
+    ("L0 L1 L2 L3 L4 L5 L6 L7 + + + + + + +", 0, 2),
+    ("L0 +", 0, 0),                  # malformed
+    ("L0 L1", 0, 0),                 # two values left
+    ("L8", 0, 0),                    # leaf index out of range
+    ("S9 L0 *", 0, 0),
+    ("L0 / L1", 0, 0),
+    ("D L0 *", 0, 0),                # D only inside a fused reduce tree
+    ("", 0, 0),
+])
+def test_signature_validation(sig, kind, expect):
+    assert _native.lib().salt_signature_kind(1, sig.encode(), None, kind) == expect
+
+
+def test_fused_signature_kind():
+    lib = _native.lib()
+    assert lib.salt_signature_kind(1, b"L0 S0 L1 * +", b"D L2 *", 2) == 1
+    assert lib.salt_signature_kind(0, b"L0 S0 L1 * +", b"D D *", 2) == 1
+    assert lib.salt_signature_kind(0, b"L0 L1 +", b"D L0 *", 2) == 2
+    assert lib.salt_signature_kind(0, b"L0 L1 +", b"D +", 2) == 0
+
+
+def test_bad_arguments_fail_before_cuda():
+    lib = _native.lib()
+    leaves, keep = _native.ptr_array([0x1000, 0x2000])
+    sc, keep2 = _native.double_array([1.0])
+    rc = lib.salt_assign(1, b"L0 L1 L2 + +", ctypes.c_void_p(0x3000), leaves, 2, sc, 1, 10, None)
+    assert rc == -1 and b"3 leaves" in lib.salt_last_error()
+    rc = lib.salt_assign(7, b"L0", ctypes.c_void_p(0x3000), leaves, 1, sc, 0, 10, None)
+    assert rc == -1 and b"dtype" in lib.salt_last_error()
+    rc = lib.salt_assign(1, b"L0 L1 ?", ctypes.c_void_p(0x3000), leaves, 2, sc, 0, 10, None)
+    assert rc == -1 and b"bad token" in lib.salt_last_error()
+    rc = lib.salt_reduce(1, b"L0 L1 *", leaves, 2, sc, 0, 10, 0, None, 0, ctypes.c_void_p(8), None, None)
+    assert rc == -4  # workspace too small
+    with pytest.raises(RuntimeError, match="libsalt error"):
+        _native.check(lib.salt_assign(1, b"L0 +", None, leaves, 1, sc, 0, 1, None))
+    # zero-length assignment is a no-op that never touches CUDA
+    assert lib.salt_assign(1, b"L0", ctypes.c_void_p(0x3000), leaves, 1, sc, 0, 0, None) == 0
+
+
+def test_nvrtc_instantiates_arbitrary_trees_without_a_gpu():
+    """The JIT compiles the same fused-kernel template for trees outside the
+    table (vector + scalar-lane variants), even after torch is imported
+    (torch bundles an older NVRTC; libsalt loads the toolkit's by path)."""
+    import torch  # noqa: F401
+
+    lib = _native.lib()
+    for dt in (0, 1):
+        assert lib.salt_prepare(dt, b"L0 L1 * L2 * S0 L3 * -", None, 0) == 0, lib.salt_last_error()
+        assert lib.salt_prepare(dt, b"L0 L1 - L2 L3 + *", None, 1) == 0, lib.salt_last_error()
+        assert lib.salt_prepare(dt, b"L0 L1 +", b"D D *", 2) == 0, lib.salt_last_error()
+    assert lib.salt_prepare(1, b"L0 +", None, 0) == -1
