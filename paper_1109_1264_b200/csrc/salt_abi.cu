@@ -447,7 +447,7 @@ void geometry(void* dst, const void* const* leaves, int nl, i64 n, int& vec, i64
     if (m % sizeof(T)) same = false;
   };
   if (dst) check(dst);
-  for (int l = 0; l < nl; ++l) check(leaves[l]);
+  for (int l = 0; leaves && l < nl; ++l) check(leaves[l]);
   if (mis == (uintptr_t)-1) mis = 0;
   if (same) {
     i64 h = (i64)(((32 - mis) % 32) / sizeof(T));
@@ -500,9 +500,12 @@ int run_fused(const Plan& p, void* dst, const void* const* leaves, int nleaves,
   if (n < 0) return fail(SALT_EINVAL, "negative length");
   const bool reduce = p.mode != salt::MODE_ASSIGN;
   if (!reduce && n == 0) return 0;  // zero length assign is a no-op (test_engine.py:147-153)
-  if (p.mode != salt::MODE_REDUCE && !dst) return fail(SALT_EINVAL, "NULL destination");
-  for (int l = 0; l < p.nl; ++l)
-    if (!leaves || !leaves[l]) return fail(SALT_EINVAL, "NULL leaf pointer");
+  // Empty vectors may legitimately have NULL storage (torch gives numel-0
+  // tensors a NULL data pointer); nothing is dereferenced when n == 0.
+  if (n > 0 && p.mode != salt::MODE_REDUCE && !dst) return fail(SALT_EINVAL, "NULL destination");
+  if (n > 0 && p.nl > 0 && !leaves) return fail(SALT_EINVAL, "NULL leaf array");
+  for (int l = 0; n > 0 && l < p.nl; ++l)
+    if (!leaves[l]) return fail(SALT_EINVAL, "NULL leaf pointer");
   if (reduce) {
     if (!out_dev) return fail(SALT_EINVAL, "NULL reduction output");
     if (!ws || ws_bytes < salt_reduce_workspace_bytes())
@@ -511,7 +514,7 @@ int run_fused(const Plan& p, void* dst, const void* const* leaves, int nleaves,
   salt::Args<T> a;
   memset(&a, 0, sizeof(a));
   a.dst = (T*)dst;
-  for (int l = 0; l < p.nl; ++l) a.leaf[l] = (const T*)leaves[l];
+  for (int l = 0; l < p.nl; ++l) a.leaf[l] = leaves ? (const T*)leaves[l] : nullptr;
   for (int s = 0; s < p.ns; ++s) a.sc[s] = (T)scalars[s];
   a.n = n;
   a.flags = flags;
