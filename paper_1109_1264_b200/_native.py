@@ -7,6 +7,7 @@ reference surfaces failures as exceptions (error
 conventions).
 """
 
+import array
 import ctypes
 import os
 import threading
@@ -52,8 +53,10 @@ _c_i64 = ctypes.c_int64
 _c_size = ctypes.c_size_t
 _c_vp = ctypes.c_void_p
 _c_str = ctypes.c_char_p
-_c_vpp = ctypes.POINTER(ctypes.c_void_p)
-_c_dp = ctypes.POINTER(ctypes.c_double)
+# Pointer arrays / scalar arrays are passed as raw addresses (array.array
+# buffers): building ctypes arrays per call costs several microseconds.
+_c_vpp = ctypes.c_void_p
+_c_dp = ctypes.c_void_p
 
 _SIGNATURES = {
     "salt_assign": (_c_int, [_c_int, _c_str, _c_vp, _c_vpp, _c_int, _c_dp, _c_int, _c_i64, _c_vp]),
@@ -117,11 +120,17 @@ def check(rc: int) -> None:
         raise RuntimeError(f"libsalt error {rc}: {msg.decode() if msg else 'unknown'}")
 
 
+_EMPTY_Q = array.array("Q", [0])
+_EMPTY_D = array.array("d", [0.0])
+
+
 def ptr_array(ptrs):
-    arr = (ctypes.c_void_p * max(1, len(ptrs)))(*[ctypes.c_void_p(p) for p in ptrs])
-    return ctypes.cast(arr, _c_vpp), arr
+    """(address, keep-alive) of a uint64 array holding `ptrs`."""
+    arr = array.array("Q", ptrs) if ptrs else _EMPTY_Q
+    return arr.buffer_info()[0], arr
 
 
 def double_array(values):
-    arr = (ctypes.c_double * max(1, len(values)))(*values)
-    return ctypes.cast(arr, _c_dp), arr
+    """(address, keep-alive) of a float64 array holding `values`."""
+    arr = array.array("d", values) if values else _EMPTY_D
+    return arr.buffer_info()[0], arr

@@ -464,37 +464,58 @@ void geometry(void* dst, const void* const* leaves, int nl, i64 n, int& vec, i64
 
 struct Plan {
   Sig sa, sr;
-  int mode;
-  int nl, ns;
+  int mode = 0;
+  int nl = 0, ns = 0;
+  Kernel* cached[2][2] = {};  // [force_jit][vec == 1]: table / JIT lookups done once
 };
 
+// Parsed signatures are cached per thread (keyed by the raw strings), so a
+// repeated call costs one hash lookup instead of a parse + type rebuild.
 int make_plan(int dtype, const char* asig, const char* rsig, int mode, int nleaves, int nscalars,
-              Plan& p) {
+              Plan*& out) {
   if (dtype != SALT_F32 && dtype != SALT_F64) return fail(SALT_EINVAL, "dtype must be SALT_F32 or SALT_F64");
-  p.mode = mode;
-  std::string err;
-  p.sa.type = p.sr.type = "salt::None";
-  if (mode != salt::MODE_REDUCE) {
-    err = parse_sig(asig, false, p.sa);
-    if (!err.empty()) return fail(SALT_EINVAL, err);
+  thread_local std::unordered_map<std::string, std::unique_ptr<Plan>> cache;
+  std::string key;
+  key.push_back(char('0' + dtype));
+  key.push_back(char('0' + mode));
+  if (mode != salt::MODE_REDUCE && asig) key += asig;
+  key.push_back('\x1f');
+  if (mode != salt::MODE_ASSIGN && rsig) key += rsig;
+  Plan* p;
+  auto it = cache.find(key);
+  if (it != cache.end()) {
+    p = it->second.get();
+  } else {
+    auto np = std::make_unique<Plan>();
+    np->mode = mode;
+    std::string err;
+    np->sa.type = np->sr.type = "salt::None";
+    if (mode != salt::MODE_REDUCE) {
+      err = parse_sig(asig, false, np->sa);
+      if (!err.empty()) return fail(SALT_EINVAL, err);
+    }
+    if (mode != salt::MODE_ASSIGN) {
+      err = parse_sig(rsig, mode == salt::MODE_ASSIGN_REDUCE, np->sr);
+      if (!err.empty()) return fail(SALT_EINVAL, err);
+    }
+    np->nl = std::max(np->sa.nl, np->sr.nl);
+    np->ns = std::max(np->sa.ns, np->sr.ns);
+    if (cache.size() > 4096) cache.clear();
+    p = np.get();
+    cache.emplace(std::move(key), std::move(np));
   }
-  if (mode != salt::MODE_ASSIGN) {
-    err = parse_sig(rsig, mode == salt::MODE_ASSIGN_REDUCE, p.sr);
-    if (!err.empty()) return fail(SALT_EINVAL, err);
-  }
-  p.nl = std::max(p.sa.nl, p.sr.nl);
-  p.ns = std::max(p.sa.ns, p.sr.ns);
-  if (nleaves < p.nl || nleaves > salt::MAX_LEAVES)
-    return fail(SALT_EINVAL, "signature references " + std::to_string(p.nl) + " leaves but " +
+  if (nleaves < p->nl || nleaves > salt::MAX_LEAVES)
+    return fail(SALT_EINVAL, "signature references " + std::to_string(p->nl) + " leaves but " +
                                  std::to_string(nleaves) + " were passed");
-  if (nscalars < p.ns || nscalars > salt::MAX_SCALARS)
-    return fail(SALT_EINVAL, "signature references " + std::to_string(p.ns) + " scalars but " +
+  if (nscalars < p->ns || nscalars > salt::MAX_SCALARS)
+    return fail(SALT_EINVAL, "signature references " + std::to_string(p->ns) + " scalars but " +
                                  std::to_string(nscalars) + " were passed");
+  out = p;
   return 0;
 }
 
 template <class T>
-int run_fused(const Plan& p, void* dst, const void* const* leaves, int nleaves,
+int run_fused(Plan& p, void* dst, const void* const* leaves, int nleaves,
               const double* scalars, int nscalars, i64 n, int flags, void* ws, size_t ws_bytes,
               void* out_dev, void* out_host, cudaStream_t st) {
   if (n < 0) return fail(SALT_EINVAL, "negative length");
@@ -520,7 +541,9 @@ int run_fused(const Plan& p, void* dst, const void* const* leaves, int nleaves,
   a.flags = flags;
   int vec;
   geometry<T>(p.mode == salt::MODE_REDUCE ? nullptr : dst, leaves, p.nl, n, vec, a.head, a.nvec);
-  Kernel* k = get_kernel(dtype_of<T>(), p.mode, vec, p.sa.type, p.sr.type);
+  Kernel*& slot = p.cached[g_force_jit.load(std::memory_order_relaxed)][vec == 1 ? 1 : 0];
+  if (!slot) slot = get_kernel(dtype_of<T>(), p.mode, vec, p.sa.type, p.sr.type);
+  Kernel* k = slot;
   if (!k) return SALT_EJIT;
   int dev, sms, occ;
   int rc = current_device(dev);
@@ -548,7 +571,7 @@ int run_fused(const Plan& p, void* dst, const void* const* leaves, int nleaves,
   return 0;
 }
 
-int dispatch(int dtype, const Plan& p, void* dst, const void* const* leaves, int nleaves,
+int dispatch(int dtype, Plan& p, void* dst, const void* const* leaves, int nleaves,
              const double* scalars, int nscalars, i64 n, int flags, void* ws, size_t ws_bytes,
              void* out_dev, void* out_host, cudaStream_t st) {
   if (dtype == SALT_F32)
@@ -590,7 +613,7 @@ constexpr i64 kMaxChunk = i64(1) << 23;
 
 // Shared by assign (reduce == false) and reduce: stream chunk c of every
 // operand through buffer c % 3; the fused kernel runs on streams[1].
-int host_pipeline(int dtype, const Plan& p, void* host_dst, const void* const* host_leaves,
+int host_pipeline(int dtype, Plan& p, void* host_dst, const void* const* host_leaves,
                   int nleaves, const double* scalars, int nscalars, i64 n, int flags,
                   void* staging, size_t staging_bytes, void* const* streams3, void* out_host) {
   const bool reduce = p.mode == salt::MODE_REDUCE;
@@ -689,45 +712,45 @@ size_t salt_reduce_workspace_bytes(void) { return kWsHeader + (size_t)kMaxGrid *
 
 int salt_signature_kind(int dtype, const char* sig, const char* reduce_sig, int kind) {
   if (kind < 0 || kind > 2) return 0;
-  Plan p;
+  Plan* p;
   const char* a = kind == 1 ? nullptr : sig;
   const char* r = kind == 0 ? nullptr : (kind == 1 ? sig : reduce_sig);
   if (make_plan(dtype, a, r, kind, salt::MAX_LEAVES, salt::MAX_SCALARS, p)) return 0;
   ensure_table();
   const int V = dtype == SALT_F32 ? 8 : 4;
   std::lock_guard<std::mutex> lk(g_table_mu);
-  return table().count(key_of(dtype, kind, V, p.sa.type, p.sr.type)) ? 1 : 2;
+  return table().count(key_of(dtype, kind, V, p->sa.type, p->sr.type)) ? 1 : 2;
 }
 
 int salt_prepare(int dtype, const char* sig, const char* reduce_sig, int kind) {
   if (kind < 0 || kind > 2) return fail(SALT_EINVAL, "kind must be 0, 1 or 2");
-  Plan p;
+  Plan* p;
   const char* a = kind == 1 ? nullptr : sig;
   const char* r = kind == 0 ? nullptr : (kind == 1 ? sig : reduce_sig);
   int rc = make_plan(dtype, a, r, kind, salt::MAX_LEAVES, salt::MAX_SCALARS, p);
   if (rc) return rc;
   const int V = dtype == SALT_F32 ? 8 : 4;
   for (int vec : {V, 1})
-    if (!get_kernel(dtype, kind, vec, p.sa.type, p.sr.type)) return SALT_EJIT;
+    if (!get_kernel(dtype, kind, vec, p->sa.type, p->sr.type)) return SALT_EJIT;
   return 0;
 }
 
 int salt_assign(int dtype, const char* sig, void* dst, const void* const* leaves, int nleaves,
                 const double* scalars, int nscalars, int64_t n, void* stream) {
-  Plan p;
+  Plan* p;
   int rc = make_plan(dtype, sig, nullptr, salt::MODE_ASSIGN, nleaves, nscalars, p);
   if (rc) return rc;
-  return dispatch(dtype, p, dst, leaves, nleaves, scalars, nscalars, n, 0, nullptr, 0, nullptr,
+  return dispatch(dtype, *p, dst, leaves, nleaves, scalars, nscalars, n, 0, nullptr, 0, nullptr,
                   nullptr, (cudaStream_t)stream);
 }
 
 int salt_reduce(int dtype, const char* sig, const void* const* leaves, int nleaves,
                 const double* scalars, int nscalars, int64_t n, int flags, void* workspace,
                 size_t workspace_bytes, void* out_dev, void* out_host, void* stream) {
-  Plan p;
+  Plan* p;
   int rc = make_plan(dtype, nullptr, sig, salt::MODE_REDUCE, nleaves, nscalars, p);
   if (rc) return rc;
-  return dispatch(dtype, p, nullptr, leaves, nleaves, scalars, nscalars, n, flags, workspace,
+  return dispatch(dtype, *p, nullptr, leaves, nleaves, scalars, nscalars, n, flags, workspace,
                   workspace_bytes, out_dev, out_host, (cudaStream_t)stream);
 }
 
@@ -735,10 +758,10 @@ int salt_assign_reduce(int dtype, const char* assign_sig, const char* reduce_sig
                        const void* const* leaves, int nleaves, const double* scalars,
                        int nscalars, int64_t n, int flags, void* workspace,
                        size_t workspace_bytes, void* out_dev, void* out_host, void* stream) {
-  Plan p;
+  Plan* p;
   int rc = make_plan(dtype, assign_sig, reduce_sig, salt::MODE_ASSIGN_REDUCE, nleaves, nscalars, p);
   if (rc) return rc;
-  return dispatch(dtype, p, dst, leaves, nleaves, scalars, nscalars, n, flags, workspace,
+  return dispatch(dtype, *p, dst, leaves, nleaves, scalars, nscalars, n, flags, workspace,
                   workspace_bytes, out_dev, out_host, (cudaStream_t)stream);
 }
 
@@ -754,22 +777,22 @@ int salt_reduce_finish(int dtype, const void* partials_dev, int count, int flags
 int salt_assign_host(int dtype, const char* sig, void* host_dst, const void* const* host_leaves,
                      int nleaves, const double* scalars, int nscalars, int64_t n, void* staging,
                      size_t staging_bytes, void* const* streams3) {
-  Plan p;
+  Plan* p;
   int rc = make_plan(dtype, sig, nullptr, salt::MODE_ASSIGN, nleaves, nscalars, p);
   if (rc) return rc;
   if (!host_dst) return fail(SALT_EINVAL, "NULL destination");
-  return host_pipeline(dtype, p, host_dst, host_leaves, nleaves, scalars, nscalars, n, 0, staging,
+  return host_pipeline(dtype, *p, host_dst, host_leaves, nleaves, scalars, nscalars, n, 0, staging,
                        staging_bytes, streams3, nullptr);
 }
 
 int salt_reduce_host(int dtype, const char* sig, const void* const* host_leaves, int nleaves,
                      const double* scalars, int nscalars, int64_t n, int flags, void* staging,
                      size_t staging_bytes, void* const* streams3, void* out_host) {
-  Plan p;
+  Plan* p;
   int rc = make_plan(dtype, nullptr, sig, salt::MODE_REDUCE, nleaves, nscalars, p);
   if (rc) return rc;
   if (!out_host) return fail(SALT_EINVAL, "NULL out_host");
-  return host_pipeline(dtype, p, nullptr, host_leaves, nleaves, scalars, nscalars, n, flags,
+  return host_pipeline(dtype, *p, nullptr, host_leaves, nleaves, scalars, nscalars, n, flags,
                        staging, staging_bytes, streams3, out_host);
 }
 

@@ -149,6 +149,16 @@ def _resolve(root, plan, backend, unroll, packages):
     return length, backend, plan
 
 
+def _length(root, plan, backend, unroll, packages) -> int:
+    """Validated length.  With no plan options the reference's default plan
+    cannot fail to resolve (footprint >= 1, length >= 0, default backend of
+    the tree's own dtype), so only the length check runs — the GPU never
+    uses the plan."""
+    if plan is None and backend is None and unroll is None and packages is None:
+        return common_length(root)
+    return _resolve(root, plan, backend, unroll, packages)[0]
+
+
 def _trace_events(plan: UnrollPlan, length: int, reduce_root: bool) -> list:
     """The call sequence of the reference's stepped executor for `plan`:
     init, load_once per slot, per iteration and package a load burst, an op
@@ -185,8 +195,7 @@ def execute_assign(root, plan: UnrollPlan = None, *, backend: LaneBackend = None
     """Evaluate an assignment tree, writing every destination element once."""
     if not isinstance(root, AssignNode):
         raise TypeError("execute_assign requires an assignment root")
-    length, _, _ = _resolve(root, plan, backend, unroll, packages)
-    _assign(root, length)
+    _assign(root, _length(root, plan, backend, unroll, packages))
 
 
 def execute_reduce(root, plan: UnrollPlan = None, *, backend: LaneBackend = None,
@@ -196,8 +205,7 @@ def execute_reduce(root, plan: UnrollPlan = None, *, backend: LaneBackend = None
     (or a DeviceScalar without host synchronisation when lazy=True)."""
     if not isinstance(root, SumNode):
         raise TypeError("execute_reduce requires a reduction root")
-    length, _, _ = _resolve(root, plan, backend, unroll, packages)
-    return _reduce(root, length, flags=_flags, lazy=lazy)
+    return _reduce(root, _length(root, plan, backend, unroll, packages), flags=_flags, lazy=lazy)
 
 
 def execute_assign_reduce(root, plan: UnrollPlan = None, *, backend: LaneBackend = None,
@@ -207,7 +215,7 @@ def execute_assign_reduce(root, plan: UnrollPlan = None, *, backend: LaneBackend
     over the freshly assigned values (e.g. axpy then dot, BASELINE config 5)."""
     if not isinstance(root, AssignReduceNode):
         raise TypeError("execute_assign_reduce requires an AssignReduceNode root")
-    length, _, _ = _resolve(root, plan, backend, unroll, packages)
+    length = _length(root, plan, backend, unroll, packages)
     lwa = lower(root.assign.source)
     lwr = lower(root.total.child, parent=lwa, dest=root.assign.dest.vector)
     return runtime.run_assign_reduce(lwa, lwr, root.assign.dest.vector, root.dtype, length,

@@ -349,3 +349,31 @@ def test_launches_are_counted_and_native():
     lv.dot(x, x)
     torch.cuda.synchronize()
     assert lib.salt_launch_count() - before == 2
+
+
+def test_cuda_graph_capture_of_fused_steps():
+    """Launch-bound loops (small n) can be captured in a CUDA graph: the
+    kernels go to the caller's current stream, lazy reductions never
+    synchronise, and the reduction workspace resets itself in-kernel."""
+    n = 1 << 16
+    g = np.random.default_rng(10)
+    x, y, z = (g.standard_normal(n) for _ in range(3))
+    X, Y, Z = dev(x, "f64"), dev(y, "f64"), dev(z, "f64")
+    eager = []
+    for _ in range(5):
+        eager.append(float(lv.axpy_dot(0.25, X, Y, Z)))
+    y_eager = Y.to_array()
+    Y2 = dev(y, "f64")
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        lv.axpy_dot(0.25, X, Y2, Z, lazy=True)  # warm-up: JIT/occupancy/workspace
+    torch.cuda.current_stream().wait_stream(s)
+    Y2.tensor.copy_(torch.from_numpy(y))
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        outs = [lv.axpy_dot(0.25, X, Y2, Z, lazy=True) for _ in range(5)]
+    graph.replay()
+    torch.cuda.synchronize()
+    assert [float(o.item()) for o in outs] == eager
+    assert Y2.to_array().tobytes() == y_eager.tobytes()

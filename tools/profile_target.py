@@ -1,0 +1,57 @@
+#!/usr/bin/env python
+"""Small, fixed launch sequence of one fused kernel for ncu captures.
+
+    python tools/profile_target.py --case dot64      # 3 warm-up + 2 profiled-candidate launches
+    ncu --set full -k regex:fused_kernel -s 3 -c 1 python tools/profile_target.py --case dot64
+
+Data is device-generated (torch.rand) — only the kernel's behaviour is of
+interest here; parity is covered by tests/.
+"""
+
+import argparse
+import sys
+from pathlib import Path
+
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import paper_1109_1264_b200 as lv  # noqa: E402
+
+CASES = {
+    # name: (dtype, n, number of vectors)
+    "t2": (torch.float64, 1 << 28, 4),
+    "t1": (torch.float64, 1 << 28, 4),
+    "dot64": (torch.float64, 1 << 28, 2),
+    "nrm2_32": (torch.float32, 1 << 28, 1),
+    "dot32": (torch.float32, 1 << 28, 2),
+    "etree32": (torch.float32, 1 << 30, 5),
+    "axpydot": (torch.float64, 1 << 28, 3),
+    "daxpy20": (torch.float64, 1 << 20, 2),
+}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--case", choices=sorted(CASES), required=True)
+    ap.add_argument("--launches", type=int, default=5)
+    a = ap.parse_args()
+    dt, n, k = CASES[a.case]
+    v = [lv.DenseVector.from_tensor(torch.rand(n, dtype=dt, device="cuda") * 2 - 1) for _ in range(k)]
+    calls = {
+        "t2": lambda: v[3].assign(1.25 * v[0] + -0.75 * (v[1] - v[2])),
+        "t1": lambda: v[3].assign(v[0] + (v[1] - v[2])),
+        "dot64": lambda: lv.dot(v[0], v[1], lazy=True),
+        "dot32": lambda: lv.dot(v[0], v[1], lazy=True),
+        "nrm2_32": lambda: lv.norm2(v[0], lazy=True),
+        "etree32": lambda: v[4].assign(1.25 * (v[0] + v[1]) - 0.75 * (v[2] - v[3]) + 0.5 * v[0]),
+        "axpydot": lambda: lv.axpy_dot(0.5, v[0], v[1], v[2], lazy=True),
+        "daxpy20": lambda: lv.axpy(0.5, v[0], v[1]),
+    }
+    for _ in range(a.launches):
+        calls[a.case]()
+    torch.cuda.synchronize()
+    print(f"{a.case}: {a.launches} launches OK")
+
+
+if __name__ == "__main__":
+    main()
