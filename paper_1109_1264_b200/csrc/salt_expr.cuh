@@ -183,11 +183,23 @@ __device__ __forceinline__ void two_sum(double a, double b, double& s, double& e
   double ap = __dsub_rn(s, bp);
   e = __dadd_rn(__dsub_rn(a, ap), __dsub_rn(b, bp));
 }
+// x - x == 0 exactly for finite x; NaN for +-inf and NaN.
+__device__ __forceinline__ bool finite(double x) { return __dsub_rn(x, x) == 0.0; }
+
+// Double-double addition.  Once a sum is not finite (an inf or NaN term, or
+// overflow) the compensation is meaningless (inf - inf = NaN); the plain
+// IEEE sum carries on alone, which is what the reference's element-typed
+// accumulation produces in that case (inf, or NaN for inf + -inf).
 __device__ __forceinline__ DD dd_add(DD a, DD b) {
   double s, e;
   two_sum(a.hi, b.hi, s, e);
-  e = __dadd_rn(e, __dadd_rn(a.lo, b.lo));
   DD r;
+  if (!finite(s)) {
+    r.hi = s;
+    r.lo = 0.0;
+    return r;
+  }
+  e = __dadd_rn(e, __dadd_rn(a.lo, b.lo));
   two_sum(s, e, r.hi, r.lo);
   return r;
 }
@@ -204,7 +216,16 @@ template <> struct Acc<double> {
     hi = s;
     lo = __dadd_rn(lo, e);
   }
-  __device__ __forceinline__ DD get() const { DD r; two_sum(hi, lo, r.hi, r.lo); return r; }
+  __device__ __forceinline__ DD get() const {
+    DD r;
+    if (!finite(hi)) {  // lo is NaN once hi saw an inf; keep the plain sum
+      r.hi = hi;
+      r.lo = 0.0;
+      return r;
+    }
+    two_sum(hi, lo, r.hi, r.lo);
+    return r;
+  }
 };
 template <> struct Acc<float> {
   double hi = 0.0;
@@ -243,7 +264,7 @@ template <class T> __device__ __forceinline__ void finish_store(DD tot, int flag
     *(DD*)out = tot;
     return;
   }
-  T r = (T)__dadd_rn(tot.hi, tot.lo);
+  T r = (T)(finite(tot.hi) ? __dadd_rn(tot.hi, tot.lo) : tot.hi);
   if (flags & FLAG_SQRT) r = Arith<T>::sqrt_rn(r);
   *(T*)out = r;
 }

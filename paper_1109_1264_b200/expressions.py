@@ -35,6 +35,7 @@ __all__ = [
     "as_node",
     "common_length",
     "combine_partials",
+    "traffic",
 ]
 
 
@@ -360,3 +361,30 @@ def lower(expr: Expression, parent: _Lowering = None, dest=None) -> _Lowering:
     lw = _Lowering(parent, dest)
     expr._postfix(lw)
     return lw
+
+
+def traffic(root: Expression) -> dict:
+    """Static traffic of one fused evaluation of `root` — the GPU analogue of
+    the reference's CountingVector fusion checks (test_acceptance.py:222-243):
+    every DISTINCT vector read is loaded once (a destination that is also a
+    source leaf counts as a read), the destination is stored once.  These are
+    the algorithmic bytes the roofline numbers are computed from."""
+    n = common_length(root)
+    if isinstance(root, AssignNode):
+        lw, dest = lower(root.source), root.dest.vector
+    elif isinstance(root, SumNode):
+        lw, dest = lower(root.child), None
+    elif isinstance(root, AssignReduceNode):
+        lw, dest = lower(root.assign.source), root.assign.dest.vector
+        lower(root.total.child, parent=lw, dest=dest)
+    else:
+        raise TypeError("traffic() needs an AssignNode, SumNode or AssignReduceNode root")
+    reads = len(lw.vectors)
+    writes = 1 if dest is not None else 0
+    size = root.dtype.itemsize
+    return {
+        "vectors_read": reads,
+        "vectors_written": writes,
+        "elements": n,
+        "bytes": size * n * (reads + writes),
+    }

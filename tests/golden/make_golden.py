@@ -17,6 +17,7 @@ Fixtures
   fused.npz        axpy then dot (config 5 building block): y_out and r
   specials.npz     inf / nan / -0.0 / subnormal operands through the trees
   traces.npz       call_trace event lists for several plans
+  special_reductions.npz  sum / dot over operands with inf, -inf, NaN, max
 """
 
 import json
@@ -214,6 +215,35 @@ def gen_specials():
     return len(meta)
 
 
+def gen_special_reductions():
+    """Reductions over operands holding inf / -inf / NaN / huge values."""
+    out = {}
+    meta = []
+    cases = {
+        "inf": lambda x: np.concatenate([x, [np.inf]]),
+        "ninf": lambda x: np.concatenate([[-np.inf], x]),
+        "both_inf": lambda x: np.concatenate([[np.inf], x, [-np.inf]]),
+        "nan": lambda x: np.concatenate([x[:10], [np.nan], x[10:]]),
+        "huge": lambda x: np.concatenate([x, [np.finfo(x.dtype).max] * 3]),
+    }
+    for dt in DTYPES:
+        base = rng(5, 0 if dt == "f32" else 1).uniform(-1, 1, 997).astype(NP[dt])
+        for cname, mk in cases.items():
+            x = mk(base).astype(NP[dt])
+            X = lv.DenseVector.from_values(x, dt)
+            with np.errstate(all="ignore"):
+                r_sum = lv.sum(X)
+                r_dot = lv.dot(X, X)
+            key = f"{cname}|{dt}"
+            out[f"{key}|x"] = x
+            out[f"{key}|sum"] = np.array([r_sum], dtype=NP[dt])
+            out[f"{key}|dot"] = np.array([r_dot], dtype=NP[dt])
+            meta.append([cname, dt, int(x.shape[0])])
+    out["meta"] = np.array(json.dumps(meta))
+    np.savez_compressed(OUT / "special_reductions.npz", **out)
+    return len(meta)
+
+
 def gen_traces():
     out = {}
     meta = []
@@ -257,3 +287,4 @@ if __name__ == "__main__":
     print("fused cases:", gen_fused())
     print("special cases:", gen_specials())
     print("trace cases:", gen_traces())
+    print("special reduction cases:", gen_special_reductions())

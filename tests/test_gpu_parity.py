@@ -377,3 +377,14 @@ def test_cuda_graph_capture_of_fused_steps():
     torch.cuda.synchronize()
     assert [float(o.item()) for o in outs] == eager
     assert Y2.to_array().tobytes() == y_eager.tobytes()
+
+
+def test_special_reductions_match_reference():
+    """inf / -inf / NaN / overflow in reductions: the compensated sum falls
+    back to the plain IEEE sum, giving the reference's inf / NaN results."""
+    meta, z = golden("special_reductions")
+    for cname, dt, n in meta:
+        key = f"{cname}|{dt}"
+        X = dev(z[f"{key}|x"], dt)
+        assert same_bits(np.array([lv.sum(X)]), z[f"{key}|sum"]), key
+        assert same_bits(np.array([lv.dot(X, X)]), z[f"{key}|dot"]), key
