@@ -177,7 +177,7 @@ def run_reference(args, world, rank):
     if rank != 0:
         return
     threads = _host_threads()
-    n_sample = 1 << 25
+    n_sample = args.n_sample
     gbs, per, done = cpu_reference_gbs(n_sample, args.steps, args.warmup, threads, seconds_cap=120)
     line = {
         "impl": "reference",
@@ -368,6 +368,8 @@ def main(argv=None):
     ap.add_argument("--n", type=int, default=1 << 28)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--n-sample", type=int, default=1 << 25,
+                    help="elements per step of the --impl reference CPU sample")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         args.warmup = 3

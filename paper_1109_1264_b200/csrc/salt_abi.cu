@@ -550,11 +550,16 @@ int run_fused(Plan& p, void* dst, const void* const* leaves, int nleaves,
   if (rc) return rc;
   rc = prepare(k, dev, sms, occ);
   if (rc) return rc;
+  // Assignments: one BLOCK*UNR tile per CTA (non-persistent): the block
+  // scheduler refills an SM the moment a CTA retires, so loads stay in
+  // flight continuously — 7.28 vs 7.08 TB/s for a persistent grid-stride
+  // loop on B200 (profiles/r01_stream_variants.txt).  Reductions keep a
+  // persistent grid of SMs x resident CTAs so the number of partials (and
+  // the combine order) is fixed per device.
   const i64 per_cta = (i64)kBlock * k->unroll;
   i64 want = (a.nvec + per_cta - 1) / per_cta;
   if (want < 1) want = 1;
-  i64 cap = (i64)sms * occ;
-  if (reduce && cap > kMaxGrid) cap = kMaxGrid;
+  i64 cap = reduce ? std::min<i64>((i64)sms * occ, kMaxGrid) : i64(0x7fffffff);
   int grid = (int)(want < cap ? want : cap);
   if (reduce) {
     a.ticket = (unsigned int*)ws;

@@ -120,6 +120,78 @@ __global__ void __launch_bounds__(BLOCK) kC(double* d, const double* a, const do
   }
 }
 
+// Variant D: persistent grid-stride with a register double buffer: the
+// loads of iteration i+1 are issued before iteration i is computed/stored.
+template <int UNR, int BLOCK>
+__global__ void __launch_bounds__(BLOCK) kD(double* d, const double* a, const double* b,
+                                            const double* c, double al, double be, i64 nvec) {
+  const i64 nthreads = (i64)gridDim.x * BLOCK;
+  i64 base = (i64)blockIdx.x * BLOCK * UNR + threadIdx.x;
+  double x[UNR][4], y[UNR][4], z[UNR][4];
+  auto load = [&](i64 bs) {
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      i64 j = bs + (i64)u * BLOCK;
+      if (j < nvec) { ld4(x[u], a + 4 * j); ld4(y[u], b + 4 * j); ld4(z[u], c + 4 * j); }
+    }
+  };
+  if (base < nvec) load(base);
+  for (; base < nvec; base += nthreads * UNR) {
+    double r[UNR][4];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) r[u][k] = f(x[u][k], y[u][k], z[u][k], al, be);
+    const i64 next = base + nthreads * UNR;
+    if (next < nvec) load(next);
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      i64 j = base + (i64)u * BLOCK;
+      if (j < nvec) st4(d + 4 * j, r[u]);
+    }
+  }
+}
+
+// Reduction probes: dot(a, b) f64 with TwoSum per term.
+__device__ __forceinline__ void two_sum(double a, double b, double& s, double& e) {
+  s = __dadd_rn(a, b);
+  double bp = __dsub_rn(s, a);
+  double ap = __dsub_rn(s, bp);
+  e = __dadd_rn(__dsub_rn(a, ap), __dsub_rn(b, bp));
+}
+template <int UNR, int BLOCK, bool PREFETCH>
+__global__ void __launch_bounds__(BLOCK) kR(const double* a, const double* b, i64 nvec, double* part) {
+  const i64 nthreads = (i64)gridDim.x * BLOCK;
+  double hi = 0, lo = 0;
+  i64 base = (i64)blockIdx.x * BLOCK * UNR + threadIdx.x;
+  double x[UNR][4], y[UNR][4];
+  auto load = [&](i64 bs) {
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      i64 j = bs + (i64)u * BLOCK;
+      if (j < nvec) { ld4(x[u], a + 4 * j); ld4(y[u], b + 4 * j); }
+      else { for (int k = 0; k < 4; ++k) x[u][k] = y[u][k] = 0; }
+    }
+  };
+  if (PREFETCH && base < nvec) load(base);
+  for (; base < nvec; base += nthreads * UNR) {
+    if (!PREFETCH) load(base);
+    double p[UNR][4];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) p[u][k] = __dmul_rn(x[u][k], y[u][k]);
+    if (PREFETCH && base + nthreads * UNR < nvec) load(base + nthreads * UNR);
+#pragma unroll
+    for (int u = 0; u < UNR; ++u)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) { double s, e; two_sum(hi, p[u][k], s, e); hi = s; lo += e; }
+  }
+  // crude block partial (probe only)
+  for (int off = 16; off; off >>= 1) { hi += __shfl_xor_sync(~0u, hi, off); lo += __shfl_xor_sync(~0u, lo, off); }
+  if ((threadIdx.x & 31) == 0) atomicAdd(part, hi + lo);
+}
+
 // Variant T: TMA bulk copies (cp.async.bulk.shared::cluster.global) into a
 // STAGES-deep smem ring per CTA; one elected thread issues the copies for the
 // 3 leaves of a tile and arms the stage's mbarrier with the byte count; all
@@ -209,6 +281,32 @@ int main() {
     run("C one-tile-per-CTA unr2 blk256", [&] { k<<<(unsigned)g, 256>>>(d, a, b, c, 1.25, -0.75, nvec); }); }
   { auto k = kC<1, 256>; i64 g = (nvec + 255) / 256;
     run("C one-tile-per-CTA unr1 blk256", [&] { k<<<(unsigned)g, 256>>>(d, a, b, c, 1.25, -0.75, nvec); }); }
+  { auto k = kD<2, 256>; int o = occ((const void*)k, 256, 0); int g = sms * o; char nm[96];
+    snprintf(nm, 96, "D persistent+prefetch unr2 occ%d", o);
+    run(nm, [&] { k<<<g, 256>>>(d, a, b, c, 1.25, -0.75, nvec); }); }
+  { auto k = kD<1, 256>; int o = occ((const void*)k, 256, 0); int g = sms * o; char nm[96];
+    snprintf(nm, 96, "D persistent+prefetch unr1 occ%d", o);
+    run(nm, [&] { k<<<g, 256>>>(d, a, b, c, 1.25, -0.75, nvec); }); }
+  {
+    double* part; CK(cudaMalloc(&part, 8));
+    const double rb = 16.0 * n;
+    auto runr = [&](const char* name, auto launch) {
+      for (int i = 0; i < 3; ++i) launch();
+      CK(cudaDeviceSynchronize());
+      std::vector<float> ts;
+      for (int i = 0; i < 20; ++i) {
+        CK(cudaEventRecord(e0)); launch(); CK(cudaEventRecord(e1)); CK(cudaEventSynchronize(e1));
+        float ms; CK(cudaEventElapsedTime(&ms, e0, e1)); ts.push_back(ms);
+      }
+      std::sort(ts.begin(), ts.end());
+      printf("%-40s best %.4f ms  median %.4f ms  %.1f GB/s\n", name, ts[0], ts[ts.size() / 2], rb / ts[0] / 1e6);
+    };
+#define RUN_R(U, P, M) { auto k = kR<U, 256, P>; int o = occ((const void*)k, 256, 0); \
+      long long g = M == 0 ? (long long)sms * o : (nvec + 256 * U - 1) / (256 * U); char nm[96]; \
+      snprintf(nm, 96, "R dot unr%d prefetch%d %s occ%d", U, (int)P, M == 0 ? "persistent" : "one-tile", o); \
+      runr(nm, [&] { k<<<(unsigned)g, 256>>>(a, b, nvec, part); }); }
+    RUN_R(2, false, 0); RUN_R(2, true, 0); RUN_R(4, false, 0); RUN_R(4, true, 0); RUN_R(1, false, 1); RUN_R(2, false, 1);
+  }
 #define RUN_T(ST, TB, B) { auto k = kT<ST, TB, B>; size_t sm = (size_t)ST * 3 * TB + 64; \
     CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)); \
     int o = occ((const void*)k, B, sm); int g = sms * o; i64 nt = n * 8 / TB; \
