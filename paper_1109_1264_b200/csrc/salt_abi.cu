@@ -36,7 +36,8 @@ namespace {
 using salt::i64;
 
 constexpr int kBlock = 256;
-constexpr int kUnrollVec = 2;     // 256-bit vectors in flight per leaf per thread
+constexpr int kUnrollVec = 2;     // 256-bit vectors in flight per leaf per thread (assign)
+constexpr int kUnrollRed = 4;     // reductions: persistent grid, deeper per-thread batches
 constexpr int kUnrollScalar = 4;  // V == 1 fallback (misaligned operands)
 constexpr int kMaxGrid = 4096;    // reduction partial slots in the workspace
 constexpr size_t kWsHeader = 256; // ticket lives in the first 256 bytes
@@ -262,9 +263,10 @@ void reg_one(const char* asig, const char* rsig) {
   if (asig) { parse_sig(asig, false, sa); ta = sa.type; }
   if (rsig) { parse_sig(rsig, MODE == salt::MODE_ASSIGN_REDUCE, sr); tr = sr.type; }
   constexpr int V = vec_of<T>();
+  constexpr int U = MODE == salt::MODE_ASSIGN ? kUnrollVec : kUnrollRed;
   auto k1 = std::make_unique<Kernel>();
-  k1->aot = (const void*)&salt::fused_kernel<T, EA, ER, MODE, V, kUnrollVec, kBlock>;
-  k1->vec = V; k1->unroll = kUnrollVec;
+  k1->aot = (const void*)&salt::fused_kernel<T, EA, ER, MODE, V, U, kBlock>;
+  k1->vec = V; k1->unroll = U;
   table()[key_of(dtype_of<T>(), MODE, V, ta, tr)] = std::move(k1);
   auto k2 = std::make_unique<Kernel>();
   k2->aot = (const void*)&salt::fused_kernel<T, EA, ER, MODE, 1, kUnrollScalar, kBlock>;
@@ -316,7 +318,7 @@ Kernel* jit_compile(int dtype, int mode, int vec, const std::string& ta, const s
   Nvrtc& nv = nvrtc();
   if (!nv.ok) { g_err = "NVRTC unavailable: " + nv.why; return nullptr; }
   const char* tname = dtype == SALT_F32 ? "float" : "double";
-  const int unroll = vec == 1 ? kUnrollScalar : kUnrollVec;
+  const int unroll = vec == 1 ? kUnrollScalar : (mode == salt::MODE_ASSIGN ? kUnrollVec : kUnrollRed);
   std::string expr = std::string("salt::fused_kernel<") + tname + "," + ta + "," + tr + "," +
                      std::to_string(mode) + "," + std::to_string(vec) + "," +
                      std::to_string(unroll) + "," + std::to_string(kBlock) + ">";

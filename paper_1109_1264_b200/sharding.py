@@ -101,8 +101,9 @@ class ShardedVector:
         )
 
     def gather_partials(self, part: torch.Tensor) -> torch.Tensor:
-        """All-gather one {hi, lo} float64 pair per rank, in rank order."""
-        if self.world == 1:
+        """All-gather one {hi, lo} float64 pair per rank, in rank order (a
+        16-byte NCCL all-gather per rank over NVLink; gloo on CPU)."""
+        if not (dist.is_available() and dist.is_initialized()):
             return part.reshape(-1)
         out = [torch.empty_like(part) for _ in range(self.world)]
         dist.all_gather(out, part, group=self.group)

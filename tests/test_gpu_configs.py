@@ -168,3 +168,29 @@ def test_sharded_vector_world1_through_public_api():
     ex = restate.exact_sum(x * y)
     assert abs(float(r) - ex) <= 1e-12 * abs(ex)
     assert lv.norm2(X) == np.sqrt(np.float64(lv.dot(X, X)))
+
+
+def test_sharded_path_under_torchrun_nccl():
+    """tools/dist_check.py under torchrun (one process per visible GPU; one
+    here): NCCL process group, per-rank partials all-gathered over NCCL,
+    fixed-order finish — checked against the oracle."""
+    import json
+    import socket
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parents[1]
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ngpu = torch.cuda.device_count()
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                        f"--nproc-per-node={ngpu}", "--master-addr", "127.0.0.1", "--master-port",
+                        str(port), str(root / "tools" / "dist_check.py")],
+                       capture_output=True, text=True, timeout=600, cwd=root)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = [ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1]
+    res = json.loads(line)
+    assert res["ok"] and res["world"] == ngpu, res

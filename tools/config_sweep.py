@@ -118,11 +118,27 @@ def main():
     ap.add_argument("--out", default="profiles/configs.jsonl")
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--quick", action="store_true")
+    ap.add_argument("--only", default="1,2,3,4,5", help="comma list of configs to run")
     a = ap.parse_args()
     out = open(a.out, "w")
     R = a.reps
     gpu = torch.cuda.get_device_name()
 
+    only = {int(c) for c in a.only.split(",")}
+    if 1 in only:
+        c1(out, R, gpu)
+    if 2 in only:
+        c2(out, R, gpu, a.quick)
+    if 3 in only:
+        c3(out, R, gpu)
+    if 4 in only:
+        c4(out, R, gpu)
+    if 5 in only:
+        c5(out, gpu)
+    out.close()
+
+
+def c1(out, R, gpu):
     # ---------------- C1: daxpy f64 2^20 (L2-resident: 24 MiB) ----------------
     n = 1 << 20
     x, y = vec(1, 0, n, np.float64), vec(1, 1, n, np.float64)
@@ -146,10 +162,12 @@ def main():
         cpu_ref_s=ct, cpu_ref_gbs=b / ct / 1e9, cpu_threads=THREADS, gpu=gpu)
     del x, y, y0
 
+
+def c2(out, R, gpu, quick):
     # ---------------- C2: a + (b - c) and alpha*a + beta*(b - c), f64 sweep ----------------
     al, be = synth.scalars(2, 2)
     sizes = [1 << p for p in range(10, 29, 2)]
-    if a.quick:
+    if quick:
         sizes = [1 << 20, 1 << 28]
     for n in sizes:
         A, B, C = (vec(2, k, n, np.float64) for k in range(3))
@@ -177,6 +195,8 @@ def main():
             rec(out, **entry)
         del A, B, C, D, ta, tb, tc, td
 
+
+def c3(out, R, gpu):
     # ---------------- C3: dot / nrm2, f32 + f64, 2^24 and 2^28 ----------------
     for dt in (np.float32, np.float64):
         for n in (1 << 24, 1 << 28):
@@ -199,6 +219,8 @@ def main():
                 rec(out, **entry)
             del X, Y
 
+
+def c4(out, R, gpu):
     # ---------------- C4: e-tree f32, global 2^30; per-GPU block at G = 1,2,4,8 ----------------
     al, be, ga = synth.scalars(4, 3)
     N = 1 << 30
@@ -221,6 +243,8 @@ def main():
         cpu_threads=THREADS)
     del ops, E, v, e
 
+
+def c5(out, gpu):
     # ---------------- C5: axpy -> dot, f64, 2^28 per GPU (2^31 / 8), 100 iterations ----------------
     n = 1 << 28
     X, Y, Z = (vec(5, k, n, np.float64) for k in range(3))
@@ -249,7 +273,6 @@ def main():
             per_step_s=el / 100, gbs=b * 100 / el / 1e9, pct_hbm=b * 100 / el / 1e9 / PEAK,
             r_last=float(rs[-1].item()), gpu=gpu,
             note="credited bytes 4*8*n per step (fused compulsory traffic)")
-    out.close()
 
 
 if __name__ == "__main__":
