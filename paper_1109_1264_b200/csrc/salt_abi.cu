@@ -36,8 +36,14 @@ namespace {
 using salt::i64;
 
 constexpr int kBlock = 256;
-constexpr int kUnrollVec = 2;     // 256-bit vectors in flight per leaf per thread (assign)
-constexpr int kUnrollRed = 4;     // reductions: persistent grid, deeper per-thread batches
+constexpr int kUnrollVec = 2;     // 256-bit vectors in flight per leaf per thread
+// Reductions run a persistent grid; two-leaf reductions (dot) keep more bytes
+// in flight with 4 vectors per leaf (7.26 vs 7.11 TB/s f64 dot 2^28), while
+// one-leaf (nrm2, sum) and fused three-leaf trees do best at 2
+// (profiles/r01_reduce_unroll.jsonl).
+constexpr int unroll_for(int mode, int nl) {
+  return (mode == 1 /*MODE_REDUCE*/ && nl == 2) ? 4 : kUnrollVec;
+}
 constexpr int kUnrollScalar = 4;  // V == 1 fallback (misaligned operands)
 constexpr int kMaxGrid = 4096;    // reduction partial slots in the workspace
 constexpr size_t kWsHeader = 256; // ticket lives in the first 256 bytes
@@ -263,7 +269,7 @@ void reg_one(const char* asig, const char* rsig) {
   if (asig) { parse_sig(asig, false, sa); ta = sa.type; }
   if (rsig) { parse_sig(rsig, MODE == salt::MODE_ASSIGN_REDUCE, sr); tr = sr.type; }
   constexpr int V = vec_of<T>();
-  constexpr int U = MODE == salt::MODE_ASSIGN ? kUnrollVec : kUnrollRed;
+  constexpr int U = unroll_for(MODE, salt::cmax(EA::NL, ER::NL));
   auto k1 = std::make_unique<Kernel>();
   k1->aot = (const void*)&salt::fused_kernel<T, EA, ER, MODE, V, U, kBlock>;
   k1->vec = V; k1->unroll = U;
@@ -313,12 +319,12 @@ void ensure_table() {
 }
 
 // Compile the tree with NVRTC; returns nullptr + g_err on failure.
-Kernel* jit_compile(int dtype, int mode, int vec, const std::string& ta, const std::string& tr,
-                    const std::string& key) {
+Kernel* jit_compile(int dtype, int mode, int vec, int nl, const std::string& ta,
+                    const std::string& tr, const std::string& key) {
   Nvrtc& nv = nvrtc();
   if (!nv.ok) { g_err = "NVRTC unavailable: " + nv.why; return nullptr; }
   const char* tname = dtype == SALT_F32 ? "float" : "double";
-  const int unroll = vec == 1 ? kUnrollScalar : (mode == salt::MODE_ASSIGN ? kUnrollVec : kUnrollRed);
+  const int unroll = vec == 1 ? kUnrollScalar : unroll_for(mode, nl);
   std::string expr = std::string("salt::fused_kernel<") + tname + "," + ta + "," + tr + "," +
                      std::to_string(mode) + "," + std::to_string(vec) + "," +
                      std::to_string(unroll) + "," + std::to_string(kBlock) + ">";
@@ -357,7 +363,8 @@ Kernel* jit_compile(int dtype, int mode, int vec, const std::string& ta, const s
 }
 
 // Look up (or JIT) the kernel; nullptr + g_err on failure.
-Kernel* get_kernel(int dtype, int mode, int vec, const std::string& ta, const std::string& tr) {
+Kernel* get_kernel(int dtype, int mode, int vec, int nl, const std::string& ta,
+                   const std::string& tr) {
   ensure_table();
   const std::string key = key_of(dtype, mode, vec, ta, tr);
   std::lock_guard<std::mutex> lk(g_table_mu);
@@ -367,7 +374,7 @@ Kernel* get_kernel(int dtype, int mode, int vec, const std::string& ta, const st
   }
   auto jt = jit_table().find(key);
   if (jt != jit_table().end()) return jt->second.get();
-  return jit_compile(dtype, mode, vec, ta, tr, key);
+  return jit_compile(dtype, mode, vec, nl, ta, tr, key);
 }
 
 struct DevInfo { int sms = 0; };
@@ -544,7 +551,7 @@ int run_fused(Plan& p, void* dst, const void* const* leaves, int nleaves,
   int vec;
   geometry<T>(p.mode == salt::MODE_REDUCE ? nullptr : dst, leaves, p.nl, n, vec, a.head, a.nvec);
   Kernel*& slot = p.cached[g_force_jit.load(std::memory_order_relaxed)][vec == 1 ? 1 : 0];
-  if (!slot) slot = get_kernel(dtype_of<T>(), p.mode, vec, p.sa.type, p.sr.type);
+  if (!slot) slot = get_kernel(dtype_of<T>(), p.mode, vec, p.nl, p.sa.type, p.sr.type);
   Kernel* k = slot;
   if (!k) return SALT_EJIT;
   int dev, sms, occ;
@@ -738,7 +745,7 @@ int salt_prepare(int dtype, const char* sig, const char* reduce_sig, int kind) {
   if (rc) return rc;
   const int V = dtype == SALT_F32 ? 8 : 4;
   for (int vec : {V, 1})
-    if (!get_kernel(dtype, kind, vec, p->sa.type, p->sr.type)) return SALT_EJIT;
+    if (!get_kernel(dtype, kind, vec, p->nl, p->sa.type, p->sr.type)) return SALT_EJIT;
   return 0;
 }
 

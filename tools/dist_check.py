@@ -58,7 +58,8 @@ def main():
     allv = [torch.empty_like(mine) for _ in range(world)]
     dist.all_gather(allv, mine)
     same = all(torch.equal(v, allv[0]) for v in allv)
-    flags = torch.tensor([ok_elem, ok_dot, ok_nrm, ok_fused, same], dtype=torch.int32, device="cuda")
+    flags = torch.tensor([int(bool(v)) for v in (ok_elem, ok_dot, ok_nrm, ok_fused, same)],
+                         dtype=torch.int32, device="cuda")
     dist.all_reduce(flags, op=dist.ReduceOp.MIN)
     if rank == 0:
         res = dict(zip(["elementwise", "dot", "norm2", "axpy_dot", "identical_on_ranks"],
