@@ -122,6 +122,13 @@ int salt_reduce_host(int dtype, const char* sig,
                      void* staging, size_t staging_bytes,
                      void* const* streams3, void* out_host);
 
+/* Host-buffer fused assign + reduce (salt_assign_reduce on host vectors). */
+int salt_assign_reduce_host(int dtype, const char* assign_sig, const char* reduce_sig,
+                            void* host_dst, const void* const* host_leaves, int nleaves,
+                            const double* scalars, int nscalars, int64_t n, int flags,
+                            void* staging, size_t staging_bytes,
+                            void* const* streams3, void* out_host);
+
 /* Bytes of device scratch salt_reduce / salt_assign_reduce need. */
 size_t salt_reduce_workspace_bytes(void);
 

@@ -39,6 +39,7 @@ HEADER_SYMBOLS = (
     "salt_reduce_finish",
     "salt_assign_host",
     "salt_reduce_host",
+    "salt_assign_reduce_host",
     "salt_reduce_workspace_bytes",
     "salt_signature_kind",
     "salt_prepare",
@@ -76,6 +77,11 @@ _SIGNATURES = {
     "salt_reduce_host": (
         _c_int,
         [_c_int, _c_str, _c_vpp, _c_int, _c_dp, _c_int, _c_i64, _c_int, _c_vp, _c_size, _c_vpp, _c_vp],
+    ),
+    "salt_assign_reduce_host": (
+        _c_int,
+        [_c_int, _c_str, _c_str, _c_vp, _c_vpp, _c_int, _c_dp, _c_int, _c_i64, _c_int, _c_vp, _c_size,
+         _c_vpp, _c_vp],
     ),
     "salt_reduce_workspace_bytes": (_c_size, []),
     "salt_signature_kind": (_c_int, [_c_int, _c_str, _c_str, _c_int]),

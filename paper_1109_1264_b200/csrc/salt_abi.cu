@@ -630,7 +630,8 @@ constexpr i64 kMaxChunk = i64(1) << 23;
 int host_pipeline(int dtype, Plan& p, void* host_dst, const void* const* host_leaves,
                   int nleaves, const double* scalars, int nscalars, i64 n, int flags,
                   void* staging, size_t staging_bytes, void* const* streams3, void* out_host) {
-  const bool reduce = p.mode == salt::MODE_REDUCE;
+  const bool reduce = p.mode != salt::MODE_ASSIGN;   // produces a sum
+  const bool has_dst = p.mode != salt::MODE_REDUCE;  // streams a destination back
   const size_t esz = dtype == SALT_F32 ? 4 : 8;
   if (n < 0) return fail(SALT_EINVAL, "negative length");
   if (!streams3 || !staging) return fail(SALT_EINVAL, "NULL staging or streams");
@@ -638,7 +639,7 @@ int host_pipeline(int dtype, Plan& p, void* host_dst, const void* const* host_le
   cudaStream_t sh = (cudaStream_t)streams3[0], sc = (cudaStream_t)streams3[1],
                sd = (cudaStream_t)streams3[2];
   const int nl = p.nl;
-  const int nbufs_per_set = nl + (reduce ? 0 : 1);
+  const int nbufs_per_set = nl + (has_dst ? 1 : 0);
   // staging: [reduce workspace][chunk partials][result 256B][kNBuf x (nl leaves + dst)]
   size_t ws = reduce ? salt_reduce_workspace_bytes() : 0;
   size_t fixed = ws + (reduce ? 256 * 1024 : 0) + 256;
@@ -677,14 +678,14 @@ int host_pipeline(int dtype, Plan& p, void* host_dst, const void* const* host_le
     }
     SALT_CUDA(cudaEventRecord(h2d.ev[b], sh));
     SALT_CUDA(cudaStreamWaitEvent(sc, h2d.ev[b], 0));
-    if (!reduce && c >= kNBuf) SALT_CUDA(cudaStreamWaitEvent(sc, d2h.ev[b], 0));
-    void* ddst = reduce ? nullptr : buf(b, nl);
+    if (has_dst && c >= kNBuf) SALT_CUDA(cudaStreamWaitEvent(sc, d2h.ev[b], 0));
+    void* ddst = has_dst ? buf(b, nl) : nullptr;
     rc = dispatch(dtype, p, ddst, dleaves, nleaves, scalars, nscalars, m,
                   reduce ? SALT_PARTIAL : 0, wsp, ws, reduce ? (void*)(parts + c) : nullptr,
                   nullptr, sc);
     if (rc) return rc;
     SALT_CUDA(cudaEventRecord(comp.ev[b], sc));
-    if (!reduce) {
+    if (has_dst) {
       SALT_CUDA(cudaStreamWaitEvent(sd, comp.ev[b], 0));
       SALT_CUDA(cudaMemcpyAsync((char*)host_dst + off * esz, ddst, m * esz,
                                 cudaMemcpyDeviceToHost, sd));
@@ -797,6 +798,19 @@ int salt_assign_host(int dtype, const char* sig, void* host_dst, const void* con
   if (!host_dst) return fail(SALT_EINVAL, "NULL destination");
   return host_pipeline(dtype, *p, host_dst, host_leaves, nleaves, scalars, nscalars, n, 0, staging,
                        staging_bytes, streams3, nullptr);
+}
+
+int salt_assign_reduce_host(int dtype, const char* assign_sig, const char* reduce_sig,
+                            void* host_dst, const void* const* host_leaves, int nleaves,
+                            const double* scalars, int nscalars, int64_t n, int flags,
+                            void* staging, size_t staging_bytes, void* const* streams3,
+                            void* out_host) {
+  Plan* p;
+  int rc = make_plan(dtype, assign_sig, reduce_sig, salt::MODE_ASSIGN_REDUCE, nleaves, nscalars, p);
+  if (rc) return rc;
+  if (!host_dst || !out_host) return fail(SALT_EINVAL, "NULL destination or out_host");
+  return host_pipeline(dtype, *p, host_dst, host_leaves, nleaves, scalars, nscalars, n, flags,
+                       staging, staging_bytes, streams3, out_host);
 }
 
 int salt_reduce_host(int dtype, const char* sig, const void* const* host_leaves, int nleaves,

@@ -306,6 +306,8 @@ def _device_reduce(dev, dt, call, flags, lazy, sharded=None):
 
 
 def _run_reduction(lw, dest, dt, n, flags, lazy, make_call, host_call):
+    """Fast path / placement for a reduction-producing call; `host_call` runs
+    it on pinned host vectors (streamed through the GPU)."""
     fast = _fast(lw.vectors, dest)
     if fast is not None:
         dev, ptrs, dptr = fast
@@ -318,10 +320,9 @@ def _run_reduction(lw, dest, dt, n, flags, lazy, make_call, host_call):
     pl = Placement(lw.vectors, dest, n)
     leaves, keep = _native.ptr_array(pl.pointers)
     if pl.kind == "host":
-        if host_call is None:
-            raise TypeError("this fused evaluation needs device-resident vectors")
         host = (ctypes.c_double * 2)()
-        _host_call(lambda st, sb, sp: host_call(leaves, pl.n, st, sb, sp, ctypes.addressof(host)))
+        _host_call(lambda st, sb, sp: host_call(leaves, pl.n, st, sb, sp, ctypes.addressof(host),
+                                                pl.dest_pointer))
         result = np.frombuffer(bytes(host)[: dt.itemsize], dtype=dt)[0]
     else:
         with _OnDevice(pl.device.index):
@@ -344,7 +345,7 @@ def run_reduce(lw, dtype, n, flags=0, lazy=False):
         return lambda fl, ws, wsb, od, oh, st: lib.salt_reduce(
             code, sig, leaves, nl, scal, ns, m, fl, ws, wsb, od, oh, st)
 
-    def host_call(leaves, m, st, sb, sp, out):
+    def host_call(leaves, m, st, sb, sp, out, _dptr):
         return lib.salt_reduce_host(code, sig, leaves, nl, scal, ns, m, flags, st, sb, sp, out)
 
     return _run_reduction(lw, None, dt, n, flags, lazy, make_call, host_call)
@@ -363,4 +364,8 @@ def run_assign_reduce(lwa, lwr, dest, dtype, n, flags=0, lazy=False):
         return lambda fl, ws, wsb, od, oh, st: lib.salt_assign_reduce(
             code, asig, rsig, dptr, leaves, nl, scal, ns, m, fl, ws, wsb, od, oh, st)
 
-    return _run_reduction(lwa, dest, dt, n, flags, lazy, make_call, None)
+    def host_call(leaves, m, st, sb, sp, out, dptr):
+        return lib.salt_assign_reduce_host(code, asig, rsig, dptr, leaves, nl, scal, ns, m, flags,
+                                           st, sb, sp, out)
+
+    return _run_reduction(lwa, dest, dt, n, flags, lazy, make_call, host_call)

@@ -388,3 +388,53 @@ def test_special_reductions_match_reference():
         X = dev(z[f"{key}|x"], dt)
         assert same_bits(np.array([lv.sum(X)]), z[f"{key}|sum"]), key
         assert same_bits(np.array([lv.dot(X, X)]), z[f"{key}|dot"]), key
+
+
+def test_concurrent_evaluation_from_threads():
+    """One expression value evaluated concurrently from several threads, each
+    on its own CUDA stream (reference contract: expressions.py:17-21).  The
+    C ABI is re-entrant and reduction workspaces are per stream."""
+    import threading
+
+    n = 1 << 20
+    g = np.random.default_rng(11)
+    a, b = g.uniform(-1, 1, n), g.uniform(-1, 1, n)
+    A, B = dev(a, "f64"), dev(b, "f64")
+    expr = 1.5 * A - 0.5 * (B - A)
+    want = restate.eval_sig("S0 L0 * S1 L1 L0 - * -", [a, b], [1.5, 0.5], "f64")
+    exact = restate.exact_sum(a * b)
+    errors = []
+
+    def worker(k):
+        try:
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                d = lv.DenseVector.empty(n, "f64", device="cuda")
+                for _ in range(20):
+                    d.assign(expr)
+                    r = lv.dot(A, B)
+                    assert abs(float(r) - exact) <= 1e-12 * abs(exact)
+                s.synchronize()
+                assert d.to_array().tobytes() == want.tobytes()
+        except Exception as exc:  # collected for the main thread
+            errors.append((k, repr(exc)))
+
+    ts = [threading.Thread(target=worker, args=(k,)) for k in range(6)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errors, errors
+
+
+def test_fused_axpy_dot_on_host_vectors():
+    g = np.random.default_rng(12)
+    for dt in ("f32", "f64"):
+        n = (1 << 23) * 2 + 99
+        x, y, z = (g.standard_normal(n).astype(NP[dt]) for _ in range(3))
+        X, Y, Z = (lv.DenseVector.from_values(v, dt, device="cpu") for v in (x, y, z))
+        r = lv.axpy_dot(-0.375, X, Y, Z)
+        y_new = restate.eval_sig("L0 S0 L1 * +", [y, x], [-0.375], dt)
+        assert same_bits(Y.to_array(), y_new)
+        exact = restate.exact_sum((y_new * z))
+        assert abs(float(r) - exact) <= TOL[dt] * abs(exact)

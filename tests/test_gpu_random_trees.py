@@ -1,0 +1,61 @@
+"""Randomised parity: seeded random expression trees (up to 8 distinct
+leaves, repeated leaves, scalars, depth <= 6) built with the public
+operators, evaluated on the GPU (compiled-in table or NVRTC JIT) and compared
+bit for bit with the NumPy restatement of the reference's node semantics;
+reductions of the same trees against the exact sum."""
+
+import numpy as np
+import pytest
+
+import paper_1109_1264_b200 as lv
+from conftest import NP, same_bits
+from oracle import restate
+from paper_1109_1264_b200.engine import execute_reduce
+from paper_1109_1264_b200.expressions import SumNode, as_node, lower
+
+pytestmark = pytest.mark.gpu
+
+
+def random_tree(rng, vecs, depth):
+    """Returns (expression, postfix-builder) using only public operators."""
+    if depth == 0 or rng.random() < 0.25:
+        return vecs[int(rng.integers(len(vecs)))]
+    kind = rng.integers(5)
+    left = random_tree(rng, vecs, depth - 1)
+    if kind == 3:
+        alpha = float(rng.uniform(-3, 3))
+        return alpha * as_node(left) if rng.random() < 0.5 else as_node(left) * alpha
+    if kind == 4:
+        return -as_node(left)
+    right = random_tree(rng, vecs, depth - 1)
+    l, r = as_node(left), as_node(right)
+    return l + r if kind == 0 else (l - r if kind == 1 else l * r)
+
+
+@pytest.mark.parametrize("dt", ["f32", "f64"])
+def test_random_trees_bit_exact(dt):
+    rng = np.random.default_rng(2026 if dt == "f32" else 2027)
+    checked = 0
+    for case in range(24):
+        n = int(rng.choice([1, 7, 33, 1000, 4099, 65_537, 1 << 20]))
+        nv = int(rng.integers(1, 9))
+        host = [rng.uniform(-2, 2, n).astype(NP[dt]) for _ in range(nv)]
+        vecs = [lv.DenseVector.from_values(h, dt, device="cuda") for h in host]
+        expr = as_node(random_tree(rng, vecs, int(rng.integers(1, 7))))
+        lw = lower(expr)
+        if len(lw.vectors) > 8:
+            continue
+        idx = [next(i for i, v in enumerate(vecs) if v is u) for u in lw.vectors]
+        want = restate.eval_sig(" ".join(lw.tokens), [host[i] for i in idx], lw.scalars, dt)
+        out = lv.DenseVector.zeros(n, dt, device="cuda")
+        out.assign(expr)
+        assert same_bits(out.to_array(), want), (case, " ".join(lw.tokens))
+        r = execute_reduce(SumNode(expr))
+        exact = restate.exact_sum(want)
+        if exact != 0 and np.isfinite(exact):
+            tol = {"f32": 1e-5, "f64": 1e-12}[dt]
+            # exact sum of the element-typed tree values; cancellation-free bound
+            scale = restate.exact_sum(np.abs(want))
+            assert abs(float(r) - exact) <= tol * max(abs(exact), 1e-3 * scale), (case, float(r), exact)
+        checked += 1
+    assert checked >= 20
