@@ -48,6 +48,11 @@ extern "C" {
 
 #define SALT_ABI_VERSION 1
 
+/* per-tree limits of one fused kernel (larger trees are split by the host
+ * layer into several fused evaluations through device temporaries) */
+#define SALT_MAX_LEAVES  16
+#define SALT_MAX_SCALARS 32
+
 /* element types (lanes.py:31-43 accepts exactly f32 / f64) */
 #define SALT_F32 0
 #define SALT_F64 1

@@ -29,8 +29,8 @@
 #include <string.h>
 
 #define OR_MAX_PROG 256
-#define OR_MAX_LEAVES 8
-#define OR_MAX_SCALARS 8
+#define OR_MAX_LEAVES 64
+#define OR_MAX_SCALARS 64
 #define OR_TILE 2048 /* multiple of every U*W (<= 128) */
 
 enum { OP_LEAF, OP_SCALAR, OP_D, OP_ADD, OP_SUB, OP_MUL };
@@ -68,8 +68,8 @@ static int parse(const char* s, prog_t* p, int nleaves, int nscalars, int allow_
         arg = arg * 10 + (t[i] - '0');
       }
       op = *t == 'L' ? OP_LEAF : OP_SCALAR;
-      if (op == OP_LEAF && arg >= nleaves) return -1;
-      if (op == OP_SCALAR && arg >= nscalars) return -1;
+      if (op == OP_LEAF && (arg >= nleaves || arg >= OR_MAX_LEAVES)) return -1;
+      if (op == OP_SCALAR && (arg >= nscalars || arg >= OR_MAX_SCALARS)) return -1;
       depth += 1;
     } else {
       return -1;

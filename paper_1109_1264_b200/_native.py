@@ -24,6 +24,8 @@ __all__ = [
     "HEADER_SYMBOLS",
 ]
 
+SALT_MAX_LEAVES = 16
+SALT_MAX_SCALARS = 32
 SALT_F32 = 0
 SALT_F64 = 1
 SALT_SQRT = 1

@@ -89,7 +89,7 @@ SALT_BINARY_NODE(Mul, mul)
 #undef SALT_BINARY_NODE
 
 // ---------------------------------------------------------------- kernel ABI
-enum { MAX_LEAVES = 8, MAX_SCALARS = 8, MODE_ASSIGN = 0, MODE_REDUCE = 1, MODE_ASSIGN_REDUCE = 2 };
+enum { MAX_LEAVES = 16, MAX_SCALARS = 32, MODE_ASSIGN = 0, MODE_REDUCE = 1, MODE_ASSIGN_REDUCE = 2 };
 enum { FLAG_SQRT = 1, FLAG_PARTIAL = 2 };
 
 struct DD { double hi, lo; };  // double-double partial (same layout as double2)

@@ -26,8 +26,16 @@ same plan (engine.py:191-240) and then evaluates the tree on the GPU.
 from collections import namedtuple
 from dataclasses import dataclass
 
-from . import runtime
-from .expressions import AssignNode, AssignReduceNode, SumNode, common_length, lower
+from . import _native, runtime
+from .expressions import (
+    AssignNode,
+    AssignReduceNode,
+    Leaf,
+    ScaleNode,
+    SumNode,
+    common_length,
+    lower,
+)
 from .lanes import LaneBackend, default_backend, scalar_backend, wide_backend
 
 __all__ = [
@@ -180,13 +188,72 @@ def _trace_events(plan: UnrollPlan, length: int, reduce_root: bool) -> list:
     return ev
 
 
+def _fits(lw) -> bool:
+    return len(lw.vectors) <= _native.SALT_MAX_LEAVES and len(lw.scalars) <= _native.SALT_MAX_SCALARS
+
+
+def _temporary_like(expr, length):
+    """Device temporary for an intermediate of `expr`, placed like its first
+    leaf (same device / same sharded partition)."""
+    from .sharding import ShardedVector
+    from .vectors import DenseVector
+
+    v = next(expr.leaves()).vector
+    seen = 0
+    while not isinstance(v, (DenseVector, ShardedVector)) and hasattr(v, "inner") and seen < 8:
+        v, seen = v.inner, seen + 1
+    if isinstance(v, ShardedVector):
+        return ShardedVector.zeros(length, expr.dtype, group=v.group, device=v.local.device)
+    device = v.device if isinstance(v, DenseVector) else None
+    return DenseVector.empty(length, expr.dtype, device=device)
+
+
+def _fit(expr, length):
+    """An equivalent tree that one fused kernel can take (<= SALT_MAX_LEAVES
+    distinct vectors, <= SALT_MAX_SCALARS scalars).  Oversized subtrees are
+    evaluated on the GPU into temporaries first; every node already rounds to
+    the element type, so materialising an intermediate changes no bit."""
+    if _fits(lower(expr)):
+        return expr
+    if isinstance(expr, ScaleNode):
+        child = _fit(expr.child, length)
+        cand = ScaleNode(expr.alpha, child)
+        return cand if _fits(lower(cand)) else ScaleNode(expr.alpha, _materialize(child, length))
+    left, right = _fit(expr.left, length), _fit(expr.right, length)
+    node = type(expr)
+    cand = node(left, right)
+    if _fits(lower(cand)):
+        return cand
+    # materialise the larger operand first (operand order is kept)
+    if len(lower(left).tokens) >= len(lower(right).tokens):
+        cand = node(_materialize(left, length), right)
+    else:
+        cand = node(left, _materialize(right, length))
+    if _fits(lower(cand)):
+        return cand
+    return node(_materialize(cand.left, length), _materialize(cand.right, length))
+
+
+def _materialize(expr, length):
+    if isinstance(expr, Leaf):
+        return expr
+    tmp = _temporary_like(expr, length)
+    node = Leaf(tmp)
+    runtime.run_assign(lower(_fit(expr, length)), tmp, expr.dtype, length)
+    return node
+
+
 def _assign(root: AssignNode, length: int):
     lw = lower(root.source)
+    if not _fits(lw):
+        lw = lower(_fit(root.source, length))
     runtime.run_assign(lw, root.dest.vector, root.dtype, length)
 
 
 def _reduce(root: SumNode, length: int, flags: int = 0, lazy: bool = False):
     lw = lower(root.child)
+    if not _fits(lw):
+        lw = lower(_fit(root.child, length))
     return runtime.run_reduce(lw, root.dtype, length, flags=flags, lazy=lazy)
 
 
@@ -218,6 +285,10 @@ def execute_assign_reduce(root, plan: UnrollPlan = None, *, backend: LaneBackend
     length = _length(root, plan, backend, unroll, packages)
     lwa = lower(root.assign.source)
     lwr = lower(root.total.child, parent=lwa, dest=root.assign.dest.vector)
+    if not _fits(lwa):
+        # too large for one fused kernel: assign, then reduce over the new values
+        _assign(root.assign, length)
+        return _reduce(root.total, length, flags=_flags, lazy=lazy)
     return runtime.run_assign_reduce(lwa, lwr, root.assign.dest.vector, root.dtype, length,
                                      flags=_flags, lazy=lazy)
 

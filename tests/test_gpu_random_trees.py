@@ -59,3 +59,27 @@ def test_random_trees_bit_exact(dt):
             assert abs(float(r) - exact) <= tol * max(abs(exact), 1e-3 * scale), (case, float(r), exact)
         checked += 1
     assert checked >= 20
+
+
+def test_trees_beyond_one_kernel_are_split_bit_exactly():
+    """20 distinct vectors and 40 scalars exceed one fused kernel
+    (SALT_MAX_LEAVES = 16, SALT_MAX_SCALARS = 32): the engine evaluates
+    subtrees into device temporaries first — same bits, since every node
+    rounds to the element type anyway."""
+    rng = np.random.default_rng(99)
+    n = 10_001
+    for dt in ("f32", "f64"):
+        host = [rng.uniform(-1, 1, n).astype(NP[dt]) for _ in range(20)]
+        vecs = [lv.DenseVector.from_values(h, dt, device="cuda") for h in host]
+        expr = as_node(vecs[0])
+        for k in range(1, 20):
+            expr = float(rng.uniform(0.5, 1.5)) * expr + float(rng.uniform(-1, 1)) * as_node(vecs[k])
+        lw = lower(expr)
+        assert len(lw.vectors) == 20 and len(lw.scalars) == 38
+        want = restate.eval_sig(" ".join(lw.tokens), host, lw.scalars, dt)
+        out = lv.DenseVector.zeros(n, dt, device="cuda")
+        out.assign(expr)
+        assert same_bits(out.to_array(), want), dt
+        r = execute_reduce(SumNode(expr))
+        exact = restate.exact_sum(want)
+        assert abs(float(r) - exact) <= {"f32": 1e-5, "f64": 1e-12}[dt] * abs(exact)
