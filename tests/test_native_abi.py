@@ -54,8 +54,9 @@ def test_abi_constants():
     ("L0 L1 L2 L3 L4 L5 L6 L7 + + + + + + +", 0, 2),
     ("L0 +", 0, 0),                  # malformed
     ("L0 L1", 0, 0),                 # two values left
-    ("L8", 0, 0),                    # leaf index out of range
-    ("S9 L0 *", 0, 0),
+    ("L16", 0, 0),                   # leaf index out of range (SALT_MAX_LEAVES = 16)
+    ("L15", 0, 2),
+    ("S32 L0 *", 0, 0),
     ("L0 / L1", 0, 0),
     ("D L0 *", 0, 0),                # D only inside a fused reduce tree
     ("", 0, 0),
