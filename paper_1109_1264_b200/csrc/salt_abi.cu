@@ -37,16 +37,9 @@ using salt::i64;
 
 constexpr int kBlock = 256;
 constexpr int kUnrollVec = 2;     // 256-bit vectors in flight per leaf per thread
-// Reductions run a persistent grid; two-leaf reductions (dot) keep more bytes
-// in flight with 4 vectors per leaf (7.26 vs 7.11 TB/s f64 dot 2^28), while
-// one-leaf (nrm2, sum) and fused three-leaf trees do best at 2
-// (profiles/r01_reduce_unroll.jsonl).
-constexpr int unroll_for(int mode, int nl) {
-  return (mode == 1 /*MODE_REDUCE*/ && nl == 2) ? 4 : kUnrollVec;
-}
+constexpr int unroll_for(int /*mode*/, int /*nl*/) { return kUnrollVec; }
 constexpr int kUnrollScalar = 4;  // V == 1 fallback (misaligned operands)
-constexpr int kMaxGrid = 4096;    // reduction partial slots in the workspace
-constexpr size_t kWsHeader = 256; // ticket lives in the first 256 bytes
+constexpr int kReduceTilesPerCta = 2;  // 2 x 512 vectors per CTA (tools/reduce_variants.cu)
 constexpr int kMaxDevices = 64;
 
 thread_local std::string g_err;
@@ -140,7 +133,6 @@ struct Driver {
   CUresult (*ModuleGetFunction)(CUfunction*, CUmodule, const char*) = nullptr;
   CUresult (*LaunchKernel)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned,
                            unsigned, CUstream, void**, void**) = nullptr;
-  CUresult (*OccupancyMaxActiveBlocksPerMultiprocessor)(int*, CUfunction, int, size_t) = nullptr;
   CUresult (*GetErrorString)(CUresult, const char**) = nullptr;
 };
 
@@ -162,8 +154,6 @@ Driver& driver() {
     d.ok = entry("cuModuleLoadData", d.ModuleLoadData, d.why) &&
            entry("cuModuleGetFunction", d.ModuleGetFunction, d.why) &&
            entry("cuLaunchKernel", d.LaunchKernel, d.why) &&
-           entry("cuOccupancyMaxActiveBlocksPerMultiprocessor",
-                 d.OccupancyMaxActiveBlocksPerMultiprocessor, d.why) &&
            entry("cuGetErrorString", d.GetErrorString, d.why);
   });
   return d;
@@ -237,7 +227,6 @@ struct Kernel {
   const void* aot = nullptr;                 // compiled-in kernel
   std::string cubin, lowered;                // JIT kernel (device independent)
   CUfunction jit_fn[kMaxDevices] = {};       // JIT module per device
-  int occ[kMaxDevices] = {};                 // resident CTAs per SM, per device
   int vec = 1;                               // lanes per vector access
   int unroll = 1;
 };
@@ -377,8 +366,6 @@ Kernel* get_kernel(int dtype, int mode, int vec, int nl, const std::string& ta,
   return jit_compile(dtype, mode, vec, nl, ta, tr, key);
 }
 
-struct DevInfo { int sms = 0; };
-DevInfo g_dev[kMaxDevices];
 std::mutex g_dev_mu;
 
 int current_device(int& dev) {
@@ -387,16 +374,11 @@ int current_device(int& dev) {
   return 0;
 }
 
-// Resolve per-device state (SM count, occupancy, JIT module) for a kernel.
-int prepare(Kernel* k, int dev, int& sms, int& occ) {
+// Resolve per-device state (the JIT module) for a kernel.
+int prepare(Kernel* k, int dev) {
+  if (k->aot) return 0;
   std::lock_guard<std::mutex> lk(g_dev_mu);
-  if (g_dev[dev].sms == 0) {
-    int v = 0;
-    SALT_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev));
-    g_dev[dev].sms = v;
-  }
-  sms = g_dev[dev].sms;
-  if (!k->aot && !k->jit_fn[dev]) {
+  if (!k->jit_fn[dev]) {
     Driver& d = driver();
     if (!d.ok) return fail(SALT_EJIT, "driver API unavailable: " + d.why);
     CUmodule mod;
@@ -409,18 +391,6 @@ int prepare(Kernel* k, int dev, int& sms, int& occ) {
     r = d.ModuleGetFunction(&k->jit_fn[dev], mod, k->lowered.c_str());
     if (r != CUDA_SUCCESS) return fail(SALT_EJIT, "cuModuleGetFunction failed for " + k->lowered);
   }
-  if (k->occ[dev] == 0) {
-    int o = 0;
-    if (k->aot) {
-      SALT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k->aot, kBlock, 0));
-    } else {
-      if (driver().OccupancyMaxActiveBlocksPerMultiprocessor(&o, k->jit_fn[dev], kBlock, 0) !=
-          CUDA_SUCCESS)
-        return fail(SALT_EJIT, "occupancy query failed");
-    }
-    k->occ[dev] = o > 0 ? o : 1;
-  }
-  occ = k->occ[dev];
   return 0;
 }
 
@@ -554,25 +524,36 @@ int run_fused(Plan& p, void* dst, const void* const* leaves, int nleaves,
   if (!slot) slot = get_kernel(dtype_of<T>(), p.mode, vec, p.nl, p.sa.type, p.sr.type);
   Kernel* k = slot;
   if (!k) return SALT_EJIT;
-  int dev, sms, occ;
+  int dev;
   int rc = current_device(dev);
   if (rc) return rc;
-  rc = prepare(k, dev, sms, occ);
+  rc = prepare(k, dev);
   if (rc) return rc;
-  // Assignments: one BLOCK*UNR tile per CTA (non-persistent): the block
-  // scheduler refills an SM the moment a CTA retires, so loads stay in
-  // flight continuously — 7.28 vs 7.08 TB/s for a persistent grid-stride
-  // loop on B200 (profiles/r01_stream_variants.txt).  Reductions keep a
-  // persistent grid of SMs x resident CTAs so the number of partials (and
-  // the combine order) is fixed per device.
-  const i64 per_cta = (i64)kBlock * k->unroll;
-  i64 want = (a.nvec + per_cta - 1) / per_cta;
-  if (want < 1) want = 1;
-  i64 cap = reduce ? std::min<i64>((i64)sms * occ, kMaxGrid) : i64(0x7fffffff);
-  int grid = (int)(want < cap ? want : cap);
+  // Work split (tools/stream_variants.cu, tools/reduce_variants.cu on B200):
+  // assignments take one BLOCK*UNR tile per CTA — the block scheduler
+  // refills an SM the moment a CTA retires, which keeps loads in flight
+  // (7.29 TB/s vs 7.06 for a persistent grid-stride loop); reductions take
+  // kReduceTilesPerCta tiles per CTA and combine per-CTA partials in two
+  // deterministic ticket levels (7.25 vs 6.88 TB/s persistent, fused
+  // axpy->dot f64 2^28).  Both grids depend only on n.
+  const i64 per_tile = (i64)kBlock * k->unroll;
+  const i64 ntiles = (a.nvec + per_tile - 1) / per_tile;
+  i64 K = 1, cap = i64(0x7fffffff);
   if (reduce) {
-    a.ticket = (unsigned int*)ws;
-    a.partials = (salt::DD*)((char*)ws + kWsHeader);
+    K = kReduceTilesPerCta;
+    cap = salt::MAX_REDUCE_CTAS;
+  }
+  if ((ntiles + K - 1) / K > cap) K = (ntiles + cap - 1) / cap;
+  i64 g64 = (ntiles + K - 1) / K;
+  if (g64 < 1) g64 = 1;
+  const int grid = (int)g64;
+  a.tiles_per_cta = K;
+  if (reduce) {
+    char* w = (char*)ws;
+    a.ticket = (unsigned int*)(w + salt::WsLayout::ticket);
+    a.group_tickets = (unsigned int*)(w + salt::WsLayout::group_tickets);
+    a.group_partials = (salt::DD*)(w + salt::WsLayout::group_partials);
+    a.partials = (salt::DD*)(w + salt::WsLayout::partials);
     a.out = out_dev;
   }
   rc = launch<T>(k, dev, grid, a, st);
@@ -659,7 +640,7 @@ int host_pipeline(int dtype, Plan& p, void* host_dst, const void* const* host_le
   auto buf = [&](int b, int i) -> void* {
     return bufs + ((size_t)b * nbufs_per_set + i) * chunk * esz;
   };
-  if (reduce) SALT_CUDA(cudaMemsetAsync(wsp, 0, kWsHeader, sc));
+  if (reduce) SALT_CUDA(cudaMemsetAsync(wsp, 0, salt::WsLayout::group_partials, sc));
   Events h2d, comp, d2h;
   int rc = h2d.make(kNBuf);
   if (!rc) rc = comp.make(kNBuf);
@@ -723,7 +704,7 @@ uint64_t salt_launch_count(void) { return g_launches.load(); }
 
 void salt_set_force_jit(int on) { g_force_jit.store(on ? 1 : 0); }
 
-size_t salt_reduce_workspace_bytes(void) { return kWsHeader + (size_t)kMaxGrid * sizeof(salt::DD); }
+size_t salt_reduce_workspace_bytes(void) { return (size_t)salt::WsLayout::bytes; }
 
 int salt_signature_kind(int dtype, const char* sig, const char* reduce_sig, int kind) {
   if (kind < 0 || kind > 2) return 0;

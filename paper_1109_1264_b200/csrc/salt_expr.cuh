@@ -102,10 +102,24 @@ template <class T> struct Args {
   i64 n;                          // elements
   i64 head;                       // scalar elements before the first aligned vector
   i64 nvec;                       // aligned vectors of V elements after `head`
-  DD* partials;                   // reduce modes: per-CTA partials (workspace)
-  unsigned int* ticket;           // reduce modes: last-CTA counter (workspace, zeroed)
-  void* out;                      // reduce modes: T result or DD partial
+  i64 tiles_per_cta;              // consecutive BLOCK*UNR-vector tiles each CTA owns
+  // reduce modes (workspace, see WsLayout): two-level deterministic combine
+  DD* partials;                   // one partial per CTA
+  DD* group_partials;             // one partial per group of GROUP CTAs
+  unsigned int* group_tickets;    // arrival counters per group (zeroed, self-resetting)
+  unsigned int* ticket;           // arrival counter of the groups (zeroed, self-resetting)
+  void* out;                      // T result or DD partial
   int flags;
+};
+
+// Reduction workspace: [ticket | group tickets | group partials | CTA partials].
+enum { GROUP = 256, MAX_GROUPS = 4096, MAX_REDUCE_CTAS = GROUP * MAX_GROUPS };
+struct WsLayout {
+  static constexpr i64 ticket = 0;
+  static constexpr i64 group_tickets = 256;
+  static constexpr i64 group_partials = group_tickets + 4 * (i64)MAX_GROUPS;
+  static constexpr i64 partials = group_partials + 16 * (i64)MAX_GROUPS;
+  static constexpr i64 bytes = partials + 16 * (i64)MAX_REDUCE_CTAS;
 };
 
 // 32-byte (256-bit) vector access: LDG.E.ENL2.256 / STG.E.ENL2.256 on sm_100a.
@@ -275,10 +289,11 @@ template <class T> __device__ __forceinline__ void finish_store(DD tot, int flag
 // MODE_ASSIGN_REDUCE: dst[i] = EA(i); out = sum_i ER(i, D = dst[i])   (one pass)
 //
 // Layout of the index space: [0, head) scalar, then nvec aligned vectors of
-// V lanes, then the scalar tail.  Each CTA walks the vectors in chunks of
-// BLOCK*UNR (grid-stride), issuing all UNR x NL 256-bit loads of a chunk
-// before any arithmetic: the GPU form of the reference's load burst /
-// vector_op burst / store burst (engine.py:209-225).
+// V lanes, then the scalar tail.  The vectors are cut into tiles of
+// BLOCK*UNR; CTA b owns tiles [b*K, b*K + K) (K = tiles_per_cta: 1 for
+// assignments, 2 for reductions).  Per tile a thread issues all UNR x NL
+// 256-bit loads before any arithmetic: the GPU form of the reference's load
+// burst / vector_op burst / store burst (engine.py:209-225).
 template <class T, class EA, class ER, int MODE, int V, int UNR, int BLOCK>
 __global__ void __launch_bounds__(BLOCK) fused_kernel(Args<T> a) {
   constexpr int NL = cmax(EA::NL, ER::NL);
@@ -311,9 +326,12 @@ __global__ void __launch_bounds__(BLOCK) fused_kernel(Args<T> a) {
     }
   }
 
-  // ---- vector body
-  for (i64 base = (i64)blockIdx.x * BLOCK * UNR + threadIdx.x; base < a.nvec;
-       base += nthreads * UNR) {
+  // ---- vector body: this CTA's run of consecutive tiles of BLOCK*UNR vectors
+  const i64 tile0 = (i64)blockIdx.x * a.tiles_per_cta;
+  const i64 ntiles = (a.nvec + (i64)BLOCK * UNR - 1) / ((i64)BLOCK * UNR);
+  const i64 tile1 = tile0 + a.tiles_per_cta < ntiles ? tile0 + a.tiles_per_cta : ntiles;
+  for (i64 t = tile0; t < tile1; ++t) {
+    const i64 base = t * BLOCK * UNR + threadIdx.x;
     E1 e[UNR];
 #pragma unroll
     for (int u = 0; u < UNR; ++u) {
@@ -344,32 +362,57 @@ __global__ void __launch_bounds__(BLOCK) fused_kernel(Args<T> a) {
   }
 
   if (REDUCE) {
+    // Two-level deterministic combine.  Every CTA publishes its partial; the
+    // last CTA to arrive in its group of GROUP consecutive CTAs folds the
+    // group's partials (thread t takes CTA t of the group, then a fixed
+    // shuffle/shared-memory tree); the last group to finish folds the group
+    // partials in group order.  Which CTA does the folding never changes
+    // the order, so the result depends only on n — not on scheduling, SM
+    // count or occupancy.
     __shared__ DD smem[BLOCK / 32];
-    __shared__ bool is_last;
+    __shared__ int stage;  // 0 done, 1 group finisher, 2 group + final finisher
     DD part = block_reduce_dd<BLOCK>(acc.get(), smem);
+    const unsigned int g = blockIdx.x / GROUP;
+    const unsigned int ngroups = (gridDim.x + GROUP - 1) / GROUP;
+    const unsigned int gsize = min((unsigned int)GROUP, gridDim.x - g * GROUP);
     if (threadIdx.x == 0) {
       a.partials[blockIdx.x] = part;
       __threadfence();
-      unsigned int t = atomicAdd(a.ticket, 1u);
-      is_last = (t == gridDim.x - 1);
+      stage = atomicAdd(&a.group_tickets[g], 1u) == gsize - 1 ? 1 : 0;
     }
     __syncthreads();
-    if (is_last) {
+    if (stage == 0) return;
+    __threadfence();
+    DD v; v.hi = 0.0; v.lo = 0.0;
+    for (unsigned int b = threadIdx.x; b < gsize; b += BLOCK) {
+      DD p;  // L2 loads: other CTAs wrote these during this launch
+      p.hi = __ldcg(&a.partials[g * GROUP + b].hi);
+      p.lo = __ldcg(&a.partials[g * GROUP + b].lo);
+      v = dd_add(v, p);
+    }
+    __syncthreads();
+    DD q = block_reduce_dd<BLOCK>(v, smem);
+    if (threadIdx.x == 0) {
+      a.group_partials[g] = q;
+      a.group_tickets[g] = 0u;  // every CTA of the group has arrived
       __threadfence();
-      // Fixed-order combine of all CTA partials: thread t folds t, t+BLOCK, ...
-      DD v; v.hi = 0.0; v.lo = 0.0;
-      for (int b = threadIdx.x; b < (int)gridDim.x; b += BLOCK) {
-        DD p;  // L2 loads: other CTAs wrote these during this launch
-        p.hi = __ldcg(&a.partials[b].hi);
-        p.lo = __ldcg(&a.partials[b].lo);
-        v = dd_add(v, p);
-      }
-      __syncthreads();
-      DD tot = block_reduce_dd<BLOCK>(v, smem);
-      if (threadIdx.x == 0) {
-        finish_store<T>(tot, a.flags, a.out);
-        *a.ticket = 0u;  // ready for the next launch on this workspace
-      }
+      stage = atomicAdd(a.ticket, 1u) == ngroups - 1 ? 2 : 1;
+    }
+    __syncthreads();
+    if (stage != 2) return;
+    __threadfence();
+    DD w; w.hi = 0.0; w.lo = 0.0;
+    for (unsigned int b = threadIdx.x; b < ngroups; b += BLOCK) {
+      DD p;
+      p.hi = __ldcg(&a.group_partials[b].hi);
+      p.lo = __ldcg(&a.group_partials[b].lo);
+      w = dd_add(w, p);
+    }
+    __syncthreads();
+    DD tot = block_reduce_dd<BLOCK>(w, smem);
+    if (threadIdx.x == 0) {
+      finish_store<T>(tot, a.flags, a.out);
+      *a.ticket = 0u;  // ready for the next launch on this workspace
     }
   }
 }
