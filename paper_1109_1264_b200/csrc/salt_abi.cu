@@ -39,7 +39,18 @@ constexpr int kBlock = 256;
 constexpr int kUnrollVec = 2;     // 256-bit vectors in flight per leaf per thread
 constexpr int unroll_for(int /*mode*/, int /*nl*/) { return kUnrollVec; }
 constexpr int kUnrollScalar = 4;  // V == 1 fallback (misaligned operands)
-constexpr int kReduceTilesPerCta = 2;  // 2 x 512 vectors per CTA (tools/reduce_variants.cu)
+// Reductions: tiles (of BLOCK*UNR vectors) per CTA, so that every CTA
+// streams ~64 KiB before paying its partial/ticket epilogue: 4 tiles for
+// one-leaf trees (nrm2, sum), 2 for two or more leaves (dot, fused axpy->dot).
+// SALT_REDUCE_TILES overrides it (tuning only; read once).
+int reduce_tiles_per_cta(int nl) {
+  static const int env = [] {
+    const char* e = getenv("SALT_REDUCE_TILES");
+    return e ? atoi(e) : 0;
+  }();
+  if (env > 0) return env;
+  return nl <= 1 ? 4 : 2;
+}
 constexpr int kMaxDevices = 64;
 
 thread_local std::string g_err;
@@ -540,7 +551,7 @@ int run_fused(Plan& p, void* dst, const void* const* leaves, int nleaves,
   const i64 ntiles = (a.nvec + per_tile - 1) / per_tile;
   i64 K = 1, cap = i64(0x7fffffff);
   if (reduce) {
-    K = kReduceTilesPerCta;
+    K = reduce_tiles_per_cta(p.nl);
     cap = salt::MAX_REDUCE_CTAS;
   }
   if ((ntiles + K - 1) / K > cap) K = (ntiles + cap - 1) / cap;
