@@ -111,6 +111,51 @@ int salt_assign_reduce(int dtype, const char* assign_sig, const char* reduce_sig
 int salt_reduce_finish(int dtype, const void* partials_dev, int count, int flags,
                        void* out_dev, void* out_host, void* stream);
 
+/* ---- sharded reductions: cross-GPU exchange over NVLink peer memory ----
+ * Each rank owns a SALT_XCHG_BUFFER_BYTES symmetric device buffer (e.g. from
+ * torch symmetric memory), zeroed once: 2 x 8 double-double slots followed
+ * by 8 uint64 flags.  slots[p] / flags[p] are rank p's buffer (slot array /
+ * flag array) mapped into this process.  epoch starts at 1 and increases by
+ * one per exchange, identically on every rank.  The reduction kernel's last
+ * CTA publishes this rank's total to every peer, waits for all of them and
+ * folds them in rank order — the collective runs inside the reduction
+ * kernel, with no NCCL call.  On timeout the result is NaN and *error = 1. */
+#define SALT_XCHG_MAX_RANKS 8
+#define SALT_XCHG_BUFFER_BYTES 512
+typedef struct salt_exchange {
+  int32_t rank, world;
+  uint64_t epoch;
+  void* slots[SALT_XCHG_MAX_RANKS];
+  void* flags[SALT_XCHG_MAX_RANKS];
+  uint64_t timeout_ns; /* 0 = wait forever */
+  void* error;         /* optional device uint32 */
+} salt_exchange;
+
+int salt_reduce_exchange(int dtype, const char* sig,
+                         const void* const* leaves, int nleaves,
+                         const double* scalars, int nscalars,
+                         int64_t n, int flags,
+                         void* workspace, size_t workspace_bytes,
+                         const salt_exchange* exchange,
+                         void* out_dev, void* out_host, void* stream);
+
+int salt_assign_reduce_exchange(int dtype, const char* assign_sig, const char* reduce_sig,
+                                void* dst, const void* const* leaves, int nleaves,
+                                const double* scalars, int nscalars,
+                                int64_t n, int flags,
+                                void* workspace, size_t workspace_bytes,
+                                const salt_exchange* exchange,
+                                void* out_dev, void* out_host, void* stream);
+
+/* Test hook: `world` thread blocks of ONE cooperative launch play the ranks
+ * of the exchange protocol for `rounds` consecutive epochs (epoch0 ...),
+ * each block publishing totals[r*world + rank] ({hi, lo} pairs) and writing
+ * the folded result to results[r*world + rank].  scratch: zeroed device
+ * memory of world * SALT_XCHG_BUFFER_BYTES bytes. */
+int salt_exchange_emulate(int world, int rounds, uint64_t epoch0,
+                          const void* totals_dev, void* results_dev,
+                          void* scratch_dev, void* stream);
+
 /* Host-buffer (end-to-end) variants: leaves / dst are HOST pointers (pinned
  * memory for full speed).  Chunks are streamed H2D -> fused kernel -> D2H
  * through `staging` (device memory, caller-owned) on three caller streams

@@ -43,6 +43,9 @@ HEADER_SYMBOLS = (
     "salt_reduce_host",
     "salt_assign_reduce_host",
     "salt_reduce_workspace_bytes",
+    "salt_reduce_exchange",
+    "salt_assign_reduce_exchange",
+    "salt_exchange_emulate",
     "salt_signature_kind",
     "salt_prepare",
     "salt_set_force_jit",
@@ -86,6 +89,17 @@ _SIGNATURES = {
          _c_vpp, _c_vp],
     ),
     "salt_reduce_workspace_bytes": (_c_size, []),
+    "salt_reduce_exchange": (
+        _c_int,
+        [_c_int, _c_str, _c_vpp, _c_int, _c_dp, _c_int, _c_i64, _c_int, _c_vp, _c_size, _c_vp, _c_vp,
+         _c_vp, _c_vp],
+    ),
+    "salt_assign_reduce_exchange": (
+        _c_int,
+        [_c_int, _c_str, _c_str, _c_vp, _c_vpp, _c_int, _c_dp, _c_int, _c_i64, _c_int, _c_vp, _c_size,
+         _c_vp, _c_vp, _c_vp, _c_vp],
+    ),
+    "salt_exchange_emulate": (_c_int, [_c_int, _c_int, ctypes.c_uint64, _c_vp, _c_vp, _c_vp, _c_vp]),
     "salt_signature_kind": (_c_int, [_c_int, _c_str, _c_str, _c_int]),
     "salt_prepare": (_c_int, [_c_int, _c_str, _c_str, _c_int]),
     "salt_set_force_jit": (None, [_c_int]),
@@ -93,6 +107,24 @@ _SIGNATURES = {
     "salt_last_error": (_c_str, []),
     "salt_abi_version": (_c_int, []),
 }
+
+XCHG_MAX_RANKS = 8
+XCHG_BUFFER_BYTES = 512
+
+
+class Exchange(ctypes.Structure):
+    """salt_exchange (include/salt.h): NVLink peer-memory exchange descriptor."""
+
+    _fields_ = [
+        ("rank", ctypes.c_int32),
+        ("world", ctypes.c_int32),
+        ("epoch", ctypes.c_uint64),
+        ("slots", ctypes.c_void_p * XCHG_MAX_RANKS),
+        ("flags", ctypes.c_void_p * XCHG_MAX_RANKS),
+        ("timeout_ns", ctypes.c_uint64),
+        ("error", ctypes.c_void_p),
+    ]
+
 
 _lock = threading.Lock()
 _lib = None

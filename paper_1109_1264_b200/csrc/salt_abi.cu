@@ -507,7 +507,7 @@ int make_plan(int dtype, const char* asig, const char* rsig, int mode, int nleav
 template <class T>
 int run_fused(Plan& p, void* dst, const void* const* leaves, int nleaves,
               const double* scalars, int nscalars, i64 n, int flags, void* ws, size_t ws_bytes,
-              void* out_dev, void* out_host, cudaStream_t st) {
+              void* out_dev, void* out_host, cudaStream_t st, const salt_exchange* x) {
   if (n < 0) return fail(SALT_EINVAL, "negative length");
   const bool reduce = p.mode != salt::MODE_ASSIGN;
   if (!reduce && n == 0) return 0;  // zero length assign is a no-op (test_engine.py:147-153)
@@ -566,6 +566,22 @@ int run_fused(Plan& p, void* dst, const void* const* leaves, int nleaves,
     a.group_partials = (salt::DD*)(w + salt::WsLayout::group_partials);
     a.partials = (salt::DD*)(w + salt::WsLayout::partials);
     a.out = out_dev;
+    if (x) {
+      if (x->world < 1 || x->world > salt::XCHG_MAX_RANKS || x->rank < 0 || x->rank >= x->world ||
+          x->epoch == 0)
+        return fail(SALT_EINVAL, "bad exchange descriptor (world 1..8, 0 <= rank < world, epoch >= 1)");
+      if (flags & SALT_PARTIAL) return fail(SALT_EINVAL, "SALT_PARTIAL cannot be combined with an exchange");
+      a.xchg.rank = x->rank;
+      a.xchg.world = x->world;
+      a.xchg.epoch = x->epoch;
+      for (int r = 0; r < x->world; ++r) {
+        if (!x->slots[r] || !x->flags[r]) return fail(SALT_EINVAL, "NULL exchange buffer");
+        a.xchg.slots[r] = (salt::DD*)x->slots[r];
+        a.xchg.flags[r] = (unsigned long long*)x->flags[r];
+      }
+      a.xchg.timeout_ns = x->timeout_ns;
+      a.xchg.error = (unsigned int*)x->error;
+    }
   }
   rc = launch<T>(k, dev, grid, a, st);
   if (rc) return rc;
@@ -579,12 +595,12 @@ int run_fused(Plan& p, void* dst, const void* const* leaves, int nleaves,
 
 int dispatch(int dtype, Plan& p, void* dst, const void* const* leaves, int nleaves,
              const double* scalars, int nscalars, i64 n, int flags, void* ws, size_t ws_bytes,
-             void* out_dev, void* out_host, cudaStream_t st) {
+             void* out_dev, void* out_host, cudaStream_t st, const salt_exchange* x = nullptr) {
   if (dtype == SALT_F32)
     return run_fused<float>(p, dst, leaves, nleaves, scalars, nscalars, n, flags, ws, ws_bytes,
-                            out_dev, out_host, st);
+                            out_dev, out_host, st, x);
   return run_fused<double>(p, dst, leaves, nleaves, scalars, nscalars, n, flags, ws, ws_bytes,
-                           out_dev, out_host, st);
+                           out_dev, out_host, st, x);
 }
 
 template <class T>
@@ -770,6 +786,52 @@ int salt_assign_reduce(int dtype, const char* assign_sig, const char* reduce_sig
   if (rc) return rc;
   return dispatch(dtype, *p, dst, leaves, nleaves, scalars, nscalars, n, flags, workspace,
                   workspace_bytes, out_dev, out_host, (cudaStream_t)stream);
+}
+
+int salt_reduce_exchange(int dtype, const char* sig, const void* const* leaves, int nleaves,
+                         const double* scalars, int nscalars, int64_t n, int flags, void* workspace,
+                         size_t workspace_bytes, const salt_exchange* exchange, void* out_dev,
+                         void* out_host, void* stream) {
+  if (!exchange) return fail(SALT_EINVAL, "NULL exchange descriptor");
+  Plan* p;
+  int rc = make_plan(dtype, nullptr, sig, salt::MODE_REDUCE, nleaves, nscalars, p);
+  if (rc) return rc;
+  return dispatch(dtype, *p, nullptr, leaves, nleaves, scalars, nscalars, n, flags, workspace,
+                  workspace_bytes, out_dev, out_host, (cudaStream_t)stream, exchange);
+}
+
+int salt_assign_reduce_exchange(int dtype, const char* assign_sig, const char* reduce_sig,
+                                void* dst, const void* const* leaves, int nleaves,
+                                const double* scalars, int nscalars, int64_t n, int flags,
+                                void* workspace, size_t workspace_bytes,
+                                const salt_exchange* exchange, void* out_dev, void* out_host,
+                                void* stream) {
+  if (!exchange) return fail(SALT_EINVAL, "NULL exchange descriptor");
+  Plan* p;
+  int rc = make_plan(dtype, assign_sig, reduce_sig, salt::MODE_ASSIGN_REDUCE, nleaves, nscalars, p);
+  if (rc) return rc;
+  return dispatch(dtype, *p, dst, leaves, nleaves, scalars, nscalars, n, flags, workspace,
+                  workspace_bytes, out_dev, out_host, (cudaStream_t)stream, exchange);
+}
+
+int salt_exchange_emulate(int world, int rounds, uint64_t epoch0, const void* totals_dev,
+                          void* results_dev, void* scratch_dev, void* stream) {
+  if (world < 1 || world > salt::XCHG_MAX_RANKS || rounds < 1 || epoch0 == 0 || !totals_dev ||
+      !results_dev || !scratch_dev)
+    return fail(SALT_EINVAL, "bad exchange emulation arguments");
+  // scratch: per rank 512 bytes: [DD slots 2 x 8 | u64 flags 8]; the kernel
+  // takes the slot arrays first, then the flag arrays, so lay them out apart.
+  salt::DD* slots = (salt::DD*)scratch_dev;
+  unsigned long long* flags =
+      (unsigned long long*)((char*)scratch_dev + (size_t)world * 2 * salt::XCHG_MAX_RANKS * sizeof(salt::DD));
+  const salt::DD* totals = (const salt::DD*)totals_dev;
+  salt::DD* results = (salt::DD*)results_dev;
+  unsigned long long e0 = epoch0;
+  void* params[] = {(void*)&totals, (void*)&results, (void*)&slots, (void*)&flags, &world, &rounds, &e0};
+  SALT_CUDA(cudaLaunchCooperativeKernel((const void*)&salt::exchange_emulate_kernel, dim3(world),
+                                        dim3(32), params, 0, (cudaStream_t)stream));
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return 0;
 }
 
 int salt_reduce_finish(int dtype, const void* partials_dev, int count, int flags, void* out_dev,

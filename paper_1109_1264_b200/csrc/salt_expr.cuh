@@ -94,6 +94,21 @@ enum { FLAG_SQRT = 1, FLAG_PARTIAL = 2 };
 
 struct DD { double hi, lo; };  // double-double partial (same layout as double2)
 
+// Cross-GPU exchange of per-rank totals over NVLink peer memory (sharded
+// reductions).  Every rank owns a small symmetric buffer: slots DD[2][8]
+// (double-buffered by epoch parity) followed by flags u64[8].  slots[p] /
+// flags[p] are rank p's buffers mapped into this process (peer pointers;
+// p == rank is the local one).  world == 0 disables the exchange.
+enum { XCHG_MAX_RANKS = 8 };
+struct Xchg {
+  int rank, world;
+  unsigned long long epoch;            // >= 1, +1 per exchange, same on all ranks
+  DD* slots[XCHG_MAX_RANKS];
+  unsigned long long* flags[XCHG_MAX_RANKS];
+  unsigned long long timeout_ns;       // 0: wait forever
+  unsigned int* error;                 // set to 1 on timeout (local memory)
+};
+
 // One by-value parameter block shared by AOT and JIT kernels.
 template <class T> struct Args {
   T* dst;                         // assign modes
@@ -110,6 +125,7 @@ template <class T> struct Args {
   unsigned int* ticket;           // arrival counter of the groups (zeroed, self-resetting)
   void* out;                      // T result or DD partial
   int flags;
+  Xchg xchg;                      // sharded reductions over NVLink (world 0: off)
 };
 
 // Reduction workspace: [ticket | group tickets | group partials | CTA partials].
@@ -246,6 +262,58 @@ template <> struct Acc<float> {
   __device__ __forceinline__ void add(float v) { hi = __dadd_rn(hi, (double)v); }
   __device__ __forceinline__ DD get() const { DD r; r.hi = hi; r.lo = 0.0; return r; }
 };
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" :: "l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Publish `mine` to every rank, wait for every rank's value of this epoch,
+// and fold them in rank order (identical bits on every rank).  One thread.
+//
+// Ordering: the slot stores to peer p are made visible before the release
+// store of flag[rank] at p (fence.sys); the reader's acquire load of
+// flag[q] orders its slot load after it.  Slots alternate by epoch parity: a
+// rank can only reach epoch e+2 after every rank has published e+1, which
+// each does only after finishing its epoch-e reads, so a slot is never
+// overwritten while it is still being read.
+__device__ DD exchange_dd(DD mine, const Xchg& x) {
+  const int par = (int)(x.epoch & 1ull);
+  for (int p = 0; p < x.world; ++p) {
+    volatile DD* dst = (volatile DD*)(x.slots[p] + par * XCHG_MAX_RANKS + x.rank);
+    dst->hi = mine.hi;
+    dst->lo = mine.lo;
+  }
+  __threadfence_system();
+  for (int p = 0; p < x.world; ++p) st_release_sys(x.flags[p] + x.rank, x.epoch);
+  DD acc; acc.hi = 0.0; acc.lo = 0.0;
+  const unsigned long long t0 = x.timeout_ns ? globaltimer_ns() : 0ull;
+  for (int q = 0; q < x.world; ++q) {
+    while (ld_acquire_sys(x.flags[x.rank] + q) < x.epoch) {
+      if (x.timeout_ns && globaltimer_ns() - t0 > x.timeout_ns) {
+        if (x.error) *x.error = 1u;
+        acc.hi = __longlong_as_double(0x7ff8000000000000ll);  // NaN: the peer never arrived
+        acc.lo = 0.0;
+        return acc;
+      }
+    }
+    volatile DD* src = (volatile DD*)(x.slots[x.rank] + par * XCHG_MAX_RANKS + q);
+    DD v;
+    v.hi = src->hi;
+    v.lo = src->lo;
+    acc = dd_add(acc, v);
+  }
+  return acc;
+}
 
 template <int BLOCK> __device__ __forceinline__ DD block_reduce_dd(DD v, DD* smem) {
 #pragma unroll
@@ -411,20 +479,57 @@ __global__ void __launch_bounds__(BLOCK) fused_kernel(Args<T> a) {
     __syncthreads();
     DD tot = block_reduce_dd<BLOCK>(w, smem);
     if (threadIdx.x == 0) {
-      finish_store<T>(tot, a.flags, a.out);
       *a.ticket = 0u;  // ready for the next launch on this workspace
+      // Sharded reduction: trade this rank's total with the other ranks over
+      // NVLink peer memory inside this same kernel — no separate collective.
+      if (a.xchg.world > 0) tot = exchange_dd(tot, a.xchg);
+      finish_store<T>(tot, a.flags, a.out);
     }
   }
 }
 
 // Combine `count` partials (all-gathered per-device DD values, rank order).
+// Up to XCHG_MAX_RANKS partials are folded sequentially in rank order — the
+// same arithmetic as exchange_dd, so the NCCL all-gather path and the NVLink
+// exchange path give identical bits.
 template <class T, int BLOCK>
 __global__ void __launch_bounds__(BLOCK) finish_kernel(const DD* parts, int count, int flags, void* out) {
   __shared__ DD smem[BLOCK / 32];
+  if (count <= XCHG_MAX_RANKS) {
+    if (threadIdx.x == 0) {
+      DD v; v.hi = 0.0; v.lo = 0.0;
+      for (int b = 0; b < count; ++b) v = dd_add(v, parts[b]);
+      finish_store<T>(v, flags, out);
+    }
+    return;
+  }
   DD v; v.hi = 0.0; v.lo = 0.0;
   for (int b = threadIdx.x; b < count; b += BLOCK) v = dd_add(v, parts[b]);
   DD tot = block_reduce_dd<BLOCK>(v, smem);
   if (threadIdx.x == 0) finish_store<T>(tot, flags, out);
+}
+
+// Single-GPU emulation of the exchange protocol for testing: block r plays
+// rank r (all `world` blocks are co-resident: cooperative launch), with
+// per-rank buffers in one allocation; `rounds` consecutive epochs reuse the
+// buffers exactly like consecutive sharded reductions do.
+__global__ void exchange_emulate_kernel(const DD* totals, DD* results, DD* slots,
+                                        unsigned long long* flags, int world, int rounds,
+                                        unsigned long long epoch0) {
+  if (threadIdx.x != 0) return;
+  Xchg x;
+  x.rank = blockIdx.x;
+  x.world = world;
+  x.timeout_ns = 10000000000ull;
+  x.error = nullptr;
+  for (int p = 0; p < world; ++p) {
+    x.slots[p] = slots + p * 2 * XCHG_MAX_RANKS;
+    x.flags[p] = flags + p * XCHG_MAX_RANKS;
+  }
+  for (int r = 0; r < rounds; ++r) {
+    x.epoch = epoch0 + r;
+    results[r * world + x.rank] = exchange_dd(totals[r * world + x.rank], x);
+  }
 }
 
 }  // namespace salt

@@ -285,16 +285,27 @@ def _result(dt, out, host, lazy):
     return np.frombuffer(bytes(host)[: dt.itemsize], dtype=dt)[0]
 
 
-def _device_reduce(dev, dt, call, flags, lazy, sharded=None):
-    """call(flags, ws, out_dev, out_host, stream) -> rc, on device `dev`."""
+def _device_reduce(dev, dt, call, flags, lazy, sharded=None, xcall=None):
+    """call(flags, ws, wsb, out_dev, out_host, stream) -> rc on device `dev`;
+    xcall(..., exchange, out_dev, out_host, stream) is the NVLink-exchange
+    variant used for sharded operands when peer memory is available."""
     lib = _native.lib()
     stream = _raw_stream(dev)
     ws = _workspace(dev, stream)
     out = torch.empty(1, dtype=torch.float64, device=torch.device("cuda", dev))
     host = None if lazy else (ctypes.c_double * 2)()
     hptr = ctypes.addressof(host) if host is not None else None
+    xchg = None
+    if sharded is not None and xcall is not None:
+        from .sharding import peer_exchange
+
+        xchg = peer_exchange(sharded.group, torch.device("cuda", dev))
     if sharded is None:
         _native.check(call(flags, ws.data_ptr(), ws.numel(), out.data_ptr(), hptr, stream))
+    elif xchg is not None:
+        desc = xchg.next()
+        _native.check(xcall(flags, ws.data_ptr(), ws.numel(), ctypes.addressof(desc),
+                            out.data_ptr(), hptr, stream))
     else:
         part = torch.empty(2, dtype=torch.float64, device=out.device)
         _native.check(call(flags | _native.SALT_PARTIAL, ws.data_ptr(), ws.numel(), part.data_ptr(),
@@ -305,7 +316,7 @@ def _device_reduce(dev, dt, call, flags, lazy, sharded=None):
     return _result(dt, out, host, lazy)
 
 
-def _run_reduction(lw, dest, dt, n, flags, lazy, make_call, host_call):
+def _run_reduction(lw, dest, dt, n, flags, lazy, make_call, host_call, make_xcall=None):
     """Fast path / placement for a reduction-producing call; `host_call` runs
     it on pinned host vectors (streamed through the GPU)."""
     fast = _fast(lw.vectors, dest)
@@ -325,9 +336,10 @@ def _run_reduction(lw, dest, dt, n, flags, lazy, make_call, host_call):
                                                 pl.dest_pointer))
         result = np.frombuffer(bytes(host)[: dt.itemsize], dtype=dt)[0]
     else:
+        xcall = make_xcall(leaves, pl.dest_pointer, pl.n) if make_xcall is not None else None
         with _OnDevice(pl.device.index):
             result = _device_reduce(pl.device.index, dt, make_call(leaves, pl.dest_pointer, pl.n),
-                                    flags, lazy, pl.sharded)
+                                    flags, lazy, pl.sharded, xcall)
     pl.finish()
     _record_counts(lw, dest, n)
     return result
@@ -348,7 +360,11 @@ def run_reduce(lw, dtype, n, flags=0, lazy=False):
     def host_call(leaves, m, st, sb, sp, out, _dptr):
         return lib.salt_reduce_host(code, sig, leaves, nl, scal, ns, m, flags, st, sb, sp, out)
 
-    return _run_reduction(lw, None, dt, n, flags, lazy, make_call, host_call)
+    def make_xcall(leaves, _dptr, m):
+        return lambda fl, ws, wsb, x, od, oh, st: lib.salt_reduce_exchange(
+            code, sig, leaves, nl, scal, ns, m, fl, ws, wsb, x, od, oh, st)
+
+    return _run_reduction(lw, None, dt, n, flags, lazy, make_call, host_call, make_xcall)
 
 
 def run_assign_reduce(lwa, lwr, dest, dtype, n, flags=0, lazy=False):
@@ -368,4 +384,8 @@ def run_assign_reduce(lwa, lwr, dest, dtype, n, flags=0, lazy=False):
         return lib.salt_assign_reduce_host(code, asig, rsig, dptr, leaves, nl, scal, ns, m, flags,
                                            st, sb, sp, out)
 
-    return _run_reduction(lwa, dest, dt, n, flags, lazy, make_call, host_call)
+    def make_xcall(leaves, dptr, m):
+        return lambda fl, ws, wsb, x, od, oh, st: lib.salt_assign_reduce_exchange(
+            code, asig, rsig, dptr, leaves, nl, scal, ns, m, fl, ws, wsb, x, od, oh, st)
+
+    return _run_reduction(lwa, dest, dt, n, flags, lazy, make_call, host_call, make_xcall)

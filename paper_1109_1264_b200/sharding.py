@@ -8,11 +8,25 @@ into contiguous blocks, one per rank:
     multiple of 64 elements, so every block base stays 256-byte aligned.
 
 Elementwise trees over ShardedVectors run on each rank's block with no
-communication.  Reductions compute one double-double partial per rank
-(SALT_PARTIAL), all-gather the partials (a 16-byte NCCL all-gather over
-NVLink/NVSwitch, or gloo on CPU), and every rank combines them in rank order
-(salt_reduce_finish) — deterministic and identical on all ranks.
+communication.  Reductions exchange one double-double total per rank and
+every rank folds them in rank order — deterministic and identical on all
+ranks — by one of two routes:
+
+  peer  (default on GPUs with symmetric memory): the reduction kernel's last
+        CTA writes its total straight into every peer's symmetric buffer
+        over NVLink, raises a flag there, waits for all peers' flags and
+        folds — the collective happens inside the reduction kernel
+        (salt_reduce_exchange), no NCCL launch, no host involvement;
+  nccl  (fallback, and gloo on CPU): the kernel writes its partial
+        (SALT_PARTIAL), a 16-byte all-gather collects them, and
+        salt_reduce_finish folds them.
+
+Both fold the same values in the same order, so they give identical bits.
+SALT_EXCHANGE=nccl forces the fallback.
 """
+
+import os
+import threading
 
 import numpy as np
 import torch
@@ -37,6 +51,71 @@ def shard_bounds(n: int, world: int, rank: int, align: int = SHARD_ALIGN):
     lo = min(n, rank * per)
     hi = min(n, lo + per)
     return lo, hi
+
+
+class PeerExchange:
+    """Symmetric NVLink buffers + epoch counter of one process group on one
+    device (torch symmetric memory supplies the peer mappings)."""
+
+    TIMEOUT_NS = 60_000_000_000  # a peer that never arrives yields NaN, not a hang
+
+    def __init__(self, group, device):
+        import torch.distributed._symmetric_memory as symm_mem
+
+        from ._native import XCHG_BUFFER_BYTES, XCHG_MAX_RANKS, Exchange
+
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        if self.world > XCHG_MAX_RANKS:
+            raise ValueError(f"peer exchange supports up to {XCHG_MAX_RANKS} ranks")
+        name = (group or dist.group.WORLD).group_name
+        try:
+            symm_mem.enable_symm_mem_for_group(name)
+        except Exception:  # newer torch enables it on demand
+            pass
+        self.buffer = symm_mem.empty(XCHG_BUFFER_BYTES // 8, dtype=torch.int64, device=device)
+        self.buffer.zero_()
+        self.error = torch.zeros(1, dtype=torch.int32, device=device)
+        torch.cuda.synchronize(device)
+        self.handle = symm_mem.rendezvous(self.buffer, name)
+        dist.barrier(group)
+        ptrs = list(self.handle.buffer_ptrs)
+        self.desc = Exchange()
+        self.desc.rank = self.rank
+        self.desc.world = self.world
+        self.desc.timeout_ns = self.TIMEOUT_NS
+        self.desc.error = self.error.data_ptr()
+        for p, base in enumerate(ptrs):
+            self.desc.slots[p] = base                     # DD[2][8]
+            self.desc.flags[p] = base + 2 * XCHG_MAX_RANKS * 16  # u64[8]
+        self.epoch = 0
+
+    def next(self):
+        """Descriptor for the next exchange (epochs advance in SPMD order)."""
+        self.epoch += 1
+        self.desc.epoch = self.epoch
+        return self.desc
+
+
+_exchanges = {}
+_exchange_lock = threading.Lock()
+
+
+def peer_exchange(group, device):
+    """The PeerExchange of (group, device), or None when peer exchange is
+    unavailable or disabled (then reductions use the NCCL all-gather)."""
+    if os.environ.get("SALT_EXCHANGE", "peer") != "peer" or device.type != "cuda":
+        return None
+    if not (dist.is_available() and dist.is_initialized()):
+        return None
+    key = (id(group), device.index)
+    with _exchange_lock:
+        if key not in _exchanges:
+            try:
+                _exchanges[key] = PeerExchange(group, device)
+            except Exception:
+                _exchanges[key] = None
+        return _exchanges[key]
 
 
 def _world(group):

@@ -170,10 +170,7 @@ def test_sharded_vector_world1_through_public_api():
     assert lv.norm2(X) == np.sqrt(np.float64(lv.dot(X, X)))
 
 
-def test_sharded_path_under_torchrun_nccl():
-    """tools/dist_check.py under torchrun (one process per visible GPU; one
-    here): NCCL process group, per-rank partials all-gathered over NCCL,
-    fixed-order finish — checked against the oracle."""
+def _torchrun_dist_check(exchange):
     import json
     import socket
     import subprocess
@@ -186,11 +183,50 @@ def test_sharded_path_under_torchrun_nccl():
     port = s.getsockname()[1]
     s.close()
     ngpu = torch.cuda.device_count()
+    env = {**os.environ, "SALT_EXCHANGE": exchange}
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
                         f"--nproc-per-node={ngpu}", "--master-addr", "127.0.0.1", "--master-port",
                         str(port), str(root / "tools" / "dist_check.py")],
-                       capture_output=True, text=True, timeout=600, cwd=root)
+                       capture_output=True, text=True, timeout=600, cwd=root, env=env)
     assert r.returncode == 0, r.stderr[-3000:]
     line = [ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1]
     res = json.loads(line)
     assert res["ok"] and res["world"] == ngpu, res
+    return res
+
+
+def test_sharded_path_under_torchrun_peer_and_nccl_agree():
+    """tools/dist_check.py under torchrun (one process per visible GPU; one
+    here), once with the in-kernel NVLink peer exchange and once with the
+    NCCL all-gather fallback: both pass the oracle checks and give the same
+    bits."""
+    peer = _torchrun_dist_check("peer")
+    nccl = _torchrun_dist_check("nccl")
+    assert peer["values"] == nccl["values"]
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 4, 8])
+def test_exchange_protocol_emulated_on_one_gpu(world):
+    """The NVLink exchange protocol (publish to every peer, release flag,
+    acquire-wait all flags, fold in rank order; epoch-parity double
+    buffering) with `world` ranks played by the blocks of ONE cooperative
+    launch, over 64 consecutive epochs: every rank gets the same bits, equal
+    to the rank-order fold salt_reduce_finish computes."""
+    lib = _native.lib()
+    rounds = 64
+    g = np.random.default_rng(world)
+    hi = g.standard_normal((rounds, world)) * 1e3
+    lo = hi * 1e-17 * g.standard_normal((rounds, world))
+    totals = torch.tensor(np.stack([hi, lo], axis=-1).reshape(-1), dtype=torch.float64, device="cuda")
+    results = torch.zeros(rounds * world * 2, dtype=torch.float64, device="cuda")
+    scratch = torch.zeros(world * _native.XCHG_BUFFER_BYTES, dtype=torch.uint8, device="cuda")
+    stream = torch.cuda.current_stream().cuda_stream
+    _native.check(lib.salt_exchange_emulate(world, rounds, 1, totals.data_ptr(), results.data_ptr(),
+                                            scratch.data_ptr(), stream))
+    res = results.view(rounds, world, 2).cpu().numpy()
+    out = torch.empty(1, dtype=torch.float64, device="cuda")
+    for r in range(rounds):
+        assert all(res[r, k].tobytes() == res[r, 0].tobytes() for k in range(world)), r
+        _native.check(lib.salt_reduce_finish(1, totals[r * world * 2:].data_ptr(), world, 0,
+                                             out.data_ptr(), None, stream))
+        assert np.float64(res[r, 0, 0] + res[r, 0, 1]) == out.item(), r

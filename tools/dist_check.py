@@ -65,6 +65,8 @@ def main():
         res = dict(zip(["elementwise", "dot", "norm2", "axpy_dot", "identical_on_ranks"],
                        [bool(v) for v in flags.tolist()]))
         res["world"] = world
+        res["values"] = [float(r).hex(), float(nr).hex(), float(rr).hex()]
+        res["exchange"] = os.environ.get("SALT_EXCHANGE", "peer")
         res["ok"] = all(res[k] for k in ("elementwise", "dot", "norm2", "axpy_dot", "identical_on_ranks"))
         print(json.dumps(res), flush=True)
     dist.destroy_process_group()
