@@ -17,10 +17,14 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+#include <sys/stat.h>
+#include <unistd.h>
 
 #include <atomic>
 #include <cstdio>
 #include <cstring>
+#include <fstream>
+#include <sstream>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -319,6 +323,50 @@ void ensure_table() {
 }
 
 // Compile the tree with NVRTC; returns nullptr + g_err on failure.
+// On-disk cubin cache for JIT kernels: $SALT_JIT_CACHE (default
+// ~/.cache/salt_jit; "off" disables), one file per (source, options, kernel)
+// hash holding the lowered name and the cubin.  Only a start-up cost saver:
+// a miss simply compiles.
+std::string jit_cache_dir() {
+  const char* e = getenv("SALT_JIT_CACHE");
+  if (e && std::string(e) == "off") return "";
+  if (e && *e) return e;
+  const char* home = getenv("HOME");
+  return home ? std::string(home) + "/.cache/salt_jit" : "";
+}
+
+uint64_t fnv1a(const std::string& s, uint64_t h = 1469598103934665603ull) {
+  for (unsigned char c : s) h = (h ^ c) * 1099511628211ull;
+  return h;
+}
+
+bool jit_cache_load(const std::string& path, Kernel& k) {
+  std::ifstream f(path, std::ios::binary);
+  if (!f) return false;
+  std::string name;
+  if (!std::getline(f, name) || name.empty()) return false;
+  std::stringstream ss;
+  ss << f.rdbuf();
+  std::string bin = ss.str();
+  if (bin.size() < 16) return false;
+  k.lowered = name;
+  k.cubin = bin;
+  return true;
+}
+
+void jit_cache_store(const std::string& dir, const std::string& path, const Kernel& k) {
+  mkdir(dir.c_str(), 0755);  // parent of the default dir: ~/.cache
+  std::string tmp = path + ".tmp" + std::to_string(getpid());
+  {
+    std::ofstream f(tmp, std::ios::binary);
+    if (!f) return;
+    f << k.lowered << "\n";
+    f.write(k.cubin.data(), (std::streamsize)k.cubin.size());
+    if (!f) return;
+  }
+  rename(tmp.c_str(), path.c_str());
+}
+
 Kernel* jit_compile(int dtype, int mode, int vec, int nl, const std::string& ta,
                     const std::string& tr, const std::string& key) {
   Nvrtc& nv = nvrtc();
@@ -328,15 +376,36 @@ Kernel* jit_compile(int dtype, int mode, int vec, int nl, const std::string& ta,
   std::string expr = std::string("salt::fused_kernel<") + tname + "," + ta + "," + tr + "," +
                      std::to_string(mode) + "," + std::to_string(vec) + "," +
                      std::to_string(unroll) + "," + std::to_string(kBlock) + ">";
+  const char* opts[] = {"--gpu-architecture=sm_100a", "-fmad=false", "--std=c++17",
+                        "-lineinfo", "-default-device", "-DSALT_NO_256BIT"};
+  const int nopts = nv.has_256bit ? 5 : 6;
+  std::string cache_path;
+  const std::string cdir = jit_cache_dir();
+  if (!cdir.empty()) {
+    std::string id = expr;
+    for (int i = 0; i < nopts; ++i) id += std::string("|") + opts[i];
+    int maj = 0, min = 0;
+    nv.Version(&maj, &min);
+    id += "|nvrtc" + std::to_string(maj) + "." + std::to_string(min);
+    char hex[32];
+    snprintf(hex, sizeof hex, "%016llx", (unsigned long long)fnv1a(id, fnv1a(kExprSource)));
+    cache_path = cdir + "/" + hex + ".salt";
+    auto k = std::make_unique<Kernel>();
+    if (jit_cache_load(cache_path, *k)) {
+      k->vec = vec;
+      k->unroll = unroll;
+      Kernel* raw = k.get();
+      jit_table()[key] = std::move(k);
+      return raw;
+    }
+  }
   void* prog = nullptr;
   if (nv.CreateProgram(&prog, kExprSource, "salt_expr_jit.cu", 0, nullptr, nullptr) != 0) {
     g_err = "nvrtcCreateProgram failed";
     return nullptr;
   }
   nv.AddNameExpression(prog, expr.c_str());
-  const char* opts[] = {"--gpu-architecture=sm_100a", "-fmad=false", "--std=c++17",
-                        "-lineinfo", "-default-device", "-DSALT_NO_256BIT"};
-  int rc = nv.CompileProgram(prog, nv.has_256bit ? 5 : 6, opts);
+  int rc = nv.CompileProgram(prog, nopts, opts);
   if (rc != 0) {
     size_t ls = 0;
     nv.GetProgramLogSize(prog, &ls);
@@ -357,6 +426,11 @@ Kernel* jit_compile(int dtype, int mode, int vec, int nl, const std::string& ta,
   nv.DestroyProgram(&prog);
   k->vec = vec;
   k->unroll = unroll;
+  if (!cache_path.empty()) {
+    std::string parent = cdir.substr(0, cdir.find_last_of('/'));
+    if (!parent.empty()) mkdir(parent.c_str(), 0755);
+    jit_cache_store(cdir, cache_path, *k);
+  }
   Kernel* raw = k.get();
   jit_table()[key] = std::move(k);
   return raw;

@@ -202,6 +202,8 @@ def test_sharded_path_under_torchrun_peer_and_nccl_agree():
     bits."""
     peer = _torchrun_dist_check("peer")
     nccl = _torchrun_dist_check("nccl")
+    assert peer["peer_exchange_active"] and peer["peer_epochs"] == 3  # dot, norm2, axpy_dot
+    assert not nccl["peer_exchange_active"]
     assert peer["values"] == nccl["values"]
 
 

@@ -103,3 +103,22 @@ def test_nvrtc_instantiates_arbitrary_trees_without_a_gpu():
         assert lib.salt_prepare(dt, b"L0 L1 - L2 L3 + *", None, 1) == 0, lib.salt_last_error()
         assert lib.salt_prepare(dt, b"L0 L1 +", b"D D *", 2) == 0, lib.salt_last_error()
     assert lib.salt_prepare(1, b"L0 +", None, 0) == -1
+
+
+def test_jit_disk_cache(tmp_path):
+    """JIT cubins are cached on disk (SALT_JIT_CACHE); a second process loads
+    them instead of recompiling."""
+    import os
+    import sys
+
+    code = ("import time; from paper_1109_1264_b200 import _native; l = _native.lib(); "
+            "t = time.time(); assert l.salt_prepare(0, b'L0 L1 - L0 * L2 -', None, 0) == 0; "
+            "print(time.time() - t)")
+    env = {**os.environ, "SALT_JIT_CACHE": str(tmp_path / "jit")}
+    first = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                           cwd=ROOT, check=True)
+    files = sorted((tmp_path / "jit").glob("*.salt"))
+    assert len(files) == 2  # vector and scalar-lane variants
+    second = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                            cwd=ROOT, check=True)
+    assert float(second.stdout) < float(first.stdout)

@@ -67,6 +67,11 @@ def main():
         res["world"] = world
         res["values"] = [float(r).hex(), float(nr).hex(), float(rr).hex()]
         res["exchange"] = os.environ.get("SALT_EXCHANGE", "peer")
+        from paper_1109_1264_b200 import sharding
+
+        ex = [e for e in sharding._exchanges.values() if e is not None]
+        res["peer_exchange_active"] = bool(ex)
+        res["peer_epochs"] = ex[0].epoch if ex else 0
         res["ok"] = all(res[k] for k in ("elementwise", "dot", "norm2", "axpy_dot", "identical_on_ranks"))
         print(json.dumps(res), flush=True)
     dist.destroy_process_group()
