@@ -441,6 +441,13 @@ __global__ void __launch_bounds__(BLOCK) fused_kernel(Args<T> a) {
     __shared__ DD smem[BLOCK / 32];
     __shared__ int stage;  // 0 done, 1 group finisher, 2 group + final finisher
     DD part = block_reduce_dd<BLOCK>(acc.get(), smem);
+    if (gridDim.x == 1) {  // small n: no partials, no tickets, no fences
+      if (threadIdx.x == 0) {
+        if (a.xchg.world > 0) part = exchange_dd(part, a.xchg);
+        finish_store<T>(part, a.flags, a.out);
+      }
+      return;
+    }
     const unsigned int g = blockIdx.x / GROUP;
     const unsigned int ngroups = (gridDim.x + GROUP - 1) / GROUP;
     const unsigned int gsize = min((unsigned int)GROUP, gridDim.x - g * GROUP);
@@ -461,6 +468,14 @@ __global__ void __launch_bounds__(BLOCK) fused_kernel(Args<T> a) {
     }
     __syncthreads();
     DD q = block_reduce_dd<BLOCK>(v, smem);
+    if (ngroups == 1) {  // one group: its finisher holds the total
+      if (threadIdx.x == 0) {
+        a.group_tickets[g] = 0u;
+        if (a.xchg.world > 0) q = exchange_dd(q, a.xchg);
+        finish_store<T>(q, a.flags, a.out);
+      }
+      return;
+    }
     if (threadIdx.x == 0) {
       a.group_partials[g] = q;
       a.group_tickets[g] = 0u;  // every CTA of the group has arrived

@@ -309,14 +309,30 @@ def combine_partials(rows, remainder):
 
 def common_length(root: Expression) -> int:
     """Length shared by every leaf (the destination included); checked before
-    any element is touched."""
+    any element is touched.  Leaves are visited in the reference's order
+    (destination first, then left to right), so the first mismatch reported
+    is the same one the reference reports."""
     length = None
-    for leaf in root.leaves():
-        n = len(leaf.vector)
-        if length is None:
-            length = n
-        elif n != length:
-            raise LengthMismatchError(f"expression mixes vectors of length {length} and {n}")
+    stack = [root]
+    while stack:
+        node = stack.pop()
+        if isinstance(node, Leaf):
+            n = len(node.vector)
+            if length is None:
+                length = n
+            elif n != length:
+                raise LengthMismatchError(f"expression mixes vectors of length {length} and {n}")
+            continue
+        if isinstance(node, _BinaryNode):
+            stack.append(node.right)
+            stack.append(node.left)
+        elif isinstance(node, (ScaleNode, SumNode)):
+            stack.append(node.child)
+        elif isinstance(node, AssignNode):
+            stack.append(node.source)
+            stack.append(node.dest)
+        else:  # AssignReduceNode and any other composite root
+            stack.extend(reversed(list(node.leaves())))
     if length is None:
         raise TypeError("expression has no vector leaves")
     return length
