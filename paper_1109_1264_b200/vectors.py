@@ -112,6 +112,25 @@ class DenseVector:
             raise TypeError(f"unsupported element type {tensor.dtype}; use float32 or float64")
         return cls(tensor, _NP_DTYPES[tensor.dtype])
 
+    @classmethod
+    def from_dlpack(cls, obj) -> "DenseVector":
+        """Zero-copy import of any DLPack producer (CuPy, JAX, NumPy, torch)
+        holding a 1-D contiguous f32/f64 array."""
+        return cls.from_tensor(torch.from_dlpack(obj))
+
+    def __dlpack__(self, **kwargs):
+        return self._data.__dlpack__(**kwargs)
+
+    def __dlpack_device__(self):
+        return self._data.__dlpack_device__()
+
+    @property
+    def __cuda_array_interface__(self):
+        """CUDA array interface (CuPy / Numba) for device-resident vectors."""
+        if self._data.device.type != "cuda":
+            raise AttributeError("host vectors have no __cuda_array_interface__")
+        return self._data.__cuda_array_interface__
+
     # ------------------------------------------------------------ properties
     @property
     def dtype(self) -> np.dtype:

@@ -331,3 +331,17 @@ def test_public_names_cover_reference_surface():
     }
     missing = [n for n in reference_names if not hasattr(lv, n)]
     assert not missing, missing
+
+
+def test_dlpack_round_trip_is_zero_copy():
+    import numpy as np
+
+    a = np.arange(10, dtype=np.float64)
+    v = lv.DenseVector.from_dlpack(a)
+    assert v.to_values() == list(a) and v.dtype == np.float64
+    a[3] = 42.0  # shares memory
+    assert v.get(3) == 42.0
+    back = np.from_dlpack(v)
+    assert back[3] == 42.0
+    with pytest.raises(AttributeError):
+        v.__cuda_array_interface__
