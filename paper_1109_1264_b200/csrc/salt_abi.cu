@@ -308,13 +308,18 @@ void register_aot() {
       "S0 L0 * S1 L1 L2 - * +", nullptr);
   reg<Add<Sub<Mul<S<0>, Add<L<0>, L<1>>>, Mul<S<1>, Sub<L<2>, L<3>>>>, Mul<S<2>, L<0>>>, None,
       A>("S0 L0 L1 + * S1 L2 L3 - * - S2 L0 * +", nullptr);               // C4 e-tree
+  reg<Add<Mul<S<0>, L<0>>, Mul<S<1>, L<1>>>, None, A>("S0 L0 * S1 L1 * +", nullptr);  // axpby
+  reg<Sub<L<0>, Mul<S<0>, L<1>>>, None, A>("L0 S0 L1 * -", nullptr);      // y - a*x (CG residual)
   // --- reductions
   reg<None, L<0>, R>(nullptr, "L0");                                      // sum
   reg<None, Mul<L<0>, L<1>>, R>(nullptr, "L0 L1 *");                      // dot
   reg<None, Mul<L<0>, L<0>>, R>(nullptr, "L0 L0 *");                      // dot(x,x) / nrm2
+  reg<None, Mul<Sub<L<0>, L<1>>, Sub<L<0>, L<1>>>, R>(nullptr, "L0 L1 - L0 L1 - *");  // ||x-y||^2
+  reg<None, Mul<Mul<L<0>, L<1>>, L<2>>, R>(nullptr, "L0 L1 * L2 *");       // weighted dot
   // --- fused assign + reduce (C5: y = y + a*x ; r = dot(y, z))
   reg<Add<L<0>, Mul<S<0>, L<1>>>, Mul<D, L<2>>, AR>("L0 S0 L1 * +", "D L2 *");
   reg<Add<L<0>, Mul<S<0>, L<1>>>, Mul<D, D>, AR>("L0 S0 L1 * +", "D D *");
+  reg<Sub<L<0>, Mul<S<0>, L<1>>>, Mul<D, D>, AR>("L0 S0 L1 * -", "D D *");  // CG: r -= a*q; r.r
 }
 
 void ensure_table() {

@@ -16,7 +16,7 @@ from conftest import NP, golden, same_bits
 from oracle import restate
 from paper_1109_1264_b200 import _native
 from paper_1109_1264_b200.engine import execute_reduce
-from paper_1109_1264_b200.expressions import AssignNode, ScaleNode, SumNode, as_node
+from paper_1109_1264_b200.expressions import AssignNode, AssignReduceNode, ScaleNode, SumNode, as_node
 
 pytestmark = pytest.mark.gpu
 
@@ -176,6 +176,8 @@ def test_aot_and_jit_kernels_agree_bit_for_bit():
             lambda v, d: d.assign(v[0] + (v[1] - v[2])),
             lambda v, d: d.assign(1.25 * v[0] + -0.5 * (v[1] - v[2])),
             lambda v, d: d.assign(1.25 * (v[0] + v[1]) - 0.5 * (v[2] - v[3]) + 0.3 * v[0]),
+            lambda v, d: d.assign(1.25 * v[0] + -0.5 * v[1]),
+            lambda v, d: d.assign(v[0] - 0.75 * v[1]),
         ]
         for k, case in enumerate(cases):
             outs = []
@@ -193,8 +195,13 @@ def test_aot_and_jit_kernels_agree_bit_for_bit():
             lib.salt_set_force_jit(force)
             try:
                 vecs = [dev(a, dt) for a in ops]
+                x0, x1, x2 = (as_node(v) for v in vecs[:3])
+                cg = AssignReduceNode(AssignNode(x1, x1 - ScaleNode(0.5, x0)), SumNode(x1 * x1))
                 r = (lv.dot(vecs[0], vecs[1]), lv.sum(vecs[0]), lv.norm2(vecs[0]),
-                     lv.axpy_dot(0.5, vecs[0], vecs[1], vecs[2]))
+                     lv.axpy_dot(0.5, vecs[0], vecs[1], vecs[2]),
+                     execute_reduce(SumNode((x0 - x1) * (x0 - x1))),
+                     execute_reduce(SumNode(x0 * x1 * x2)),
+                     lv.execute_assign_reduce(cg))
             finally:
                 lib.salt_set_force_jit(0)
             if force == 0:
