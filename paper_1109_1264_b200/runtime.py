@@ -296,7 +296,10 @@ def _device_reduce(dev, dt, call, flags, lazy, sharded=None, xcall=None):
     host = None if lazy else (ctypes.c_double * 2)()
     hptr = ctypes.addressof(host) if host is not None else None
     xchg = None
-    if sharded is not None and xcall is not None:
+    # The peer exchange advances an epoch per call on the host, so it cannot
+    # be baked into a CUDA graph; while capturing, the (capturable) NCCL
+    # all-gather path is used instead — same bits.
+    if sharded is not None and xcall is not None and not torch.cuda.is_current_stream_capturing():
         from .sharding import peer_exchange
 
         xchg = peer_exchange(sharded.group, torch.device("cuda", dev))
