@@ -202,6 +202,9 @@ def measure(op, variant, n, dtype="f32", reps=25, warmup=5, seed=0, flush_l2=Fal
             torch.cuda.synchronize()
             times.append(time.perf_counter() - t0)
         else:
+            # queue ~50 us of GPU work first so the events bracket device time,
+            # not the host's launch latency
+            torch.cuda._sleep(100_000)
             s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             s.record()
             call()
