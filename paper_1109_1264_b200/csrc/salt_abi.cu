@@ -47,6 +47,15 @@ constexpr int kUnrollScalar = 4;  // V == 1 fallback (misaligned operands)
 // streams ~64 KiB before paying its partial/ticket epilogue: 4 tiles for
 // one-leaf trees (nrm2, sum), 2 for two or more leaves (dot, fused axpy->dot).
 // SALT_REDUCE_TILES overrides it (tuning only; read once).
+// Assignments: one tile per CTA (SALT_ASSIGN_TILES overrides; tuning only).
+int assign_tiles_per_cta() {
+  static const int env = [] {
+    const char* e = getenv("SALT_ASSIGN_TILES");
+    return e ? atoi(e) : 0;
+  }();
+  return env > 0 ? env : 1;
+}
+
 int reduce_tiles_per_cta(int nl) {
   static const int env = [] {
     const char* e = getenv("SALT_REDUCE_TILES");
@@ -628,7 +637,7 @@ int run_fused(Plan& p, void* dst, const void* const* leaves, int nleaves,
   // axpy->dot f64 2^28).  Both grids depend only on n.
   const i64 per_tile = (i64)kBlock * k->unroll;
   const i64 ntiles = (a.nvec + per_tile - 1) / per_tile;
-  i64 K = 1, cap = i64(0x7fffffff);
+  i64 K = assign_tiles_per_cta(), cap = i64(0x7fffffff);
   if (reduce) {
     K = reduce_tiles_per_cta(p.nl);
     cap = salt::MAX_REDUCE_CTAS;
