@@ -28,7 +28,7 @@ ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
 
 import paper_1109_1264_b200 as lv  # noqa: E402
-from paper_1109_1264_b200 import _native, synth  # noqa: E402
+from paper_1109_1264_b200 import synth  # noqa: E402
 
 PEAK = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"] if (
     ROOT / "MEASURED_PEAKS.json").exists() else 6650.0
