@@ -264,6 +264,15 @@ template <> struct Acc<float> {
   __device__ __forceinline__ DD get() const { DD r; r.hi = hi; r.lo = 0.0; return r; }
 };
 
+// Ticket increment with acquire-release semantics at GPU scope: it publishes
+// this CTA's partial (release) and, for the CTA that turns out to be last,
+// makes every other CTA's partial visible (acquire) — no separate fences.
+__device__ __forceinline__ unsigned int ticket_add(unsigned int* p) {
+  unsigned int old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(p) : "memory");
+  return old;
+}
+
 __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
   unsigned long long v;
   asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -453,12 +462,10 @@ __global__ void __launch_bounds__(BLOCK) fused_kernel(Args<T> a) {
     const unsigned int gsize = min((unsigned int)GROUP, gridDim.x - g * GROUP);
     if (threadIdx.x == 0) {
       a.partials[blockIdx.x] = part;
-      __threadfence();
-      stage = atomicAdd(&a.group_tickets[g], 1u) == gsize - 1 ? 1 : 0;
+      stage = ticket_add(&a.group_tickets[g]) == gsize - 1 ? 1 : 0;
     }
     __syncthreads();
     if (stage == 0) return;
-    __threadfence();
     DD v; v.hi = 0.0; v.lo = 0.0;
     for (unsigned int b = threadIdx.x; b < gsize; b += BLOCK) {
       DD p;  // L2 loads: other CTAs wrote these during this launch
@@ -479,12 +486,10 @@ __global__ void __launch_bounds__(BLOCK) fused_kernel(Args<T> a) {
     if (threadIdx.x == 0) {
       a.group_partials[g] = q;
       a.group_tickets[g] = 0u;  // every CTA of the group has arrived
-      __threadfence();
-      stage = atomicAdd(a.ticket, 1u) == ngroups - 1 ? 2 : 1;
+      stage = ticket_add(a.ticket) == ngroups - 1 ? 2 : 1;
     }
     __syncthreads();
     if (stage != 2) return;
-    __threadfence();
     DD w; w.hi = 0.0; w.lo = 0.0;
     for (unsigned int b = threadIdx.x; b < ngroups; b += BLOCK) {
       DD p;
