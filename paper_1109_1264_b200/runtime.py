@@ -198,7 +198,15 @@ def _require_cuda() -> torch.device:
     return torch.device("cuda", torch.cuda.current_device())
 
 
+_MAX_CACHED_WORKSPACES = 64
+_TICKET_BYTES = 256 + 4 * 4096  # ticket + group tickets (salt::WsLayout)
+
+
 def _workspace(index: int, stream_ptr: int) -> torch.Tensor:
+    """Reduction scratch of (device, stream): zeroed once, then kept — the
+    kernels reset their tickets themselves, so consecutive reductions on one
+    stream share it safely.  Beyond _MAX_CACHED_WORKSPACES streams a fresh
+    scratch is made per call (tickets zeroed, tied to the stream)."""
     key = (index, stream_ptr)
     ws = _workspaces.get(key)
     if ws is None:
@@ -206,8 +214,14 @@ def _workspace(index: int, stream_ptr: int) -> torch.Tensor:
             ws = _workspaces.get(key)
             if ws is None:
                 nbytes = _native.lib().salt_reduce_workspace_bytes()
-                ws = torch.zeros(nbytes, dtype=torch.uint8, device=torch.device("cuda", index))
-                _workspaces[key] = ws
+                device = torch.device("cuda", index)
+                if len(_workspaces) < _MAX_CACHED_WORKSPACES:
+                    ws = torch.zeros(nbytes, dtype=torch.uint8, device=device)
+                    _workspaces[key] = ws
+                else:
+                    ws = torch.empty(nbytes, dtype=torch.uint8, device=device)
+                    ws[:_TICKET_BYTES].zero_()
+                    ws.record_stream(torch.cuda.current_stream(device))
     return ws
 
 
