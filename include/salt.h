@@ -179,7 +179,10 @@ int salt_assign_reduce_host(int dtype, const char* assign_sig, const char* reduc
                             void* staging, size_t staging_bytes,
                             void* const* streams3, void* out_host);
 
-/* Bytes of device scratch salt_reduce / salt_assign_reduce need. */
+/* Bytes of device scratch salt_reduce / salt_assign_reduce need.  Only the
+ * first SALT_WORKSPACE_TICKET_BYTES (the arrival counters) must be zero
+ * before the first use; the kernels reset them after every reduction. */
+#define SALT_WORKSPACE_TICKET_BYTES 16640
 size_t salt_reduce_workspace_bytes(void);
 
 /* 0 = invalid signature, 1 = compiled-in (AOT) kernel, 2 = needs the NVRTC

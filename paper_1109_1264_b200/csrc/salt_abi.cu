@@ -40,6 +40,8 @@ namespace {
 using salt::i64;
 
 constexpr int kBlock = 256;
+static_assert(SALT_WORKSPACE_TICKET_BYTES == salt::WsLayout::group_partials,
+              "salt.h ticket prefix must match the kernel workspace layout");
 constexpr int kUnrollVec = 2;     // 256-bit vectors in flight per leaf per thread
 constexpr int unroll_for(int /*mode*/, int /*nl*/) { return kUnrollVec; }
 constexpr int kUnrollScalar = 4;  // V == 1 fallback (misaligned operands)
@@ -760,7 +762,7 @@ int host_pipeline(int dtype, Plan& p, void* host_dst, const void* const* host_le
   auto buf = [&](int b, int i) -> void* {
     return bufs + ((size_t)b * nbufs_per_set + i) * chunk * esz;
   };
-  if (reduce) SALT_CUDA(cudaMemsetAsync(wsp, 0, salt::WsLayout::group_partials, sc));
+  if (reduce) SALT_CUDA(cudaMemsetAsync(wsp, 0, SALT_WORKSPACE_TICKET_BYTES, sc));
   Events h2d, comp, d2h;
   int rc = h2d.make(kNBuf);
   if (!rc) rc = comp.make(kNBuf);

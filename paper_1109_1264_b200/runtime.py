@@ -199,7 +199,6 @@ def _require_cuda() -> torch.device:
 
 
 _MAX_CACHED_WORKSPACES = 64
-_TICKET_BYTES = 256 + 4 * 4096  # ticket + group tickets (salt::WsLayout)
 
 
 def _workspace(index: int, stream_ptr: int) -> torch.Tensor:
@@ -220,7 +219,7 @@ def _workspace(index: int, stream_ptr: int) -> torch.Tensor:
                     _workspaces[key] = ws
                 else:
                     ws = torch.empty(nbytes, dtype=torch.uint8, device=device)
-                    ws[:_TICKET_BYTES].zero_()
+                    ws[: _native.SALT_WORKSPACE_TICKET_BYTES].zero_()
                     ws.record_stream(torch.cuda.current_stream(device))
     return ws
 
