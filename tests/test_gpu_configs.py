@@ -232,3 +232,24 @@ def test_exchange_protocol_emulated_on_one_gpu(world):
         _native.check(lib.salt_reduce_finish(1, totals[r * world * 2:].data_ptr(), world, 0,
                                              out.data_ptr(), None, stream))
         assert np.float64(res[r, 0, 0] + res[r, 0, 1]) == out.item(), r
+
+
+def test_config5_full_length_on_one_gpu_int64_indexing():
+    """Config 5's full global length (2^31 + 5 f64 elements, > INT32_MAX) on
+    ONE B200 (3 x 16 GiB resident): the fused axpy->dot step indexes with
+    64-bit offsets; y bit-exact and r within 1e-12 of the exact value."""
+    n = (1 << 31) + 5
+    g = torch.Generator(device="cuda").manual_seed(1109)
+    X, Y, Z = (lv.DenseVector.from_tensor(torch.randn(n, dtype=torch.float64, device="cuda", generator=g))
+               for _ in range(3))
+    x, y, z = (v.to_array() for v in (X, Y, Z))
+    alpha = -0.4375
+    r = lv.axpy_dot(alpha, X, Y, Z)
+    ex = coracle.reduce_exact("D L2 *", [y, x, z], [alpha], np.float64, threads=THREADS,
+                              assign_sig="L0 S0 L1 * +")
+    assert abs(float(r) - ex) <= 1e-12 * abs(ex), (float(r), ex)
+    coracle.assign("L0 S0 L1 * +", y, [y, x], [alpha], threads=THREADS)
+    got = Y.to_array()
+    assert got.tobytes() == y.tobytes()
+    # the last elements (beyond 2^31) were written
+    assert got[-1] == y[-1] and got[(1 << 31) + 1] == y[(1 << 31) + 1]
