@@ -445,3 +445,28 @@ def test_fused_axpy_dot_on_host_vectors():
         assert same_bits(Y.to_array(), y_new)
         exact = restate.exact_sum((y_new * z))
         assert abs(float(r) - exact) <= TOL[dt] * abs(exact)
+
+
+def test_no_writes_outside_the_destination():
+    """compute-sanitizer is closed on this pool, so out-of-bounds writes are
+    checked with canaries: destinations are views inside a larger buffer
+    filled with a sentinel; after every kind of evaluation (vector body,
+    scalar head/tail, V=1 fallback, fused assign+reduce) everything outside
+    the view still holds the sentinel."""
+    g = np.random.default_rng(13)
+    for dt in ("f32", "f64"):
+        tdt = torch.float32 if dt == "f32" else torch.float64
+        for n in (1, 3, 8, 9, 31, 1023, 1025, 65_541):
+            for off in (0, 1, 2, 5):
+                src = [torch.from_numpy(g.uniform(-1, 1, n + 64)).to(tdt).cuda() for _ in range(3)]
+                buf = torch.full((n + 64,), 12345.0, dtype=tdt, device="cuda")
+                a, b, c = (lv.DenseVector.from_tensor(t[off:off + n]) for t in src)
+                mis = (off + 1) % 4  # also a misalignment different from the sources
+                for doff in (off, mis):
+                    buf.fill_(12345.0)
+                    d = lv.DenseVector.from_tensor(buf[doff:doff + n])
+                    d.assign(0.5 * a - b * c)
+                    lv.axpy_dot(0.5, a, d, b)
+                    outside = torch.cat([buf[:doff], buf[doff + n:]])
+                    assert bool((outside == 12345.0).all()), (dt, n, off, doff)
+                    assert bool((buf[doff:doff + n] != 12345.0).all())
