@@ -127,7 +127,7 @@ class Exchange(ctypes.Structure):
     ]
 
 
-_lock = threading.Lock()
+_lock = threading.RLock()
 _lib = None
 
 
@@ -153,6 +153,42 @@ def lib() -> ctypes.CDLL:
                 raise RuntimeError("libsalt.so ABI version mismatch; rebuild it")
             _lib = handle
     return _lib
+
+
+_fast = None
+_fast_tried = False
+
+
+def fastpath():
+    """The C host fast path (csrc/fastpath.c) bound to this libsalt instance,
+    or None if the extension was not built (the Python path then runs)."""
+    global _fast, _fast_tried
+    if _fast_tried:
+        return _fast
+    with _lock:
+        if not _fast_tried:
+            try:
+                import torch
+
+                from . import _fastpath, runtime
+                from .expressions import AddNode, Leaf, MulNode, ScaleNode, SubNode
+                from .vectors import DenseVector
+                import numpy as np
+
+                h = lib()
+                addr = lambda f: ctypes.cast(f, ctypes.c_void_p).value  # noqa: E731
+                _fastpath.init(
+                    addr(h.salt_assign), addr(h.salt_reduce), addr(h.salt_assign_reduce),
+                    addr(h.salt_last_error), h.salt_reduce_workspace_bytes(),
+                    Leaf, AddNode, SubNode, MulNode, ScaleNode, DenseVector,
+                    torch._C._cuda_getCurrentRawStream, torch.cuda.current_device,
+                    runtime._workspace, np.float32, np.float64,
+                )
+                _fast = _fastpath
+            except (ImportError, AttributeError):
+                _fast = None
+            _fast_tried = True
+    return _fast
 
 
 def check(rc: int) -> None:

@@ -1,0 +1,336 @@
+/*
+ * fastpath.c — CPython extension `_fastpath`: the common case of the host
+ * layer in C.
+ *
+ * For trees whose leaves and destination are plain device DenseVectors on the
+ * current CUDA device, this walks the node objects (Leaf / AddNode / SubNode /
+ * MulNode / ScaleNode), builds the same canonical postfix signature as
+ * expressions.lower(), collects the leaf pointers and element-typed scalars,
+ * and calls libsalt.so's C ABI directly — replacing ~10 us of Python per call
+ * (profiles/r01_api_overhead.json) by ~1 us.  Anything else (other vector
+ * types, host or sharded vectors, mismatched lengths/dtypes/devices, trees
+ * beyond one kernel, plan options) returns "not handled" and the Python path
+ * runs — which also raises the reference's exceptions.  It is a host-side
+ * accelerator only: there is no CPU arithmetic here.
+ *
+ * libsalt.so's entry points are passed in as addresses from the ctypes
+ * handle (init()), so both share one library instance.
+ */
+#define PY_SSIZE_T_CLEAN
+#include <Python.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#define MAX_LEAVES 16
+#define MAX_SCALARS 32
+#define MAX_SIG 1024
+
+typedef int (*assign_fn)(int, const char*, void*, const void* const*, int, const double*, int,
+                         int64_t, void*);
+typedef int (*reduce_fn)(int, const char*, const void* const*, int, const double*, int, int64_t,
+                         int, void*, size_t, void*, void*, void*);
+typedef int (*assign_reduce_fn)(int, const char*, const char*, void*, const void* const*, int,
+                                const double*, int, int64_t, int, void*, size_t, void*, void*,
+                                void*);
+typedef const char* (*last_error_fn)(void);
+
+static assign_fn p_assign;
+static reduce_fn p_reduce;
+static assign_reduce_fn p_assign_reduce;
+static last_error_fn p_last_error;
+static size_t ws_bytes;
+
+static PyObject *T_Leaf, *T_Add, *T_Sub, *T_Mul, *T_Scale, *T_Dense;
+static PyObject *get_stream, *current_device, *workspace_fn, *np_f32, *np_f64;
+static PyObject *s_vector, *s_left, *s_right, *s_child, *s_alpha, *s_ptr, *s_dev, *s_n, *s_code,
+    *s_data_ptr;
+
+typedef struct {
+  char sig[MAX_SIG];
+  int len;
+  PyObject* vecs[MAX_LEAVES];
+  void* ptrs[MAX_LEAVES];
+  int nvec;
+  double sc[MAX_SCALARS];
+  int nsc;
+  int dev, code;
+  long long n;
+  PyObject* dest;  /* reduce tree of a fused root: the destination reads as D */
+} Walk;
+
+/* 1 = ok, 0 = not eligible (fall back), -1 = Python error */
+static int emit(Walk* w, const char* tok) {
+  int k = (int)strlen(tok);
+  if (w->len + k + 1 >= MAX_SIG) return 0;
+  if (w->len) w->sig[w->len++] = ' ';
+  memcpy(w->sig + w->len, tok, (size_t)k);
+  w->len += k;
+  w->sig[w->len] = '\0';
+  return 1;
+}
+
+static int long_attr(PyObject* o, PyObject* name, long long* out) {
+  PyObject* v = PyObject_GetAttr(o, name);
+  if (!v) return -1;
+  *out = PyLong_AsLongLong(v);
+  Py_DECREF(v);
+  return (*out == -1 && PyErr_Occurred()) ? -1 : 1;
+}
+
+static int leaf(Walk* w, PyObject* vec) {
+  char tok[16];
+  if (w->dest && vec == w->dest) return emit(w, "D");
+  for (int k = 0; k < w->nvec; ++k)
+    if (w->vecs[k] == vec) {
+      snprintf(tok, sizeof tok, "L%d", k);
+      return emit(w, tok);
+    }
+  if ((PyObject*)Py_TYPE(vec) != T_Dense || w->nvec == MAX_LEAVES) return 0;
+  long long dev, code, n, ptr;
+  if (long_attr(vec, s_dev, &dev) < 0 || long_attr(vec, s_code, &code) < 0 ||
+      long_attr(vec, s_n, &n) < 0 || long_attr(vec, s_ptr, &ptr) < 0)
+    return -1;
+  if (dev != w->dev || code != w->code || n != w->n) return 0;
+  w->vecs[w->nvec] = vec;
+  w->ptrs[w->nvec] = (void*)(intptr_t)ptr;
+  snprintf(tok, sizeof tok, "L%d", w->nvec++);
+  return emit(w, tok);
+}
+
+static int walk(Walk* w, PyObject* node) {
+  PyObject* t = (PyObject*)Py_TYPE(node);
+  int rc;
+  if (t == T_Leaf) {
+    PyObject* v = PyObject_GetAttr(node, s_vector);
+    if (!v) return -1;
+    rc = leaf(w, v);
+    Py_DECREF(v);
+    return rc;
+  }
+  if (t == T_Dense) return leaf(w, node); /* a bare vector used as a tree */
+  if (t == T_Scale) {
+    if (w->nsc == MAX_SCALARS) return 0;
+    PyObject* a = PyObject_GetAttr(node, s_alpha);
+    if (!a) return -1;
+    double v = PyFloat_AsDouble(a); /* alpha is already element-typed */
+    Py_DECREF(a);
+    if (v == -1.0 && PyErr_Occurred()) return -1;
+    char tok[16];
+    snprintf(tok, sizeof tok, "S%d", w->nsc);
+    w->sc[w->nsc++] = v;
+    if ((rc = emit(w, tok)) != 1) return rc;
+    PyObject* c = PyObject_GetAttr(node, s_child);
+    if (!c) return -1;
+    rc = walk(w, c);
+    Py_DECREF(c);
+    return rc == 1 ? emit(w, "*") : rc;
+  }
+  const char* op = t == T_Add ? "+" : t == T_Sub ? "-" : t == T_Mul ? "*" : NULL;
+  if (!op) return 0;
+  PyObject* l = PyObject_GetAttr(node, s_left);
+  if (!l) return -1;
+  rc = walk(w, l);
+  Py_DECREF(l);
+  if (rc != 1) return rc;
+  PyObject* r = PyObject_GetAttr(node, s_right);
+  if (!r) return -1;
+  rc = walk(w, r);
+  Py_DECREF(r);
+  return rc == 1 ? emit(w, op) : rc;
+}
+
+/* Destination checks; fills dev/code/n. 1 ok, 0 not eligible, -1 error. */
+static int start(Walk* w, PyObject* dest, void** dptr) {
+  memset(w, 0, sizeof *w);
+  if ((PyObject*)Py_TYPE(dest) != T_Dense) return 0;
+  long long dev, code, n, ptr;
+  if (long_attr(dest, s_dev, &dev) < 0 || long_attr(dest, s_code, &code) < 0 ||
+      long_attr(dest, s_n, &n) < 0 || long_attr(dest, s_ptr, &ptr) < 0)
+    return -1;
+  if (dev < 0) return 0;
+  w->dev = (int)dev;
+  w->code = (int)code;
+  w->n = n;
+  if (dptr) *dptr = (void*)(intptr_t)ptr;
+  return 1;
+}
+
+/* Current device must be w->dev; returns the current stream handle. */
+static int stream_for(Walk* w, void** stream) {
+  PyObject* cur = PyObject_CallNoArgs(current_device);
+  if (!cur) return -1;
+  long c = PyLong_AsLong(cur);
+  Py_DECREF(cur);
+  if (c == -1 && PyErr_Occurred()) return -1;
+  if (c != w->dev) return 0;
+  PyObject* d = PyLong_FromLong(w->dev);
+  PyObject* s = PyObject_CallOneArg(get_stream, d);
+  Py_DECREF(d);
+  if (!s) return -1;
+  *stream = PyLong_AsVoidPtr(s);
+  Py_DECREF(s);
+  return PyErr_Occurred() ? -1 : 1;
+}
+
+static PyObject* check(int rc) {
+  if (rc != 0) {
+    PyErr_Format(PyExc_RuntimeError, "libsalt error %d: %s", rc, p_last_error());
+    return NULL;
+  }
+  Py_RETURN_TRUE;
+}
+
+/* Workspace of (device, stream) from runtime._workspace; its last 256 bytes
+ * hold the fast path's result slot (non-lazy reductions only). */
+static int workspace(Walk* w, void* stream, void** ws, void** slot) {
+  PyObject* t = PyObject_CallFunction(workspace_fn, "iK", w->dev,
+                                      (unsigned long long)(uintptr_t)stream);
+  if (!t) return -1;
+  PyObject* p = PyObject_CallMethodNoArgs(t, s_data_ptr);
+  Py_DECREF(t);
+  if (!p) return -1;
+  *ws = PyLong_AsVoidPtr(p);
+  Py_DECREF(p);
+  *slot = (char*)*ws + ws_bytes;
+  return PyErr_Occurred() ? -1 : 1;
+}
+
+static PyObject* scalar_result(Walk* w, const double* host) {
+  if (w->code == 0) {
+    float f;
+    memcpy(&f, host, sizeof f);
+    return PyObject_CallFunction(np_f32, "d", (double)f);
+  }
+  return PyObject_CallFunction(np_f64, "d", host[0]);
+}
+
+#define TRY(expr)                 \
+  do {                            \
+    int rc_ = (expr);             \
+    if (rc_ < 0) return NULL;     \
+    if (rc_ == 0) Py_RETURN_FALSE; \
+  } while (0)
+
+/* assign(dest, source) -> True if launched, False if not eligible */
+static PyObject* fp_assign(PyObject* self, PyObject* args) {
+  PyObject *dest, *src;
+  if (!PyArg_ParseTuple(args, "OO", &dest, &src)) return NULL;
+  Walk w;
+  void *dptr, *stream;
+  TRY(start(&w, dest, &dptr));
+  TRY(walk(&w, src));
+  if (w.nvec == 0) Py_RETURN_FALSE;
+  TRY(stream_for(&w, &stream));
+  if (w.n == 0) Py_RETURN_TRUE;
+  return check(p_assign(w.code, w.sig, dptr, (const void* const*)w.ptrs, w.nvec, w.sc, w.nsc,
+                        w.n, stream));
+}
+
+/* reduce(child, flags) -> element-typed NumPy scalar, or None if not eligible */
+static PyObject* fp_reduce(PyObject* self, PyObject* args) {
+  PyObject* child;
+  int flags;
+  if (!PyArg_ParseTuple(args, "Oi", &child, &flags)) return NULL;
+  Walk w;
+  memset(&w, 0, sizeof w);
+  /* the first leaf fixes device / dtype / length */
+  PyObject* first = child;
+  while ((PyObject*)Py_TYPE(first) != T_Leaf && (PyObject*)Py_TYPE(first) != T_Dense) {
+    PyObject* t = (PyObject*)Py_TYPE(first);
+    PyObject* nxt = PyObject_GetAttr(first, t == T_Scale ? s_child : s_left);
+    if (!nxt) { PyErr_Clear(); Py_RETURN_NONE; }
+    Py_DECREF(nxt); /* nodes are kept alive by their parents */
+    first = nxt;
+  }
+  PyObject* v0 = (PyObject*)Py_TYPE(first) == T_Leaf ? PyObject_GetAttr(first, s_vector) : (Py_INCREF(first), first);
+  if (!v0) return NULL;
+  int rc = start(&w, v0, NULL);
+  Py_DECREF(v0);
+  if (rc < 0) return NULL;
+  if (rc == 0) Py_RETURN_NONE;
+  rc = walk(&w, child);
+  if (rc < 0) return NULL;
+  void* stream;
+  if (rc == 0 || (rc = stream_for(&w, &stream)) == 0) Py_RETURN_NONE;
+  if (rc < 0) return NULL;
+  void *ws, *slot;
+  if (workspace(&w, stream, &ws, &slot) < 0) return NULL;
+  double host[2] = {0.0, 0.0};
+  rc = p_reduce(w.code, w.sig, (const void* const*)w.ptrs, w.nvec, w.sc, w.nsc, w.n, flags, ws,
+                ws_bytes, slot, host, stream);
+  if (rc != 0) return check(rc);
+  return scalar_result(&w, host);
+}
+
+/* assign_reduce(dest, assign_source, reduce_child, flags) -> scalar or None */
+static PyObject* fp_assign_reduce(PyObject* self, PyObject* args) {
+  PyObject *dest, *src, *child;
+  int flags;
+  if (!PyArg_ParseTuple(args, "OOOi", &dest, &src, &child, &flags)) return NULL;
+  Walk w;
+  void *dptr, *stream;
+  int rc = start(&w, dest, &dptr);
+  if (rc <= 0) { if (rc < 0) return NULL; Py_RETURN_NONE; }
+  rc = walk(&w, src);
+  if (rc <= 0) { if (rc < 0) return NULL; Py_RETURN_NONE; }
+  char asig[MAX_SIG];
+  memcpy(asig, w.sig, (size_t)w.len + 1);
+  w.len = 0;
+  w.sig[0] = '\0';
+  w.dest = dest;
+  rc = walk(&w, child);
+  if (rc <= 0) { if (rc < 0) return NULL; Py_RETURN_NONE; }
+  if (w.nvec == 0) Py_RETURN_NONE;
+  rc = stream_for(&w, &stream);
+  if (rc <= 0) { if (rc < 0) return NULL; Py_RETURN_NONE; }
+  void *ws, *slot;
+  if (workspace(&w, stream, &ws, &slot) < 0) return NULL;
+  double host[2] = {0.0, 0.0};
+  rc = p_assign_reduce(w.code, asig, w.sig, dptr, (const void* const*)w.ptrs, w.nvec, w.sc, w.nsc,
+                       w.n, flags, ws, ws_bytes, slot, host, stream);
+  if (rc != 0) return check(rc);
+  return scalar_result(&w, host);
+}
+
+static PyObject* fp_init(PyObject* self, PyObject* args) {
+  unsigned long long a, r, ar, le;
+  Py_ssize_t wsb;
+  if (!PyArg_ParseTuple(args, "KKKKnOOOOOOOOOOO", &a, &r, &ar, &le, &wsb, &T_Leaf, &T_Add, &T_Sub,
+                        &T_Mul, &T_Scale, &T_Dense, &get_stream, &current_device, &workspace_fn,
+                        &np_f32, &np_f64))
+    return NULL;
+  PyObject* keep[] = {T_Leaf, T_Add, T_Sub, T_Mul, T_Scale, T_Dense, get_stream, current_device,
+                      workspace_fn, np_f32, np_f64};
+  for (size_t i = 0; i < sizeof keep / sizeof keep[0]; ++i) Py_INCREF(keep[i]);
+  p_assign = (assign_fn)(uintptr_t)a;
+  p_reduce = (reduce_fn)(uintptr_t)r;
+  p_assign_reduce = (assign_reduce_fn)(uintptr_t)ar;
+  p_last_error = (last_error_fn)(uintptr_t)le;
+  ws_bytes = (size_t)wsb;
+  Py_RETURN_NONE;
+}
+
+static PyMethodDef methods[] = {
+    {"init", fp_init, METH_VARARGS, "bind libsalt entry points and the Python types"},
+    {"assign", fp_assign, METH_VARARGS, "assign(dest, source) -> bool"},
+    {"reduce", fp_reduce, METH_VARARGS, "reduce(child, flags) -> scalar or None"},
+    {"assign_reduce", fp_assign_reduce, METH_VARARGS,
+     "assign_reduce(dest, source, child, flags) -> scalar or None"},
+    {NULL, NULL, 0, NULL}};
+
+static struct PyModuleDef module = {PyModuleDef_HEAD_INIT, "_fastpath", NULL, -1, methods};
+
+PyMODINIT_FUNC PyInit__fastpath(void) {
+  s_vector = PyUnicode_InternFromString("vector");
+  s_left = PyUnicode_InternFromString("left");
+  s_right = PyUnicode_InternFromString("right");
+  s_child = PyUnicode_InternFromString("child");
+  s_alpha = PyUnicode_InternFromString("alpha");
+  s_ptr = PyUnicode_InternFromString("_ptr");
+  s_dev = PyUnicode_InternFromString("_dev");
+  s_n = PyUnicode_InternFromString("_n");
+  s_code = PyUnicode_InternFromString("_code");
+  s_data_ptr = PyUnicode_InternFromString("data_ptr");
+  return PyModule_Create(&module);
+}

@@ -262,6 +262,10 @@ def execute_assign(root, plan: UnrollPlan = None, *, backend: LaneBackend = None
     """Evaluate an assignment tree, writing every destination element once."""
     if not isinstance(root, AssignNode):
         raise TypeError("execute_assign requires an assignment root")
+    if plan is None and backend is None and unroll is None and packages is None:
+        fast = _native.fastpath()
+        if fast is not None and fast.assign(root.dest.vector, root.source):
+            return
     _assign(root, _length(root, plan, backend, unroll, packages))
 
 
@@ -272,6 +276,12 @@ def execute_reduce(root, plan: UnrollPlan = None, *, backend: LaneBackend = None
     (or a DeviceScalar without host synchronisation when lazy=True)."""
     if not isinstance(root, SumNode):
         raise TypeError("execute_reduce requires a reduction root")
+    if not lazy and plan is None and backend is None and unroll is None and packages is None:
+        fast = _native.fastpath()
+        if fast is not None:
+            r = fast.reduce(root.child, _flags)
+            if r is not None:
+                return r
     return _reduce(root, _length(root, plan, backend, unroll, packages), flags=_flags, lazy=lazy)
 
 
@@ -282,6 +292,13 @@ def execute_assign_reduce(root, plan: UnrollPlan = None, *, backend: LaneBackend
     over the freshly assigned values (e.g. axpy then dot, BASELINE config 5)."""
     if not isinstance(root, AssignReduceNode):
         raise TypeError("execute_assign_reduce requires an AssignReduceNode root")
+    if not lazy and plan is None and backend is None and unroll is None and packages is None:
+        fast = _native.fastpath()
+        if fast is not None:
+            r = fast.assign_reduce(root.assign.dest.vector, root.assign.source, root.total.child,
+                                   _flags)
+            if r is not None:
+                return r
     length = _length(root, plan, backend, unroll, packages)
     lwa = lower(root.assign.source)
     lwr = lower(root.total.child, parent=lwa, dest=root.assign.dest.vector)

@@ -212,7 +212,8 @@ def _workspace(index: int, stream_ptr: int) -> torch.Tensor:
         with _ws_lock:
             ws = _workspaces.get(key)
             if ws is None:
-                nbytes = _native.lib().salt_reduce_workspace_bytes()
+                # + 256 bytes: the C fast path's result slot (csrc/fastpath.c)
+                nbytes = _native.lib().salt_reduce_workspace_bytes() + 256
                 device = torch.device("cuda", index)
                 if len(_workspaces) < _MAX_CACHED_WORKSPACES:
                     ws = torch.zeros(nbytes, dtype=torch.uint8, device=device)

@@ -70,11 +70,16 @@ def _aligned_empty(n: int, dt: np.dtype, device: torch.device) -> torch.Tensor:
 class DenseVector:
     """Fixed-length contiguous f32/f64 vector (reference vectors.py:18-31)."""
 
-    __slots__ = ("_data", "_dtype")
+    # _ptr/_dev/_n/_code cache what the C fast path (csrc/fastpath.c) reads
+    __slots__ = ("_data", "_dtype", "_ptr", "_dev", "_n", "_code")
 
     def __init__(self, data: torch.Tensor, dtype):
         self._data = data
         self._dtype = as_dtype(dtype)
+        self._ptr = data.data_ptr()
+        self._dev = data.get_device()  # -1 for host storage
+        self._n = int(data.shape[0])
+        self._code = 0 if self._dtype.itemsize == 4 else 1
 
     # ------------------------------------------------------------ creation
     @classmethod

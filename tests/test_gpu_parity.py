@@ -470,3 +470,27 @@ def test_no_writes_outside_the_destination():
                     outside = torch.cat([buf[:doff], buf[doff + n:]])
                     assert bool((outside == 12345.0).all()), (dt, n, off, doff)
                     assert bool((buf[doff:doff + n] != 12345.0).all())
+
+
+def test_c_fast_path_matches_python_path():
+    """The C host fast path (csrc/fastpath.c) is active for device vectors
+    and produces exactly what the Python lowering path produces (plan
+    keywords force the Python path)."""
+    fast = _native.fastpath()
+    assert fast is not None
+    g = np.random.default_rng(14)
+    for dt in ("f32", "f64"):
+        n = 100_003
+        a, b, c = (dev(g.uniform(-1, 1, n), dt) for _ in range(3))
+        d1, d2 = (lv.DenseVector.zeros(n, dt, device="cuda") for _ in range(2))
+        assert fast.assign(d1, (1.5 * a - b * c).left) is True  # a bare ScaleNode tree
+        d1.assign(1.5 * a - b * c)
+        d2.assign(1.5 * a - b * c, unroll=1)
+        assert d1.to_array().tobytes() == d2.to_array().tobytes()
+        r1, r2 = lv.dot(a, b), lv.dot(a, b, unroll=1)
+        assert r1.tobytes() == r2.tobytes() and type(r1) is type(r2) is NP[dt]
+        assert lv.norm2(a).tobytes() == lv.norm2(a, unroll=1).tobytes()
+        y1, y2 = dev(b.to_array(), dt), dev(b.to_array(), dt)
+        s1, s2 = lv.axpy_dot(0.5, a, y1, c), lv.axpy_dot(0.5, a, y2, c, unroll=1)
+        assert s1.tobytes() == s2.tobytes()
+        assert y1.to_array().tobytes() == y2.to_array().tobytes()

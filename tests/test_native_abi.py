@@ -122,3 +122,21 @@ def test_jit_disk_cache(tmp_path):
     second = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
                             cwd=ROOT, check=True)
     assert float(second.stdout) < float(first.stdout)
+
+
+def test_c_fast_path_declines_what_it_cannot_take():
+    """The fast path only takes plain device vectors; everything else is
+    declined (False / None) so the Python path handles it (and raises the
+    reference's errors)."""
+    import paper_1109_1264_b200 as lv
+    from paper_1109_1264_b200.expressions import ScaleNode, as_node
+
+    fast = _native.fastpath()
+    assert fast is not None
+    x = lv.DenseVector.zeros(10, "f64", device="cpu")
+    y = lv.DenseVector.zeros(10, "f64", device="cpu")
+    assert fast.assign(y, as_node(y) + ScaleNode(0.5, as_node(x))) is False
+    assert fast.reduce(as_node(x) * as_node(y), 0) is None
+    assert fast.assign_reduce(y, as_node(y) + ScaleNode(0.5, as_node(x)), as_node(y) * as_node(x), 0) is None
+    cv = lv.CountingVector.zeros(10, "f64", device="cpu")
+    assert fast.assign(cv, as_node(x)) is False
