@@ -182,7 +182,7 @@ def fastpath():
                     addr(h.salt_last_error), h.salt_reduce_workspace_bytes(),
                     Leaf, AddNode, SubNode, MulNode, ScaleNode, DenseVector,
                     torch._C._cuda_getCurrentRawStream, torch.cuda.current_device,
-                    runtime._workspace, np.float32, np.float64,
+                    runtime._workspace, np.float32, np.float64, runtime._lazy_out,
                 )
                 _fast = _fastpath
             except (ImportError, AttributeError):

@@ -42,7 +42,7 @@ static last_error_fn p_last_error;
 static size_t ws_bytes;
 
 static PyObject *T_Leaf, *T_Add, *T_Sub, *T_Mul, *T_Scale, *T_Dense;
-static PyObject *get_stream, *current_device, *workspace_fn, *np_f32, *np_f64;
+static PyObject *get_stream, *current_device, *workspace_fn, *np_f32, *np_f64, *lazy_out;
 static PyObject *s_vector, *s_left, *s_right, *s_child, *s_alpha, *s_ptr, *s_dev, *s_n, *s_code,
     *s_data_ptr;
 
@@ -227,11 +227,26 @@ static PyObject* fp_assign(PyObject* self, PyObject* args) {
                         w.n, stream));
 }
 
-/* reduce(child, flags) -> element-typed NumPy scalar, or None if not eligible */
+/* Device result of a lazy reduction: (DeviceScalar, out pointer) from the
+ * Python helper runtime._lazy_out(device, code). */
+static PyObject* lazy_slot(Walk* w, void** out) {
+  PyObject* r = PyObject_CallFunction(lazy_out, "ii", w->dev, w->code);
+  if (!r) return NULL;
+  PyObject* ds = PyTuple_GetItem(r, 0);
+  PyObject* ptr = PyTuple_GetItem(r, 1);
+  if (!ds || !ptr) { Py_DECREF(r); return NULL; }
+  *out = PyLong_AsVoidPtr(ptr);
+  Py_INCREF(ds);
+  Py_DECREF(r);
+  return ds;
+}
+
+/* reduce(child, flags, lazy) -> NumPy scalar (or DeviceScalar if lazy), or
+ * None if not eligible */
 static PyObject* fp_reduce(PyObject* self, PyObject* args) {
   PyObject* child;
-  int flags;
-  if (!PyArg_ParseTuple(args, "Oi", &child, &flags)) return NULL;
+  int flags, lazy = 0;
+  if (!PyArg_ParseTuple(args, "Oi|p", &child, &flags, &lazy)) return NULL;
   Walk w;
   memset(&w, 0, sizeof w);
   /* the first leaf fixes device / dtype / length */
@@ -256,6 +271,15 @@ static PyObject* fp_reduce(PyObject* self, PyObject* args) {
   if (rc < 0) return NULL;
   void *ws, *slot;
   if (workspace(&w, stream, &ws, &slot) < 0) return NULL;
+  if (lazy) {
+    void* out;
+    PyObject* ds = lazy_slot(&w, &out);
+    if (!ds) return NULL;
+    rc = p_reduce(w.code, w.sig, (const void* const*)w.ptrs, w.nvec, w.sc, w.nsc, w.n, flags, ws,
+                  ws_bytes, out, NULL, stream);
+    if (rc != 0) { Py_DECREF(ds); return check(rc); }
+    return ds;
+  }
   double host[2] = {0.0, 0.0};
   rc = p_reduce(w.code, w.sig, (const void* const*)w.ptrs, w.nvec, w.sc, w.nsc, w.n, flags, ws,
                 ws_bytes, slot, host, stream);
@@ -266,8 +290,8 @@ static PyObject* fp_reduce(PyObject* self, PyObject* args) {
 /* assign_reduce(dest, assign_source, reduce_child, flags) -> scalar or None */
 static PyObject* fp_assign_reduce(PyObject* self, PyObject* args) {
   PyObject *dest, *src, *child;
-  int flags;
-  if (!PyArg_ParseTuple(args, "OOOi", &dest, &src, &child, &flags)) return NULL;
+  int flags, lazy = 0;
+  if (!PyArg_ParseTuple(args, "OOOi|p", &dest, &src, &child, &flags, &lazy)) return NULL;
   Walk w;
   void *dptr, *stream;
   int rc = start(&w, dest, &dptr);
@@ -286,6 +310,15 @@ static PyObject* fp_assign_reduce(PyObject* self, PyObject* args) {
   if (rc <= 0) { if (rc < 0) return NULL; Py_RETURN_NONE; }
   void *ws, *slot;
   if (workspace(&w, stream, &ws, &slot) < 0) return NULL;
+  if (lazy) {
+    void* out;
+    PyObject* ds = lazy_slot(&w, &out);
+    if (!ds) return NULL;
+    rc = p_assign_reduce(w.code, asig, w.sig, dptr, (const void* const*)w.ptrs, w.nvec, w.sc,
+                         w.nsc, w.n, flags, ws, ws_bytes, out, NULL, stream);
+    if (rc != 0) { Py_DECREF(ds); return check(rc); }
+    return ds;
+  }
   double host[2] = {0.0, 0.0};
   rc = p_assign_reduce(w.code, asig, w.sig, dptr, (const void* const*)w.ptrs, w.nvec, w.sc, w.nsc,
                        w.n, flags, ws, ws_bytes, slot, host, stream);
@@ -296,12 +329,12 @@ static PyObject* fp_assign_reduce(PyObject* self, PyObject* args) {
 static PyObject* fp_init(PyObject* self, PyObject* args) {
   unsigned long long a, r, ar, le;
   Py_ssize_t wsb;
-  if (!PyArg_ParseTuple(args, "KKKKnOOOOOOOOOOO", &a, &r, &ar, &le, &wsb, &T_Leaf, &T_Add, &T_Sub,
+  if (!PyArg_ParseTuple(args, "KKKKnOOOOOOOOOOOO", &a, &r, &ar, &le, &wsb, &T_Leaf, &T_Add, &T_Sub,
                         &T_Mul, &T_Scale, &T_Dense, &get_stream, &current_device, &workspace_fn,
-                        &np_f32, &np_f64))
+                        &np_f32, &np_f64, &lazy_out))
     return NULL;
   PyObject* keep[] = {T_Leaf, T_Add, T_Sub, T_Mul, T_Scale, T_Dense, get_stream, current_device,
-                      workspace_fn, np_f32, np_f64};
+                      workspace_fn, np_f32, np_f64, lazy_out};
   for (size_t i = 0; i < sizeof keep / sizeof keep[0]; ++i) Py_INCREF(keep[i]);
   p_assign = (assign_fn)(uintptr_t)a;
   p_reduce = (reduce_fn)(uintptr_t)r;
@@ -314,9 +347,9 @@ static PyObject* fp_init(PyObject* self, PyObject* args) {
 static PyMethodDef methods[] = {
     {"init", fp_init, METH_VARARGS, "bind libsalt entry points and the Python types"},
     {"assign", fp_assign, METH_VARARGS, "assign(dest, source) -> bool"},
-    {"reduce", fp_reduce, METH_VARARGS, "reduce(child, flags) -> scalar or None"},
+    {"reduce", fp_reduce, METH_VARARGS, "reduce(child, flags, lazy=False) -> scalar or None"},
     {"assign_reduce", fp_assign_reduce, METH_VARARGS,
-     "assign_reduce(dest, source, child, flags) -> scalar or None"},
+     "assign_reduce(dest, source, child, flags, lazy=False) -> scalar or None"},
     {NULL, NULL, 0, NULL}};
 
 static struct PyModuleDef module = {PyModuleDef_HEAD_INIT, "_fastpath", NULL, -1, methods};

@@ -276,10 +276,10 @@ def execute_reduce(root, plan: UnrollPlan = None, *, backend: LaneBackend = None
     (or a DeviceScalar without host synchronisation when lazy=True)."""
     if not isinstance(root, SumNode):
         raise TypeError("execute_reduce requires a reduction root")
-    if not lazy and plan is None and backend is None and unroll is None and packages is None:
+    if plan is None and backend is None and unroll is None and packages is None:
         fast = _native.fastpath()
         if fast is not None:
-            r = fast.reduce(root.child, _flags)
+            r = fast.reduce(root.child, _flags, lazy)
             if r is not None:
                 return r
     return _reduce(root, _length(root, plan, backend, unroll, packages), flags=_flags, lazy=lazy)
@@ -292,11 +292,11 @@ def execute_assign_reduce(root, plan: UnrollPlan = None, *, backend: LaneBackend
     over the freshly assigned values (e.g. axpy then dot, BASELINE config 5)."""
     if not isinstance(root, AssignReduceNode):
         raise TypeError("execute_assign_reduce requires an AssignReduceNode root")
-    if not lazy and plan is None and backend is None and unroll is None and packages is None:
+    if plan is None and backend is None and unroll is None and packages is None:
         fast = _native.fastpath()
         if fast is not None:
             r = fast.assign_reduce(root.assign.dest.vector, root.assign.source, root.total.child,
-                                   _flags)
+                                   _flags, lazy)
             if r is not None:
                 return r
     length = _length(root, plan, backend, unroll, packages)

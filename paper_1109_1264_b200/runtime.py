@@ -225,6 +225,13 @@ def _workspace(index: int, stream_ptr: int) -> torch.Tensor:
     return ws
 
 
+def _lazy_out(index: int, code: int):
+    """(DeviceScalar, device pointer) for a lazy reduction result (C fast path)."""
+    out = torch.empty(1, dtype=torch.float64, device=torch.device("cuda", index))
+    dt = np.dtype(np.float32 if code == _native.SALT_F32 else np.float64)
+    return _result(dt, out, None, True), out.data_ptr()
+
+
 def _host_resources(device: torch.device):
     st = _host_state.get(device.index)
     if st is None:

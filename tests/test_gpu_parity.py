@@ -490,6 +490,8 @@ def test_c_fast_path_matches_python_path():
         r1, r2 = lv.dot(a, b), lv.dot(a, b, unroll=1)
         assert r1.tobytes() == r2.tobytes() and type(r1) is type(r2) is NP[dt]
         assert lv.norm2(a).tobytes() == lv.norm2(a, unroll=1).tobytes()
+        lz = lv.dot(a, b, lazy=True)
+        assert isinstance(lz, lv.DeviceScalar) and lz.item().tobytes() == r1.tobytes()
         y1, y2 = dev(b.to_array(), dt), dev(b.to_array(), dt)
         s1, s2 = lv.axpy_dot(0.5, a, y1, c), lv.axpy_dot(0.5, a, y2, c, unroll=1)
         assert s1.tobytes() == s2.tobytes()

@@ -57,6 +57,7 @@ def main():
         "lv.axpy": lambda: lv.axpy(0.5, x, y),
         "d.assign(alpha*a+beta*(b-c))": lambda: w.assign(1.25 * x + -0.5 * (y - z)),
         "lv.dot(lazy=True)": lambda: lv.dot(x, y, lazy=True),
+        "lv.dot (returns host scalar, synchronises)": lambda: lv.dot(x, y),
         "lv.axpy_dot(lazy=True)": lambda: lv.axpy_dot(0.5, x, y, z, lazy=True),
         "C ABI salt_assign (prebuilt args)": lambda: lib.salt_assign(1, sig, tw.data_ptr(), leaves, 3, sc, 2,
                                                                    n, stream),
