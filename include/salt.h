@@ -106,6 +106,21 @@ int salt_assign_reduce(int dtype, const char* assign_sig, const char* reduce_sig
                        void* workspace, size_t workspace_bytes,
                        void* out_dev, void* out_host, void* stream);
 
+/* Several statements in ONE pass: up to SALT_MAX_ROOTS assignment roots
+ * (postfix trees separated by ';' in assign_sigs; root r may read the value
+ * root r' < r has just assigned as D<r'>) and optionally one reduction
+ * (reduce_sig, may read D<r>; NULL for none).  Per element the roots run in
+ * order, so the result equals running the statements one after another,
+ * e.g. a conjugate-gradient update
+ *     x = x + a*p ; r = r - a*q ; rr = sum(r*r)
+ *     "L0 S0 L1 * + ; L2 S1 L3 * -"  with  "D1 D1 *",  dsts {x, r}. */
+#define SALT_MAX_ROOTS 4
+int salt_fused(int dtype, const char* assign_sigs, const char* reduce_sig,
+               void* const* dsts, int ndst, const void* const* leaves, int nleaves,
+               const double* scalars, int nscalars, int64_t n, int flags,
+               void* workspace, size_t workspace_bytes,
+               void* out_dev, void* out_host, void* stream);
+
 /* Combine `count` {hi, lo} partials (e.g. all-gathered from the ranks, in
  * rank order) in fixed order, round to dtype, optional SALT_SQRT. */
 int salt_reduce_finish(int dtype, const void* partials_dev, int count, int flags,

@@ -27,6 +27,7 @@ __all__ = [
 SALT_WORKSPACE_TICKET_BYTES = 16640
 SALT_MAX_LEAVES = 16
 SALT_MAX_SCALARS = 32
+SALT_MAX_ROOTS = 4
 SALT_F32 = 0
 SALT_F64 = 1
 SALT_SQRT = 1
@@ -39,6 +40,7 @@ HEADER_SYMBOLS = (
     "salt_assign",
     "salt_reduce",
     "salt_assign_reduce",
+    "salt_fused",
     "salt_reduce_finish",
     "salt_assign_host",
     "salt_reduce_host",
@@ -75,6 +77,11 @@ _SIGNATURES = {
         _c_int,
         [_c_int, _c_str, _c_str, _c_vp, _c_vpp, _c_int, _c_dp, _c_int, _c_i64, _c_int, _c_vp, _c_size,
          _c_vp, _c_vp, _c_vp],
+    ),
+    "salt_fused": (
+        _c_int,
+        [_c_int, _c_str, _c_str, _c_vpp, _c_int, _c_vpp, _c_int, _c_dp, _c_int, _c_i64, _c_int,
+         _c_vp, _c_size, _c_vp, _c_vp, _c_vp],
     ),
     "salt_reduce_finish": (_c_int, [_c_int, _c_vp, _c_int, _c_int, _c_vp, _c_vp, _c_vp]),
     "salt_assign_host": (

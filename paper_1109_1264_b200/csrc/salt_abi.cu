@@ -87,39 +87,39 @@ int cuda_fail(cudaError_t e, const char* what) {
 
 // ------------------------------------------------------------------ signatures
 struct Sig {
-  std::string canon;  // tokens joined by single spaces
+  std::string canon;  // tokens joined by single spaces (roots joined by " ; ")
   std::string type;   // C++ type of the tree, e.g. salt::Add<salt::L<0>,salt::L<1>>
   int nl = 0, ns = 0;
+  int nroots = 0;     // assignment roots (Multi<...> when > 1)
   bool uses_d = false;
 };
 
-bool parse_index(const std::string& t, int& k) {
-  if (t.size() < 2 || t.size() > 3) return false;
+bool parse_index(const std::string& t, size_t from, int& k) {
+  if (t.size() <= from || t.size() > from + 2) return false;
   k = 0;
-  for (size_t i = 1; i < t.size(); ++i) {
+  for (size_t i = from; i < t.size(); ++i) {
     if (t[i] < '0' || t[i] > '9') return false;
     k = k * 10 + (t[i] - '0');
   }
   return true;
 }
 
-// Returns "" on success, else an error message.
-std::string parse_sig(const char* s, bool allow_d, Sig& out) {
-  if (!s) return "signature is NULL";
+// One postfix tree.  `d_limit` = how many earlier roots' values (D0 ..) it
+// may read; "D" is D0.  Returns "" on success, else an error message.
+std::string parse_tree(const std::string& s, int d_limit, Sig& out) {
   std::vector<std::string> toks;
   std::string cur;
-  for (const char* p = s;; ++p) {
-    if (*p == ' ' || *p == '\t' || *p == '\0') {
+  for (size_t i = 0; i <= s.size(); ++i) {
+    char c = i < s.size() ? s[i] : '\0';
+    if (c == ' ' || c == '\t' || c == '\0') {
       if (!cur.empty()) toks.push_back(cur), cur.clear();
-      if (*p == '\0') break;
     } else {
-      cur.push_back(*p);
+      cur.push_back(c);
     }
   }
   if (toks.empty()) return "empty signature";
   if (toks.size() > 256) return "signature too long";
   std::vector<std::string> st;
-  out = Sig();
   for (const auto& t : toks) {
     int k = 0;
     if (t == "+" || t == "-" || t == "*") {
@@ -128,17 +128,19 @@ std::string parse_sig(const char* s, bool allow_d, Sig& out) {
       std::string a = st.back(); st.pop_back();
       const char* node = t == "+" ? "salt::Add<" : t == "-" ? "salt::Sub<" : "salt::Mul<";
       st.push_back(std::string(node) + a + "," + b + ">");
-    } else if (t[0] == 'L' && parse_index(t, k)) {
+    } else if (t[0] == 'L' && parse_index(t, 1, k)) {
       if (k >= salt::MAX_LEAVES) return "leaf index out of range: " + t;
       out.nl = std::max(out.nl, k + 1);
       st.push_back("salt::L<" + std::to_string(k) + ">");
-    } else if (t[0] == 'S' && parse_index(t, k)) {
+    } else if (t[0] == 'S' && parse_index(t, 1, k)) {
       if (k >= salt::MAX_SCALARS) return "scalar index out of range: " + t;
       out.ns = std::max(out.ns, k + 1);
       st.push_back("salt::S<" + std::to_string(k) + ">");
-    } else if (t == "D" && allow_d) {
+    } else if (t[0] == 'D' && (t.size() == 1 || parse_index(t, 1, k)) && d_limit > 0) {
+      if (t.size() == 1) k = 0;
+      if (k >= d_limit) return "'" + t + "' reads a root that is not computed before it";
       out.uses_d = true;
-      st.push_back("salt::D");
+      st.push_back("salt::Dk<" + std::to_string(k) + ">");
     } else {
       return "bad token '" + t + "' in signature '" + s + "'";
     }
@@ -148,6 +150,48 @@ std::string parse_sig(const char* s, bool allow_d, Sig& out) {
   if (st.size() != 1) return std::string("signature leaves ") + std::to_string(st.size()) +
                             " values on the stack: '" + s + "'";
   out.type = st.back();
+  return "";
+}
+
+// A reduce tree (d_limit = roots of the fused assignment, 0 for none).
+std::string parse_sig(const char* s, int d_limit, Sig& out) {
+  if (!s) return "signature is NULL";
+  out = Sig();
+  return parse_tree(s, d_limit, out);
+}
+
+// Assignment roots separated by ';'; root r may read D0 .. D(r-1).
+std::string parse_assign(const char* s, Sig& out) {
+  if (!s) return "signature is NULL";
+  out = Sig();
+  std::string all(s);
+  std::vector<std::string> types;
+  size_t pos = 0;
+  while (true) {
+    size_t semi = all.find(';', pos);
+    std::string part = all.substr(pos, semi == std::string::npos ? std::string::npos : semi - pos);
+    if ((int)types.size() == salt::MAX_ROOTS)
+      return "more than " + std::to_string((int)salt::MAX_ROOTS) + " assignment roots";
+    Sig r;
+    std::string err = parse_tree(part, (int)types.size(), r);
+    if (!err.empty()) return err;
+    out.nl = std::max(out.nl, r.nl);
+    out.ns = std::max(out.ns, r.ns);
+    out.uses_d = out.uses_d || r.uses_d;
+    if (!out.canon.empty()) out.canon += " ; ";
+    out.canon += r.canon;
+    types.push_back(r.type);
+    if (semi == std::string::npos) break;
+    pos = semi + 1;
+  }
+  out.nroots = (int)types.size();
+  if (types.size() == 1) {
+    out.type = types[0];
+  } else {
+    out.type = "salt::Multi<";
+    for (size_t i = 0; i < types.size(); ++i) out.type += (i ? "," : "") + types[i];
+    out.type += ">";
+  }
   return "";
 }
 
@@ -281,8 +325,8 @@ template <class T, class EA, class ER, int MODE>
 void reg_one(const char* asig, const char* rsig) {
   Sig sa, sr;
   std::string ta = "salt::None", tr = "salt::None";
-  if (asig) { parse_sig(asig, false, sa); ta = sa.type; }
-  if (rsig) { parse_sig(rsig, MODE == salt::MODE_ASSIGN_REDUCE, sr); tr = sr.type; }
+  if (asig) { parse_assign(asig, sa); ta = sa.type; }
+  if (rsig) { parse_sig(rsig, MODE == salt::MODE_ASSIGN_REDUCE ? sa.nroots : 0, sr); tr = sr.type; }
   constexpr int V = vec_of<T>();
   constexpr int U = unroll_for(MODE, salt::cmax(EA::NL, ER::NL));
   auto k1 = std::make_unique<Kernel>();
@@ -331,6 +375,9 @@ void register_aot() {
   reg<Add<L<0>, Mul<S<0>, L<1>>>, Mul<D, L<2>>, AR>("L0 S0 L1 * +", "D L2 *");
   reg<Add<L<0>, Mul<S<0>, L<1>>>, Mul<D, D>, AR>("L0 S0 L1 * +", "D D *");
   reg<Sub<L<0>, Mul<S<0>, L<1>>>, Mul<D, D>, AR>("L0 S0 L1 * -", "D D *");  // CG: r -= a*q; r.r
+  // CG iteration body in one pass: x += a*p ; r -= a*q ; rr = r.r
+  reg<Multi<Add<L<0>, Mul<S<0>, L<1>>>, Sub<L<2>, Mul<S<1>, L<3>>>>, Mul<Dk<1>, Dk<1>>, AR>(
+      "L0 S0 L1 * + ; L2 S1 L3 * -", "D1 D1 *");
 }
 
 void ensure_table() {
@@ -515,8 +562,8 @@ template <class T> int launch(Kernel* k, int dev, int grid, salt::Args<T>& args,
 
 // Common 32-byte misalignment of all operands -> (vec, head, nvec).
 template <class T>
-void geometry(void* dst, const void* const* leaves, int nl, i64 n, int& vec, i64& head,
-              i64& nvec) {
+void geometry(void* const* dsts, int ndst, const void* const* leaves, int nl, i64 n, int& vec,
+              i64& head, i64& nvec) {
   constexpr int V = vec_of<T>();
   uintptr_t mis = (uintptr_t)-1;
   bool same = true;
@@ -526,7 +573,7 @@ void geometry(void* dst, const void* const* leaves, int nl, i64 n, int& vec, i64
     else if (m != mis) same = false;
     if (m % sizeof(T)) same = false;
   };
-  if (dst) check(dst);
+  for (int r = 0; dsts && r < ndst; ++r) check(dsts[r]);
   for (int l = 0; leaves && l < nl; ++l) check(leaves[l]);
   if (mis == (uintptr_t)-1) mis = 0;
   if (same) {
@@ -571,11 +618,11 @@ int make_plan(int dtype, const char* asig, const char* rsig, int mode, int nleav
     std::string err;
     np->sa.type = np->sr.type = "salt::None";
     if (mode != salt::MODE_REDUCE) {
-      err = parse_sig(asig, false, np->sa);
+      err = parse_assign(asig, np->sa);
       if (!err.empty()) return fail(SALT_EINVAL, err);
     }
     if (mode != salt::MODE_ASSIGN) {
-      err = parse_sig(rsig, mode == salt::MODE_ASSIGN_REDUCE, np->sr);
+      err = parse_sig(rsig, mode == salt::MODE_ASSIGN_REDUCE ? np->sa.nroots : 0, np->sr);
       if (!err.empty()) return fail(SALT_EINVAL, err);
     }
     np->nl = std::max(np->sa.nl, np->sr.nl);
@@ -595,7 +642,7 @@ int make_plan(int dtype, const char* asig, const char* rsig, int mode, int nleav
 }
 
 template <class T>
-int run_fused(Plan& p, void* dst, const void* const* leaves, int nleaves,
+int run_fused(Plan& p, void* const* dsts, int ndst, const void* const* leaves, int nleaves,
               const double* scalars, int nscalars, i64 n, int flags, void* ws, size_t ws_bytes,
               void* out_dev, void* out_host, cudaStream_t st, const salt_exchange* x) {
   if (n < 0) return fail(SALT_EINVAL, "negative length");
@@ -603,7 +650,12 @@ int run_fused(Plan& p, void* dst, const void* const* leaves, int nleaves,
   if (!reduce && n == 0) return 0;  // zero length assign is a no-op (test_engine.py:147-153)
   // Empty vectors may legitimately have NULL storage (torch gives numel-0
   // tensors a NULL data pointer); nothing is dereferenced when n == 0.
-  if (n > 0 && p.mode != salt::MODE_REDUCE && !dst) return fail(SALT_EINVAL, "NULL destination");
+  const int nroots = p.mode == salt::MODE_REDUCE ? 0 : p.sa.nroots;
+  if (ndst != nroots)
+    return fail(SALT_EINVAL, "signature has " + std::to_string(nroots) + " assignment roots but " +
+                                 std::to_string(ndst) + " destinations were passed");
+  for (int r = 0; n > 0 && r < nroots; ++r)
+    if (!dsts || !dsts[r]) return fail(SALT_EINVAL, "NULL destination");
   if (n > 0 && p.nl > 0 && !leaves) return fail(SALT_EINVAL, "NULL leaf array");
   for (int l = 0; n > 0 && l < p.nl; ++l)
     if (!leaves[l]) return fail(SALT_EINVAL, "NULL leaf pointer");
@@ -614,13 +666,13 @@ int run_fused(Plan& p, void* dst, const void* const* leaves, int nleaves,
   }
   salt::Args<T> a;
   memset(&a, 0, sizeof(a));
-  a.dst = (T*)dst;
+  for (int r = 0; r < nroots; ++r) a.dst[r] = (T*)dsts[r];
   for (int l = 0; l < p.nl; ++l) a.leaf[l] = leaves ? (const T*)leaves[l] : nullptr;
   for (int s = 0; s < p.ns; ++s) a.sc[s] = (T)scalars[s];
   a.n = n;
   a.flags = flags;
   int vec;
-  geometry<T>(p.mode == salt::MODE_REDUCE ? nullptr : dst, leaves, p.nl, n, vec, a.head, a.nvec);
+  geometry<T>(dsts, nroots, leaves, p.nl, n, vec, a.head, a.nvec);
   Kernel*& slot = p.cached[g_force_jit.load(std::memory_order_relaxed)][vec == 1 ? 1 : 0];
   if (!slot) slot = get_kernel(dtype_of<T>(), p.mode, vec, p.nl, p.sa.type, p.sr.type);
   Kernel* k = slot;
@@ -688,14 +740,15 @@ int run_fused(Plan& p, void* dst, const void* const* leaves, int nleaves,
   return 0;
 }
 
-int dispatch(int dtype, Plan& p, void* dst, const void* const* leaves, int nleaves,
-             const double* scalars, int nscalars, i64 n, int flags, void* ws, size_t ws_bytes,
-             void* out_dev, void* out_host, cudaStream_t st, const salt_exchange* x = nullptr) {
+int dispatch(int dtype, Plan& p, void* const* dsts, int ndst, const void* const* leaves,
+             int nleaves, const double* scalars, int nscalars, i64 n, int flags, void* ws,
+             size_t ws_bytes, void* out_dev, void* out_host, cudaStream_t st,
+             const salt_exchange* x = nullptr) {
   if (dtype == SALT_F32)
-    return run_fused<float>(p, dst, leaves, nleaves, scalars, nscalars, n, flags, ws, ws_bytes,
-                            out_dev, out_host, st, x);
-  return run_fused<double>(p, dst, leaves, nleaves, scalars, nscalars, n, flags, ws, ws_bytes,
-                           out_dev, out_host, st, x);
+    return run_fused<float>(p, dsts, ndst, leaves, nleaves, scalars, nscalars, n, flags, ws,
+                            ws_bytes, out_dev, out_host, st, x);
+  return run_fused<double>(p, dsts, ndst, leaves, nleaves, scalars, nscalars, n, flags, ws,
+                           ws_bytes, out_dev, out_host, st, x);
 }
 
 template <class T>
@@ -741,6 +794,8 @@ int host_pipeline(int dtype, Plan& p, void* host_dst, const void* const* host_le
   if (!reduce && n == 0) return 0;
   cudaStream_t sh = (cudaStream_t)streams3[0], sc = (cudaStream_t)streams3[1],
                sd = (cudaStream_t)streams3[2];
+  if (has_dst && p.sa.nroots != 1)
+    return fail(SALT_EINVAL, "host streaming takes exactly one assignment root");
   const int nl = p.nl;
   const int nbufs_per_set = nl + (has_dst ? 1 : 0);
   // staging: [reduce workspace][chunk partials][result 256B][kNBuf x (nl leaves + dst)]
@@ -783,7 +838,7 @@ int host_pipeline(int dtype, Plan& p, void* host_dst, const void* const* host_le
     SALT_CUDA(cudaStreamWaitEvent(sc, h2d.ev[b], 0));
     if (has_dst && c >= kNBuf) SALT_CUDA(cudaStreamWaitEvent(sc, d2h.ev[b], 0));
     void* ddst = has_dst ? buf(b, nl) : nullptr;
-    rc = dispatch(dtype, p, ddst, dleaves, nleaves, scalars, nscalars, m,
+    rc = dispatch(dtype, p, &ddst, has_dst ? 1 : 0, dleaves, nleaves, scalars, nscalars, m,
                   reduce ? SALT_PARTIAL : 0, wsp, ws, reduce ? (void*)(parts + c) : nullptr,
                   nullptr, sc);
     if (rc) return rc;
@@ -798,7 +853,8 @@ int host_pipeline(int dtype, Plan& p, void* host_dst, const void* const* host_le
   if (reduce) {
     if (nchunks == 0) {
       // zero length: the sum is dtype(0) (test_engine.py:147-153)
-      rc = dispatch(dtype, p, nullptr, host_leaves, nleaves, scalars, nscalars, 0, flags, wsp, ws,
+      void* hdst = host_dst;
+      rc = dispatch(dtype, p, &hdst, has_dst ? 1 : 0, host_leaves, nleaves, scalars, nscalars, 0, flags, wsp, ws,
                     result, out_host, sc);
       if (rc) return rc;
     } else {
@@ -858,7 +914,7 @@ int salt_assign(int dtype, const char* sig, void* dst, const void* const* leaves
   Plan* p;
   int rc = make_plan(dtype, sig, nullptr, salt::MODE_ASSIGN, nleaves, nscalars, p);
   if (rc) return rc;
-  return dispatch(dtype, *p, dst, leaves, nleaves, scalars, nscalars, n, 0, nullptr, 0, nullptr,
+  return dispatch(dtype, *p, &dst, 1, leaves, nleaves, scalars, nscalars, n, 0, nullptr, 0, nullptr,
                   nullptr, (cudaStream_t)stream);
 }
 
@@ -868,7 +924,7 @@ int salt_reduce(int dtype, const char* sig, const void* const* leaves, int nleav
   Plan* p;
   int rc = make_plan(dtype, nullptr, sig, salt::MODE_REDUCE, nleaves, nscalars, p);
   if (rc) return rc;
-  return dispatch(dtype, *p, nullptr, leaves, nleaves, scalars, nscalars, n, flags, workspace,
+  return dispatch(dtype, *p, nullptr, 0, leaves, nleaves, scalars, nscalars, n, flags, workspace,
                   workspace_bytes, out_dev, out_host, (cudaStream_t)stream);
 }
 
@@ -879,7 +935,7 @@ int salt_assign_reduce(int dtype, const char* assign_sig, const char* reduce_sig
   Plan* p;
   int rc = make_plan(dtype, assign_sig, reduce_sig, salt::MODE_ASSIGN_REDUCE, nleaves, nscalars, p);
   if (rc) return rc;
-  return dispatch(dtype, *p, dst, leaves, nleaves, scalars, nscalars, n, flags, workspace,
+  return dispatch(dtype, *p, &dst, 1, leaves, nleaves, scalars, nscalars, n, flags, workspace,
                   workspace_bytes, out_dev, out_host, (cudaStream_t)stream);
 }
 
@@ -891,7 +947,7 @@ int salt_reduce_exchange(int dtype, const char* sig, const void* const* leaves, 
   Plan* p;
   int rc = make_plan(dtype, nullptr, sig, salt::MODE_REDUCE, nleaves, nscalars, p);
   if (rc) return rc;
-  return dispatch(dtype, *p, nullptr, leaves, nleaves, scalars, nscalars, n, flags, workspace,
+  return dispatch(dtype, *p, nullptr, 0, leaves, nleaves, scalars, nscalars, n, flags, workspace,
                   workspace_bytes, out_dev, out_host, (cudaStream_t)stream, exchange);
 }
 
@@ -905,7 +961,7 @@ int salt_assign_reduce_exchange(int dtype, const char* assign_sig, const char* r
   Plan* p;
   int rc = make_plan(dtype, assign_sig, reduce_sig, salt::MODE_ASSIGN_REDUCE, nleaves, nscalars, p);
   if (rc) return rc;
-  return dispatch(dtype, *p, dst, leaves, nleaves, scalars, nscalars, n, flags, workspace,
+  return dispatch(dtype, *p, &dst, 1, leaves, nleaves, scalars, nscalars, n, flags, workspace,
                   workspace_bytes, out_dev, out_host, (cudaStream_t)stream, exchange);
 }
 
@@ -927,6 +983,18 @@ int salt_exchange_emulate(int world, int rounds, uint64_t epoch0, const void* to
                                         dim3(32), params, 0, (cudaStream_t)stream));
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return 0;
+}
+
+int salt_fused(int dtype, const char* assign_sigs, const char* reduce_sig, void* const* dsts,
+               int ndst, const void* const* leaves, int nleaves, const double* scalars,
+               int nscalars, int64_t n, int flags, void* workspace, size_t workspace_bytes,
+               void* out_dev, void* out_host, void* stream) {
+  Plan* p;
+  const int mode = reduce_sig ? salt::MODE_ASSIGN_REDUCE : salt::MODE_ASSIGN;
+  int rc = make_plan(dtype, assign_sigs, reduce_sig, mode, nleaves, nscalars, p);
+  if (rc) return rc;
+  return dispatch(dtype, *p, dsts, ndst, leaves, nleaves, scalars, nscalars, n, flags, workspace,
+                  workspace_bytes, out_dev, out_host, (cudaStream_t)stream);
 }
 
 int salt_reduce_finish(int dtype, const void* partials_dev, int count, int flags, void* out_dev,

@@ -61,12 +61,16 @@ template <int I> struct S {
     return e.s[I];
   }
 };
-struct D {
+// Dk<R>: the value root R of the same fused kernel has just assigned (the
+// reduce tree of an assign+reduce kernel, or a later root of a multi-root
+// kernel, reading an earlier root's destination).  D is Dk<0>.
+template <int R> struct Dk {
   enum { NL = 0, NS = 0, USES_D = 1 };
   template <class Env> static __device__ __forceinline__ typename Env::T ev(const Env& e, int k) {
-    return e.d[k];
+    return e.d[R][k];
   }
 };
+typedef Dk<0> D;
 // Placeholder for "no tree" (reduce-only kernels have no assign tree and
 // vice versa).
 struct None {
@@ -88,8 +92,39 @@ SALT_BINARY_NODE(Sub, sub)
 SALT_BINARY_NODE(Mul, mul)
 #undef SALT_BINARY_NODE
 
+// Multi<E0, E1, ...>: several assignment roots fused into one kernel (one
+// destination each), evaluated in order per element, so root R may read the
+// new value of an earlier root's destination through Dk<R'> — the
+// sequential semantics of the same statements run one after another.
+template <class... Es> struct Multi;
+template <class E0> struct Multi<E0> {
+  enum { NL = E0::NL, NS = E0::NS, ND = 1 };
+};
+template <class E0, class E1, class... Es> struct Multi<E0, E1, Es...> {
+  enum {
+    NL = cmax(E0::NL, Multi<E1, Es...>::NL),
+    NS = cmax(E0::NS, Multi<E1, Es...>::NS),
+    ND = 1 + Multi<E1, Es...>::ND
+  };
+};
+template <int R, class... Es> struct TypeAt;
+template <class E0, class... Es> struct TypeAt<0, E0, Es...> { typedef E0 type; };
+template <int R, class E0, class... Es> struct TypeAt<R, E0, Es...> {
+  typedef typename TypeAt<R - 1, Es...>::type type;
+};
+// Roots of an assign tree: a plain tree is one root.
+template <class EA> struct Roots {
+  enum { N = 1 };
+  template <int R> struct At { typedef EA type; };
+};
+template <class... Es> struct Roots<Multi<Es...>> {
+  enum { N = sizeof...(Es) };
+  template <int R> struct At { typedef typename TypeAt<R, Es...>::type type; };
+};
+
 // ---------------------------------------------------------------- kernel ABI
-enum { MAX_LEAVES = 16, MAX_SCALARS = 32, MODE_ASSIGN = 0, MODE_REDUCE = 1, MODE_ASSIGN_REDUCE = 2 };
+enum { MAX_LEAVES = 16, MAX_SCALARS = 32, MAX_ROOTS = 4 };
+enum { MODE_ASSIGN = 0, MODE_REDUCE = 1, MODE_ASSIGN_REDUCE = 2 };
 enum { FLAG_SQRT = 1, FLAG_PARTIAL = 2 };
 
 struct DD { double hi, lo; };  // double-double partial (same layout as double2)
@@ -111,7 +146,7 @@ struct Xchg {
 
 // One by-value parameter block shared by AOT and JIT kernels.
 template <class T> struct Args {
-  T* dst;                         // assign modes
+  T* dst[MAX_ROOTS];              // assign modes: one destination per root
   const T* leaf[MAX_LEAVES];
   T sc[MAX_SCALARS];
   i64 n;                          // elements
@@ -198,11 +233,23 @@ template <class T> struct VecIO<T, 1> {
 
 // Registers of one unroll slot: V lanes of every leaf, the scalars, and the
 // assigned value (read back by D in fused assign+reduce trees).
-template <class T_, int NL, int NS, int V> struct Env {
+template <class T_, int NL, int NS, int ND, int V> struct Env {
   typedef T_ T;
   T x[NL > 0 ? NL : 1][V];
   T s[NS > 0 ? NS : 1];
-  T d[V];
+  T d[ND][V];
+};
+
+// Evaluate roots R..N-1 for the V lanes of one vector and store them.
+template <class EA, int R, int N> struct AssignRoots {
+  template <class T, class E>
+  static __device__ __forceinline__ void vec(E& e, T* const* dst, i64 off);
+  template <class T, class E>
+  static __device__ __forceinline__ void one(E& e, T* const* dst, i64 i);
+};
+template <class EA, int N> struct AssignRoots<EA, N, N> {
+  template <class T, class E> static __device__ __forceinline__ void vec(E&, T* const*, i64) {}
+  template <class T, class E> static __device__ __forceinline__ void one(E&, T* const*, i64) {}
 };
 
 // ---------------------------------------------------------------- reductions
@@ -361,6 +408,25 @@ template <class T> __device__ __forceinline__ void finish_store(DD tot, int flag
   *(T*)out = r;
 }
 
+template <class EA, int R, int N>
+template <class T, class E>
+__device__ __forceinline__ void AssignRoots<EA, R, N>::vec(E& e, T* const* dst, i64 off) {
+  typedef typename Roots<EA>::template At<R>::type Root;
+  constexpr int V = sizeof(e.d[R]) / sizeof(T);
+#pragma unroll
+  for (int k = 0; k < V; ++k) e.d[R][k] = Root::ev(e, k);
+  VecIO<T, V>::store(dst[R] + off, e.d[R]);
+  AssignRoots<EA, R + 1, N>::template vec<T>(e, dst, off);
+}
+template <class EA, int R, int N>
+template <class T, class E>
+__device__ __forceinline__ void AssignRoots<EA, R, N>::one(E& e, T* const* dst, i64 i) {
+  typedef typename Roots<EA>::template At<R>::type Root;
+  e.d[R][0] = Root::ev(e, 0);
+  dst[R][i] = e.d[R][0];
+  AssignRoots<EA, R + 1, N>::template one<T>(e, dst, i);
+}
+
 // ---------------------------------------------------------------- the kernel
 // MODE_ASSIGN:        dst[i] = EA(i)
 // MODE_REDUCE:        out    = sum_i ER(i)
@@ -378,10 +444,11 @@ __global__ void __launch_bounds__(BLOCK) fused_kernel(Args<T> a) {
   constexpr int NS = cmax(EA::NS, ER::NS);
   constexpr bool ASSIGN = MODE != MODE_REDUCE;
   constexpr bool REDUCE = MODE != MODE_ASSIGN;
-  typedef Env<T, NL, NS, V> E1;
-  typedef Env<T, NL, NS, 1> ES;
+  typedef Env<T, NL, NS, Roots<EA>::N, V> E1;
+  typedef Env<T, NL, NS, Roots<EA>::N, 1> ES;
 
   Acc<T> acc;
+  constexpr int ND = Roots<EA>::N;
   const i64 nthreads = (i64)gridDim.x * BLOCK;
   const i64 gtid = (i64)blockIdx.x * BLOCK + threadIdx.x;
 
@@ -396,10 +463,7 @@ __global__ void __launch_bounds__(BLOCK) fused_kernel(Args<T> a) {
       for (int l = 0; l < NL; ++l) e.x[l][0] = a.leaf[l][i];
 #pragma unroll
       for (int s = 0; s < NS; ++s) e.s[s] = a.sc[s];
-      if (ASSIGN) {
-        e.d[0] = EA::ev(e, 0);
-        a.dst[i] = e.d[0];
-      }
+      if (ASSIGN) AssignRoots<EA, 0, ND>::template one<T>(e, a.dst, i);
       if (REDUCE) acc.add(ER::ev(e, 0));
     }
   }
@@ -426,11 +490,7 @@ __global__ void __launch_bounds__(BLOCK) fused_kernel(Args<T> a) {
       if (j < a.nvec) {
 #pragma unroll
         for (int s = 0; s < NS; ++s) e[u].s[s] = a.sc[s];
-        if (ASSIGN) {
-#pragma unroll
-          for (int k = 0; k < V; ++k) e[u].d[k] = EA::ev(e[u], k);
-          VecIO<T, V>::store(a.dst + a.head + j * V, e[u].d);
-        }
+        if (ASSIGN) AssignRoots<EA, 0, ND>::template vec<T>(e[u], a.dst, a.head + j * V);
         if (REDUCE) {
 #pragma unroll
           for (int k = 0; k < V; ++k) acc.add(ER::ev(e[u], k));

@@ -30,6 +30,7 @@ from . import _native, runtime
 from .expressions import (
     AssignNode,
     AssignReduceNode,
+    FusedNode,
     Leaf,
     ScaleNode,
     SumNode,
@@ -46,6 +47,7 @@ __all__ = [
     "execute_assign",
     "execute_reduce",
     "execute_assign_reduce",
+    "execute_fused",
     "call_trace",
     "TraceEvent",
     "UNROLL_FACTORS",
@@ -308,6 +310,28 @@ def execute_assign_reduce(root, plan: UnrollPlan = None, *, backend: LaneBackend
         return _reduce(root.total, length, flags=_flags, lazy=lazy)
     return runtime.run_assign_reduce(lwa, lwr, root.assign.dest.vector, root.dtype, length,
                                      flags=_flags, lazy=lazy)
+
+
+def execute_fused(root, *, lazy: bool = False, _flags: int = 0):
+    """Evaluate a FusedNode: all its assignments (and its final reduction,
+    whose value is returned) in ONE pass when every vector is a plain device
+    DenseVector and the statements fit one kernel; otherwise statement by
+    statement — the same results either way."""
+    if not isinstance(root, FusedNode):
+        raise TypeError("execute_fused requires a FusedNode root")
+    length = common_length(root)
+    if len(root.assigns) <= _native.SALT_MAX_ROOTS:
+        asig, rsig, lw, dests = root.lower()
+        if _fits(lw):
+            handled, result = runtime.run_fused(asig, rsig, lw, dests, root.dtype, length,
+                                                flags=_flags, lazy=lazy)
+            if handled:
+                return result
+    for s in root.assigns:
+        _assign(s, length)
+    if root.total is not None:
+        return _reduce(root.total, length, flags=_flags, lazy=lazy)
+    return None
 
 
 def call_trace(root, plan: UnrollPlan = None, *, backend: LaneBackend = None,

@@ -31,6 +31,7 @@ __all__ = [
     "AssignNode",
     "SumNode",
     "AssignReduceNode",
+    "FusedNode",
     "LengthMismatchError",
     "as_node",
     "common_length",
@@ -83,22 +84,26 @@ class _Lowering:
     """Collects leaves (deduplicated by vector identity, numbered by first
     appearance in postfix order) and scalars (numbered by appearance)."""
 
-    __slots__ = ("tokens", "vectors", "_ids", "scalars", "occurrences", "dest_id")
+    __slots__ = ("tokens", "vectors", "_ids", "scalars", "occurrences", "dests")
 
-    def __init__(self, parent: "_Lowering" = None, dest=None):
-        # A child lowering (the reduce tree of a fused assign+reduce root)
-        # shares the parent's leaf table and scalar list; its references to
-        # the destination become `D`, the value just assigned.
+    def __init__(self, parent: "_Lowering" = None, dest=None, dests=None):
+        # A child lowering (a later tree of the same fused kernel) shares the
+        # parent's leaf table and scalar list; its references to a vector
+        # assigned earlier in the kernel become `D<k>`, the value root k has
+        # just computed (`dest` alone is root 0).
         self.tokens = []
         self.vectors = parent.vectors if parent else []
         self._ids = parent._ids if parent else {}
         self.scalars = parent.scalars if parent else []
         self.occurrences = parent.occurrences if parent else []
-        self.dest_id = id(dest) if dest is not None else None
+        self.dests = dict(dests or {})
+        if dest is not None:
+            self.dests[id(dest)] = 0
 
     def leaf(self, vector):
-        if self.dest_id is not None and id(vector) == self.dest_id:
-            self.tokens.append("D")
+        k = self.dests.get(id(vector))
+        if k is not None:
+            self.tokens.append(f"D{k}")
             return
         k = self._ids.get(id(vector))
         if k is None:
@@ -372,11 +377,71 @@ class AssignReduceNode(Expression):
         return f"AssignReduce({self.assign!r}; {self.total!r})"
 
 
-def lower(expr: Expression, parent: _Lowering = None, dest=None) -> _Lowering:
+def lower(expr: Expression, parent: _Lowering = None, dest=None, dests=None) -> _Lowering:
     """Postfix signature of an elementwise tree (leaves + scalars collected)."""
-    lw = _Lowering(parent, dest)
+    lw = _Lowering(parent, dest, dests)
     expr._postfix(lw)
     return lw
+
+
+class FusedNode(Expression):
+    """Several statements evaluated in ONE pass over memory: up to four
+    assignments and optionally one final reduction (no reference
+    counterpart — the reference runs one traversal per statement).
+
+    Per element the statements run in order, so the results are exactly
+    those of running them one after another: a statement that reads a
+    vector assigned by an earlier statement sees the new value (the kernel
+    reads it from registers, not memory).  Example, one conjugate-gradient
+    update:
+
+        FusedNode([AssignNode(x, x + a*p), AssignNode(r, r - a*q)], SumNode(r*r))
+    """
+
+    __slots__ = ("assigns", "total", "dtype")
+
+    def __init__(self, assigns, total=None):
+        assigns = list(assigns)
+        if not assigns or not all(isinstance(s, AssignNode) for s in assigns):
+            raise TypeError("FusedNode needs one or more AssignNode statements")
+        if total is not None and not isinstance(total, SumNode):
+            raise TypeError("the final statement of a FusedNode must be a SumNode")
+        dts = {s.dtype for s in assigns} | ({total.dtype} if total is not None else set())
+        if len(dts) != 1:
+            raise TypeError(f"mixed element types in fused statements: {sorted(map(str, dts))}")
+        self.assigns = assigns
+        self.total = total
+        self.dtype = assigns[0].dtype
+
+    @property
+    def register_footprint(self) -> int:
+        fp = sum(s.register_footprint for s in self.assigns)
+        return fp + (self.total.register_footprint if self.total is not None else 0)
+
+    def leaves(self):
+        for s in self.assigns:
+            yield from s.leaves()
+        if self.total is not None:
+            yield from self.total.leaves()
+
+    def lower(self):
+        """(assign signature with roots joined by ' ; ', reduce signature or
+        None, shared _Lowering, destination vectors)."""
+        lw = _Lowering()
+        parts, dests, written = [], [], {}
+        for k, s in enumerate(self.assigns):
+            sub = lower(s.source, parent=lw, dests=written)
+            parts.append(" ".join(sub.tokens))
+            dests.append(s.dest.vector)
+            written[id(s.dest.vector)] = k
+        rsig = None
+        if self.total is not None:
+            rsig = " ".join(lower(self.total.child, parent=lw, dests=written).tokens)
+        return " ; ".join(parts), rsig, lw, dests
+
+    def __repr__(self):
+        body = "; ".join(repr(s) for s in self.assigns)
+        return f"Fused({body}" + (f"; {self.total!r})" if self.total is not None else ")")
 
 
 def traffic(root: Expression) -> dict:

@@ -16,10 +16,18 @@ synchronisation (for solver loops).
 """
 
 from . import _native
-from .engine import execute_assign, execute_assign_reduce, execute_reduce
-from .expressions import AssignNode, AssignReduceNode, MulNode, ScaleNode, SumNode, as_node
+from .engine import execute_assign, execute_assign_reduce, execute_fused, execute_reduce
+from .expressions import (
+    AssignNode,
+    AssignReduceNode,
+    FusedNode,
+    MulNode,
+    ScaleNode,
+    SumNode,
+    as_node,
+)
 
-__all__ = ["dot", "scal", "axpy", "scaled_copy", "sum", "norm2", "axpy_dot"]
+__all__ = ["dot", "scal", "axpy", "scaled_copy", "sum", "norm2", "axpy_dot", "fused"]
 
 
 def dot(x, y, **options):
@@ -64,3 +72,23 @@ def axpy_dot(alpha, x, y, z, **options):
         SumNode(MulNode(as_node(y), as_node(z))),
     )
     return execute_assign_reduce(root, **options)
+
+
+def fused(*statements, lazy=False):
+    """Run statements in one pass: `(dest, expression)` pairs for
+    assignments, optionally a final bare expression to sum, e.g. a
+    conjugate-gradient update
+
+        rr = lv.fused((x, x + a * p), (r, r - a * q), r * r)
+
+    Same results as running them one after another (later statements see
+    earlier assignments); returns the sum, or None without one."""
+    assigns, total = [], None
+    for k, st in enumerate(statements):
+        if isinstance(st, tuple) and len(st) == 2:
+            assigns.append(AssignNode(as_node(st[0]), as_node(st[1])))
+        elif k == len(statements) - 1:
+            total = SumNode(as_node(st))
+        else:
+            raise TypeError("only the last statement may be a bare expression (the sum)")
+    return execute_fused(FusedNode(assigns, total), lazy=lazy)

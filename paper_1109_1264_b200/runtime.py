@@ -32,7 +32,7 @@ from . import _native
 from .lanes import as_dtype
 from .vectors import DenseVector, DeviceScalar
 
-__all__ = ["run_assign", "run_reduce", "run_assign_reduce", "Placement"]
+__all__ = ["run_assign", "run_reduce", "run_assign_reduce", "run_fused", "Placement"]
 
 _ws_lock = threading.Lock()
 _workspaces = {}
@@ -413,3 +413,34 @@ def run_assign_reduce(lwa, lwr, dest, dtype, n, flags=0, lazy=False):
             code, asig, rsig, dptr, leaves, nl, scal, ns, m, fl, ws, wsb, x, od, oh, st)
 
     return _run_reduction(lwa, dest, dt, n, flags, lazy, make_call, host_call, make_xcall)
+
+
+def run_fused(asig, rsig, lw, dests, dtype, n, flags=0, lazy=False):
+    """Multi-root fused evaluation (salt_fused).  Returns (handled, result):
+    not handled unless every leaf and destination is a plain device
+    DenseVector on one device (the caller then runs the statements one by
+    one)."""
+    fast = _fast(list(lw.vectors) + list(dests), None)
+    if fast is None:
+        return False, None
+    dev, ptrs, _ = fast
+    nl = len(lw.vectors)
+    leaves, keep_l = _native.ptr_array(ptrs[:nl])
+    dsts, keep_d = _native.ptr_array(ptrs[nl:])
+    scal, keep_s = _native.double_array(lw.scalars)
+    dt = as_dtype(dtype)
+    code = _dtype_code(dt)
+    lib = _native.lib()
+    a, r = asig.encode(), (rsig.encode() if rsig is not None else None)
+    with _OnDevice(dev):
+        if rsig is None:
+            _native.check(lib.salt_fused(code, a, None, dsts, len(dests), leaves, nl, scal,
+                                         len(lw.scalars), n, 0, None, 0, None, None,
+                                         _raw_stream(dev)))
+            return True, None
+
+        def call(fl, ws, wsb, od, oh, st):
+            return lib.salt_fused(code, a, r, dsts, len(dests), leaves, nl, scal, len(lw.scalars),
+                                  n, fl, ws, wsb, od, oh, st)
+
+        return True, _device_reduce(dev, dt, call, flags, lazy)

@@ -1,0 +1,111 @@
+"""Multi-statement fusion (FusedNode / lv.fused / salt_fused): several
+assignments and a final reduction in one pass, with the results of running
+the statements one after another."""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_1109_1264_b200 as lv
+from conftest import NP, same_bits
+from oracle import restate
+from paper_1109_1264_b200 import _native
+from paper_1109_1264_b200.expressions import AssignNode, FusedNode, SumNode, as_node
+
+pytestmark = pytest.mark.gpu
+TOL = {"f32": 1e-5, "f64": 1e-12}
+
+
+def dev(v, dt):
+    return lv.DenseVector.from_values(v, dt, device="cuda")
+
+
+@pytest.mark.parametrize("dt", ["f32", "f64"])
+def test_cg_update_one_pass_matches_sequential(dt):
+    g = np.random.default_rng(21)
+    for n in (1, 7, 1000, 65_537, 1 << 20):
+        x, p, r, q = (g.uniform(-1, 1, n).astype(NP[dt]) for _ in range(4))
+        a = 0.3125
+        X, P, R, Q = (dev(v, dt) for v in (x, p, r, q))
+        launches = _native.lib().salt_launch_count()
+        rr = lv.fused((X, X + a * P), (R, R - a * Q), R * R)
+        torch.cuda.synchronize()
+        assert _native.lib().salt_launch_count() - launches == 1  # one kernel
+        x1 = restate.eval_sig("L0 S0 L1 * +", [x, p], [a], dt)
+        r1 = restate.eval_sig("L0 S0 L1 * -", [r, q], [a], dt)
+        assert same_bits(X.to_array(), x1) and same_bits(R.to_array(), r1)
+        exact = restate.exact_sum(r1 * r1)
+        assert abs(float(rr) - exact) <= TOL[dt] * exact
+        assert type(rr) is NP[dt]
+
+
+def test_later_statements_see_earlier_assignments():
+    g = np.random.default_rng(22)
+    n = 50_001
+    for dt in ("f32", "f64"):
+        a, b, c = (g.uniform(-1, 1, n).astype(NP[dt]) for _ in range(3))
+        A, B, C = (dev(v, dt) for v in (a, b, c))
+        # b = a + b ; c = b * c (new b) ; b = c - b (new c, new b) ; sum(a + c)
+        s = lv.fused((B, A + B), (C, B * C), (B, C - B), A + C)
+        b1 = restate.eval_sig("L0 L1 +", [a, b], [], dt)
+        c1 = restate.eval_sig("L0 L1 *", [b1, c], [], dt)
+        b2 = restate.eval_sig("L0 L1 -", [c1, b1], [], dt)
+        assert same_bits(B.to_array(), b2) and same_bits(C.to_array(), c1)
+        assert same_bits(A.to_array(), a)
+        exact = restate.exact_sum(restate.eval_sig("L0 L1 +", [a, c1], [], dt))
+        assert abs(float(s) - exact) <= TOL[dt] * abs(exact)
+
+
+def test_assign_only_fusion_and_lazy_result():
+    g = np.random.default_rng(23)
+    n = 100_003
+    a, b = g.uniform(-1, 1, n), g.uniform(-1, 1, n)
+    A, B = dev(a, "f64"), dev(b, "f64")
+    D1, D2 = lv.DenseVector.zeros(n, "f64", device="cuda"), lv.DenseVector.zeros(n, "f64", device="cuda")
+    assert lv.fused((D1, A + B), (D2, A - B)) is None
+    assert same_bits(D1.to_array(), a + b) and same_bits(D2.to_array(), a - b)
+    r = lv.fused((D1, 2.0 * D1), D1 * D2, lazy=True)
+    assert isinstance(r, lv.DeviceScalar)
+    d1 = 2.0 * (a + b)
+    assert abs(float(r.item()) - restate.exact_sum(d1 * (a - b))) <= 1e-12 * abs(restate.exact_sum(np.abs(d1 * (a - b))))
+
+
+def test_fallback_runs_statements_one_by_one():
+    """CountingVector operands (not plain device vectors) take the
+    statement-by-statement path: same values, the reference's traffic."""
+    x = lv.CountingVector.from_values(np.arange(100.0), "f64", device="cuda")
+    y = lv.CountingVector.from_values(np.ones(100), "f64", device="cuda")
+    s = lv.fused((y, as_node(y) + 2.0 * as_node(x)), y * y)
+    want = 1.0 + 2.0 * np.arange(100.0)
+    assert y.to_values() == list(want) and s == np.sum(want * want)
+    assert x.read_count == 100 and y.write_count == 100
+
+
+def test_fused_update_is_faster_than_separate_passes():
+    """x += a p; r -= a q; rr = r.r moves 4 reads + 2 writes once fused
+    instead of 4 reads + 2 writes + 1 extra read of r in three passes."""
+    n = 1 << 26
+    X, P, R, Q = (lv.DenseVector.from_tensor(torch.rand(n, dtype=torch.float64, device="cuda"))
+                  for _ in range(4))
+
+    def t(fn):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(10):
+            fn()
+        e.record()
+        e.synchronize()
+        return s.elapsed_time(e) / 10
+
+    fused = t(lambda: lv.fused((X, X + 0.5 * P), (R, R - 0.5 * Q), R * R, lazy=True))
+
+    def separate():
+        lv.axpy(0.5, P, X)
+        R.assign(R - 0.5 * Q)
+        lv.dot(R, R, lazy=True)
+
+    sep = t(separate)
+    assert sep / fused >= 1.15, (sep, fused)

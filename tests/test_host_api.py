@@ -213,7 +213,15 @@ def test_lowering_signatures_of_named_ops_and_configs():
     y, x, z = hv([1.0]), hv([2.0]), hv([3.0])
     lwa = lower(as_node(y) + ScaleNode(0.5, as_node(x)))
     lwr = lower(as_node(y) * as_node(z), parent=lwa, dest=y)
-    assert " ".join(lwa.tokens) == "L0 S0 L1 * +" and " ".join(lwr.tokens) == "D L2 *"
+    assert " ".join(lwa.tokens) == "L0 S0 L1 * +" and " ".join(lwr.tokens) == "D0 L2 *"
+    # multi-statement fusion: later statements read earlier destinations as D<k>
+    p, q = hv([4.0]), hv([5.0])
+    fz = lv.FusedNode([AssignNode(as_node(x), as_node(x) + 0.5 * as_node(p)),
+                       AssignNode(as_node(y), as_node(y) - 0.5 * as_node(q) + as_node(x))],
+                      SumNode(as_node(y) * as_node(y)))
+    asig, rsig, lw2, dests = fz.lower()
+    assert asig == "L0 S0 L1 * + ; L2 S1 L3 * - D0 +" and rsig == "D1 D1 *"
+    assert lw2.vectors == [x, p, y, q] and dests == [x, y]
 
 
 def test_building_touches_no_elements():
