@@ -273,6 +273,33 @@ def c5(out, gpu):
             per_step_s=el / 100, gbs=b * 100 / el / 1e9, pct_hbm=b * 100 / el / 1e9 / PEAK,
             r_last=float(rs[-1].item()), gpu=gpu,
             note="credited bytes 4*8*n per step (fused compulsory traffic)")
+    # a whole CG update (x += a p; r -= a q; rr = r.r) fused vs three passes
+    P = Z
+    Q = lv.DenseVector.empty(n, "f64", device="cuda")
+    Q.tensor.copy_(X.tensor)
+    R = Y
+    for mode in ("fused", "three-pass"):
+        if mode == "fused":
+            step = lambda: lv.fused((X, X + al * P), (R, R - al * Q), R * R, lazy=True)
+        else:
+            def step():
+                lv.axpy(al, P, X)
+                R.assign(R - al * Q)
+                return lv.dot(R, R, lazy=True)
+        for _ in range(3):
+            step()
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(20):
+            step()
+        e.record()
+        e.synchronize()
+        el = s.elapsed_time(e) / 1e3 / 20
+        b = 48.0 * n  # 4 reads + 2 writes, fused compulsory traffic
+        rec(out, config=5, op=f"cg_update-{mode}", dtype="f64", n_per_gpu=n, per_step_s=el,
+            gbs=b / el / 1e9, pct_hbm=b / el / 1e9 / PEAK, gpu=gpu,
+            note="x += a p; r -= a q; rr = r.r; credited bytes 6*8*n per step")
 
 
 if __name__ == "__main__":
