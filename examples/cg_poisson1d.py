@@ -76,6 +76,30 @@ def cg(b: lv.DenseVector, iters: int, tol: float = 1e-10):
     return u, k, (rr / rr0) ** 0.5
 
 
+class DeviceCG:
+    """The same CG iteration with every scalar kept on the device
+    (DeviceScalar): no host synchronisation per iteration, so step() can be
+    captured in a CUDA graph and replayed."""
+
+    def __init__(self, b: lv.DenseVector):
+        n = len(b)
+        self.u = lv.DenseVector.zeros(n, "f64")
+        self.r = lv.DenseVector.zeros(n, "f64")
+        self.r.assign(b)
+        self.p = lv.DenseVector.zeros(n, "f64")
+        self.p.assign(self.r)
+        self.q = lv.DenseVector.zeros(n, "f64")
+        self.rr = lv.dot(self.r, self.r, lazy=True)
+
+    def step(self):
+        u, r, p, q = self.u, self.r, self.p, self.q
+        matvec(q, p)
+        alpha = self.rr / lv.dot(p, q, lazy=True)
+        rr_new = lv.fused((u, u + alpha * p), (r, r - alpha * q), r * r, lazy=True)
+        p.assign(r + (rr_new / self.rr) * p)
+        self.rr = rr_new
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--n", type=int, default=1 << 20)
@@ -94,8 +118,36 @@ def main():
     au[1:] -= ut[:-1]
     au[:-1] -= ut[1:]
     res = float(torch.linalg.vector_norm(bt - au) / torch.linalg.vector_norm(bt))
-    print(f"n={a.n} iterations={k} relative residual (CG recurrence) {rel:.3e}, "
+    print(f"host-scalar CG: n={a.n} iterations={k} relative residual (CG recurrence) {rel:.3e}, "
           f"recomputed {res:.3e}, {dt * 1e3:.1f} ms ({dt / k * 1e6:.1f} us/iteration)")
+
+    # device-resident scalars, eager and captured in a CUDA graph
+    cg_dev = DeviceCG(b)
+    cg_dev.step()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(k):
+        cg_dev.step()
+    torch.cuda.synchronize()
+    de = time.perf_counter() - t0
+    cg_g = DeviceCG(b)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        cg_g.step()
+    torch.cuda.current_stream().wait_stream(s)
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        cg_g.step()
+    graph.replay()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(k):
+        graph.replay()
+    torch.cuda.synchronize()
+    dg = time.perf_counter() - t0
+    print(f"device-scalar CG: {de / k * 1e6:.1f} us/iteration eager, "
+          f"{dg / k * 1e6:.1f} us/iteration as a CUDA graph")
 
 
 if __name__ == "__main__":

@@ -113,11 +113,18 @@ int salt_assign_reduce(int dtype, const char* assign_sig, const char* reduce_sig
  * order, so the result equals running the statements one after another,
  * e.g. a conjugate-gradient update
  *     x = x + a*p ; r = r - a*q ; rr = sum(r*r)
- *     "L0 S0 L1 * + ; L2 S1 L3 * -"  with  "D1 D1 *",  dsts {x, r}. */
+ *     "L0 S0 L1 * + ; L2 S1 L3 * -"  with  "D1 D1 *",  dsts {x, r}.
+ * assign_sigs may be NULL (a pure reduction).  Trees may also read up to
+ * SALT_MAX_PSCALARS scalars from DEVICE memory as P<k> (pscalars[k] points
+ * to one element of `dtype`): a solver's alpha computed on the GPU is used
+ * without a host round trip, so whole iterations can be graph-captured. */
+#define SALT_MAX_PSCALARS 8
 #define SALT_MAX_ROOTS 4
 int salt_fused(int dtype, const char* assign_sigs, const char* reduce_sig,
                void* const* dsts, int ndst, const void* const* leaves, int nleaves,
-               const double* scalars, int nscalars, int64_t n, int flags,
+               const double* scalars, int nscalars,
+               const void* const* pscalars, int npscalars,
+               int64_t n, int flags,
                void* workspace, size_t workspace_bytes,
                void* out_dev, void* out_host, void* stream);
 

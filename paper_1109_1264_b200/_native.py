@@ -28,6 +28,7 @@ SALT_WORKSPACE_TICKET_BYTES = 16640
 SALT_MAX_LEAVES = 16
 SALT_MAX_SCALARS = 32
 SALT_MAX_ROOTS = 4
+SALT_MAX_PSCALARS = 8
 SALT_F32 = 0
 SALT_F64 = 1
 SALT_SQRT = 1
@@ -80,8 +81,8 @@ _SIGNATURES = {
     ),
     "salt_fused": (
         _c_int,
-        [_c_int, _c_str, _c_str, _c_vpp, _c_int, _c_vpp, _c_int, _c_dp, _c_int, _c_i64, _c_int,
-         _c_vp, _c_size, _c_vp, _c_vp, _c_vp],
+        [_c_int, _c_str, _c_str, _c_vpp, _c_int, _c_vpp, _c_int, _c_dp, _c_int, _c_vpp, _c_int,
+         _c_i64, _c_int, _c_vp, _c_size, _c_vp, _c_vp, _c_vp],
     ),
     "salt_reduce_finish": (_c_int, [_c_int, _c_vp, _c_int, _c_int, _c_vp, _c_vp, _c_vp]),
     "salt_assign_host": (
@@ -179,7 +180,7 @@ def fastpath():
 
                 from . import _fastpath, runtime
                 from .expressions import AddNode, Leaf, MulNode, ScaleNode, SubNode
-                from .vectors import DenseVector
+                from .vectors import DenseVector, DeviceScalar
                 import numpy as np
 
                 h = lib()
@@ -187,7 +188,7 @@ def fastpath():
                 _fastpath.init(
                     addr(h.salt_assign), addr(h.salt_reduce), addr(h.salt_assign_reduce),
                     addr(h.salt_last_error), h.salt_reduce_workspace_bytes(),
-                    Leaf, AddNode, SubNode, MulNode, ScaleNode, DenseVector,
+                    Leaf, AddNode, SubNode, MulNode, ScaleNode, DenseVector, DeviceScalar,
                     torch._C._cuda_getCurrentRawStream, torch.cuda.current_device,
                     runtime._workspace, np.float32, np.float64, runtime._lazy_out,
                 )

@@ -41,7 +41,7 @@ static assign_reduce_fn p_assign_reduce;
 static last_error_fn p_last_error;
 static size_t ws_bytes;
 
-static PyObject *T_Leaf, *T_Add, *T_Sub, *T_Mul, *T_Scale, *T_Dense;
+static PyObject *T_Leaf, *T_Add, *T_Sub, *T_Mul, *T_Scale, *T_Dense, *T_DevScalar;
 static PyObject *get_stream, *current_device, *workspace_fn, *np_f32, *np_f64, *lazy_out;
 static PyObject *s_vector, *s_left, *s_right, *s_child, *s_alpha, *s_ptr, *s_dev, *s_n, *s_code,
     *s_data_ptr;
@@ -113,6 +113,10 @@ static int walk(Walk* w, PyObject* node) {
     if (w->nsc == MAX_SCALARS) return 0;
     PyObject* a = PyObject_GetAttr(node, s_alpha);
     if (!a) return -1;
+    if ((PyObject*)Py_TYPE(a) == T_DevScalar) { /* device-resident alpha: Python path */
+      Py_DECREF(a);
+      return 0;
+    }
     double v = PyFloat_AsDouble(a); /* alpha is already element-typed */
     Py_DECREF(a);
     if (v == -1.0 && PyErr_Occurred()) return -1;
@@ -329,12 +333,12 @@ static PyObject* fp_assign_reduce(PyObject* self, PyObject* args) {
 static PyObject* fp_init(PyObject* self, PyObject* args) {
   unsigned long long a, r, ar, le;
   Py_ssize_t wsb;
-  if (!PyArg_ParseTuple(args, "KKKKnOOOOOOOOOOOO", &a, &r, &ar, &le, &wsb, &T_Leaf, &T_Add, &T_Sub,
-                        &T_Mul, &T_Scale, &T_Dense, &get_stream, &current_device, &workspace_fn,
-                        &np_f32, &np_f64, &lazy_out))
+  if (!PyArg_ParseTuple(args, "KKKKnOOOOOOOOOOOOO", &a, &r, &ar, &le, &wsb, &T_Leaf, &T_Add,
+                        &T_Sub, &T_Mul, &T_Scale, &T_Dense, &T_DevScalar, &get_stream,
+                        &current_device, &workspace_fn, &np_f32, &np_f64, &lazy_out))
     return NULL;
-  PyObject* keep[] = {T_Leaf, T_Add, T_Sub, T_Mul, T_Scale, T_Dense, get_stream, current_device,
-                      workspace_fn, np_f32, np_f64, lazy_out};
+  PyObject* keep[] = {T_Leaf, T_Add, T_Sub, T_Mul, T_Scale, T_Dense, T_DevScalar, get_stream,
+                      current_device, workspace_fn, np_f32, np_f64, lazy_out};
   for (size_t i = 0; i < sizeof keep / sizeof keep[0]; ++i) Py_INCREF(keep[i]);
   p_assign = (assign_fn)(uintptr_t)a;
   p_reduce = (reduce_fn)(uintptr_t)r;

@@ -89,7 +89,7 @@ int cuda_fail(cudaError_t e, const char* what) {
 struct Sig {
   std::string canon;  // tokens joined by single spaces (roots joined by " ; ")
   std::string type;   // C++ type of the tree, e.g. salt::Add<salt::L<0>,salt::L<1>>
-  int nl = 0, ns = 0;
+  int nl = 0, ns = 0, np = 0;
   int nroots = 0;     // assignment roots (Multi<...> when > 1)
   bool uses_d = false;
 };
@@ -136,6 +136,10 @@ std::string parse_tree(const std::string& s, int d_limit, Sig& out) {
       if (k >= salt::MAX_SCALARS) return "scalar index out of range: " + t;
       out.ns = std::max(out.ns, k + 1);
       st.push_back("salt::S<" + std::to_string(k) + ">");
+    } else if (t[0] == 'P' && parse_index(t, 1, k)) {
+      if (k >= salt::MAX_PSCALARS) return "device scalar index out of range: " + t;
+      out.np = std::max(out.np, k + 1);
+      st.push_back("salt::P<" + std::to_string(k) + ">");
     } else if (t[0] == 'D' && (t.size() == 1 || parse_index(t, 1, k)) && d_limit > 0) {
       if (t.size() == 1) k = 0;
       if (k >= d_limit) return "'" + t + "' reads a root that is not computed before it";
@@ -177,6 +181,7 @@ std::string parse_assign(const char* s, Sig& out) {
     if (!err.empty()) return err;
     out.nl = std::max(out.nl, r.nl);
     out.ns = std::max(out.ns, r.ns);
+    out.np = std::max(out.np, r.np);
     out.uses_d = out.uses_d || r.uses_d;
     if (!out.canon.empty()) out.canon += " ; ";
     out.canon += r.canon;
@@ -592,7 +597,7 @@ void geometry(void* const* dsts, int ndst, const void* const* leaves, int nl, i6
 struct Plan {
   Sig sa, sr;
   int mode = 0;
-  int nl = 0, ns = 0;
+  int nl = 0, ns = 0, np = 0;
   Kernel* cached[2][2] = {};  // [force_jit][vec == 1]: table / JIT lookups done once
 };
 
@@ -627,6 +632,7 @@ int make_plan(int dtype, const char* asig, const char* rsig, int mode, int nleav
     }
     np->nl = std::max(np->sa.nl, np->sr.nl);
     np->ns = std::max(np->sa.ns, np->sr.ns);
+    np->np = std::max(np->sa.np, np->sr.np);
     if (cache.size() > 4096) cache.clear();
     p = np.get();
     cache.emplace(std::move(key), std::move(np));
@@ -644,7 +650,8 @@ int make_plan(int dtype, const char* asig, const char* rsig, int mode, int nleav
 template <class T>
 int run_fused(Plan& p, void* const* dsts, int ndst, const void* const* leaves, int nleaves,
               const double* scalars, int nscalars, i64 n, int flags, void* ws, size_t ws_bytes,
-              void* out_dev, void* out_host, cudaStream_t st, const salt_exchange* x) {
+              void* out_dev, void* out_host, cudaStream_t st, const salt_exchange* x,
+              const void* const* pscalars, int npscalars) {
   if (n < 0) return fail(SALT_EINVAL, "negative length");
   const bool reduce = p.mode != salt::MODE_ASSIGN;
   if (!reduce && n == 0) return 0;  // zero length assign is a no-op (test_engine.py:147-153)
@@ -669,6 +676,13 @@ int run_fused(Plan& p, void* const* dsts, int ndst, const void* const* leaves, i
   for (int r = 0; r < nroots; ++r) a.dst[r] = (T*)dsts[r];
   for (int l = 0; l < p.nl; ++l) a.leaf[l] = leaves ? (const T*)leaves[l] : nullptr;
   for (int s = 0; s < p.ns; ++s) a.sc[s] = (T)scalars[s];
+  if (npscalars < p.np || npscalars > salt::MAX_PSCALARS)
+    return fail(SALT_EINVAL, "signature reads " + std::to_string(p.np) + " device scalars but " +
+                                 std::to_string(npscalars) + " were passed");
+  for (int q = 0; q < p.np; ++q) {
+    if (!pscalars || !pscalars[q]) return fail(SALT_EINVAL, "NULL device scalar");
+    a.ps[q] = (const T*)pscalars[q];
+  }
   a.n = n;
   a.flags = flags;
   int vec;
@@ -743,12 +757,13 @@ int run_fused(Plan& p, void* const* dsts, int ndst, const void* const* leaves, i
 int dispatch(int dtype, Plan& p, void* const* dsts, int ndst, const void* const* leaves,
              int nleaves, const double* scalars, int nscalars, i64 n, int flags, void* ws,
              size_t ws_bytes, void* out_dev, void* out_host, cudaStream_t st,
-             const salt_exchange* x = nullptr) {
+             const salt_exchange* x = nullptr, const void* const* pscalars = nullptr,
+             int npscalars = 0) {
   if (dtype == SALT_F32)
     return run_fused<float>(p, dsts, ndst, leaves, nleaves, scalars, nscalars, n, flags, ws,
-                            ws_bytes, out_dev, out_host, st, x);
+                            ws_bytes, out_dev, out_host, st, x, pscalars, npscalars);
   return run_fused<double>(p, dsts, ndst, leaves, nleaves, scalars, nscalars, n, flags, ws,
-                           ws_bytes, out_dev, out_host, st, x);
+                           ws_bytes, out_dev, out_host, st, x, pscalars, npscalars);
 }
 
 template <class T>
@@ -987,14 +1002,18 @@ int salt_exchange_emulate(int world, int rounds, uint64_t epoch0, const void* to
 
 int salt_fused(int dtype, const char* assign_sigs, const char* reduce_sig, void* const* dsts,
                int ndst, const void* const* leaves, int nleaves, const double* scalars,
-               int nscalars, int64_t n, int flags, void* workspace, size_t workspace_bytes,
-               void* out_dev, void* out_host, void* stream) {
+               int nscalars, const void* const* pscalars, int npscalars, int64_t n, int flags,
+               void* workspace, size_t workspace_bytes, void* out_dev, void* out_host,
+               void* stream) {
   Plan* p;
-  const int mode = reduce_sig ? salt::MODE_ASSIGN_REDUCE : salt::MODE_ASSIGN;
+  if (!assign_sigs && !reduce_sig) return fail(SALT_EINVAL, "nothing to evaluate");
+  const int mode = !assign_sigs ? salt::MODE_REDUCE
+                   : reduce_sig ? salt::MODE_ASSIGN_REDUCE : salt::MODE_ASSIGN;
   int rc = make_plan(dtype, assign_sigs, reduce_sig, mode, nleaves, nscalars, p);
   if (rc) return rc;
   return dispatch(dtype, *p, dsts, ndst, leaves, nleaves, scalars, nscalars, n, flags, workspace,
-                  workspace_bytes, out_dev, out_host, (cudaStream_t)stream);
+                  workspace_bytes, out_dev, out_host, (cudaStream_t)stream, nullptr, pscalars,
+                  npscalars);
 }
 
 int salt_reduce_finish(int dtype, const void* partials_dev, int count, int flags, void* out_dev,

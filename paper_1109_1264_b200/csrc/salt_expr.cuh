@@ -50,13 +50,13 @@ __host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
 // Each node exposes: NL (leaves referenced = max index + 1), NS (scalars),
 // USES_D (reads the just-assigned value) and ev(env, k) for lane k.
 template <int I> struct L {
-  enum { NL = I + 1, NS = 0, USES_D = 0 };
+  enum { NL = I + 1, NS = 0, NP = 0, USES_D = 0 };
   template <class Env> static __device__ __forceinline__ typename Env::T ev(const Env& e, int k) {
     return e.x[I][k];
   }
 };
 template <int I> struct S {
-  enum { NL = 0, NS = I + 1, USES_D = 0 };
+  enum { NL = 0, NS = I + 1, NP = 0, USES_D = 0 };
   template <class Env> static __device__ __forceinline__ typename Env::T ev(const Env& e, int) {
     return e.s[I];
   }
@@ -64,8 +64,16 @@ template <int I> struct S {
 // Dk<R>: the value root R of the same fused kernel has just assigned (the
 // reduce tree of an assign+reduce kernel, or a later root of a multi-root
 // kernel, reading an earlier root's destination).  D is Dk<0>.
+// P<I>: a scalar read from device memory (a DeviceScalar operand: e.g. the
+// alpha of a solver step computed on the GPU), loaded once per thread.
+template <int I> struct P {
+  enum { NL = 0, NS = 0, NP = I + 1, USES_D = 0 };
+  template <class Env> static __device__ __forceinline__ typename Env::T ev(const Env& e, int) {
+    return e.p[I];
+  }
+};
 template <int R> struct Dk {
-  enum { NL = 0, NS = 0, USES_D = 1 };
+  enum { NL = 0, NS = 0, NP = 0, USES_D = 1 };
   template <class Env> static __device__ __forceinline__ typename Env::T ev(const Env& e, int k) {
     return e.d[R][k];
   }
@@ -74,7 +82,7 @@ typedef Dk<0> D;
 // Placeholder for "no tree" (reduce-only kernels have no assign tree and
 // vice versa).
 struct None {
-  enum { NL = 0, NS = 0, USES_D = 0 };
+  enum { NL = 0, NS = 0, NP = 0, USES_D = 0 };
   template <class Env> static __device__ __forceinline__ typename Env::T ev(const Env&, int) {
     return typename Env::T(0);
   }
@@ -82,7 +90,8 @@ struct None {
 
 #define SALT_BINARY_NODE(NAME, FN)                                                       \
   template <class A, class B> struct NAME {                                              \
-    enum { NL = cmax(A::NL, B::NL), NS = cmax(A::NS, B::NS), USES_D = A::USES_D | B::USES_D }; \
+    enum { NL = cmax(A::NL, B::NL), NS = cmax(A::NS, B::NS), NP = cmax(A::NP, B::NP),      \
+           USES_D = A::USES_D | B::USES_D };                                             \
     template <class Env> static __device__ __forceinline__ typename Env::T ev(const Env& e, int k) { \
       return Arith<typename Env::T>::FN(A::ev(e, k), B::ev(e, k));                      \
     }                                                                                    \
@@ -98,12 +107,13 @@ SALT_BINARY_NODE(Mul, mul)
 // sequential semantics of the same statements run one after another.
 template <class... Es> struct Multi;
 template <class E0> struct Multi<E0> {
-  enum { NL = E0::NL, NS = E0::NS, ND = 1 };
+  enum { NL = E0::NL, NS = E0::NS, NP = E0::NP, ND = 1 };
 };
 template <class E0, class E1, class... Es> struct Multi<E0, E1, Es...> {
   enum {
     NL = cmax(E0::NL, Multi<E1, Es...>::NL),
     NS = cmax(E0::NS, Multi<E1, Es...>::NS),
+    NP = cmax(E0::NP, Multi<E1, Es...>::NP),
     ND = 1 + Multi<E1, Es...>::ND
   };
 };
@@ -123,7 +133,7 @@ template <class... Es> struct Roots<Multi<Es...>> {
 };
 
 // ---------------------------------------------------------------- kernel ABI
-enum { MAX_LEAVES = 16, MAX_SCALARS = 32, MAX_ROOTS = 4 };
+enum { MAX_LEAVES = 16, MAX_SCALARS = 32, MAX_ROOTS = 4, MAX_PSCALARS = 8 };
 enum { MODE_ASSIGN = 0, MODE_REDUCE = 1, MODE_ASSIGN_REDUCE = 2 };
 enum { FLAG_SQRT = 1, FLAG_PARTIAL = 2 };
 
@@ -149,6 +159,7 @@ template <class T> struct Args {
   T* dst[MAX_ROOTS];              // assign modes: one destination per root
   const T* leaf[MAX_LEAVES];
   T sc[MAX_SCALARS];
+  const T* ps[MAX_PSCALARS];      // device-resident scalars (P<k>)
   i64 n;                          // elements
   i64 head;                       // scalar elements before the first aligned vector
   i64 nvec;                       // aligned vectors of V elements after `head`
@@ -233,10 +244,11 @@ template <class T> struct VecIO<T, 1> {
 
 // Registers of one unroll slot: V lanes of every leaf, the scalars, and the
 // assigned value (read back by D in fused assign+reduce trees).
-template <class T_, int NL, int NS, int ND, int V> struct Env {
+template <class T_, int NL, int NS, int NP, int ND, int V> struct Env {
   typedef T_ T;
   T x[NL > 0 ? NL : 1][V];
   T s[NS > 0 ? NS : 1];
+  T p[NP > 0 ? NP : 1];
   T d[ND][V];
 };
 
@@ -442,10 +454,14 @@ template <class T, class EA, class ER, int MODE, int V, int UNR, int BLOCK>
 __global__ void __launch_bounds__(BLOCK) fused_kernel(Args<T> a) {
   constexpr int NL = cmax(EA::NL, ER::NL);
   constexpr int NS = cmax(EA::NS, ER::NS);
+  constexpr int NP = cmax(EA::NP, ER::NP);
   constexpr bool ASSIGN = MODE != MODE_REDUCE;
   constexpr bool REDUCE = MODE != MODE_ASSIGN;
-  typedef Env<T, NL, NS, Roots<EA>::N, V> E1;
-  typedef Env<T, NL, NS, Roots<EA>::N, 1> ES;
+  typedef Env<T, NL, NS, NP, Roots<EA>::N, V> E1;
+  typedef Env<T, NL, NS, NP, Roots<EA>::N, 1> ES;
+  T pv[NP > 0 ? NP : 1];  // device scalars, loaded once per thread
+#pragma unroll
+  for (int q = 0; q < NP; ++q) pv[q] = __ldg(a.ps[q]);
 
   Acc<T> acc;
   constexpr int ND = Roots<EA>::N;
@@ -463,6 +479,8 @@ __global__ void __launch_bounds__(BLOCK) fused_kernel(Args<T> a) {
       for (int l = 0; l < NL; ++l) e.x[l][0] = a.leaf[l][i];
 #pragma unroll
       for (int s = 0; s < NS; ++s) e.s[s] = a.sc[s];
+#pragma unroll
+      for (int q = 0; q < NP; ++q) e.p[q] = pv[q];
       if (ASSIGN) AssignRoots<EA, 0, ND>::template one<T>(e, a.dst, i);
       if (REDUCE) acc.add(ER::ev(e, 0));
     }
@@ -490,6 +508,8 @@ __global__ void __launch_bounds__(BLOCK) fused_kernel(Args<T> a) {
       if (j < a.nvec) {
 #pragma unroll
         for (int s = 0; s < NS; ++s) e[u].s[s] = a.sc[s];
+#pragma unroll
+        for (int q = 0; q < NP; ++q) e[u].p[q] = pv[q];
         if (ASSIGN) AssignRoots<EA, 0, ND>::template vec<T>(e[u], a.dst, a.head + j * V);
         if (REDUCE) {
 #pragma unroll

@@ -20,6 +20,7 @@ import numbers
 import numpy as np
 
 from .lanes import LaneVector, horizontal_sum
+from .vectors import DenseVector, DeviceScalar
 
 __all__ = [
     "Expression",
@@ -51,6 +52,8 @@ def _is_vector(obj) -> bool:
 
 def as_node(obj) -> "Expression":
     """Wrap a vector in a Leaf; pass expressions through."""
+    if type(obj) is DenseVector:
+        return Leaf(obj)
     if isinstance(obj, Expression):
         return obj
     if _is_vector(obj):
@@ -67,7 +70,7 @@ def sub_nodes(a, b):
 
 
 def mul_nodes(a, b):
-    if isinstance(b, numbers.Real):
+    if isinstance(b, (numbers.Real, DeviceScalar)):
         return ScaleNode(b, as_node(a))
     return MulNode(as_node(a), as_node(b))
 
@@ -84,7 +87,7 @@ class _Lowering:
     """Collects leaves (deduplicated by vector identity, numbered by first
     appearance in postfix order) and scalars (numbered by appearance)."""
 
-    __slots__ = ("tokens", "vectors", "_ids", "scalars", "occurrences", "dests")
+    __slots__ = ("tokens", "vectors", "_ids", "scalars", "occurrences", "dests", "pscalars")
 
     def __init__(self, parent: "_Lowering" = None, dest=None, dests=None):
         # A child lowering (a later tree of the same fused kernel) shares the
@@ -96,6 +99,7 @@ class _Lowering:
         self._ids = parent._ids if parent else {}
         self.scalars = parent.scalars if parent else []
         self.occurrences = parent.occurrences if parent else []
+        self.pscalars = parent.pscalars if parent else []  # DeviceScalar operands
         self.dests = dict(dests or {})
         if dest is not None:
             self.dests[id(dest)] = 0
@@ -115,6 +119,11 @@ class _Lowering:
         self.tokens.append(f"L{k}")
 
     def scalar(self, value):
+        if isinstance(value, DeviceScalar):
+            # read by the kernel from device memory: no host round trip
+            self.tokens.append(f"P{len(self.pscalars)}")
+            self.pscalars.append(value)
+            return
         self.tokens.append(f"S{len(self.scalars)}")
         self.scalars.append(float(value))
 
@@ -142,7 +151,7 @@ class Expression:
         return mul_nodes(self, other)
 
     def __rmul__(self, other):
-        if isinstance(other, numbers.Real):
+        if isinstance(other, (numbers.Real, DeviceScalar)):
             return ScaleNode(other, self)
         return mul_nodes(other, self)
 
@@ -227,7 +236,13 @@ class ScaleNode(Expression):
     def __init__(self, alpha, child: Expression):
         self.child = child
         self.dtype = child.dtype
-        self.alpha = self.dtype.type(alpha)
+        if isinstance(alpha, DeviceScalar):
+            # a device-resident alpha is already element-typed; keep it there
+            if alpha.dtype != self.dtype:
+                raise TypeError(f"mixed element types: scalar {alpha.dtype} vs {self.dtype}")
+            self.alpha = alpha
+        else:
+            self.alpha = self.dtype.type(alpha)
 
     @property
     def register_footprint(self) -> int:
@@ -243,7 +258,8 @@ class ScaleNode(Expression):
         lw.tokens.append("*")
 
     def __repr__(self):
-        return f"({float(self.alpha)!r} * {self.child!r})"
+        a = "device" if isinstance(self.alpha, DeviceScalar) else repr(float(self.alpha))
+        return f"({a} * {self.child!r})"
 
 
 class AssignNode(Expression):

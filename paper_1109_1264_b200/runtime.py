@@ -270,6 +270,9 @@ def _host_call(fn):
 
 # ---------------------------------------------------------------- assign
 def run_assign(lw, dest, dtype, n):
+    if lw.pscalars:
+        handled, _ = run_fused(" ".join(lw.tokens), None, lw, [dest], dtype, n)
+        return _device_scalars_only(handled)
     lib = _native.lib()
     code = _dtype_code(dtype)
     sig = " ".join(lw.tokens).encode()
@@ -370,6 +373,10 @@ def _run_reduction(lw, dest, dt, n, flags, lazy, make_call, host_call, make_xcal
 
 
 def run_reduce(lw, dtype, n, flags=0, lazy=False):
+    if lw.pscalars:
+        handled, r = run_fused(None, " ".join(lw.tokens), lw, [], dtype, n, flags, lazy)
+        _device_scalars_only(handled)
+        return r
     lib = _native.lib()
     dt = as_dtype(dtype)
     code = _dtype_code(dt)
@@ -392,6 +399,11 @@ def run_reduce(lw, dtype, n, flags=0, lazy=False):
 
 
 def run_assign_reduce(lwa, lwr, dest, dtype, n, flags=0, lazy=False):
+    if lwa.pscalars:
+        handled, r = run_fused(" ".join(lwa.tokens), " ".join(lwr.tokens), lwa, [dest], dtype, n,
+                               flags, lazy)
+        _device_scalars_only(handled)
+        return r
     lib = _native.lib()
     dt = as_dtype(dtype)
     code = _dtype_code(dt)
@@ -416,31 +428,43 @@ def run_assign_reduce(lwa, lwr, dest, dtype, n, flags=0, lazy=False):
 
 
 def run_fused(asig, rsig, lw, dests, dtype, n, flags=0, lazy=False):
-    """Multi-root fused evaluation (salt_fused).  Returns (handled, result):
-    not handled unless every leaf and destination is a plain device
-    DenseVector on one device (the caller then runs the statements one by
-    one)."""
+    """salt_fused: several assignment roots (asig, ' ; '-separated, or None)
+    and/or a reduction (rsig or None), with device-scalar operands
+    (lw.pscalars).  Returns (handled, result): not handled unless every leaf
+    and destination is a plain device DenseVector on one device."""
     fast = _fast(list(lw.vectors) + list(dests), None)
     if fast is None:
         return False, None
     dev, ptrs, _ = fast
+    for ds in lw.pscalars:
+        if ds.tensor.get_device() != dev:
+            raise ValueError("a device scalar must live on the vectors' device")
     nl = len(lw.vectors)
     leaves, keep_l = _native.ptr_array(ptrs[:nl])
     dsts, keep_d = _native.ptr_array(ptrs[nl:])
     scal, keep_s = _native.double_array(lw.scalars)
+    pscal, keep_p = _native.ptr_array([ds.tensor.data_ptr() for ds in lw.pscalars])
     dt = as_dtype(dtype)
     code = _dtype_code(dt)
     lib = _native.lib()
-    a, r = asig.encode(), (rsig.encode() if rsig is not None else None)
+    a = asig.encode() if asig is not None else None
+    r = rsig.encode() if rsig is not None else None
+    np_ = len(lw.pscalars)
     with _OnDevice(dev):
         if rsig is None:
             _native.check(lib.salt_fused(code, a, None, dsts, len(dests), leaves, nl, scal,
-                                         len(lw.scalars), n, 0, None, 0, None, None,
+                                         len(lw.scalars), pscal, np_, n, 0, None, 0, None, None,
                                          _raw_stream(dev)))
             return True, None
 
         def call(fl, ws, wsb, od, oh, st):
             return lib.salt_fused(code, a, r, dsts, len(dests), leaves, nl, scal, len(lw.scalars),
-                                  n, fl, ws, wsb, od, oh, st)
+                                  pscal, np_, n, fl, ws, wsb, od, oh, st)
 
         return True, _device_reduce(dev, dt, call, flags, lazy)
+
+
+def _device_scalars_only(handled):
+    if not handled:
+        raise TypeError("trees with device-scalar operands need plain device DenseVector "
+                        "operands on one device")

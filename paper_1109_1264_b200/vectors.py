@@ -245,18 +245,36 @@ class DenseVector:
 
 
 class DeviceScalar:
-    """A reduction result left in device memory (no host synchronisation).
+    """An element-typed scalar that lives in device memory.
 
-    Returned by reductions called with `lazy=True`; `.item()` (or float())
-    copies it to the host and returns the element-typed NumPy scalar the
-    reference returns (test_ops.py:29-31).
+    Returned by reductions called with `lazy=True` (no host
+    synchronisation).  It can scale an expression like a Python number —
+    `a * p` with `a` a DeviceScalar builds a ScaleNode whose alpha the fused
+    kernel reads from device memory — and DeviceScalars combine with + - * /
+    on the device (one tiny torch op each, IEEE round-to-nearest in the
+    element type).  So a whole solver iteration (dot -> alpha = rr / pq ->
+    fused update) runs without a host round trip and can be captured in a
+    CUDA graph.  `.item()` / float() copy it to the host and return the
+    element-typed NumPy scalar the reference returns (test_ops.py:29-31).
     """
 
     __slots__ = ("tensor", "dtype")
 
+    __array_ufunc__ = None
+
     def __init__(self, tensor: torch.Tensor, dtype):
         self.tensor = tensor
         self.dtype = as_dtype(dtype)
+
+    @classmethod
+    def full(cls, value, dtype="f64", device=None) -> "DeviceScalar":
+        dt = as_dtype(dtype)
+        return cls(torch.full((1,), float(dt.type(value)), dtype=_TORCH_DTYPES[dt],
+                              device=_as_device(device)), dt)
+
+    @property
+    def address(self) -> int:
+        return self.tensor.data_ptr()
 
     def item(self):
         return self.dtype.type(self.tensor.item())
@@ -264,5 +282,49 @@ class DeviceScalar:
     def __float__(self):
         return float(self.item())
 
+    # ---- scalar arithmetic on the device (torch ops on one element) ----
+    def _other(self, other):
+        if isinstance(other, DeviceScalar):
+            if other.dtype != self.dtype:
+                raise TypeError(f"mixed element types: {self.dtype} vs {other.dtype}")
+            return other.tensor
+        return float(self.dtype.type(other))
+
+    def __truediv__(self, other):
+        return DeviceScalar(torch.div(self.tensor, self._other(other)), self.dtype)
+
+    def __rtruediv__(self, other):
+        return DeviceScalar(torch.div(self._other(other), self.tensor), self.dtype)
+
+    def __add__(self, other):
+        if isinstance(other, (DeviceScalar, int, float, np.floating)):
+            return DeviceScalar(torch.add(self.tensor, self._other(other)), self.dtype)
+        return NotImplemented
+
+    __radd__ = __add__
+
+    def __sub__(self, other):
+        if isinstance(other, (DeviceScalar, int, float, np.floating)):
+            return DeviceScalar(torch.sub(self.tensor, self._other(other)), self.dtype)
+        return NotImplemented
+
+    def __rsub__(self, other):
+        return DeviceScalar(torch.sub(self._other(other), self.tensor), self.dtype)
+
+    def __neg__(self):
+        return DeviceScalar(torch.neg(self.tensor), self.dtype)
+
+    def __mul__(self, other):
+        if isinstance(other, (DeviceScalar, int, float, np.floating)):
+            return DeviceScalar(torch.mul(self.tensor, self._other(other)), self.dtype)
+        from .expressions import scale_node
+
+        return scale_node(self, other)  # scalar * vector expression
+
+    def __rmul__(self, other):
+        if isinstance(other, (int, float, np.floating)):
+            return DeviceScalar(torch.mul(self._other(other), self.tensor), self.dtype)
+        return NotImplemented
+
     def __repr__(self):
-        return f"DeviceScalar({self.item()!r})"
+        return f"DeviceScalar({self.item()!r}, dtype={self.dtype})"
