@@ -97,7 +97,7 @@ class DeviceCG:
         alpha = self.rr / lv.dot(p, q, lazy=True)
         rr_new = lv.fused((u, u + alpha * p), (r, r - alpha * q), r * r, lazy=True)
         p.assign(r + (rr_new / self.rr) * p)
-        self.rr = rr_new
+        self.rr.copy_(rr_new)  # in place: a captured graph re-reads the same address
 
 
 def main():

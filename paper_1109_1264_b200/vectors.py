@@ -294,7 +294,14 @@ class DeviceScalar:
         return DeviceScalar(torch.div(self.tensor, self._other(other)), self.dtype)
 
     def __rtruediv__(self, other):
-        return DeviceScalar(torch.div(self._other(other), self.tensor), self.dtype)
+        return DeviceScalar(self._other(other) / self.tensor, self.dtype)
+
+    def copy_(self, other) -> "DeviceScalar":
+        """In-place assignment (keeps this scalar's device address, so a
+        CUDA graph that reads it sees the new value on the next replay)."""
+        self.tensor.copy_(other.tensor if isinstance(other, DeviceScalar) else
+                          torch.tensor([float(self.dtype.type(other))], dtype=self.tensor.dtype))
+        return self
 
     def __add__(self, other):
         if isinstance(other, (DeviceScalar, int, float, np.floating)):

@@ -150,6 +150,8 @@ def test_device_scalar_operands():
         av, bv = a.item(), b.item()
         assert alpha.item().tobytes() == (av / bv).tobytes()  # IEEE division in dtype
         assert (-alpha).item() == -(av / bv) and (alpha * 2.0).item() == (av / bv) * NP[dt](2.0)
+        assert (1.0 / alpha).item() == NP[dt](1.0) / (av / bv)
+        assert (alpha - b).item() == (av / bv) - bv
         D = lv.DenseVector.zeros(n, dt, device="cuda")
         launches = _native.lib().salt_launch_count()
         D.assign(alpha * X + Y)
