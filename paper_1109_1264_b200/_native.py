@@ -187,7 +187,7 @@ def fastpath():
                 addr = lambda f: ctypes.cast(f, ctypes.c_void_p).value  # noqa: E731
                 _fastpath.init(
                     addr(h.salt_assign), addr(h.salt_reduce), addr(h.salt_assign_reduce),
-                    addr(h.salt_last_error), h.salt_reduce_workspace_bytes(),
+                    addr(h.salt_fused), addr(h.salt_last_error), h.salt_reduce_workspace_bytes(),
                     Leaf, AddNode, SubNode, MulNode, ScaleNode, DenseVector, DeviceScalar,
                     torch._C._cuda_getCurrentRawStream, torch.cuda.current_device,
                     runtime._workspace, np.float32, np.float64, runtime._lazy_out,

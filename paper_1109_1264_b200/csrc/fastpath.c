@@ -5,7 +5,8 @@
  * For trees whose leaves and destination are plain device DenseVectors on the
  * current CUDA device, this walks the node objects (Leaf / AddNode / SubNode /
  * MulNode / ScaleNode), builds the same canonical postfix signature as
- * expressions.lower(), collects the leaf pointers and element-typed scalars,
+ * expressions.lower(), collects the leaf pointers, element-typed scalars and
+ * DeviceScalar addresses (P<k>),
  * and calls libsalt.so's C ABI directly — replacing ~10 us of Python per call
  * (profiles/r01_api_overhead.json) by ~1 us.  Anything else (other vector
  * types, host or sharded vectors, mismatched lengths/dtypes/devices, trees
@@ -25,6 +26,8 @@
 #define MAX_LEAVES 16
 #define MAX_SCALARS 32
 #define MAX_SIG 1024
+#define MAX_PSCALARS 8
+#define MAX_ROOTS 4
 
 typedef int (*assign_fn)(int, const char*, void*, const void* const*, int, const double*, int,
                          int64_t, void*);
@@ -33,18 +36,22 @@ typedef int (*reduce_fn)(int, const char*, const void* const*, int, const double
 typedef int (*assign_reduce_fn)(int, const char*, const char*, void*, const void* const*, int,
                                 const double*, int, int64_t, int, void*, size_t, void*, void*,
                                 void*);
+typedef int (*fused_fn)(int, const char*, const char*, void* const*, int, const void* const*, int,
+                        const double*, int, const void* const*, int, int64_t, int, void*, size_t,
+                        void*, void*, void*);
 typedef const char* (*last_error_fn)(void);
 
 static assign_fn p_assign;
 static reduce_fn p_reduce;
 static assign_reduce_fn p_assign_reduce;
+static fused_fn p_fused;
 static last_error_fn p_last_error;
 static size_t ws_bytes;
 
 static PyObject *T_Leaf, *T_Add, *T_Sub, *T_Mul, *T_Scale, *T_Dense, *T_DevScalar;
 static PyObject *get_stream, *current_device, *workspace_fn, *np_f32, *np_f64, *lazy_out;
 static PyObject *s_vector, *s_left, *s_right, *s_child, *s_alpha, *s_ptr, *s_dev, *s_n, *s_code,
-    *s_data_ptr;
+    *s_data_ptr, *s_tensor, *s_get_device;
 
 typedef struct {
   char sig[MAX_SIG];
@@ -54,9 +61,14 @@ typedef struct {
   int nvec;
   double sc[MAX_SCALARS];
   int nsc;
+  const void* ps[MAX_PSCALARS]; /* DeviceScalar operands (P<k>) */
+  int nps;
   int dev, code;
   long long n;
-  PyObject* dest;  /* reduce tree of a fused root: the destination reads as D */
+  /* vectors assigned by earlier roots of the same kernel: a later tree reads
+   * them as D<k>, the value root k has just computed (latest root wins) */
+  PyObject* dests[MAX_ROOTS];
+  int ndests;
 } Walk;
 
 /* 1 = ok, 0 = not eligible (fall back), -1 = Python error */
@@ -80,7 +92,11 @@ static int long_attr(PyObject* o, PyObject* name, long long* out) {
 
 static int leaf(Walk* w, PyObject* vec) {
   char tok[16];
-  if (w->dest && vec == w->dest) return emit(w, "D");
+  for (int k = w->ndests - 1; k >= 0; --k)
+    if (w->dests[k] == vec) {
+      snprintf(tok, sizeof tok, "D%d", k);
+      return emit(w, tok);
+    }
   for (int k = 0; k < w->nvec; ++k)
     if (w->vecs[k] == vec) {
       snprintf(tok, sizeof tok, "L%d", k);
@@ -98,6 +114,25 @@ static int leaf(Walk* w, PyObject* vec) {
   return emit(w, tok);
 }
 
+/* DeviceScalar -> w->ps[w->nps++]; must live on the kernel's device */
+static int device_scalar(Walk* w, PyObject* ds) {
+  if (w->nps == MAX_PSCALARS) return 0;
+  PyObject* t = PyObject_GetAttr(ds, s_tensor);
+  if (!t) return -1;
+  PyObject* d = PyObject_CallMethodNoArgs(t, s_get_device);
+  PyObject* p = d ? PyObject_CallMethodNoArgs(t, s_data_ptr) : NULL;
+  Py_DECREF(t);
+  if (!p) { Py_XDECREF(d); return -1; }
+  long dev = PyLong_AsLong(d);
+  void* ptr = PyLong_AsVoidPtr(p);
+  Py_DECREF(d);
+  Py_DECREF(p);
+  if (PyErr_Occurred()) return -1;
+  if (dev != w->dev) return 0;
+  w->ps[w->nps++] = ptr;
+  return 1;
+}
+
 static int walk(Walk* w, PyObject* node) {
   PyObject* t = (PyObject*)Py_TYPE(node);
   int rc;
@@ -113,16 +148,21 @@ static int walk(Walk* w, PyObject* node) {
     if (w->nsc == MAX_SCALARS) return 0;
     PyObject* a = PyObject_GetAttr(node, s_alpha);
     if (!a) return -1;
-    if ((PyObject*)Py_TYPE(a) == T_DevScalar) { /* device-resident alpha: Python path */
-      Py_DECREF(a);
-      return 0;
-    }
-    double v = PyFloat_AsDouble(a); /* alpha is already element-typed */
-    Py_DECREF(a);
-    if (v == -1.0 && PyErr_Occurred()) return -1;
     char tok[16];
-    snprintf(tok, sizeof tok, "S%d", w->nsc);
-    w->sc[w->nsc++] = v;
+    if ((PyObject*)Py_TYPE(a) == T_DevScalar) {
+      /* device-resident alpha (element type checked by ScaleNode): the
+       * kernel reads it from device memory */
+      rc = device_scalar(w, a);
+      Py_DECREF(a);
+      if (rc != 1) return rc;
+      snprintf(tok, sizeof tok, "P%d", w->nps - 1);
+    } else {
+      double v = PyFloat_AsDouble(a); /* alpha is already element-typed */
+      Py_DECREF(a);
+      if (v == -1.0 && PyErr_Occurred()) return -1;
+      snprintf(tok, sizeof tok, "S%d", w->nsc);
+      w->sc[w->nsc++] = v;
+    }
     if ((rc = emit(w, tok)) != 1) return rc;
     PyObject* c = PyObject_GetAttr(node, s_child);
     if (!c) return -1;
@@ -227,6 +267,9 @@ static PyObject* fp_assign(PyObject* self, PyObject* args) {
   if (w.nvec == 0) Py_RETURN_FALSE;
   TRY(stream_for(&w, &stream));
   if (w.n == 0) Py_RETURN_TRUE;
+  if (w.nps)
+    return check(p_fused(w.code, w.sig, NULL, &dptr, 1, (const void* const*)w.ptrs, w.nvec, w.sc,
+                         w.nsc, w.ps, w.nps, w.n, 0, NULL, 0, NULL, NULL, stream));
   return check(p_assign(w.code, w.sig, dptr, (const void* const*)w.ptrs, w.nvec, w.sc, w.nsc,
                         w.n, stream));
 }
@@ -243,6 +286,32 @@ static PyObject* lazy_slot(Walk* w, void** out) {
   Py_INCREF(ds);
   Py_DECREF(r);
   return ds;
+}
+
+/* One reducing launch: reduce-only (asig NULL) or assignments + reduction.
+ * Lazy: the result stays on the device (DeviceScalar); else the NumPy scalar. */
+static PyObject* launch_reduce(Walk* w, const char* asig, void* const* dptrs, int ndst, int flags,
+                               int lazy, void* ws, void* slot, void* stream) {
+  PyObject* ds = NULL;
+  void* out = slot;
+  double host[2] = {0.0, 0.0};
+  if (lazy && !(ds = lazy_slot(w, &out))) return NULL;
+  const void* const* leaves = (const void* const*)w->ptrs;
+  int rc;
+  if (w->nps || ndst > 1)
+    rc = p_fused(w->code, asig, w->sig, dptrs, ndst, leaves, w->nvec, w->sc, w->nsc, w->ps, w->nps,
+                 w->n, flags, ws, ws_bytes, out, lazy ? NULL : host, stream);
+  else if (asig)
+    rc = p_assign_reduce(w->code, asig, w->sig, dptrs[0], leaves, w->nvec, w->sc, w->nsc, w->n,
+                         flags, ws, ws_bytes, out, lazy ? NULL : host, stream);
+  else
+    rc = p_reduce(w->code, w->sig, leaves, w->nvec, w->sc, w->nsc, w->n, flags, ws, ws_bytes, out,
+                  lazy ? NULL : host, stream);
+  if (rc != 0) {
+    Py_XDECREF(ds);
+    return check(rc);
+  }
+  return lazy ? ds : scalar_result(w, host);
 }
 
 /* reduce(child, flags, lazy) -> NumPy scalar (or DeviceScalar if lazy), or
@@ -275,20 +344,7 @@ static PyObject* fp_reduce(PyObject* self, PyObject* args) {
   if (rc < 0) return NULL;
   void *ws, *slot;
   if (workspace(&w, stream, &ws, &slot) < 0) return NULL;
-  if (lazy) {
-    void* out;
-    PyObject* ds = lazy_slot(&w, &out);
-    if (!ds) return NULL;
-    rc = p_reduce(w.code, w.sig, (const void* const*)w.ptrs, w.nvec, w.sc, w.nsc, w.n, flags, ws,
-                  ws_bytes, out, NULL, stream);
-    if (rc != 0) { Py_DECREF(ds); return check(rc); }
-    return ds;
-  }
-  double host[2] = {0.0, 0.0};
-  rc = p_reduce(w.code, w.sig, (const void* const*)w.ptrs, w.nvec, w.sc, w.nsc, w.n, flags, ws,
-                ws_bytes, slot, host, stream);
-  if (rc != 0) return check(rc);
-  return scalar_result(&w, host);
+  return launch_reduce(&w, NULL, NULL, 0, flags, lazy, ws, slot, stream);
 }
 
 /* assign_reduce(dest, assign_source, reduce_child, flags) -> scalar or None */
@@ -306,7 +362,7 @@ static PyObject* fp_assign_reduce(PyObject* self, PyObject* args) {
   memcpy(asig, w.sig, (size_t)w.len + 1);
   w.len = 0;
   w.sig[0] = '\0';
-  w.dest = dest;
+  w.dests[w.ndests++] = dest;
   rc = walk(&w, child);
   if (rc <= 0) { if (rc < 0) return NULL; Py_RETURN_NONE; }
   if (w.nvec == 0) Py_RETURN_NONE;
@@ -314,26 +370,81 @@ static PyObject* fp_assign_reduce(PyObject* self, PyObject* args) {
   if (rc <= 0) { if (rc < 0) return NULL; Py_RETURN_NONE; }
   void *ws, *slot;
   if (workspace(&w, stream, &ws, &slot) < 0) return NULL;
-  if (lazy) {
-    void* out;
-    PyObject* ds = lazy_slot(&w, &out);
-    if (!ds) return NULL;
-    rc = p_assign_reduce(w.code, asig, w.sig, dptr, (const void* const*)w.ptrs, w.nvec, w.sc,
-                         w.nsc, w.n, flags, ws, ws_bytes, out, NULL, stream);
-    if (rc != 0) { Py_DECREF(ds); return check(rc); }
-    return ds;
+  return launch_reduce(&w, asig, &dptr, 1, flags, lazy, ws, slot, stream);
+}
+
+/* fused(((dest, source), ...), total_child or None, flags, lazy) -> (result,)
+ * if launched (result None without a total), None if not eligible.  The
+ * statements run in order in ONE kernel (a later tree reads an earlier
+ * destination as D<k>); same signatures as FusedNode.lower(). */
+static PyObject* fp_fused(PyObject* self, PyObject* args) {
+  PyObject *assigns, *total;
+  int flags, lazy = 0;
+  if (!PyArg_ParseTuple(args, "OOi|p", &assigns, &total, &flags, &lazy)) return NULL;
+  if (!PyTuple_Check(assigns) && !PyList_Check(assigns)) Py_RETURN_NONE;
+  Py_ssize_t na = PySequence_Fast_GET_SIZE(assigns);
+  if (na < 1 || na > MAX_ROOTS) Py_RETURN_NONE;
+  PyObject** items = PySequence_Fast_ITEMS(assigns);
+  Walk w;
+  void* dptrs[MAX_ROOTS];
+  char asig[MAX_SIG];
+  int alen = 0, rc;
+  for (Py_ssize_t k = 0; k < na; ++k) {
+    PyObject* st = items[k];
+    if (!PyTuple_Check(st) || PyTuple_GET_SIZE(st) != 2) Py_RETURN_NONE;
+    PyObject *dest = PyTuple_GET_ITEM(st, 0), *src = PyTuple_GET_ITEM(st, 1);
+    if (k == 0) {
+      rc = start(&w, dest, &dptrs[0]);
+    } else {
+      Walk d;
+      rc = start(&d, dest, &dptrs[k]);
+      if (rc == 1 && (d.dev != w.dev || d.code != w.code || d.n != w.n)) rc = 0;
+    }
+    if (rc <= 0) { if (rc < 0) return NULL; Py_RETURN_NONE; }
+    w.len = 0;
+    w.sig[0] = '\0';
+    rc = walk(&w, src);
+    if (rc <= 0) { if (rc < 0) return NULL; Py_RETURN_NONE; }
+    if (alen + w.len + 4 >= MAX_SIG) Py_RETURN_NONE;
+    if (k) { memcpy(asig + alen, " ; ", 3); alen += 3; }
+    memcpy(asig + alen, w.sig, (size_t)w.len + 1);
+    alen += w.len;
+    w.dests[w.ndests++] = dest;
   }
-  double host[2] = {0.0, 0.0};
-  rc = p_assign_reduce(w.code, asig, w.sig, dptr, (const void* const*)w.ptrs, w.nvec, w.sc, w.nsc,
-                       w.n, flags, ws, ws_bytes, slot, host, stream);
-  if (rc != 0) return check(rc);
-  return scalar_result(&w, host);
+  w.len = 0;
+  w.sig[0] = '\0';
+  if (total != Py_None) {
+    rc = walk(&w, total);
+    if (rc <= 0) { if (rc < 0) return NULL; Py_RETURN_NONE; }
+  }
+  if (w.nvec == 0) Py_RETURN_NONE;
+  void* stream;
+  rc = stream_for(&w, &stream);
+  if (rc <= 0) { if (rc < 0) return NULL; Py_RETURN_NONE; }
+  PyObject* result;
+  if (total == Py_None) {
+    if (w.n) {
+      rc = p_fused(w.code, asig, NULL, dptrs, (int)na, (const void* const*)w.ptrs, w.nvec, w.sc,
+                   w.nsc, w.ps, w.nps, w.n, 0, NULL, 0, NULL, NULL, stream);
+      if (rc != 0) return check(rc);
+    }
+    Py_INCREF(Py_None);
+    result = Py_None;
+  } else {
+    void *ws, *slot;
+    if (workspace(&w, stream, &ws, &slot) < 0) return NULL;
+    result = launch_reduce(&w, asig, dptrs, (int)na, flags, lazy, ws, slot, stream);
+    if (!result) return NULL;
+  }
+  PyObject* t = PyTuple_Pack(1, result);
+  Py_DECREF(result);
+  return t;
 }
 
 static PyObject* fp_init(PyObject* self, PyObject* args) {
-  unsigned long long a, r, ar, le;
+  unsigned long long a, r, ar, fu, le;
   Py_ssize_t wsb;
-  if (!PyArg_ParseTuple(args, "KKKKnOOOOOOOOOOOOO", &a, &r, &ar, &le, &wsb, &T_Leaf, &T_Add,
+  if (!PyArg_ParseTuple(args, "KKKKKnOOOOOOOOOOOOO", &a, &r, &ar, &fu, &le, &wsb, &T_Leaf, &T_Add,
                         &T_Sub, &T_Mul, &T_Scale, &T_Dense, &T_DevScalar, &get_stream,
                         &current_device, &workspace_fn, &np_f32, &np_f64, &lazy_out))
     return NULL;
@@ -343,6 +454,7 @@ static PyObject* fp_init(PyObject* self, PyObject* args) {
   p_assign = (assign_fn)(uintptr_t)a;
   p_reduce = (reduce_fn)(uintptr_t)r;
   p_assign_reduce = (assign_reduce_fn)(uintptr_t)ar;
+  p_fused = (fused_fn)(uintptr_t)fu;
   p_last_error = (last_error_fn)(uintptr_t)le;
   ws_bytes = (size_t)wsb;
   Py_RETURN_NONE;
@@ -354,6 +466,8 @@ static PyMethodDef methods[] = {
     {"reduce", fp_reduce, METH_VARARGS, "reduce(child, flags, lazy=False) -> scalar or None"},
     {"assign_reduce", fp_assign_reduce, METH_VARARGS,
      "assign_reduce(dest, source, child, flags, lazy=False) -> scalar or None"},
+    {"fused", fp_fused, METH_VARARGS,
+     "fused(((dest, source), ...), total_child_or_None, flags, lazy=False) -> (result,) or None"},
     {NULL, NULL, 0, NULL}};
 
 static struct PyModuleDef module = {PyModuleDef_HEAD_INIT, "_fastpath", NULL, -1, methods};
@@ -369,5 +483,7 @@ PyMODINIT_FUNC PyInit__fastpath(void) {
   s_n = PyUnicode_InternFromString("_n");
   s_code = PyUnicode_InternFromString("_code");
   s_data_ptr = PyUnicode_InternFromString("data_ptr");
+  s_tensor = PyUnicode_InternFromString("tensor");
+  s_get_device = PyUnicode_InternFromString("get_device");
   return PyModule_Create(&module);
 }

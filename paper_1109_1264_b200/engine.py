@@ -319,6 +319,13 @@ def execute_fused(root, *, lazy: bool = False, _flags: int = 0):
     statement — the same results either way."""
     if not isinstance(root, FusedNode):
         raise TypeError("execute_fused requires a FusedNode root")
+    if root.assigns and len(root.assigns) <= _native.SALT_MAX_ROOTS:
+        fast = _native.fastpath()
+        if fast is not None:
+            r = fast.fused(tuple((s.dest.vector, s.source) for s in root.assigns),
+                           None if root.total is None else root.total.child, _flags, lazy)
+            if r is not None:
+                return r[0]
     length = common_length(root)
     if len(root.assigns) <= _native.SALT_MAX_ROOTS:
         asig, rsig, lw, dests = root.lower()

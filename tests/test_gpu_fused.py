@@ -204,3 +204,38 @@ def test_device_resident_cg_iteration_captured_in_a_graph():
     torch.cuda.synchronize()
     assert graphed3.u.to_array().tobytes() == eager.u.to_array().tobytes()
     assert graphed3.rr.item().tobytes() == eager.rr.item().tobytes()
+
+
+def test_c_fast_path_matches_python_path(monkeypatch):
+    """The C host fast path (csrc/fastpath.c) takes fused statements and
+    DeviceScalar operands and launches exactly what the Python path does."""
+    g = np.random.default_rng(12)
+    n = 70_001
+    fast = _native.fastpath()
+    assert fast is not None
+    host = [g.uniform(-1, 1, n) for _ in range(4)]
+
+    def run():
+        x, r, p, q = (dev(h, "f64") for h in host)
+        a = lv.dot(r, r, lazy=True) / lv.dot(p, q, lazy=True)
+        y = lv.DenseVector.zeros(n, "f64", device="cuda")
+        y.assign(a * x + p)                                   # assign with a P operand
+        s1 = lv.sum(a * q, lazy=True)                         # reduce with a P operand
+        s2 = lv.axpy_dot(a, x, y, r)                          # assign+reduce, P operand
+        rr = lv.fused((x, x + a * p), (r, r - a * q), r * r, lazy=True)  # fused, two P operands
+        lv.fused((p, r + a * p), (q, p - q))                 # fused assign-only, reads new p as D0
+        return [v.to_array() for v in (x, r, p, q, y)] + [s1.item(), s2, rr.item()]
+
+    assert fast.fused(((dev(host[0], "f64"), dev(host[1], "f64") * 2.0),), None, 0) is not None
+    launches = _native.lib().salt_launch_count()
+    want_fast = run()
+    torch.cuda.synchronize()
+    used = _native.lib().salt_launch_count() - launches
+    monkeypatch.setattr(_native, "_fast", None)
+    want_py = run()
+    for a, b in zip(want_fast, want_py):
+        assert np.asarray(a).tobytes() == np.asarray(b).tobytes()
+    assert used == 2 + 1 + 1 + 1 + 1 + 1  # one kernel per statement group
+    # zero length through the fast path
+    e = lv.DenseVector.zeros(0, "f64", device="cuda")
+    assert lv.fused((e, e * 2.0), e * e) == 0.0

@@ -53,12 +53,18 @@ def main():
     sc, keep2 = _native.double_array([1.25, -0.5])
     stream = torch.cuda.current_stream().cuda_stream
     res = {"n": n, "gpu": torch.cuda.get_device_name()}
+    ds = lv.DeviceScalar.full(0.5, "f64", device="cuda")
     cases = {
         "lv.axpy": lambda: lv.axpy(0.5, x, y),
         "d.assign(alpha*a+beta*(b-c))": lambda: w.assign(1.25 * x + -0.5 * (y - z)),
         "lv.dot(lazy=True)": lambda: lv.dot(x, y, lazy=True),
         "lv.dot (returns host scalar, synchronises)": lambda: lv.dot(x, y),
         "lv.axpy_dot(lazy=True)": lambda: lv.axpy_dot(0.5, x, y, z, lazy=True),
+        "lv.fused CG update (host scalar, lazy)": lambda: lv.fused((x, x + 0.5 * y), (z, z - 0.5 * w),
+                                                                   z * z, lazy=True),
+        "lv.fused CG update (DeviceScalar alpha, lazy)": lambda: lv.fused((x, x + ds * y), (z, z - ds * w),
+                                                                          z * z, lazy=True),
+        "d.assign(DeviceScalar*a + b)": lambda: w.assign(ds * x + y),
         "C ABI salt_assign (prebuilt args)": lambda: lib.salt_assign(1, sig, tw.data_ptr(), leaves, 3, sc, 2,
                                                                    n, stream),
         "torch eager alpha*a+beta*(b-c)": lambda: tw.copy_(torch.add(torch.mul(tx, 1.25),
