@@ -42,14 +42,30 @@ using salt::i64;
 constexpr int kBlock = 256;
 static_assert(SALT_WORKSPACE_TICKET_BYTES == salt::WsLayout::group_partials,
               "salt.h ticket prefix must match the kernel workspace layout");
-constexpr int kUnrollVec = 2;     // 256-bit vectors in flight per leaf per thread
-constexpr int unroll_for(int /*mode*/, int /*nl*/) { return kUnrollVec; }
+// 256-bit vectors in flight per leaf per thread.  2 for assignments; 4 for
+// pure reductions unless f64 with two or more leaves (profiles/
+// r01_reduce_unroll_sweep.txt: nrm2 f64 6.72 -> 7.13 TB/s at 2^28 and
+// +11 % at 2^24, sdot +25 % at 2^24; ddot is best at 2: TwoSum accumulation
+// of two f64 streams needs the registers).
+constexpr int unroll_for(int mode, int nl, int elem_bytes) {
+  return mode == salt::MODE_REDUCE && (elem_bytes == 4 || nl <= 1) ? 4 : 2;
+}
 constexpr int kUnrollScalar = 4;  // V == 1 fallback (misaligned operands)
 // Reductions: tiles (of BLOCK*UNR vectors) per CTA, so that every CTA
 // streams ~64 KiB before paying its partial/ticket epilogue: 4 tiles for
 // one-leaf trees (nrm2, sum), 2 for two or more leaves (dot, fused axpy->dot).
 // SALT_REDUCE_TILES overrides it (tuning only; read once).
 // Assignments: one tile per CTA (SALT_ASSIGN_TILES overrides; tuning only).
+// SALT_UNROLL=U (tuning only): every vector kernel is JIT-built with UNR=U
+// instead of the compiled-in choice.
+int tuning_unroll() {
+  static const int env = [] {
+    const char* e = getenv("SALT_UNROLL");
+    return e ? atoi(e) : 0;
+  }();
+  return env;
+}
+
 int assign_tiles_per_cta() {
   static const int env = [] {
     const char* e = getenv("SALT_ASSIGN_TILES");
@@ -333,7 +349,7 @@ void reg_one(const char* asig, const char* rsig) {
   if (asig) { parse_assign(asig, sa); ta = sa.type; }
   if (rsig) { parse_sig(rsig, MODE == salt::MODE_ASSIGN_REDUCE ? sa.nroots : 0, sr); tr = sr.type; }
   constexpr int V = vec_of<T>();
-  constexpr int U = unroll_for(MODE, salt::cmax(EA::NL, ER::NL));
+  constexpr int U = unroll_for(MODE, salt::cmax(EA::NL, ER::NL), (int)sizeof(T));
   auto k1 = std::make_unique<Kernel>();
   k1->aot = (const void*)&salt::fused_kernel<T, EA, ER, MODE, V, U, kBlock>;
   k1->vec = V; k1->unroll = U;
@@ -440,7 +456,9 @@ Kernel* jit_compile(int dtype, int mode, int vec, int nl, const std::string& ta,
   Nvrtc& nv = nvrtc();
   if (!nv.ok) { g_err = "NVRTC unavailable: " + nv.why; return nullptr; }
   const char* tname = dtype == SALT_F32 ? "float" : "double";
-  const int unroll = vec == 1 ? kUnrollScalar : unroll_for(mode, nl);
+  const int unroll = vec == 1 ? kUnrollScalar
+                     : tuning_unroll() > 0 ? tuning_unroll()
+                                             : unroll_for(mode, nl, dtype == SALT_F32 ? 4 : 8);
   std::string expr = std::string("salt::fused_kernel<") + tname + "," + ta + "," + tr + "," +
                      std::to_string(mode) + "," + std::to_string(vec) + "," +
                      std::to_string(unroll) + "," + std::to_string(kBlock) + ">";
@@ -510,7 +528,7 @@ Kernel* get_kernel(int dtype, int mode, int vec, int nl, const std::string& ta,
   ensure_table();
   const std::string key = key_of(dtype, mode, vec, ta, tr);
   std::lock_guard<std::mutex> lk(g_table_mu);
-  if (!g_force_jit.load()) {
+  if (!g_force_jit.load() && tuning_unroll() <= 0) {
     auto it = table().find(key);
     if (it != table().end()) return it->second.get();
   }
