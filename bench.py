@@ -366,6 +366,9 @@ def run_gpu(args, world, rank, local):
                 "frac": round(achieved / peak, 4),
                 "traffic": _traffic(),
                 "peak_source": peak_src,
+                # the measured copy peak is a torch copy kernel's rate, below
+                # what a 3-read/1-write stream reaches; also vs HBM3e nominal
+                "frac_of_nominal_8000": round(achieved / 8000.0, 4),
                 "kernel_avg_ms": round(kavg, 5),
                 "algorithmic_bytes_per_launch": int(bytes_step),
             },

@@ -66,6 +66,35 @@ int tuning_unroll() {
   return env;
 }
 
+// Reductions whose tiles fit max_cluster() CTAs x cluster_tiles() run as
+// ONE thread-block cluster (SALT_CLUSTER = max CTAs, 0 disables, <= 16;
+// SALT_CLUSTER_TILES = tiles per CTA at most; tuning only).
+int max_cluster() {
+  static const int env = [] {
+    const char* e = getenv("SALT_CLUSTER");
+    int v = e ? atoi(e) : 16;
+    return v < 0 ? 0 : v > 16 ? 16 : v;
+  }();
+  return env;
+}
+int cluster_tiles() {
+  static const int env = [] {
+    const char* e = getenv("SALT_CLUSTER_TILES");
+    return e ? atoi(e) : 2;
+  }();
+  return env > 0 ? env : 2;
+}
+
+// SALT_CLUSTER_COMBINE=0 (test hook): keep the cluster-sized grid but
+// combine through the workspace tickets — must give the same bits.
+bool cluster_combine() {
+  static const bool env = [] {
+    const char* e = getenv("SALT_CLUSTER_COMBINE");
+    return !(e && atoi(e) == 0);
+  }();
+  return env;
+}
+
 int assign_tiles_per_cta() {
   static const int env = [] {
     const char* e = getenv("SALT_ASSIGN_TILES");
@@ -225,6 +254,9 @@ struct Driver {
   CUresult (*LaunchKernel)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned,
                            unsigned, CUstream, void**, void**) = nullptr;
   CUresult (*GetErrorString)(CUresult, const char**) = nullptr;
+  // optional (cluster launches of JIT kernels)
+  CUresult (*LaunchKernelEx)(const CUlaunchConfig*, CUfunction, void**, void**) = nullptr;
+  CUresult (*FuncSetAttribute)(CUfunction, CUfunction_attribute, int) = nullptr;
 };
 
 template <class F> bool entry(const char* name, F& fp, std::string& why) {
@@ -246,6 +278,10 @@ Driver& driver() {
            entry("cuModuleGetFunction", d.ModuleGetFunction, d.why) &&
            entry("cuLaunchKernel", d.LaunchKernel, d.why) &&
            entry("cuGetErrorString", d.GetErrorString, d.why);
+    std::string ignore;
+    if (!entry("cuLaunchKernelEx", d.LaunchKernelEx, ignore) ||
+        !entry("cuFuncSetAttribute", d.FuncSetAttribute, ignore))
+      d.LaunchKernelEx = nullptr;
   });
   return d;
 }
@@ -320,6 +356,8 @@ struct Kernel {
   CUfunction jit_fn[kMaxDevices] = {};       // JIT module per device
   int vec = 1;                               // lanes per vector access
   int unroll = 1;
+  // cluster launches (reductions at small n): 0 unknown, 1 ok, -1 refused
+  std::atomic<int> cluster_ok[kMaxDevices] = {};
 };
 
 std::string key_of(int dtype, int mode, int vec, const std::string& ta, const std::string& tr) {
@@ -565,6 +603,75 @@ int prepare(Kernel* k, int dev) {
   return 0;
 }
 
+// One cluster of `grid` CTAs (2..16; > 8 needs the non-portable opt-in).
+// Returns false (without an error) if this kernel/device refuses clusters
+// of that size, so the caller launches the ticket-combine grid instead.
+template <class T> bool launch_cluster(Kernel* k, int dev, int grid, salt::Args<T>& args,
+                                       cudaStream_t st, int& rc) {
+  rc = 0;
+  std::atomic<int>& ok = k->cluster_ok[dev];
+  if (ok.load(std::memory_order_relaxed) < 0) return false;
+  void* params[] = {&args};
+  if (k->aot) {
+    if (ok.load(std::memory_order_relaxed) == 0) {
+      if (cudaFuncSetAttribute(k->aot, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
+          cudaSuccess) {
+        cudaGetLastError();
+        ok.store(-1);
+        return false;
+      }
+      ok.store(1);
+    }
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = (unsigned)grid;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kBlock);
+    cfg.stream = st;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelExC(&cfg, k->aot, params);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      ok.store(-1);
+      return false;
+    }
+  } else {
+    Driver& d = driver();
+    if (!d.LaunchKernelEx) return false;
+    if (ok.load(std::memory_order_relaxed) == 0) {
+      if (d.FuncSetAttribute(k->jit_fn[dev], CU_FUNC_ATTRIBUTE_NON_PORTABLE_CLUSTER_SIZE_ALLOWED,
+                             1) != CUDA_SUCCESS) {
+        ok.store(-1);
+        return false;
+      }
+      ok.store(1);
+    }
+    CUlaunchConfig cfg = {};
+    CUlaunchAttribute attr[1];
+    attr[0].id = CU_LAUNCH_ATTRIBUTE_CLUSTER_DIMENSION;
+    attr[0].value.clusterDim.x = (unsigned)grid;
+    attr[0].value.clusterDim.y = 1;
+    attr[0].value.clusterDim.z = 1;
+    cfg.gridDimX = (unsigned)grid;
+    cfg.gridDimY = cfg.gridDimZ = 1;
+    cfg.blockDimX = kBlock;
+    cfg.blockDimY = cfg.blockDimZ = 1;
+    cfg.hStream = (CUstream)st;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (d.LaunchKernelEx(&cfg, k->jit_fn[dev], params, nullptr) != CUDA_SUCCESS) {
+      ok.store(-1);
+      return false;
+    }
+  }
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return true;
+}
+
 template <class T> int launch(Kernel* k, int dev, int grid, salt::Args<T>& args, cudaStream_t st) {
   void* params[] = {&args};
   if (k->aot) {
@@ -724,7 +831,16 @@ int run_fused(Plan& p, void* const* dsts, int ndst, const void* const* leaves, i
   const i64 per_tile = (i64)kBlock * k->unroll;
   const i64 ntiles = (a.nvec + per_tile - 1) / per_tile;
   i64 K = assign_tiles_per_cta(), cap = i64(0x7fffffff);
-  if (reduce) {
+  bool cluster = false;
+  if (reduce && ntiles > 2 && ntiles <= (i64)max_cluster() * cluster_tiles()) {
+    // Small n (3 .. 16 x 2 tiles; up to 2 tiles one CTA is quicker): one cluster
+    // of <= 16 CTAs, partials combined in distributed shared memory — no
+    // workspace round trip, no ticket atomics.  B200, back-to-back launches
+    // (profiles/r01_cluster_reduce.txt): nrm2 f64 2^16 6.33 -> 4.13 us,
+    // sdot 2^17 5.35 -> 4.28 us, fused axpy->dot 2^14 5.18 -> 4.07 us.
+    K = (ntiles + max_cluster() - 1) / max_cluster();
+    cluster = true;
+  } else if (reduce) {
     K = reduce_tiles_per_cta(p.nl);
     cap = salt::MAX_REDUCE_CTAS;
     // Mid sizes: if at most 8 tiles per CTA fit everything into one group of
@@ -762,8 +878,19 @@ int run_fused(Plan& p, void* const* dsts, int ndst, const void* const* leaves, i
       a.xchg.error = (unsigned int*)x->error;
     }
   }
-  rc = launch<T>(k, dev, grid, a, st);
-  if (rc) return rc;
+  a.cluster = cluster && grid > 1 && cluster_combine() ? 1 : 0;
+  bool launched = false;
+  if (a.cluster) {
+    launched = launch_cluster<T>(k, dev, grid, a, st, rc);
+    if (rc) return rc;
+    // refused (e.g. no 16-CTA cluster fits): same grid, ticket combine —
+    // identical bits, since both fold the partials in CTA order
+    if (!launched) a.cluster = 0;
+  }
+  if (!launched) {
+    rc = launch<T>(k, dev, grid, a, st);
+    if (rc) return rc;
+  }
   if (reduce && out_host) {
     size_t bytes = (flags & SALT_PARTIAL) ? sizeof(salt::DD) : sizeof(T);
     SALT_CUDA(cudaMemcpyAsync(out_host, out_dev, bytes, cudaMemcpyDeviceToHost, st));

@@ -171,6 +171,7 @@ template <class T> struct Args {
   unsigned int* ticket;           // arrival counter of the groups (zeroed, self-resetting)
   void* out;                      // T result or DD partial
   int flags;
+  int cluster;                    // reduce modes: 1 = the grid is ONE thread-block cluster
   Xchg xchg;                      // sharded reductions over NVLink (world 0: off)
 };
 
@@ -322,6 +323,22 @@ template <> struct Acc<float> {
   __device__ __forceinline__ void add(float v) { hi = __dadd_rn(hi, (double)v); }
   __device__ __forceinline__ DD get() const { DD r; r.hi = hi; r.lo = 0.0; return r; }
 };
+
+// Thread-block cluster helpers (sm_90+ PTX): a barrier across every thread
+// of the cluster with release/acquire semantics for shared memory, and a
+// load from another CTA's shared memory (distributed shared memory).
+__device__ __forceinline__ void cluster_barrier() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\t"
+               "barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ double ld_dsmem(const double* local, unsigned int rank) {
+  const unsigned int addr = (unsigned int)__cvta_generic_to_shared(local);
+  unsigned int remote;
+  double v;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(addr), "r"(rank));
+  asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(remote) : "memory");
+  return v;
+}
 
 // Ticket increment with acquire-release semantics at GPU scope: it publishes
 // this CTA's partial (release) and, for the CTA that turns out to be last,
@@ -534,6 +551,31 @@ __global__ void __launch_bounds__(BLOCK) fused_kernel(Args<T> a) {
       if (threadIdx.x == 0) {
         if (a.xchg.world > 0) part = exchange_dd(part, a.xchg);
         finish_store<T>(part, a.flags, a.out);
+      }
+      return;
+    }
+    if (a.cluster) {
+      // Small n: the whole grid is one cluster (<= 16 CTAs).  Partials meet
+      // in distributed shared memory behind one cluster barrier instead of
+      // global partials + ticket atomics.  CTA 0 folds them exactly like the
+      // single-group ticket path below (thread t takes CTA t, then the same
+      // block tree), so both paths give the same bits.
+      __shared__ DD cpart;
+      if (threadIdx.x == 0) cpart = part;
+      cluster_barrier();
+      DD v; v.hi = 0.0; v.lo = 0.0;
+      if (blockIdx.x == 0 && threadIdx.x < gridDim.x) {
+        DD p;
+        p.hi = ld_dsmem(&cpart.hi, threadIdx.x);
+        p.lo = ld_dsmem(&cpart.lo, threadIdx.x);
+        v = dd_add(v, p);
+      }
+      cluster_barrier();  // every CTA's shared memory stays alive until read
+      if (blockIdx.x != 0) return;
+      DD q = block_reduce_dd<BLOCK>(v, smem);
+      if (threadIdx.x == 0) {
+        if (a.xchg.world > 0) q = exchange_dd(q, a.xchg);
+        finish_store<T>(q, a.flags, a.out);
       }
       return;
     }

@@ -15,16 +15,26 @@ import paper_1109_1264_b200 as lv  # noqa: E402
 
 
 def main():
+    import argparse
+
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--logn", default="12,16,18,20,22,24")
+    ap.add_argument("--ops", default="axpy,t2,dot,axpy_dot")
+    args = ap.parse_args()
     out = {}
-    for logn in (12, 16, 18, 20, 22, 24):
+    for logn in map(int, args.logn.split(",")):
         n = 1 << logn
         v = [lv.DenseVector.from_tensor(torch.rand(n, dtype=torch.float64, device="cuda")) for _ in range(4)]
+        f = [lv.DenseVector.from_tensor(torch.rand(n, dtype=torch.float32, device="cuda")) for _ in range(2)]
         cases = {
             "axpy": (lambda: lv.axpy(0.5, v[0], v[1]), 24),
             "t2": (lambda: v[3].assign(1.25 * v[0] + -0.5 * (v[1] - v[2])), 32),
             "dot": (lambda: lv.dot(v[0], v[1], lazy=True), 16),
+            "nrm2": (lambda: lv.norm2(v[0], lazy=True), 8),
+            "sdot": (lambda: lv.dot(f[0], f[1], lazy=True), 8),
             "axpy_dot": (lambda: lv.axpy_dot(0.5, v[0], v[1], v[2], lazy=True), 32),
         }
+        cases = {k: c for k, c in cases.items() if k in args.ops.split(",")}
         for name, (fn, bpe) in cases.items():
             for _ in range(20):
                 fn()
