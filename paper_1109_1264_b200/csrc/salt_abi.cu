@@ -843,11 +843,14 @@ int run_fused(Plan& p, void* const* dsts, int ndst, const void* const* leaves, i
   } else if (reduce) {
     K = reduce_tiles_per_cta(p.nl);
     cap = salt::MAX_REDUCE_CTAS;
-    // Mid sizes: if at most 8 tiles per CTA fit everything into one group of
-    // CTAs, take it — the single-group combine skips the second ticket level
-    // (f64 dot at 2^22: 7.2 vs 5.1 TB/s, profiles/r01_small_n/).
-    if (ntiles > K * salt::GROUP && ntiles <= 8 * salt::GROUP)
-      K = (ntiles + salt::GROUP - 1) / salt::GROUP;
+    // Small and mid sizes: if at most 8 tiles per CTA fit everything into
+    // one group of CTAs, use one group with as many CTAs as possible — the
+    // single-group combine skips the second ticket level (f64 dot at 2^22:
+    // 7.2 vs 5.1 TB/s) and more CTAs keep more SMs streaming (nrm2 f64 at
+    // 2^19: 6.39 -> 4.67 us; profiles/r01_small_n/).
+    // Up to 2 tiles: one CTA (no combine at all).
+    if (ntiles <= 2) K = ntiles > 0 ? ntiles : 1;
+    else if (ntiles <= 8 * salt::GROUP) K = (ntiles + salt::GROUP - 1) / salt::GROUP;
   }
   if ((ntiles + K - 1) / K > cap) K = (ntiles + cap - 1) / cap;
   i64 g64 = (ntiles + K - 1) / K;
