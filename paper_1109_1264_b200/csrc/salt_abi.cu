@@ -95,6 +95,17 @@ bool cluster_combine() {
   return env;
 }
 
+// Reductions of up to group_tiles() x 256 tiles run as one group of CTAs
+// (SALT_GROUP_TILES overrides; tuning only).  16 (profiles/r01_group_tiles.txt):
+// ddot 2^23 27.5 -> 25.8 us, sdot 2^25 44.1 -> 42.2 us vs 8; 1-4 are worse.
+int group_tiles() {
+  static const int env = [] {
+    const char* e = getenv("SALT_GROUP_TILES");
+    return e ? atoi(e) : 16;
+  }();
+  return env >= 0 ? env : 16;
+}
+
 int assign_tiles_per_cta() {
   static const int env = [] {
     const char* e = getenv("SALT_ASSIGN_TILES");
@@ -843,14 +854,15 @@ int run_fused(Plan& p, void* const* dsts, int ndst, const void* const* leaves, i
   } else if (reduce) {
     K = reduce_tiles_per_cta(p.nl);
     cap = salt::MAX_REDUCE_CTAS;
-    // Small and mid sizes: if at most 8 tiles per CTA fit everything into
+    // Small and mid sizes: if at most 16 tiles per CTA fit everything into
     // one group of CTAs, use one group with as many CTAs as possible — the
     // single-group combine skips the second ticket level (f64 dot at 2^22:
     // 7.2 vs 5.1 TB/s) and more CTAs keep more SMs streaming (nrm2 f64 at
     // 2^19: 6.39 -> 4.67 us; profiles/r01_small_n/).
     // Up to 2 tiles: one CTA (no combine at all).
     if (ntiles <= 2) K = ntiles > 0 ? ntiles : 1;
-    else if (ntiles <= 8 * salt::GROUP) K = (ntiles + salt::GROUP - 1) / salt::GROUP;
+    else if (ntiles <= (i64)group_tiles() * salt::GROUP)
+      K = (ntiles + salt::GROUP - 1) / salt::GROUP;
   }
   if ((ntiles + K - 1) / K > cap) K = (ntiles + cap - 1) / cap;
   i64 g64 = (ntiles + K - 1) / K;
