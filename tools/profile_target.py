@@ -23,6 +23,8 @@ CASES = {
     "t1": (torch.float64, 1 << 28, 4),
     "dot64": (torch.float64, 1 << 28, 2),
     "nrm2_32": (torch.float32, 1 << 28, 1),
+    "nrm2_64": (torch.float64, 1 << 28, 1),
+    "cgupdate": (torch.float64, 1 << 28, 4),
     "dot32": (torch.float32, 1 << 28, 2),
     "etree32": (torch.float32, 1 << 30, 5),
     "axpydot": (torch.float64, 1 << 28, 3),
@@ -37,12 +39,17 @@ def main():
     a = ap.parse_args()
     dt, n, k = CASES[a.case]
     v = [lv.DenseVector.from_tensor(torch.rand(n, dtype=dt, device="cuda") * 2 - 1) for _ in range(k)]
+    alpha = lv.DeviceScalar.full(1e-3, "f64" if dt == torch.float64 else "f32", device="cuda")
     calls = {
         "t2": lambda: v[3].assign(1.25 * v[0] + -0.75 * (v[1] - v[2])),
         "t1": lambda: v[3].assign(v[0] + (v[1] - v[2])),
         "dot64": lambda: lv.dot(v[0], v[1], lazy=True),
         "dot32": lambda: lv.dot(v[0], v[1], lazy=True),
         "nrm2_32": lambda: lv.norm2(v[0], lazy=True),
+        "nrm2_64": lambda: lv.norm2(v[0], lazy=True),
+        # x += a p ; r -= a q ; rr = r.r with a device-resident a: one kernel
+        "cgupdate": lambda: lv.fused((v[0], v[0] + alpha * v[1]), (v[2], v[2] - alpha * v[3]),
+                                     v[2] * v[2], lazy=True),
         "etree32": lambda: v[4].assign(1.25 * (v[0] + v[1]) - 0.75 * (v[2] - v[3]) + 0.5 * v[0]),
         "axpydot": lambda: lv.axpy_dot(0.5, v[0], v[1], v[2], lazy=True),
         "daxpy20": lambda: lv.axpy(0.5, v[0], v[1]),
