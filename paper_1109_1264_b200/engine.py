@@ -191,7 +191,8 @@ def _trace_events(plan: UnrollPlan, length: int, reduce_root: bool) -> list:
 
 
 def _fits(lw) -> bool:
-    return len(lw.vectors) <= _native.SALT_MAX_LEAVES and len(lw.scalars) <= _native.SALT_MAX_SCALARS
+    return (len(lw.vectors) <= _native.SALT_MAX_LEAVES and len(lw.scalars) <= _native.SALT_MAX_SCALARS
+            and len(lw.pscalars) <= _native.SALT_MAX_PSCALARS)
 
 
 def _temporary_like(expr, length):
@@ -212,7 +213,8 @@ def _temporary_like(expr, length):
 
 def _fit(expr, length):
     """An equivalent tree that one fused kernel can take (<= SALT_MAX_LEAVES
-    distinct vectors, <= SALT_MAX_SCALARS scalars).  Oversized subtrees are
+    distinct vectors, <= SALT_MAX_SCALARS scalars, <= SALT_MAX_PSCALARS
+    device scalars).  Oversized subtrees are
     evaluated on the GPU into temporaries first; every node already rounds to
     the element type, so materialising an intermediate changes no bit."""
     if _fits(lower(expr)):

@@ -83,3 +83,81 @@ def test_trees_beyond_one_kernel_are_split_bit_exactly():
         r = execute_reduce(SumNode(expr))
         exact = restate.exact_sum(want)
         assert abs(float(r) - exact) <= {"f32": 1e-5, "f64": 1e-12}[dt] * abs(exact)
+
+
+def random_tree_ds(rng, vecs, depth, dt):
+    """Like random_tree, but half of the scalars are DeviceScalars."""
+    if depth == 0 or rng.random() < 0.25:
+        return vecs[int(rng.integers(len(vecs)))]
+    kind = rng.integers(5)
+    left = random_tree_ds(rng, vecs, depth - 1, dt)
+    if kind == 3:
+        alpha = float(rng.uniform(-3, 3))
+        if rng.random() < 0.5:
+            alpha = lv.DeviceScalar.full(alpha, dt, device="cuda")
+        return alpha * as_node(left) if rng.random() < 0.5 else as_node(left) * alpha
+    if kind == 4:
+        return -as_node(left)
+    right = random_tree_ds(rng, vecs, depth - 1, dt)
+    l, r = as_node(left), as_node(right)
+    return l + r if kind == 0 else (l - r if kind == 1 else l * r)
+
+
+def host_signature(lw):
+    """Postfix signature with every P<k> (device scalar) replaced by an S<j>
+    carrying its value: the tree the oracle evaluates."""
+    toks, vals = [], []
+    for t in lw.tokens:
+        if t[0] == "S":
+            toks.append(f"S{len(vals)}")
+            vals.append(lw.scalars[int(t[1:])])
+        elif t[0] == "P":
+            toks.append(f"S{len(vals)}")
+            vals.append(float(lw.pscalars[int(t[1:])].item()))
+        else:
+            toks.append(t)
+    return " ".join(toks), vals
+
+
+@pytest.mark.parametrize("dt", ["f32", "f64"])
+def test_random_trees_with_device_scalars(dt):
+    """Scalars read from device memory (P<k>) give the same bits as the
+    same values passed from the host; more than 8 device scalars in one tree
+    (SALT_MAX_PSCALARS) are handled by splitting."""
+    rng = np.random.default_rng(3030 if dt == "f32" else 3031)
+    seen_p = 0
+    for case in range(24):
+        n = int(rng.choice([1, 33, 4099, 65_537, 1 << 20]))
+        nv = int(rng.integers(1, 7))
+        host = [rng.uniform(-2, 2, n).astype(NP[dt]) for _ in range(nv)]
+        vecs = [lv.DenseVector.from_values(h, dt, device="cuda") for h in host]
+        expr = as_node(random_tree_ds(rng, vecs, int(rng.integers(2, 8)), dt))
+        lw = lower(expr)
+        seen_p += len(lw.pscalars)
+        idx = [next(i for i, v in enumerate(vecs) if v is u) for u in lw.vectors]
+        sig, vals = host_signature(lw)
+        want = restate.eval_sig(sig, [host[i] for i in idx], vals, dt)
+        out = lv.DenseVector.zeros(n, dt, device="cuda")
+        out.assign(expr)
+        assert same_bits(out.to_array(), want), (case, " ".join(lw.tokens))
+        r = execute_reduce(SumNode(expr))
+        exact = restate.exact_sum(want)
+        if exact != 0 and np.isfinite(exact):
+            tol = {"f32": 1e-5, "f64": 1e-12}[dt]
+            scale = restate.exact_sum(np.abs(want))
+            assert abs(float(r) - exact) <= tol * max(abs(exact), 1e-3 * scale), (case, float(r), exact)
+    assert seen_p >= 10
+    # 12 device scalars in one tree: more than one kernel takes
+    n = 5003
+    host = [rng.uniform(-1, 1, n).astype(NP[dt]) for _ in range(3)]
+    vecs = [lv.DenseVector.from_values(h, dt, device="cuda") for h in host]
+    expr = as_node(vecs[0])
+    for k in range(12):
+        expr = lv.DeviceScalar.full(0.5 + k / 16, dt, device="cuda") * expr + as_node(vecs[k % 3])
+    lw = lower(expr)
+    assert len(lw.pscalars) == 12
+    sig, vals = host_signature(lw)
+    want = restate.eval_sig(sig, host, vals, dt)
+    out = lv.DenseVector.zeros(n, dt, device="cuda")
+    out.assign(expr)
+    assert same_bits(out.to_array(), want)
