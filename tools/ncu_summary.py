@@ -12,6 +12,7 @@ import argparse
 import csv
 import io
 import json
+import os
 import subprocess
 import sys
 
@@ -36,7 +37,7 @@ UNITS = {"ms": 1e-3, "us": 1e-6, "ns": 1e-9, "s": 1.0, "Gbyte": 1e9, "Mbyte": 1e
 
 
 def _raw(rep):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+    out = subprocess.run([os.environ.get("NCU", "ncu"), "-i", rep, "--page", "raw", "--csv"], capture_output=True,
                          text=True, check=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     hdr, units = rows[0], rows[1]
