@@ -107,6 +107,7 @@ def main():
     a = ap.parse_args()
     g = np.random.default_rng(0)
     b = lv.DenseVector.from_values(g.standard_normal(a.n), "f64")
+    cg(b, 2)  # warm-up: first-use kernel builds (NVRTC) are not part of the timing
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     u, k, rel = cg(b, a.iters)
