@@ -433,9 +433,21 @@ def run_fused(asig, rsig, lw, dests, dtype, n, flags=0, lazy=False):
     (lw.pscalars).  Returns (handled, result): not handled unless every leaf
     and destination is a plain device DenseVector on one device."""
     fast = _fast(list(lw.vectors) + list(dests), None)
+    sharded = None
     if fast is None:
-        return False, None
-    dev, ptrs, _ = fast
+        # Sharded operands: every rank runs the same kernel on its blocks;
+        # a reduction's per-rank partials meet in a 16-byte all-gather and a
+        # fixed-order finish (same bits on every rank), so device scalars
+        # computed from it stay identical across ranks.
+        shards = _sharded_operands(list(lw.vectors) + list(dests))
+        if shards is None:
+            return False, None
+        sharded = shards[0]
+        dev = sharded.local.device.index
+        ptrs = [s.local.tensor.data_ptr() for s in shards]
+        n = len(sharded.local)
+    else:
+        dev, ptrs, _ = fast
     for ds in lw.pscalars:
         if ds.tensor.get_device() != dev:
             raise ValueError("a device scalar must live on the vectors' device")
@@ -461,7 +473,24 @@ def run_fused(asig, rsig, lw, dests, dtype, n, flags=0, lazy=False):
             return lib.salt_fused(code, a, r, dsts, len(dests), leaves, nl, scal, len(lw.scalars),
                                   pscal, np_, n, fl, ws, wsb, od, oh, st)
 
-        return True, _device_reduce(dev, dt, call, flags, lazy)
+        return True, _device_reduce(dev, dt, call, flags, lazy, sharded)
+
+
+def _sharded_operands(vectors):
+    """The ShardedVectors behind `vectors` if ALL are sharded, share one
+    partition and live on a CUDA device; else None."""
+    from .sharding import ShardedVector
+
+    shards = [_shard_of(v) for v in vectors]
+    if not shards or not all(isinstance(s, ShardedVector) for s in shards):
+        return None
+    first = shards[0]
+    if first.local.device.type != "cuda":
+        return None
+    for s in shards[1:]:
+        if not first.same_partition(s):
+            raise ValueError("sharded vectors in one expression must share a partition")
+    return shards
 
 
 def _device_scalars_only(handled):

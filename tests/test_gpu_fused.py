@@ -239,3 +239,26 @@ def test_c_fast_path_matches_python_path(monkeypatch):
     # zero length through the fast path
     e = lv.DenseVector.zeros(0, "f64", device="cuda")
     assert lv.fused((e, e * 2.0), e * e) == 0.0
+
+
+def test_sharded_fused_update_with_device_scalars():
+    """A CG update over ShardedVectors (here one rank) with a device-resident
+    step length: one kernel per rank, the reduction's partial through the
+    all-gather + fixed-order finish — same bits as the unsharded update."""
+    from paper_1109_1264_b200.sharding import ShardedVector
+
+    g = np.random.default_rng(77)
+    n = 300_007
+    host = [g.standard_normal(n) for _ in range(4)]
+
+    def step(make):
+        x, r, p, q = (make(h) for h in host)
+        a = lv.dot(r, r, lazy=True) / lv.dot(p, q, lazy=True)
+        rr = lv.fused((x, x + a * p), (r, r - a * q), r * r, lazy=True)
+        lv.fused((p, r + (rr / a) * p))
+        return [v.to_array() for v in (x, r, p)] + [rr.item(), a.item()]
+
+    dense = step(lambda h: lv.DenseVector.from_values(h, "f64", device="cuda"))
+    shard = step(lambda h: ShardedVector.from_global(h, "f64", device="cuda"))
+    for u, v in zip(dense, shard):
+        assert np.asarray(u).tobytes() == np.asarray(v).tobytes()
