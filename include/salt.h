@@ -169,6 +169,18 @@ int salt_assign_reduce_exchange(int dtype, const char* assign_sig, const char* r
                                 const salt_exchange* exchange,
                                 void* out_dev, void* out_host, void* stream);
 
+/* salt_fused with the reduction's total exchanged in-kernel over NVLink
+ * (as salt_reduce_exchange): statements + device scalars on sharded data.
+ * reduce_sig must be non-NULL. */
+int salt_fused_exchange(int dtype, const char* assign_sigs, const char* reduce_sig,
+                        void* const* dsts, int ndst, const void* const* leaves, int nleaves,
+                        const double* scalars, int nscalars,
+                        const void* const* pscalars, int npscalars,
+                        int64_t n, int flags,
+                        void* workspace, size_t workspace_bytes,
+                        const salt_exchange* exchange,
+                        void* out_dev, void* out_host, void* stream);
+
 /* Test hook: `world` thread blocks of ONE cooperative launch play the ranks
  * of the exchange protocol for `rounds` consecutive epochs (epoch0 ...),
  * each block publishing totals[r*world + rank] ({hi, lo} pairs) and writing

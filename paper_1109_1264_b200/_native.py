@@ -49,6 +49,7 @@ HEADER_SYMBOLS = (
     "salt_reduce_workspace_bytes",
     "salt_reduce_exchange",
     "salt_assign_reduce_exchange",
+    "salt_fused_exchange",
     "salt_exchange_emulate",
     "salt_signature_kind",
     "salt_prepare",
@@ -107,6 +108,11 @@ _SIGNATURES = {
         _c_int,
         [_c_int, _c_str, _c_str, _c_vp, _c_vpp, _c_int, _c_dp, _c_int, _c_i64, _c_int, _c_vp, _c_size,
          _c_vp, _c_vp, _c_vp, _c_vp],
+    ),
+    "salt_fused_exchange": (
+        _c_int,
+        [_c_int, _c_str, _c_str, _c_vpp, _c_int, _c_vpp, _c_int, _c_dp, _c_int, _c_vpp, _c_int,
+         _c_i64, _c_int, _c_vp, _c_size, _c_vp, _c_vp, _c_vp, _c_vp],
     ),
     "salt_exchange_emulate": (_c_int, [_c_int, _c_int, ctypes.c_uint64, _c_vp, _c_vp, _c_vp, _c_vp]),
     "salt_signature_kind": (_c_int, [_c_int, _c_str, _c_str, _c_int]),

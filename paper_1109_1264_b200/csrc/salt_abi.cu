@@ -1140,6 +1140,23 @@ int salt_assign_reduce_exchange(int dtype, const char* assign_sig, const char* r
                   workspace_bytes, out_dev, out_host, (cudaStream_t)stream, exchange);
 }
 
+int salt_fused_exchange(int dtype, const char* assign_sigs, const char* reduce_sig,
+                        void* const* dsts, int ndst, const void* const* leaves, int nleaves,
+                        const double* scalars, int nscalars, const void* const* pscalars,
+                        int npscalars, int64_t n, int flags, void* workspace,
+                        size_t workspace_bytes, const salt_exchange* exchange, void* out_dev,
+                        void* out_host, void* stream) {
+  if (!exchange) return fail(SALT_EINVAL, "NULL exchange descriptor");
+  if (!reduce_sig) return fail(SALT_EINVAL, "salt_fused_exchange needs a reduction");
+  Plan* p;
+  const int mode = assign_sigs ? salt::MODE_ASSIGN_REDUCE : salt::MODE_REDUCE;
+  int rc = make_plan(dtype, assign_sigs, reduce_sig, mode, nleaves, nscalars, p);
+  if (rc) return rc;
+  return dispatch(dtype, *p, dsts, ndst, leaves, nleaves, scalars, nscalars, n, flags, workspace,
+                  workspace_bytes, out_dev, out_host, (cudaStream_t)stream, exchange, pscalars,
+                  npscalars);
+}
+
 int salt_exchange_emulate(int world, int rounds, uint64_t epoch0, const void* totals_dev,
                           void* results_dev, void* scratch_dev, void* stream) {
   if (world < 1 || world > salt::XCHG_MAX_RANKS || rounds < 1 || epoch0 == 0 || !totals_dev ||

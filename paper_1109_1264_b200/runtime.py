@@ -473,7 +473,13 @@ def run_fused(asig, rsig, lw, dests, dtype, n, flags=0, lazy=False):
             return lib.salt_fused(code, a, r, dsts, len(dests), leaves, nl, scal, len(lw.scalars),
                                   pscal, np_, n, fl, ws, wsb, od, oh, st)
 
-        return True, _device_reduce(dev, dt, call, flags, lazy, sharded)
+        def xcall(fl, ws, wsb, x, od, oh, st):
+            return lib.salt_fused_exchange(code, a, r, dsts, len(dests), leaves, nl, scal,
+                                           len(lw.scalars), pscal, np_, n, fl, ws, wsb, x, od, oh,
+                                           st)
+
+        return True, _device_reduce(dev, dt, call, flags, lazy, sharded,
+                                    xcall if sharded is not None else None)
 
 
 def _sharded_operands(vectors):
