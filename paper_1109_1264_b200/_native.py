@@ -195,7 +195,8 @@ def fastpath():
                     addr(h.salt_assign), addr(h.salt_reduce), addr(h.salt_assign_reduce),
                     addr(h.salt_fused), addr(h.salt_last_error), h.salt_reduce_workspace_bytes(),
                     Leaf, AddNode, SubNode, MulNode, ScaleNode, DenseVector, DeviceScalar,
-                    torch._C._cuda_getCurrentRawStream, torch.cuda.current_device,
+                    # raw C getters: CUDA is initialised once a device vector exists
+                    torch._C._cuda_getCurrentRawStream, torch._C._cuda_getDevice,
                     runtime._workspace, np.float32, np.float64, runtime._lazy_out,
                 )
                 _fast = _fastpath

@@ -441,6 +441,75 @@ static PyObject* fp_fused(PyObject* self, PyObject* args) {
   return t;
 }
 
+/* op(sig, dest_or_None, leaves_tuple, alpha_or_None, flags, lazy): a named
+ * operation (ops.py) without building node objects.  `sig` is the
+ * signature expressions.lower() gives that operation for these operands
+ * (the caller picks it, deduplicating repeated vectors); `alpha` is coerced
+ * to the element type like ScaleNode does.  Assignments return True,
+ * reductions their result; None = not eligible (the node path runs). */
+static PyObject* fp_op(PyObject* self, PyObject* args) {
+  const char* sig;
+  PyObject *dest, *leaves, *alpha;
+  int flags, lazy = 0;
+  if (!PyArg_ParseTuple(args, "yOO!Oi|p", &sig, &dest, &PyTuple_Type, &leaves, &alpha, &flags,
+                        &lazy))
+    return NULL;
+  Py_ssize_t nl = PyTuple_GET_SIZE(leaves);
+  if (nl < 1 || nl > MAX_LEAVES) Py_RETURN_NONE;
+  Walk w;
+  void* dptr = NULL;
+  int rc = start(&w, dest != Py_None ? dest : PyTuple_GET_ITEM(leaves, 0),
+                 dest != Py_None ? &dptr : NULL);
+  if (rc <= 0) { if (rc < 0) return NULL; Py_RETURN_NONE; }
+  for (Py_ssize_t k = 0; k < nl; ++k) {
+    PyObject* v = PyTuple_GET_ITEM(leaves, k);
+    if ((PyObject*)Py_TYPE(v) != T_Dense) Py_RETURN_NONE;
+    long long dev, code, n, ptr;
+    if (long_attr(v, s_dev, &dev) < 0 || long_attr(v, s_code, &code) < 0 ||
+        long_attr(v, s_n, &n) < 0 || long_attr(v, s_ptr, &ptr) < 0)
+      return NULL;
+    if (dev != w.dev || code != w.code || n != w.n) Py_RETURN_NONE;
+    w.ptrs[k] = (void*)(intptr_t)ptr;
+  }
+  w.nvec = (int)nl;
+  if (alpha != Py_None) {
+    /* Python floats, small ints and NumPy floating scalars only; anything
+     * else (DeviceScalar, huge ints, arrays) takes the node path */
+    double a;
+    if (PyFloat_Check(alpha)) {
+      a = PyFloat_AS_DOUBLE(alpha);
+    } else if (PyLong_Check(alpha)) {
+      long long i = PyLong_AsLongLong(alpha);
+      if (i == -1 && PyErr_Occurred()) { PyErr_Clear(); Py_RETURN_NONE; }
+      if (i > (1LL << 53) || i < -(1LL << 53)) Py_RETURN_NONE;
+      a = (double)i;
+    } else if ((PyObject*)Py_TYPE(alpha) == np_f64 || (PyObject*)Py_TYPE(alpha) == np_f32) {
+      a = PyFloat_AsDouble(alpha);
+      if (a == -1.0 && PyErr_Occurred()) return NULL;
+    } else {
+      Py_RETURN_NONE;
+    }
+    if (w.code == 0) a = (double)(float)a; /* round to the element type (ScaleNode) */
+    w.sc[0] = a;
+    w.nsc = 1;
+  }
+  void* stream;
+  rc = stream_for(&w, &stream);
+  if (rc <= 0) { if (rc < 0) return NULL; Py_RETURN_NONE; }
+  size_t len = strlen(sig);
+  if (len >= MAX_SIG) Py_RETURN_NONE;
+  memcpy(w.sig, sig, len + 1);
+  w.len = (int)len;
+  if (dest != Py_None) {
+    if (w.n == 0) Py_RETURN_TRUE;
+    return check(p_assign(w.code, w.sig, dptr, (const void* const*)w.ptrs, w.nvec, w.sc, w.nsc,
+                          w.n, stream));
+  }
+  void *ws, *slot;
+  if (workspace(&w, stream, &ws, &slot) < 0) return NULL;
+  return launch_reduce(&w, NULL, NULL, 0, flags, lazy, ws, slot, stream);
+}
+
 static PyObject* fp_init(PyObject* self, PyObject* args) {
   unsigned long long a, r, ar, fu, le;
   Py_ssize_t wsb;
@@ -466,6 +535,8 @@ static PyMethodDef methods[] = {
     {"reduce", fp_reduce, METH_VARARGS, "reduce(child, flags, lazy=False) -> scalar or None"},
     {"assign_reduce", fp_assign_reduce, METH_VARARGS,
      "assign_reduce(dest, source, child, flags, lazy=False) -> scalar or None"},
+    {"op", fp_op, METH_VARARGS,
+     "op(sig, dest_or_None, leaves, alpha_or_None, flags, lazy=False) -> True / result, or None"},
     {"fused", fp_fused, METH_VARARGS,
      "fused(((dest, source), ...), total_child_or_None, flags, lazy=False) -> (result,) or None"},
     {NULL, NULL, 0, NULL}};

@@ -30,34 +30,67 @@ from .expressions import (
 __all__ = ["dot", "scal", "axpy", "scaled_copy", "sum", "norm2", "axpy_dot", "fused"]
 
 
+def _op(sig, dest, leaves, alpha=None, flags=0, lazy=False):
+    """C fast path for a named operation on plain device vectors (no node
+    objects; csrc/fastpath.c `op`): the same signature, scalars and kernel
+    as the node path below.  None = not eligible."""
+    fast = _native.fastpath()
+    if fast is None:
+        return None
+    return fast.op(sig, dest, leaves, alpha, flags, lazy)
+
+
+def _lazy_only(options):
+    return not options or (len(options) == 1 and "lazy" in options)
+
+
 def dot(x, y, **options):
     """Sum of elementwise products of two equal-length vectors."""
+    if _lazy_only(options):
+        r = _op(b"L0 L0 *" if x is y else b"L0 L1 *", None, (x,) if x is y else (x, y),
+                lazy=options.get("lazy", False))
+        if r is not None:
+            return r
     return execute_reduce(SumNode(MulNode(as_node(x), as_node(y))), **options)
 
 
 def scal(alpha, x, **options) -> None:
     """In-place x = alpha * x (exact aliasing of source and destination)."""
+    if not options and _op(b"S0 L0 *", x, (x,), alpha) is not None:
+        return
     execute_assign(AssignNode(as_node(x), ScaleNode(alpha, as_node(x))), **options)
 
 
 def axpy(alpha, x, y, **options) -> None:
     """In-place y = y + alpha * x."""
+    if not options and x is not y and _op(b"L0 S0 L1 * +", y, (y, x), alpha) is not None:
+        return
     execute_assign(AssignNode(as_node(y), as_node(y) + ScaleNode(alpha, as_node(x))), **options)
 
 
 def scaled_copy(alpha, x, out, **options) -> None:
     """out = alpha * x in one traversal (n reads + n writes); out must not
     overlap x."""
+    if not options and _op(b"S0 L0 *", out, (x,), alpha) is not None:
+        return
     execute_assign(AssignNode(as_node(out), ScaleNode(alpha, as_node(x))), **options)
 
 
 def sum(x, **options):  # noqa: A001 - reference name
     """Sum of all elements."""
+    if _lazy_only(options):
+        r = _op(b"L0", None, (x,), lazy=options.get("lazy", False))
+        if r is not None:
+            return r
     return execute_reduce(SumNode(as_node(x)), **options)
 
 
 def norm2(x, **options):
     """Euclidean norm sqrt(dot(x, x)), no overflow scaling (as the reference)."""
+    if _lazy_only(options):
+        r = _op(b"L0 L0 *", None, (x,), flags=_native.SALT_SQRT, lazy=options.get("lazy", False))
+        if r is not None:
+            return r
     return execute_reduce(
         SumNode(MulNode(as_node(x), as_node(x))), _flags=_native.SALT_SQRT, **options
     )

@@ -243,3 +243,41 @@ def test_assign_accepts_plan_overrides():
     d = lv.DenseVector.zeros(5, "f32", device="cuda")
     d.assign(a + a, unroll=2, packages=1, backend=wide_backend("f32", 8))
     assert d.to_values() == [2, 4, 6, 8, 10]
+
+
+def test_named_ops_fast_path_is_taken_and_matches_the_node_path(monkeypatch):
+    """ops.* on plain device vectors go straight to the C fast path (no
+    node objects, csrc/fastpath.c `op`) and give the node path's bits; the
+    alpha coercion matches ScaleNode's for every scalar type."""
+    import paper_1109_1264_b200.ops as ops_mod
+
+    g = np.random.default_rng(12)
+    alphas = [0.7, 3, True, np.float32(-1.3), np.float64(2.0 ** -30 + 1.0), 1e300]
+    for dtype in DTYPES:
+        xv, yv = (g.standard_normal(50_003).astype(NPT[dtype]) for _ in range(2))
+
+        def run():
+            out = []
+            for a in alphas:
+                x, y, o = vec(xv, dtype), vec(yv, dtype), lv.DenseVector.zeros(50_003, dtype, device="cuda")
+                lv.axpy(a, x, y)
+                lv.scal(a, x)
+                lv.scaled_copy(a, y, o)
+                out += [x.to_array(), y.to_array(), o.to_array()]
+            x, y = vec(xv, dtype), vec(yv, dtype)
+            out += [np.array([lv.dot(x, y), lv.dot(x, x), lv.sum(x), lv.norm2(y),
+                              lv.dot(x, y, lazy=True).item(), lv.norm2(x, lazy=True).item()])]
+            return out
+
+        calls = []
+        real_assign, real_reduce = ops_mod.execute_assign, ops_mod.execute_reduce
+        monkeypatch.setattr(ops_mod, "execute_assign", lambda *a, **k: calls.append(1) or real_assign(*a, **k))
+        monkeypatch.setattr(ops_mod, "execute_reduce", lambda *a, **k: calls.append(1) or real_reduce(*a, **k))
+        fast = run()
+        assert not calls  # every call above took the C fast path
+        monkeypatch.setattr(_native, "_fast", None)
+        slow = run()
+        assert calls
+        monkeypatch.undo()
+        for u, v in zip(fast, slow):
+            assert u.tobytes() == v.tobytes()
