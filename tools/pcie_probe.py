@@ -53,6 +53,37 @@ def main():
             "h2d_two_streams_gbs": round(bw(two_h2d, n), 2),
             "bidirectional_total_gbs": round(bw(both, 2 * n), 2),
         }
+    # The end-to-end step's shape with no kernel at all: 3 bytes up for every
+    # byte down (T2: a, b, c in; d out), both directions at once, in 8 chunks
+    # so the D2H of chunk k overlaps the H2D of chunk k+1 — the ceiling of
+    # bench.py's e2e number.
+    n = 768 << 20
+    h = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    ho = torch.empty(n // 3, dtype=torch.uint8, pin_memory=True)
+    d = torch.empty(n, dtype=torch.uint8, device="cuda")
+    do = torch.empty(n // 3, dtype=torch.uint8, device="cuda")
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+
+    def mix():
+        k, ko = n // 8, n // 24
+        evs = []
+        for c in range(8):
+            with torch.cuda.stream(s1):
+                d[c * k:(c + 1) * k].copy_(h[c * k:(c + 1) * k], non_blocking=True)
+                e = torch.cuda.Event()
+                e.record(s1)
+            s2.wait_event(e)
+            with torch.cuda.stream(s2):
+                ho[c * ko:(c + 1) * ko].copy_(do[c * ko:(c + 1) * ko], non_blocking=True)
+            evs.append(e)
+        s1.synchronize()
+        s2.synchronize()
+
+    res["t2_shape_3up_1down"] = {
+        "effective_gbs": round(bw(mix, n + n // 3), 2),
+        "note": "768 MiB H2D + 256 MiB D2H per step in 8 chunks, D2H of chunk k overlapping H2D "
+                "of chunk k+1; no kernel: the ceiling of the e2e path",
+    }
     print(json.dumps(res, indent=1))
 
 
