@@ -65,6 +65,15 @@ int tuning_unroll() {
   }();
   return env;
 }
+// SALT_JIT_MINB=B (tuning only): JIT-build every vector kernel with
+// __launch_bounds__(256, B), i.e. registers capped for B CTAs per SM.
+int tuning_minb() {
+  static const int env = [] {
+    const char* e = getenv("SALT_JIT_MINB");
+    return e ? atoi(e) : 0;
+  }();
+  return env;
+}
 
 // Reductions whose tiles fit max_cluster() CTAs x cluster_tiles() run as
 // ONE thread-block cluster (SALT_CLUSTER = max CTAs, 0 disables, <= 16;
@@ -511,9 +520,12 @@ Kernel* jit_compile(int dtype, int mode, int vec, int nl, const std::string& ta,
   std::string expr = std::string("salt::fused_kernel<") + tname + "," + ta + "," + tr + "," +
                      std::to_string(mode) + "," + std::to_string(vec) + "," +
                      std::to_string(unroll) + "," + std::to_string(kBlock) + ">";
-  const char* opts[] = {"--gpu-architecture=sm_100a", "-fmad=false", "--std=c++17",
-                        "-lineinfo", "-default-device", "-DSALT_NO_256BIT"};
-  const int nopts = nv.has_256bit ? 5 : 6;
+  const std::string minb = "-DSALT_MIN_BLOCKS=" + std::to_string(tuning_minb());
+  const char* opts[8] = {"--gpu-architecture=sm_100a", "-fmad=false", "--std=c++17",
+                         "-lineinfo", "-default-device"};
+  int nopts = 5;
+  if (!nv.has_256bit) opts[nopts++] = "-DSALT_NO_256BIT";
+  if (tuning_minb() > 0 && vec != 1) opts[nopts++] = minb.c_str();
   std::string cache_path;
   const std::string cdir = jit_cache_dir();
   if (!cdir.empty()) {
@@ -577,7 +589,7 @@ Kernel* get_kernel(int dtype, int mode, int vec, int nl, const std::string& ta,
   ensure_table();
   const std::string key = key_of(dtype, mode, vec, ta, tr);
   std::lock_guard<std::mutex> lk(g_table_mu);
-  if (!g_force_jit.load() && tuning_unroll() <= 0) {
+  if (!g_force_jit.load() && tuning_unroll() <= 0 && tuning_minb() <= 0) {
     auto it = table().find(key);
     if (it != table().end()) return it->second.get();
   }

@@ -468,7 +468,16 @@ __device__ __forceinline__ void AssignRoots<EA, R, N>::one(E& e, T* const* dst, 
 // 256-bit loads before any arithmetic: the GPU form of the reference's load
 // burst / vector_op burst / store burst (engine.py:209-225).
 template <class T, class EA, class ER, int MODE, int V, int UNR, int BLOCK>
-__global__ void __launch_bounds__(BLOCK) fused_kernel(Args<T> a) {
+// SALT_MIN_BLOCKS (tuning: SALT_JIT_MINB JIT-builds with it) caps registers
+// for that many CTAs per SM.  Left undefined on purpose: an explicit
+// minimum of 1 lets ptxas spend more registers (ddot 56 -> 78) and costs
+// ~10 % bandwidth (profiles/r01_launch_bounds.txt).
+#ifdef SALT_MIN_BLOCKS
+#define SALT_BOUNDS(B) __launch_bounds__(B, SALT_MIN_BLOCKS)
+#else
+#define SALT_BOUNDS(B) __launch_bounds__(B)
+#endif
+__global__ void SALT_BOUNDS(BLOCK) fused_kernel(Args<T> a) {
   constexpr int NL = cmax(EA::NL, ER::NL);
   constexpr int NS = cmax(EA::NS, ER::NS);
   constexpr int NP = cmax(EA::NP, ER::NP);

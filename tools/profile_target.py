@@ -36,6 +36,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--case", choices=sorted(CASES), required=True)
     ap.add_argument("--launches", type=int, default=5)
+    ap.add_argument("--time", action="store_true",
+                    help="instead: best-of-20 CUDA-event time per launch and algorithmic GB/s")
     a = ap.parse_args()
     dt, n, k = CASES[a.case]
     v = [lv.DenseVector.from_tensor(torch.rand(n, dtype=dt, device="cuda") * 2 - 1) for _ in range(k)]
@@ -54,6 +56,36 @@ def main():
         "axpydot": lambda: lv.axpy_dot(0.5, v[0], v[1], v[2], lazy=True),
         "daxpy20": lambda: lv.axpy(0.5, v[0], v[1]),
     }
+    if a.time:
+        import json
+
+        per = {"t2": 4, "t1": 4, "dot64": 2, "dot32": 2, "nrm2_32": 1, "nrm2_64": 1, "cgupdate": 6,
+               "etree32": 5, "axpydot": 4, "daxpy20": 3}[a.case]
+        nbytes = per * n * torch.empty(0, dtype=dt).element_size()
+        for _ in range(3):
+            calls[a.case]()
+        ts = []
+        for _ in range(20):
+            torch.cuda._sleep(100_000)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            calls[a.case]()
+            e1.record()
+            e1.synchronize()
+            ts.append(e0.elapsed_time(e1) * 1e-3)
+        # back to back: 20 launches between two events
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(20):
+            calls[a.case]()
+        e1.record()
+        e1.synchronize()
+        b2b = e0.elapsed_time(e1) * 1e-3 / 20
+        ts.sort()
+        print(json.dumps({"case": a.case, "best_s": ts[0], "gbs": round(nbytes / ts[0] / 1e9, 1),
+                          "median_gbs": round(nbytes / ts[len(ts) // 2] / 1e9, 1),
+                          "b2b_gbs": round(nbytes / b2b / 1e9, 1)}))
+        return
     for _ in range(a.launches):
         calls[a.case]()
     torch.cuda.synchronize()
