@@ -192,6 +192,10 @@ def measure(op, variant, n, dtype="f32", reps=25, warmup=5, seed=0, flush_l2=Fal
         restore()
         call()
     torch.cuda.synchronize()
+    # Device variants without an L2 flush: below 64 MB of traffic a call
+    # lasts a few microseconds, close to the ~1-2 us tick of the event
+    # clock, so one rep times `inner` back-to-back calls and divides.
+    inner = 1 if host or flush is not None or bytes_moved(op, n, dt) >= (64 << 20) else 16
     times = []
     for _ in range(reps):
         restore()
@@ -202,15 +206,16 @@ def measure(op, variant, n, dtype="f32", reps=25, warmup=5, seed=0, flush_l2=Fal
             torch.cuda.synchronize()
             times.append(time.perf_counter() - t0)
         else:
-            # queue ~50 us of GPU work first so the events bracket device time,
+            # queue ~50 us of GPU work per call first so the events bracket device time,
             # not the host's launch latency
-            torch.cuda._sleep(100_000)
+            torch.cuda._sleep(100_000 * inner)
             s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             s.record()
-            call()
+            for _ in range(inner):
+                call()
             e.record()
             e.synchronize()
-            times.append(s.elapsed_time(e) / 1e3)
+            times.append(s.elapsed_time(e) / 1e3 / inner)
     best = min(times)
     med = statistics.median(times)
     gbytes = bytes_moved(op, n, dt) / best / 1e9

@@ -854,7 +854,7 @@ int run_fused(Plan& p, void* const* dsts, int ndst, const void* const* leaves, i
   const i64 per_tile = (i64)kBlock * k->unroll;
   const i64 ntiles = (a.nvec + per_tile - 1) / per_tile;
   i64 K = assign_tiles_per_cta(), cap = i64(0x7fffffff);
-  bool cluster = false;
+  bool cluster = false, one_group = false;
   if (reduce && ntiles > 2 && ntiles <= (i64)max_cluster() * cluster_tiles()) {
     // Small n (3 .. 16 x 2 tiles; up to 2 tiles one CTA is quicker): one cluster
     // of <= 16 CTAs, partials combined in distributed shared memory — no
@@ -872,15 +872,30 @@ int run_fused(Plan& p, void* const* dsts, int ndst, const void* const* leaves, i
     // 7.2 vs 5.1 TB/s) and more CTAs keep more SMs streaming (nrm2 f64 at
     // 2^19: 6.39 -> 4.67 us; profiles/r01_small_n/).
     // Up to 2 tiles: one CTA (no combine at all).
+    // The one group may hold 2 x GROUP = 512 CTAs when a thread keeps at
+    // most 128 bytes of loads in flight per tile (nrm2 / sum: one leaf x 4
+    // vectors; f64 dot: two leaves x 2): 256 such CTAs leave HBM short of
+    // requests at 2^23-2^25 (tools/midred_probe.cu, profiles/
+    // r01_midred_probe.txt: dnrm2 2^24 28.5 -> 26.3 us, ddot 2^24 46.9 ->
+    // 44.2 us, snrm2 2^24 17.4 -> 15.8 us); with more bytes in flight per
+    // thread (f32 dot, 3+ leaves) 512 CTAs are slower than 256.
+    const i64 vbytes = vec == 1 ? (i64)sizeof(T) : 32;
+    const i64 one = (i64)k->unroll * p.nl * vbytes <= 128 ? 2 * salt::GROUP : salt::GROUP;
     if (ntiles <= 2) K = ntiles > 0 ? ntiles : 1;
-    else if (ntiles <= (i64)group_tiles() * salt::GROUP)
-      K = (ntiles + salt::GROUP - 1) / salt::GROUP;
+    else if (ntiles <= (i64)group_tiles() * one) {
+      K = (ntiles + one - 1) / one;
+      one_group = true;
+    }
   }
   if ((ntiles + K - 1) / K > cap) K = (ntiles + cap - 1) / cap;
   i64 g64 = (ntiles + K - 1) / K;
   if (g64 < 1) g64 = 1;
   const int grid = (int)g64;
   a.tiles_per_cta = K;
+  // CTAs per combine group: the whole grid when it was sized as one group
+  // (at most 2 x GROUP), else GROUP (a grid of <= GROUP CTAs is one group
+  // either way).
+  a.group = one_group ? grid : salt::GROUP;
   if (reduce) {
     char* w = (char*)ws;
     a.ticket = (unsigned int*)(w + salt::WsLayout::ticket);

@@ -172,11 +172,13 @@ template <class T> struct Args {
   void* out;                      // T result or DD partial
   int flags;
   int cluster;                    // reduce modes: 1 = the grid is ONE thread-block cluster
+  int group;                      // reduce modes: CTAs per group (GROUP, or the whole grid
+                                  // when it is one group of <= MAX_ONE_GROUP CTAs)
   Xchg xchg;                      // sharded reductions over NVLink (world 0: off)
 };
 
 // Reduction workspace: [ticket | group tickets | group partials | CTA partials].
-enum { GROUP = 256, MAX_GROUPS = 4096, MAX_REDUCE_CTAS = GROUP * MAX_GROUPS };
+enum { GROUP = 256, MAX_GROUPS = 4096, MAX_REDUCE_CTAS = GROUP * MAX_GROUPS, MAX_ONE_GROUP = 1024 };
 struct WsLayout {
   static constexpr i64 ticket = 0;
   static constexpr i64 group_tickets = 256;
@@ -547,12 +549,14 @@ __global__ void SALT_BOUNDS(BLOCK) fused_kernel(Args<T> a) {
 
   if (REDUCE) {
     // Two-level deterministic combine.  Every CTA publishes its partial; the
-    // last CTA to arrive in its group of GROUP consecutive CTAs folds the
+    // last CTA to arrive in its group of a.group consecutive CTAs (GROUP, or
+    // the whole grid when it is a single group) folds the
     // group's partials (thread t takes CTA t of the group, then a fixed
     // shuffle/shared-memory tree); the last group to finish folds the group
     // partials in group order.  Which CTA does the folding never changes
     // the order, so the result depends only on n — not on scheduling, SM
     // count or occupancy.
+    static_assert(MAX_ONE_GROUP % BLOCK == 0 && GROUP <= MAX_ONE_GROUP, "group fold layout");
     __shared__ DD smem[BLOCK / 32];
     __shared__ int stage;  // 0 done, 1 group finisher, 2 group + final finisher
     DD part = block_reduce_dd<BLOCK>(acc.get(), smem);
@@ -588,21 +592,34 @@ __global__ void SALT_BOUNDS(BLOCK) fused_kernel(Args<T> a) {
       }
       return;
     }
-    const unsigned int g = blockIdx.x / GROUP;
-    const unsigned int ngroups = (gridDim.x + GROUP - 1) / GROUP;
-    const unsigned int gsize = min((unsigned int)GROUP, gridDim.x - g * GROUP);
+    const unsigned int G = (unsigned int)a.group;
+    const unsigned int g = blockIdx.x / G;
+    const unsigned int ngroups = (gridDim.x + G - 1) / G;
+    const unsigned int gsize = min(G, gridDim.x - g * G);
     if (threadIdx.x == 0) {
       a.partials[blockIdx.x] = part;
       stage = ticket_add(&a.group_tickets[g]) == gsize - 1 ? 1 : 0;
     }
     __syncthreads();
     if (stage == 0) return;
+    // Thread t folds CTAs t, t + BLOCK, ... of the group in that order (a
+    // group has at most MAX_ONE_GROUP = 4 * BLOCK CTAs); the loads (L2:
+    // other CTAs wrote these during this launch) are issued before the
+    // first add so they overlap.
     DD v; v.hi = 0.0; v.lo = 0.0;
-    for (unsigned int b = threadIdx.x; b < gsize; b += BLOCK) {
-      DD p;  // L2 loads: other CTAs wrote these during this launch
-      p.hi = __ldcg(&a.partials[g * GROUP + b].hi);
-      p.lo = __ldcg(&a.partials[g * GROUP + b].lo);
-      v = dd_add(v, p);
+    {
+      DD p[MAX_ONE_GROUP / BLOCK];
+#pragma unroll
+      for (int i = 0; i < MAX_ONE_GROUP / BLOCK; ++i) {
+        const unsigned int b = threadIdx.x + i * BLOCK;
+        if (b < gsize) {
+          p[i].hi = __ldcg(&a.partials[g * G + b].hi);
+          p[i].lo = __ldcg(&a.partials[g * G + b].lo);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < MAX_ONE_GROUP / BLOCK; ++i)
+        if (threadIdx.x + i * BLOCK < gsize) v = dd_add(v, p[i]);
     }
     __syncthreads();
     DD q = block_reduce_dd<BLOCK>(v, smem);

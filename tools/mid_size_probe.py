@@ -7,6 +7,10 @@ For each size and op, device time per launch measured three ways:
   b2b         20 back-to-back launches between two events, averaged
   b2b_clean   same, but each launch preceded by a 512 MiB READ sweep that
               leaves the L2 full of clean lines (no inputs resident)
+  diff        R x (read sweep + launch) minus R x (read sweep), per launch:
+              the clean-L2 cost without the ~2 us tick of the event clock
+  diff_dirty  the same with a 512 MiB fill (L2 full of dirty lines, the
+              flush config_sweep and the driver's rules use)
 and the same for the torch library call (torch.dot / vector_norm / eager T1).
 
     python tools/mid_size_probe.py [--out profiles/r01_mid_sizes.json]
@@ -71,6 +75,36 @@ def b2b(fn, reps=20, clean=False):
     return best
 
 
+DIRTY = None
+
+
+def dirty_l2():
+    global DIRTY
+    if DIRTY is None:
+        DIRTY = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+    DIRTY.fill_(7)
+
+
+def diff(fn, reps=40, dirty=False):
+    sweep = dirty_l2 if dirty else clean_l2
+    best = float("inf")
+    for _ in range(3):
+        a, b, c = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        sweep()
+        fn()
+        a.record()
+        for _ in range(reps):
+            sweep()
+            fn()
+        b.record()
+        for _ in range(reps):
+            sweep()
+        c.record()
+        c.synchronize()
+        best = min(best, (a.elapsed_time(b) - b.elapsed_time(c)) * 1e3 / reps)
+    return best
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=None)
@@ -104,7 +138,8 @@ def main():
                 row = {"op": op, "dtype": dt, "n": n, "MB": round(bpe * n / 1e6, 1)}
                 for name, f in (("salt", fn), ("torch", tfn))[: 1 if args.no_torch else 2]:
                     for mode, m in (("single", lambda f=f: single(f)), ("b2b", lambda f=f: b2b(f)),
-                                    ("b2b_clean", lambda f=f: b2b(f, clean=True))):
+                                    ("b2b_clean", lambda f=f: b2b(f, clean=True)),
+                                    ("diff", lambda f=f: diff(f)), ("diff_dirty", lambda f=f: diff(f, dirty=True))):
                         if mode not in args.modes.split(","):
                             continue
                         us = m()
