@@ -190,6 +190,30 @@ int salt_exchange_emulate(int world, int rounds, uint64_t epoch0,
                           const void* totals_dev, void* results_dev,
                           void* scratch_dev, void* stream);
 
+/* ---- single-process multi-GPU: one host thread drives G devices ----
+ * each device's reduction writes its {hi, lo} partial
+ * (salt_reduce / salt_assign_reduce / salt_fused with SALT_PARTIAL); one
+ * NCCL group of all-gathers over NVLink and a fixed rank-order fold leave
+ * the total, rounded to dtype (sqrt with SALT_SQRT), in out_dev_per_gpu[g]
+ * on every device — the bits of salt_reduce_finish / the in-kernel
+ * exchange.  Replaces the reference's single-threaded Sum over the whole
+ * vector (SumNode, expressions.py:401-480; engine.py:267-292) when the
+ * vector is block-sharded across the devices of one process.
+ *   out_dev_per_gpu[g]  device pointer on comms[g]'s device, >= 16 bytes:
+ *                       the partial in, the scalar out (stream-ordered)
+ *   comms               ncclComm_t[G] with comms[g] = rank g (e.g. from
+ *                       salt_nccl_comm_init_all)
+ *   streams             cudaStream_t[G], streams[g] on comms[g]'s device
+ * Enqueues only (no host synchronisation).  NCCL is loaded at run time
+ * ($SALT_NCCL_LIB, else libnccl.so.2). */
+int salt_allreduce_sum(void* out_dev_per_gpu[], int G, int dtype, void* comms, void* streams[]);
+int salt_allreduce_sum_flags(void* out_dev_per_gpu[], int G, int dtype, void* comms,
+                             void* streams[], int flags);
+/* ncclCommInitAll(G, devices) through the same runtime-loaded NCCL; comms_out
+ * receives G ncclComm_t.  devices NULL = 0..G-1. */
+int salt_nccl_comm_init_all(int G, const int* devices, void** comms_out);
+int salt_nccl_comm_destroy(int G, void** comms);
+
 /* Host-buffer (end-to-end) variants: leaves / dst are HOST pointers (pinned
  * memory for full speed).  Chunks are streamed H2D -> fused kernel -> D2H
  * through `staging` (device memory, caller-owned) on three caller streams

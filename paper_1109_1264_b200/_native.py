@@ -51,6 +51,10 @@ HEADER_SYMBOLS = (
     "salt_assign_reduce_exchange",
     "salt_fused_exchange",
     "salt_exchange_emulate",
+    "salt_allreduce_sum",
+    "salt_allreduce_sum_flags",
+    "salt_nccl_comm_init_all",
+    "salt_nccl_comm_destroy",
     "salt_signature_kind",
     "salt_prepare",
     "salt_set_force_jit",
@@ -115,6 +119,10 @@ _SIGNATURES = {
          _c_i64, _c_int, _c_vp, _c_size, _c_vp, _c_vp, _c_vp, _c_vp],
     ),
     "salt_exchange_emulate": (_c_int, [_c_int, _c_int, ctypes.c_uint64, _c_vp, _c_vp, _c_vp, _c_vp]),
+    "salt_allreduce_sum": (_c_int, [_c_vpp, _c_int, _c_int, _c_vpp, _c_vpp]),
+    "salt_allreduce_sum_flags": (_c_int, [_c_vpp, _c_int, _c_int, _c_vpp, _c_vpp, _c_int]),
+    "salt_nccl_comm_init_all": (_c_int, [_c_int, _c_vp, _c_vpp]),
+    "salt_nccl_comm_destroy": (_c_int, [_c_int, _c_vpp]),
     "salt_signature_kind": (_c_int, [_c_int, _c_str, _c_str, _c_int]),
     "salt_prepare": (_c_int, [_c_int, _c_str, _c_str, _c_int]),
     "salt_set_force_jit": (None, [_c_int]),

@@ -969,6 +969,125 @@ int finish(const void* parts, int count, int flags, void* out_dev, void* out_hos
   return 0;
 }
 
+// ------------------------------------------------------------------ single-process multi-GPU
+// NCCL is loaded at run time (no link-time dependency): $SALT_NCCL_LIB, else
+// the soname libnccl.so.2 — which resolves to the copy torch already loaded
+// when torch is in the process — else the system library.
+typedef int ncclResult_v;
+struct Nccl {
+  bool ok = false;
+  std::string why;
+  ncclResult_v (*CommInitAll)(void** comms, int ndev, const int* devlist) = nullptr;
+  ncclResult_v (*CommDestroy)(void* comm) = nullptr;
+  ncclResult_v (*CommCuDevice)(void* comm, int* device) = nullptr;
+  ncclResult_v (*CommCount)(void* comm, int* count) = nullptr;
+  ncclResult_v (*CommUserRank)(void* comm, int* rank) = nullptr;
+  ncclResult_v (*GroupStart)() = nullptr;
+  ncclResult_v (*GroupEnd)() = nullptr;
+  ncclResult_v (*AllGather)(const void* send, void* recv, size_t count, int datatype, void* comm,
+                            cudaStream_t stream) = nullptr;
+  const char* (*GetErrorString)(ncclResult_v) = nullptr;
+};
+constexpr int kNcclFloat64 = 8;  // ncclFloat64 (nccl.h)
+
+Nccl& nccl() {
+  static Nccl n;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    const char* env = getenv("SALT_NCCL_LIB");
+    const char* cands[] = {env, "libnccl.so.2", "/usr/lib/x86_64-linux-gnu/libnccl.so.2"};
+    void* h = nullptr;
+    for (const char* c : cands) {
+      if (!c) continue;
+      h = dlopen(c, RTLD_NOW | RTLD_LOCAL);
+      if (h) break;
+    }
+    if (!h) {
+      n.why = "libnccl.so.2 not found (set SALT_NCCL_LIB)";
+      return;
+    }
+#define SYM(F, NAME)                                        \
+  n.F = reinterpret_cast<decltype(n.F)>(dlsym(h, NAME));    \
+  if (!n.F) { n.why = std::string("nccl symbol missing: ") + NAME; return; }
+    SYM(CommInitAll, "ncclCommInitAll");
+    SYM(CommDestroy, "ncclCommDestroy");
+    SYM(CommCuDevice, "ncclCommCuDevice");
+    SYM(CommCount, "ncclCommCount");
+    SYM(CommUserRank, "ncclCommUserRank");
+    SYM(GroupStart, "ncclGroupStart");
+    SYM(GroupEnd, "ncclGroupEnd");
+    SYM(AllGather, "ncclAllGather");
+    SYM(GetErrorString, "ncclGetErrorString");
+#undef SYM
+    n.ok = true;
+  });
+  return n;
+}
+
+int nccl_fail(ncclResult_v r, const char* what) {
+  return fail(SALT_ECUDA, std::string(what) + ": " + (nccl().GetErrorString ? nccl().GetErrorString(r) : "nccl error"));
+}
+
+// Restores the caller's current device on scope exit.
+struct DeviceGuard {
+  int dev = -1;
+  DeviceGuard() { cudaGetDevice(&dev); }
+  ~DeviceGuard() { if (dev >= 0) cudaSetDevice(dev); }
+};
+
+// G per-device {hi, lo} partials -> every device holds the rank-ordered fold
+// (finish_kernel: the same arithmetic as salt_reduce_finish and the NVLink
+// exchange, so all three multi-GPU paths give identical bits).  One group of
+// G all-gathers of 16 bytes, then one finish kernel per device, all
+// enqueued on the callers' streams; gathered partials live in stream-ordered
+// allocations freed on the same streams.
+int allreduce_sum(void* const* out_dev, int G, int dtype, void* const* comms, void* const* streams,
+                  int flags) {
+  if (G < 1 || !out_dev || !comms || !streams) return fail(SALT_EINVAL, "bad allreduce arguments");
+  if (dtype != SALT_F32 && dtype != SALT_F64) return fail(SALT_EINVAL, "dtype must be SALT_F32 or SALT_F64");
+  if (flags & ~SALT_SQRT) return fail(SALT_EINVAL, "allreduce flags: only SALT_SQRT");
+  Nccl& nc = nccl();
+  if (!nc.ok) return fail(SALT_ECUDA, nc.why);
+  DeviceGuard guard;
+  std::vector<int> devs(G);
+  std::vector<void*> gathered(G, nullptr);
+  auto release = [&]() {
+    for (int g = 0; g < G; ++g)
+      if (gathered[g]) {
+        cudaSetDevice(devs[g]);
+        cudaFreeAsync(gathered[g], (cudaStream_t)streams[g]);
+      }
+  };
+  for (int g = 0; g < G; ++g) {
+    if (!out_dev[g] || !comms[g]) return fail(SALT_EINVAL, "NULL partial or communicator");
+    int count = 0, rank = -1;
+    ncclResult_v r = nc.CommCuDevice(comms[g], &devs[g]);
+    if (!r) r = nc.CommCount(comms[g], &count);
+    if (!r) r = nc.CommUserRank(comms[g], &rank);
+    if (r) return nccl_fail(r, "ncclComm query");
+    if (count != G || rank != g) return fail(SALT_EINVAL, "comms[g] must be rank g of a G-rank communicator");
+  }
+  for (int g = 0; g < G; ++g) {
+    cudaError_t e = cudaSetDevice(devs[g]);
+    if (e == cudaSuccess) e = cudaMallocAsync(&gathered[g], (size_t)G * sizeof(salt::DD), (cudaStream_t)streams[g]);
+    if (e != cudaSuccess) { release(); return cuda_fail(e, "cudaMallocAsync(gathered partials)"); }
+  }
+  ncclResult_v r = nc.GroupStart();
+  for (int g = 0; g < G && !r; ++g)
+    r = nc.AllGather(out_dev[g], gathered[g], 2, kNcclFloat64, comms[g], (cudaStream_t)streams[g]);
+  ncclResult_v r2 = nc.GroupEnd();
+  if (r || r2) { release(); return nccl_fail(r ? r : r2, "ncclAllGather"); }
+  int rc = 0;
+  for (int g = 0; g < G && !rc; ++g) {
+    cudaError_t e = cudaSetDevice(devs[g]);
+    if (e != cudaSuccess) { rc = cuda_fail(e, "cudaSetDevice"); break; }
+    rc = dtype == SALT_F32 ? finish<float>(gathered[g], G, flags, out_dev[g], nullptr, (cudaStream_t)streams[g])
+                           : finish<double>(gathered[g], G, flags, out_dev[g], nullptr, (cudaStream_t)streams[g]);
+  }
+  release();
+  return rc;
+}
+
 // ------------------------------------------------------------------ host streaming
 struct Events {
   std::vector<cudaEvent_t> ev;
@@ -1262,6 +1381,38 @@ int salt_reduce_host(int dtype, const char* sig, const void* const* host_leaves,
   if (!out_host) return fail(SALT_EINVAL, "NULL out_host");
   return host_pipeline(dtype, *p, nullptr, host_leaves, nleaves, scalars, nscalars, n, flags,
                        staging, staging_bytes, streams3, out_host);
+}
+
+int salt_nccl_comm_init_all(int G, const int* devices, void** comms_out) {
+  if (G < 1 || !comms_out) return fail(SALT_EINVAL, "bad communicator arguments");
+  Nccl& nc = nccl();
+  if (!nc.ok) return fail(SALT_ECUDA, nc.why);
+  DeviceGuard guard;
+  ncclResult_v r = nc.CommInitAll(comms_out, G, devices);
+  return r ? nccl_fail(r, "ncclCommInitAll") : 0;
+}
+
+int salt_nccl_comm_destroy(int G, void** comms) {
+  if (G < 1 || !comms) return fail(SALT_EINVAL, "bad communicator arguments");
+  Nccl& nc = nccl();
+  if (!nc.ok) return fail(SALT_ECUDA, nc.why);
+  int rc = 0;
+  for (int g = 0; g < G; ++g)
+    if (comms[g]) {
+      ncclResult_v r = nc.CommDestroy(comms[g]);
+      if (r && !rc) rc = nccl_fail(r, "ncclCommDestroy");
+      comms[g] = nullptr;
+    }
+  return rc;
+}
+
+int salt_allreduce_sum(void* out_dev_per_gpu[], int G, int dtype, void* comms, void* streams[]) {
+  return allreduce_sum(out_dev_per_gpu, G, dtype, (void* const*)comms, streams, 0);
+}
+
+int salt_allreduce_sum_flags(void* out_dev_per_gpu[], int G, int dtype, void* comms,
+                             void* streams[], int flags) {
+  return allreduce_sum(out_dev_per_gpu, G, dtype, (void* const*)comms, streams, flags);
 }
 
 }  // extern "C"

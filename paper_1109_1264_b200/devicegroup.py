@@ -1,0 +1,143 @@
+"""Single-process multi-GPU: one host thread drives G devices.
+
+SURVEY.md §8(e) names two ways to block-shard a vector across the GPUs of
+one box: one process per GPU (sharding.py, torch.distributed — what
+bench.py runs under torchrun) and one process driving every device with
+NCCL communicators from ncclCommInitAll.  This module is the second:
+
+    with DeviceGroup([0, 1, 2, 3]) as dg:
+        xs = dg.scatter(x_values, "f64")          # block g on cuda:g
+        ys = dg.scatter(y_values, "f64")
+        for g in range(dg.size):                  # elementwise: no exchange,
+            ys[g].assign(ys[g] + 0.5 * xs[g])     # launches run concurrently
+        r = dg.reduce([y * x for y, x in zip(ys, xs)])   # dot over all blocks
+
+Blocks follow the same partition as ShardedVector (shard_bounds: 64-element
+aligned bases).  A reduction runs one fused kernel per device writing its
+double-double partial (SALT_PARTIAL), then salt_allreduce_sum — one NCCL
+group of 16-byte all-gathers and a rank-order fold on every device — so the
+result has the bits of the multi-process paths (salt_reduce_finish and the
+in-kernel NVLink exchange) and of the reference's single Sum over the whole
+vector up to the ≤ 1 ulp compensated-sum bound (expressions.py:401-480).
+"""
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _native
+from .expressions import Expression, lower
+from .lanes import as_dtype
+from .runtime import _dtype_code, _OnDevice, _raw_stream, _require_cuda, _workspace
+from .sharding import shard_bounds
+from .vectors import DenseVector, DeviceScalar
+
+__all__ = ["DeviceGroup"]
+
+
+class DeviceGroup:
+    """G CUDA devices of this process and their NCCL communicators."""
+
+    def __init__(self, devices=None):
+        _require_cuda()
+        if devices is None:
+            devices = list(range(torch.cuda.device_count()))
+        devices = [int(d) for d in devices]
+        if not devices or len(set(devices)) != len(devices):
+            raise ValueError(f"need distinct devices, got {devices}")
+        self.devices = devices
+        self.size = len(devices)
+        self._comms = (ctypes.c_void_p * self.size)()
+        devs = (ctypes.c_int * self.size)(*devices)
+        _native.check(_native.lib().salt_nccl_comm_init_all(self.size, ctypes.addressof(devs),
+                                                            ctypes.addressof(self._comms)))
+
+    def close(self) -> None:
+        if self._comms is not None:
+            _native.check(_native.lib().salt_nccl_comm_destroy(self.size, ctypes.addressof(self._comms)))
+            self._comms = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- data placement
+    def bounds(self, n: int):
+        """[(lo, hi)] of every device's block of a length-n vector."""
+        return [shard_bounds(n, self.size, g) for g in range(self.size)]
+
+    def scatter(self, values, dtype="f32"):
+        """One DenseVector per device holding its block of `values`."""
+        arr = np.asarray(values)
+        return [DenseVector.from_values(arr[lo:hi], dtype, device=torch.device("cuda", d))
+                for (lo, hi), d in zip(self.bounds(len(arr)), self.devices)]
+
+    def zeros(self, n: int, dtype="f32"):
+        return [DenseVector.zeros(hi - lo, dtype, device=torch.device("cuda", d))
+                for (lo, hi), d in zip(self.bounds(n), self.devices)]
+
+    @staticmethod
+    def gather(blocks) -> np.ndarray:
+        return np.concatenate([b.to_array() for b in blocks])
+
+    # ---- reductions
+    def reduce(self, summands, *, sqrt=False, lazy=False):
+        """Sum over every device's block of summands[g] (an elementwise tree
+        over device g's vectors).  lazy=True returns one DeviceScalar per
+        device (identical bits, no host synchronisation); otherwise the
+        element-typed NumPy scalar."""
+        summands = list(summands)
+        if len(summands) != self.size:
+            raise ValueError(f"need one summand per device ({self.size}), got {len(summands)}")
+        lib = _native.lib()
+        dts = {s.dtype for s in summands}
+        if len(dts) != 1 or not all(isinstance(s, Expression) for s in summands):
+            raise TypeError("summands must be expressions of one element type")
+        dt = as_dtype(dts.pop())
+        code = _dtype_code(dt)
+        parts, streams, keep = [], [], []
+        for g, (expr, d) in enumerate(zip(summands, self.devices)):
+            lw = lower(expr)
+            if lw.pscalars:
+                raise TypeError("device-resident scalars are not supported in DeviceGroup.reduce")
+            vecs = lw.vectors
+            lengths = {len(v) for v in vecs}
+            if len(lengths) != 1:
+                raise ValueError(f"summand {g}: operands of different lengths {sorted(lengths)}")
+            for v in vecs:
+                if not isinstance(v, DenseVector) or v.tensor.device != torch.device("cuda", d):
+                    raise ValueError(f"summand {g}: every operand must be a DenseVector on cuda:{d}")
+            n = lengths.pop()
+            with _OnDevice(d):
+                stream = _raw_stream(d)
+                ws = _workspace(d, stream)
+                part = torch.empty(2, dtype=torch.float64, device=torch.device("cuda", d))
+                leaves, k1 = _native.ptr_array([v.tensor.data_ptr() for v in vecs])
+                scal, k2 = _native.double_array(lw.scalars)
+                _native.check(lib.salt_reduce(code, " ".join(lw.tokens).encode(), leaves, len(vecs), scal,
+                                              len(lw.scalars), n, _native.SALT_PARTIAL, ws.data_ptr(),
+                                              ws.numel(), part.data_ptr(), None, stream))
+            parts.append(part)
+            streams.append(stream)
+            keep += [k1, k2]
+        outs, k3 = _native.ptr_array([p.data_ptr() for p in parts])
+        strs, k4 = _native.ptr_array(streams)
+        _native.check(lib.salt_allreduce_sum_flags(outs, self.size, code, ctypes.addressof(self._comms),
+                                                   strs, _native.SALT_SQRT if sqrt else 0))
+        scalars = [DeviceScalar(p.view(torch.float32)[:1] if dt.itemsize == 4 else p[:1], dt) for p in parts]
+        return scalars if lazy else scalars[0].item()
+
+    def dot(self, xs, ys, **kw):
+        return self.reduce([x * y for x, y in zip(xs, ys)], **kw)
+
+    def norm2(self, xs, **kw):
+        return self.reduce([x * x for x in xs], sqrt=True, **kw)

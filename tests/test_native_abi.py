@@ -89,6 +89,14 @@ def test_bad_arguments_fail_before_cuda():
         _native.check(lib.salt_assign(1, b"L0 +", None, leaves, 1, sc, 0, 1, None))
     # zero-length assignment is a no-op that never touches CUDA
     assert lib.salt_assign(1, b"L0", ctypes.c_void_p(0x3000), leaves, 1, sc, 0, 0, None) == 0
+    # single-process all-reduce: arguments are validated before NCCL or CUDA
+    outs, keep3 = _native.ptr_array([0x1000])
+    assert lib.salt_allreduce_sum(outs, 0, 1, None, outs) == -1
+    assert lib.salt_allreduce_sum(outs, 1, 7, outs, outs) == -1 and b"dtype" in lib.salt_last_error()
+    assert lib.salt_allreduce_sum_flags(outs, 1, 1, outs, outs, _native.SALT_PARTIAL) == -1
+    assert b"flags" in lib.salt_last_error()
+    assert lib.salt_nccl_comm_init_all(0, None, outs) == -1
+    assert lib.salt_nccl_comm_destroy(1, None) == -1
 
 
 def test_nvrtc_instantiates_arbitrary_trees_without_a_gpu():
