@@ -293,8 +293,11 @@ def run_gpu(args, world, rank, local):
         n_e2e = n
         hv = []
         for k in range(3):
+            # the same synthetic values, copied down from the device vectors
+            # (drawing 3 x 2^28 values on the host would cost each rank
+            # seconds of CPU time at N = 8)
             h = lv.DenseVector.empty(n_e2e, "f64", device="cpu")
-            h.tensor.copy_(torch.from_numpy(synth.block(2, k, rank * n, rank * n + n_e2e, np.float64)))
+            h.tensor.copy_(vecs[k].tensor[:n_e2e])
             hv.append(h)
         hd = lv.DenseVector.empty(n_e2e, "f64", device="cpu")
         ha, hb, hc = hv

@@ -29,6 +29,9 @@ CASES = {
     "etree32": (torch.float32, 1 << 30, 5),
     "axpydot": (torch.float64, 1 << 28, 3),
     "daxpy20": (torch.float64, 1 << 20, 2),
+    # BASELINE config 3 at its smaller size (one combine group of 512 CTAs)
+    "nrm2_64_mid": (torch.float64, 1 << 24, 1),
+    "dot64_mid": (torch.float64, 1 << 24, 2),
 }
 
 
@@ -55,12 +58,14 @@ def main():
         "etree32": lambda: v[4].assign(1.25 * (v[0] + v[1]) - 0.75 * (v[2] - v[3]) + 0.5 * v[0]),
         "axpydot": lambda: lv.axpy_dot(0.5, v[0], v[1], v[2], lazy=True),
         "daxpy20": lambda: lv.axpy(0.5, v[0], v[1]),
+        "nrm2_64_mid": lambda: lv.norm2(v[0], lazy=True),
+        "dot64_mid": lambda: lv.dot(v[0], v[1], lazy=True),
     }
     if a.time:
         import json
 
         per = {"t2": 4, "t1": 4, "dot64": 2, "dot32": 2, "nrm2_32": 1, "nrm2_64": 1, "cgupdate": 6,
-               "etree32": 5, "axpydot": 4, "daxpy20": 3}[a.case]
+               "etree32": 5, "axpydot": 4, "daxpy20": 3, "nrm2_64_mid": 1, "dot64_mid": 2}[a.case]
         nbytes = per * n * torch.empty(0, dtype=dt).element_size()
         for _ in range(3):
             calls[a.case]()
