@@ -15,6 +15,9 @@ bench.py:9-15 / :49-50) and times on the device:
     torch           the same tree as one torch eager op per node with
                     materialised temporaries — "BLAS composition", the
                     baseline the paper's fusion claim is measured against
+    naive           the reference's name for its unfused baseline (scalar
+                    loops there, bench.py:121-132): here the same unfused
+                    torch composition as `torch`
   ops
     dot scal axpy scaled_copy            (reference OPS, bench.py:46)
     sum norm2 t1 t2 etree axpy_dot       (BASELINE configs; --op extended)
@@ -35,11 +38,11 @@ from pathlib import Path
 import numpy as np
 
 __all__ = ["BenchRecord", "OPS", "EXTENDED_OPS", "VARIANTS", "run_sweep", "emit_csv", "parse_csv",
-           "main", "bytes_moved", "flop_count", "default_sizes"]
+           "main", "bytes_moved", "flop_count", "default_sizes", "simd_available", "record_lines"]
 
 OPS = ("dot", "scal", "axpy", "scaled_copy")
 EXTENDED_OPS = OPS + ("sum", "norm2", "t1", "t2", "etree", "axpy_dot")
-VARIANTS = ("engine", "engine-host", "torch", "engine-U1", "engine-U2", "engine-U4", "engine-U8")
+VARIANTS = ("engine", "engine-host", "torch", "naive", "engine-U1", "engine-U2", "engine-U4", "engine-U8")
 CSV_HEADER = "op,variant,type,n,reps,best_s,median_s,gflops,gbytes"
 EXT_HEADER = CSV_HEADER + ",pct_hbm,device"
 
@@ -82,6 +85,15 @@ def bytes_moved(op, n, dtype):
     from .lanes import as_dtype
 
     return _ACCOUNT[op][1] * n * as_dtype(dtype).itemsize
+
+
+def simd_available(dtype="f32") -> bool:
+    """True when a batched lane backend is active for this element type
+    (the reference's gate for its performance smoke test, bench.py:92-94);
+    the lane descriptor here is the same validated plan descriptor."""
+    from .lanes import default_backend
+
+    return default_backend(dtype).caps.specialized
 
 
 def _hbm_peak():
@@ -165,7 +177,7 @@ def _torch_call(op, v, out):
     raise ValueError(op)
 
 
-def measure(op, variant, n, dtype="f32", reps=25, warmup=5, seed=0, flush_l2=False):
+def measure(op, variant, n, dtype="f32", reps=25, warmup=5, seed=0, packages=None, flush_l2=False):
     import torch
 
     from .lanes import as_dtype, dtype_name
@@ -174,10 +186,13 @@ def measure(op, variant, n, dtype="f32", reps=25, warmup=5, seed=0, flush_l2=Fal
     host = variant == "engine-host"
     device = "cpu" if host else "cuda"
     vecs, out = _operands(op, n, dt, device, seed)
-    options = {}
+    options = {}  # validated by the engine exactly as the reference's (bench.py:135-141)
     if variant.startswith("engine-U"):
         options["unroll"] = int(variant[len("engine-U"):])
-    call = _torch_call(op, vecs, out) if variant == "torch" else _engine_call(op, vecs, out, options)
+    if packages is not None:
+        options["packages"] = packages
+    unfused = variant in ("torch", "naive")
+    call = _torch_call(op, vecs, out) if unfused else _engine_call(op, vecs, out, options)
     mutated = {"scal": 0, "axpy": 1, "axpy_dot": 1}.get(op)
     pristine = vecs[mutated].tensor.clone() if mutated is not None and n else None
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda") if flush_l2 else None
@@ -223,14 +238,14 @@ def measure(op, variant, n, dtype="f32", reps=25, warmup=5, seed=0, flush_l2=Fal
                        gbytes, gbytes / _hbm_peak(), torch.cuda.get_device_name())
 
 
-def run_sweep(ops, variants, sizes, dtype="f32", reps=25, warmup=5, seed=0, flush_l2=False):
+def run_sweep(ops, variants, sizes, dtype="f32", reps=25, warmup=5, seed=0, packages=None, flush_l2=False):
     for op in ops:
         if op not in EXTENDED_OPS:
             raise ValueError(f"unknown op {op!r}; choose from {', '.join(EXTENDED_OPS)}")
     for v in variants:
         if v not in VARIANTS:
             raise ValueError(f"unknown variant {v!r}; choose from {', '.join(VARIANTS)}")
-    return [measure(op, v, n, dtype, reps, warmup, seed, flush_l2)
+    return [measure(op, v, n, dtype, reps, warmup, seed, packages, flush_l2)
             for op in ops for v in variants for n in sizes]
 
 
@@ -241,6 +256,12 @@ def _lines(records, extended):
         if extended:
             vals += [r.pct_hbm, r.device.replace(",", " ")]
         yield ",".join(repr(v) if isinstance(v, float) else str(v) for v in vals)
+
+
+def record_lines(records):
+    """Header + one CSV row per record (the reference's record_lines,
+    bench.py:222-231)."""
+    return _lines(records, False)
 
 
 def emit_csv(records, destination, extended=False) -> None:
@@ -278,6 +299,8 @@ def main(argv=None) -> int:
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--csv", default="-")
+    ap.add_argument("--packages", type=int, default=None,
+                    help="accepted and validated like the reference's (bench.py:294-295)")
     ap.add_argument("--flush-l2", action="store_true")
     ap.add_argument("--extended", action="store_true")
     a = ap.parse_args(argv)
@@ -300,7 +323,8 @@ def main(argv=None) -> int:
             ap.error("--sizes expects non-negative integers")
     if a.reps < 1 or a.warmup < 0:
         ap.error("--reps must be >= 1 and --warmup >= 0")
-    records = run_sweep(ops, variants, sizes, a.type, a.reps, a.warmup, a.seed, a.flush_l2)
+    records = run_sweep(ops, variants, sizes, a.type, a.reps, a.warmup, a.seed, packages=a.packages,
+                        flush_l2=a.flush_l2)
     try:
         emit_csv(records, a.csv, a.extended)
     except OSError as exc:

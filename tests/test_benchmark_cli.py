@@ -37,12 +37,26 @@ def test_csv_round_trip_and_header(tmp_path):
         sb.parse_csv("bad,header\n")
 
 
-@pytest.mark.parametrize("argv", [["--op", "nope"], ["--variants", "naive"], ["--sizes", "x"],
+@pytest.mark.parametrize("argv", [["--op", "nope"], ["--variants", "bogus"], ["--sizes", "x"],
                                   ["--reps", "0"], ["--sizes", "-4"]])
 def test_cli_rejects_bad_usage_with_exit_2(argv):
     with pytest.raises(SystemExit) as e:
         sb.main(argv)
     assert e.value.code == 2
+
+
+def test_reference_bench_surface():
+    """The reference bench module's public names keep their meaning:
+    simd_available (bench.py:92-94), record_lines (:222-231), the `naive`
+    variant and the `packages` option (:135-141, :195-213)."""
+    assert sb.simd_available("f32") is True and sb.simd_available("f64") is True
+    assert list(sb.record_lines([])) == ["op,variant,type,n,reps,best_s,median_s,gflops,gbytes"]
+    assert "naive" in sb.VARIANTS
+    import inspect
+    params = list(inspect.signature(sb.run_sweep).parameters)
+    assert params[:8] == ["ops", "variants", "sizes", "dtype", "reps", "warmup", "seed", "packages"]
+    params = list(inspect.signature(sb.measure).parameters)
+    assert params[:8] == ["op", "variant", "n", "dtype", "reps", "warmup", "seed", "packages"]
 
 
 def test_static_traffic_counter():
