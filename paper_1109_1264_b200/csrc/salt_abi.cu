@@ -626,6 +626,19 @@ int prepare(Kernel* k, int dev) {
   return 0;
 }
 
+// Fused kernels are launched with programmatic stream serialization (PDL):
+// the grid may be scheduled while the previous kernel on the stream drains;
+// the kernel's first instruction (griddepcontrol.wait) holds every CTA until
+// that kernel has completed and its writes are visible.  SALT_PDL=0 turns it
+// off (tuning / A-B tests only).
+bool use_pdl() {
+  static const bool env = [] {
+    const char* e = getenv("SALT_PDL");
+    return !(e && atoi(e) == 0);
+  }();
+  return env;
+}
+
 // One cluster of `grid` CTAs (2..16; > 8 needs the non-portable opt-in).
 // Returns false (without an error) if this kernel/device refuses clusters
 // of that size, so the caller launches the ticket-combine grid instead.
@@ -646,16 +659,18 @@ template <class T> bool launch_cluster(Kernel* k, int dev, int grid, salt::Args<
       ok.store(1);
     }
     cudaLaunchConfig_t cfg = {};
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = (unsigned)grid;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kBlock);
     cfg.stream = st;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = use_pdl() ? 2 : 1;
     cudaError_t e = cudaLaunchKernelExC(&cfg, k->aot, params);
     if (e != cudaSuccess) {
       cudaGetLastError();
@@ -674,18 +689,20 @@ template <class T> bool launch_cluster(Kernel* k, int dev, int grid, salt::Args<
       ok.store(1);
     }
     CUlaunchConfig cfg = {};
-    CUlaunchAttribute attr[1];
+    CUlaunchAttribute attr[2];
     attr[0].id = CU_LAUNCH_ATTRIBUTE_CLUSTER_DIMENSION;
     attr[0].value.clusterDim.x = (unsigned)grid;
     attr[0].value.clusterDim.y = 1;
     attr[0].value.clusterDim.z = 1;
+    attr[1].id = CU_LAUNCH_ATTRIBUTE_PROGRAMMATIC_STREAM_SERIALIZATION;
+    attr[1].value.programmaticStreamSerializationAllowed = 1;
     cfg.gridDimX = (unsigned)grid;
     cfg.gridDimY = cfg.gridDimZ = 1;
     cfg.blockDimX = kBlock;
     cfg.blockDimY = cfg.blockDimZ = 1;
     cfg.hStream = (CUstream)st;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = use_pdl() ? 2 : 1;
     if (d.LaunchKernelEx(&cfg, k->jit_fn[dev], params, nullptr) != CUDA_SUCCESS) {
       ok.store(-1);
       return false;
@@ -697,9 +714,37 @@ template <class T> bool launch_cluster(Kernel* k, int dev, int grid, salt::Args<
 
 template <class T> int launch(Kernel* k, int dev, int grid, salt::Args<T>& args, cudaStream_t st) {
   void* params[] = {&args};
+  const bool pdl = use_pdl();
   if (k->aot) {
-    cudaError_t e = cudaLaunchKernel(k->aot, dim3(grid), dim3(kBlock), params, 0, st);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaLaunchKernel");
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kBlock);
+    cfg.stream = st;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    cudaError_t e = cudaLaunchKernelExC(&cfg, k->aot, params);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaLaunchKernelExC");
+  } else if (pdl && driver().LaunchKernelEx) {
+    CUlaunchConfig cfg = {};
+    CUlaunchAttribute attr[1];
+    attr[0].id = CU_LAUNCH_ATTRIBUTE_PROGRAMMATIC_STREAM_SERIALIZATION;
+    attr[0].value.programmaticStreamSerializationAllowed = 1;
+    cfg.gridDimX = (unsigned)grid;
+    cfg.gridDimY = cfg.gridDimZ = 1;
+    cfg.blockDimX = kBlock;
+    cfg.blockDimY = cfg.blockDimZ = 1;
+    cfg.hStream = (CUstream)st;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CUresult r = driver().LaunchKernelEx(&cfg, k->jit_fn[dev], params, nullptr);
+    if (r != CUDA_SUCCESS) {
+      const char* s = "?";
+      driver().GetErrorString(r, &s);
+      return fail(SALT_ECUDA, std::string("cuLaunchKernelEx: ") + s);
+    }
   } else {
     CUresult r = driver().LaunchKernel(k->jit_fn[dev], grid, 1, 1, kBlock, 1, 1, 0,
                                        (CUstream)st, params, nullptr);

@@ -487,6 +487,15 @@ __global__ void SALT_BOUNDS(BLOCK) fused_kernel(Args<T> a) {
   constexpr bool REDUCE = MODE != MODE_ASSIGN;
   typedef Env<T, NL, NS, NP, Roots<EA>::N, V> E1;
   typedef Env<T, NL, NS, NP, Roots<EA>::N, 1> ES;
+  // Programmatic dependent launch: the host launches fused kernels with
+  // programmatic stream serialization, so this grid may be scheduled while
+  // the previous kernel on the stream is still finishing.  Nothing in global
+  // memory is touched before this wait returns (it returns once every
+  // prerequisite grid has completed and its writes are visible; without the
+  // launch attribute it is a no-op).  B200, 400 back-to-back axpy launches
+  // (tools/pdl_probe.cu): 2^20 f64 4.74 -> 2.87 us per launch eager,
+  // 2.97 -> 2.71 us in a CUDA graph.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   T pv[NP > 0 ? NP : 1];  // device scalars, loaded once per thread
 #pragma unroll
   for (int q = 0; q < NP; ++q) pv[q] = __ldg(a.ps[q]);
