@@ -6,7 +6,6 @@ signatures as libsalt.so.  The library is built by `make -C oracle`
 """
 
 import ctypes
-import os
 from pathlib import Path
 
 import numpy as np

@@ -10,7 +10,7 @@ import paper_1109_1264_b200 as lv
 from conftest import NP, same_bits
 from oracle import restate
 from paper_1109_1264_b200 import _native
-from paper_1109_1264_b200.expressions import AssignNode, FusedNode, SumNode, as_node
+from paper_1109_1264_b200.expressions import as_node
 
 pytestmark = pytest.mark.gpu
 TOL = {"f32": 1e-5, "f64": 1e-12}
