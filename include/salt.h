@@ -255,6 +255,11 @@ int salt_prepare(int dtype, const char* sig, const char* reduce_sig, int kind);
 /* Force (1) or forbid (0) the JIT for signatures that also have an AOT
  * kernel; default 0.  Used by tests to prove AOT == JIT bit for bit. */
 void salt_set_force_jit(int on);
+/* Test hook: evaluate every tree with the postfix interpreter kernel (the
+ * fallback used when a tree is neither compiled in nor JIT-compilable, e.g.
+ * without NVRTC).  salt_interp_launch_count() counts its launches. */
+void salt_set_force_interp(int on);
+uint64_t salt_interp_launch_count(void);
 
 /* Number of kernels this library has launched since load (all devices). */
 uint64_t salt_launch_count(void);

@@ -58,6 +58,8 @@ HEADER_SYMBOLS = (
     "salt_signature_kind",
     "salt_prepare",
     "salt_set_force_jit",
+    "salt_set_force_interp",
+    "salt_interp_launch_count",
     "salt_launch_count",
     "salt_last_error",
     "salt_abi_version",
@@ -126,6 +128,8 @@ _SIGNATURES = {
     "salt_signature_kind": (_c_int, [_c_int, _c_str, _c_str, _c_int]),
     "salt_prepare": (_c_int, [_c_int, _c_str, _c_str, _c_int]),
     "salt_set_force_jit": (None, [_c_int]),
+    "salt_set_force_interp": (None, [_c_int]),
+    "salt_interp_launch_count": (ctypes.c_uint64, []),
     "salt_launch_count": (ctypes.c_uint64, []),
     "salt_last_error": (_c_str, []),
     "salt_abi_version": (_c_int, []),

@@ -34,6 +34,7 @@
 
 #include "../../include/salt.h"
 #include "salt_expr.cuh"
+#include "salt_interp.cuh"
 
 namespace {
 
@@ -136,6 +137,8 @@ constexpr int kMaxDevices = 64;
 thread_local std::string g_err;
 std::atomic<uint64_t> g_launches{0};
 std::atomic<int> g_force_jit{0};
+std::atomic<int> g_force_interp{0};
+std::atomic<uint64_t> g_interp_launches{0};
 
 int fail(int code, const std::string& msg) {
   g_err = msg;
@@ -331,6 +334,11 @@ Nvrtc& nvrtc() {
   std::call_once(once, [] {
     // Prefer the toolkit's NVRTC (12.9, PTX ISA 8.8: 256-bit ld/st) by full
     // path: a bare soname would return torch's already-loaded 12.8 copy.
+    const char* off = getenv("SALT_NO_JIT");  // test hook: behave as if NVRTC were absent
+    if (off && atoi(off) != 0) {
+      n.why = "JIT disabled (SALT_NO_JIT)";
+      return;
+    }
     const char* env = getenv("SALT_NVRTC_LIB");
     const char* cands[] = {env, "/usr/local/cuda/lib64/libnvrtc.so.12", "libnvrtc.so.12",
                            "libnvrtc.so"};
@@ -378,6 +386,8 @@ struct Kernel {
   int unroll = 1;
   // cluster launches (reductions at small n): 0 unknown, 1 ok, -1 refused
   std::atomic<int> cluster_ok[kMaxDevices] = {};
+  bool interp = false;                       // salt::interp_kernel (program in the parameters)
+  std::atomic<int> smem_limit[kMaxDevices] = {};  // 1: dynamic shared memory cap raised on the device
 };
 
 std::string key_of(int dtype, int mode, int vec, const std::string& ta, const std::string& tr) {
@@ -600,6 +610,21 @@ Kernel* get_kernel(int dtype, int mode, int vec, int nl, const std::string& ta,
 
 std::mutex g_dev_mu;
 
+// The interpreter kernels (one per element type and vector width).
+template <class T> Kernel* interp_kernel_for(int vec) {
+  static Kernel kv, k1;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    kv.aot = (const void*)&salt::interp_kernel<T, vec_of<T>(), kBlock>;
+    kv.vec = vec_of<T>();
+    k1.aot = (const void*)&salt::interp_kernel<T, 1, kBlock>;
+    k1.vec = 1;
+    kv.unroll = k1.unroll = 1;
+    kv.interp = k1.interp = true;
+  });
+  return vec == 1 ? &k1 : &kv;
+}
+
 int current_device(int& dev) {
   SALT_CUDA(cudaGetDevice(&dev));
   if (dev < 0 || dev >= kMaxDevices) return fail(SALT_EINVAL, "device ordinal out of range");
@@ -712,8 +737,10 @@ template <class T> bool launch_cluster(Kernel* k, int dev, int grid, salt::Args<
   return true;
 }
 
-template <class T> int launch(Kernel* k, int dev, int grid, salt::Args<T>& args, cudaStream_t st) {
-  void* params[] = {&args};
+// One launch of `k` with its single by-value parameter at `argp` (Args<T>,
+// or InterpArgs<T> for the interpreter) and `smem` dynamic shared bytes.
+int launch_raw(Kernel* k, int dev, int grid, void* argp, size_t smem, cudaStream_t st) {
+  void* params[] = {argp};
   const bool pdl = use_pdl();
   if (k->aot) {
     cudaLaunchConfig_t cfg = {};
@@ -722,6 +749,7 @@ template <class T> int launch(Kernel* k, int dev, int grid, salt::Args<T>& args,
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kBlock);
+    cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cfg.attrs = attr;
     cfg.numAttrs = pdl ? 1 : 0;
@@ -758,6 +786,10 @@ template <class T> int launch(Kernel* k, int dev, int grid, salt::Args<T>& args,
   return 0;
 }
 
+template <class T> int launch(Kernel* k, int dev, int grid, salt::Args<T>& args, cudaStream_t st) {
+  return launch_raw(k, dev, grid, &args, 0, st);
+}
+
 // Common 32-byte misalignment of all operands -> (vec, head, nvec).
 template <class T>
 void geometry(void* const* dsts, int ndst, const void* const* leaves, int nl, i64 n, int& vec,
@@ -792,7 +824,74 @@ struct Plan {
   int mode = 0;
   int nl = 0, ns = 0, np = 0;
   Kernel* cached[2][2] = {};  // [force_jit][vec == 1]: table / JIT lookups done once
+  salt::Prog prog;            // the same trees as an interpreter program
+  bool prog_ok = false;
+  std::string prog_err;
 };
+
+// Encode the plan's trees for interp_kernel: assignment roots in order, each
+// followed by OP_STORE r, then the reduce tree followed by OP_ACC.  Stack
+// slots = the deepest push (the top of the stack stays in registers).
+std::string encode_prog(const Plan& p, salt::Prog& g) {
+  memset(&g, 0, sizeof(g));
+  int sp = 0;
+  auto emit = [&](int op, int arg) -> bool {
+    if (g.len >= salt::MAX_PROG) return false;
+    g.op[g.len] = (unsigned char)op;
+    g.arg[g.len] = (unsigned char)arg;
+    ++g.len;
+    if (op <= salt::OP_D) g.slots = std::max(g.slots, ++sp);
+    else if (op <= salt::OP_MUL) --sp;
+    else sp = 0;
+    return true;
+  };
+  auto tree = [&](const std::string& canon) -> bool {
+    std::istringstream in(canon);
+    std::string t;
+    while (in >> t) {
+      if (t == ";") continue;
+      bool ok;
+      if (t == "+") ok = emit(salt::OP_ADD, 0);
+      else if (t == "-") ok = emit(salt::OP_SUB, 0);
+      else if (t == "*") ok = emit(salt::OP_MUL, 0);
+      else if (t == "D") ok = emit(salt::OP_D, 0);
+      else {
+        const int k = atoi(t.c_str() + 1);
+        const int op = t[0] == 'L' ? salt::OP_LEAF : t[0] == 'S' ? salt::OP_SCALAR
+                       : t[0] == 'P' ? salt::OP_PSCALAR : salt::OP_D;
+        ok = emit(op, k);
+      }
+      if (!ok) return false;
+    }
+    return true;
+  };
+  if (p.mode != salt::MODE_REDUCE) {
+    size_t pos = 0;
+    int r = 0;
+    const std::string& all = p.sa.canon;
+    while (true) {
+      size_t semi = all.find(';', pos);
+      if (!tree(all.substr(pos, semi == std::string::npos ? std::string::npos : semi - pos)) ||
+          !emit(salt::OP_STORE, r))
+        return "tree too long for the interpreter (" + std::to_string((int)salt::MAX_PROG) + " tokens)";
+      ++r;
+      if (semi == std::string::npos) break;
+      pos = semi + 1;
+    }
+    g.nroots = r;
+  }
+  if (p.mode != salt::MODE_ASSIGN) {
+    if (!tree(p.sr.canon) || !emit(salt::OP_ACC, 0))
+      return "tree too long for the interpreter (" + std::to_string((int)salt::MAX_PROG) + " tokens)";
+    g.reduce = 1;
+  }
+  g.nl = p.nl;
+  // 8 KiB per slot (32-byte vectors x 256 threads); stay below 224 KiB
+  if (salt::interp_smem_bytes(g, 4, kBlock, 8) > 224 * 1024)
+    return "tree needs " + std::to_string(g.nl + g.slots + g.nroots) +
+           " interpreter slots (leaves + stack depth + roots > 28)";
+  return "";
+}
 
 // Parsed signatures are cached per thread (keyed by the raw strings), so a
 // repeated call costs one hash lookup instead of a parse + type rebuild.
@@ -826,6 +925,8 @@ int make_plan(int dtype, const char* asig, const char* rsig, int mode, int nleav
     np->nl = std::max(np->sa.nl, np->sr.nl);
     np->ns = std::max(np->sa.ns, np->sr.ns);
     np->np = std::max(np->sa.np, np->sr.np);
+    np->prog_err = encode_prog(*np, np->prog);
+    np->prog_ok = np->prog_err.empty();
     if (cache.size() > 4096) cache.clear();
     p = np.get();
     cache.emplace(std::move(key), std::move(np));
@@ -880,10 +981,20 @@ int run_fused(Plan& p, void* const* dsts, int ndst, const void* const* leaves, i
   a.flags = flags;
   int vec;
   geometry<T>(dsts, nroots, leaves, p.nl, n, vec, a.head, a.nvec);
-  Kernel*& slot = p.cached[g_force_jit.load(std::memory_order_relaxed)][vec == 1 ? 1 : 0];
-  if (!slot) slot = get_kernel(dtype_of<T>(), p.mode, vec, p.nl, p.sa.type, p.sr.type);
-  Kernel* k = slot;
-  if (!k) return SALT_EJIT;
+  Kernel* k = nullptr;
+  const bool force_interp = g_force_interp.load(std::memory_order_relaxed) != 0;
+  if (!force_interp) {
+    Kernel*& slot = p.cached[g_force_jit.load(std::memory_order_relaxed)][vec == 1 ? 1 : 0];
+    if (!slot) slot = get_kernel(dtype_of<T>(), p.mode, vec, p.nl, p.sa.type, p.sr.type);
+    k = slot;
+  }
+  if (!k) {
+    // Not compiled in and no JIT build (NVRTC missing or failed), or forced:
+    // the postfix interpreter evaluates the same trees (salt_interp.cuh).
+    if (!p.prog_ok)
+      return fail(SALT_EJIT, (force_interp ? std::string() : g_err + "; ") + "interpreter: " + p.prog_err);
+    k = interp_kernel_for<T>(vec);
+  }
   int dev;
   int rc = current_device(dev);
   if (rc) return rc;
@@ -900,7 +1011,7 @@ int run_fused(Plan& p, void* const* dsts, int ndst, const void* const* leaves, i
   const i64 ntiles = (a.nvec + per_tile - 1) / per_tile;
   i64 K = assign_tiles_per_cta(), cap = i64(0x7fffffff);
   bool cluster = false, one_group = false;
-  if (reduce && ntiles > 2 && ntiles <= (i64)max_cluster() * cluster_tiles()) {
+  if (reduce && !k->interp && ntiles > 2 && ntiles <= (i64)max_cluster() * cluster_tiles()) {
     // Small n (3 .. 16 x 2 tiles; up to 2 tiles one CTA is quicker): one cluster
     // of <= 16 CTAs, partials combined in distributed shared memory — no
     // workspace round trip, no ticket atomics.  B200, back-to-back launches
@@ -974,7 +1085,19 @@ int run_fused(Plan& p, void* const* dsts, int ndst, const void* const* leaves, i
     // identical bits, since both fold the partials in CTA order
     if (!launched) a.cluster = 0;
   }
-  if (!launched) {
+  if (!launched && k->interp) {
+    salt::InterpArgs<T> ia;
+    ia.a = a;
+    ia.pg = p.prog;
+    const int smem = salt::interp_smem_bytes(p.prog, vec, kBlock, (int)sizeof(T));
+    if (!k->smem_limit[dev].load(std::memory_order_acquire)) {  // once per device: the cap
+      SALT_CUDA(cudaFuncSetAttribute(k->aot, cudaFuncAttributeMaxDynamicSharedMemorySize, 224 * 1024));
+      k->smem_limit[dev].store(1, std::memory_order_release);
+    }
+    rc = launch_raw(k, dev, grid, &ia, (size_t)smem, st);
+    if (rc) return rc;
+    g_interp_launches.fetch_add(1, std::memory_order_relaxed);
+  } else if (!launched) {
     rc = launch<T>(k, dev, grid, a, st);
     if (rc) return rc;
   }
@@ -1247,6 +1370,10 @@ const char* salt_last_error(void) { return g_err.c_str(); }
 uint64_t salt_launch_count(void) { return g_launches.load(); }
 
 void salt_set_force_jit(int on) { g_force_jit.store(on ? 1 : 0); }
+
+void salt_set_force_interp(int on) { g_force_interp.store(on ? 1 : 0); }
+
+uint64_t salt_interp_launch_count(void) { return g_interp_launches.load(); }
 
 size_t salt_reduce_workspace_bytes(void) { return (size_t)salt::WsLayout::bytes; }
 

@@ -458,6 +458,119 @@ __device__ __forceinline__ void AssignRoots<EA, R, N>::one(E& e, T* const* dst, 
   AssignRoots<EA, R + 1, N>::template one<T>(e, dst, i);
 }
 
+// The reduction epilogue shared by the fused kernel and the interpreter:
+// `mine` is this thread's partial; the CTA reduces it and the grid combines
+// the CTA partials (see below).  Every thread of the CTA must call it.
+template <class T, int BLOCK>
+__device__ __forceinline__ void reduce_epilogue(DD mine, const Args<T>& a) {
+  // Two-level deterministic combine.  Every CTA publishes its partial; the
+  // last CTA to arrive in its group of a.group consecutive CTAs (GROUP, or
+  // the whole grid when it is a single group) folds the
+  // group's partials (thread t takes CTA t of the group, then a fixed
+  // shuffle/shared-memory tree); the last group to finish folds the group
+  // partials in group order.  Which CTA does the folding never changes
+  // the order, so the result depends only on n — not on scheduling, SM
+  // count or occupancy.
+  static_assert(MAX_ONE_GROUP % BLOCK == 0 && GROUP <= MAX_ONE_GROUP, "group fold layout");
+  __shared__ DD smem[BLOCK / 32];
+  __shared__ int stage;  // 0 done, 1 group finisher, 2 group + final finisher
+  DD part = block_reduce_dd<BLOCK>(mine, smem);
+  if (gridDim.x == 1) {  // small n: no partials, no tickets, no fences
+    if (threadIdx.x == 0) {
+      if (a.xchg.world > 0) part = exchange_dd(part, a.xchg);
+      finish_store<T>(part, a.flags, a.out);
+    }
+    return;
+  }
+  if (a.cluster) {
+    // Small n: the whole grid is one cluster (<= 16 CTAs).  Partials meet
+    // in distributed shared memory behind one cluster barrier instead of
+    // global partials + ticket atomics.  CTA 0 folds them exactly like the
+    // single-group ticket path below (thread t takes CTA t, then the same
+    // block tree), so both paths give the same bits.
+    __shared__ DD cpart;
+    if (threadIdx.x == 0) cpart = part;
+    cluster_barrier();
+    DD v; v.hi = 0.0; v.lo = 0.0;
+    if (blockIdx.x == 0 && threadIdx.x < gridDim.x) {
+      DD p;
+      p.hi = ld_dsmem(&cpart.hi, threadIdx.x);
+      p.lo = ld_dsmem(&cpart.lo, threadIdx.x);
+      v = dd_add(v, p);
+    }
+    cluster_barrier();  // every CTA's shared memory stays alive until read
+    if (blockIdx.x != 0) return;
+    DD q = block_reduce_dd<BLOCK>(v, smem);
+    if (threadIdx.x == 0) {
+      if (a.xchg.world > 0) q = exchange_dd(q, a.xchg);
+      finish_store<T>(q, a.flags, a.out);
+    }
+    return;
+  }
+  const unsigned int G = (unsigned int)a.group;
+  const unsigned int g = blockIdx.x / G;
+  const unsigned int ngroups = (gridDim.x + G - 1) / G;
+  const unsigned int gsize = min(G, gridDim.x - g * G);
+  if (threadIdx.x == 0) {
+    a.partials[blockIdx.x] = part;
+    stage = ticket_add(&a.group_tickets[g]) == gsize - 1 ? 1 : 0;
+  }
+  __syncthreads();
+  if (stage == 0) return;
+  // Thread t folds CTAs t, t + BLOCK, ... of the group in that order (a
+  // group has at most MAX_ONE_GROUP = 4 * BLOCK CTAs); the loads (L2:
+  // other CTAs wrote these during this launch) are issued before the
+  // first add so they overlap.
+  DD v; v.hi = 0.0; v.lo = 0.0;
+  {
+    DD p[MAX_ONE_GROUP / BLOCK];
+#pragma unroll
+    for (int i = 0; i < MAX_ONE_GROUP / BLOCK; ++i) {
+      const unsigned int b = threadIdx.x + i * BLOCK;
+      if (b < gsize) {
+        p[i].hi = __ldcg(&a.partials[g * G + b].hi);
+        p[i].lo = __ldcg(&a.partials[g * G + b].lo);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < MAX_ONE_GROUP / BLOCK; ++i)
+      if (threadIdx.x + i * BLOCK < gsize) v = dd_add(v, p[i]);
+  }
+  __syncthreads();
+  DD q = block_reduce_dd<BLOCK>(v, smem);
+  if (ngroups == 1) {  // one group: its finisher holds the total
+    if (threadIdx.x == 0) {
+      a.group_tickets[g] = 0u;
+      if (a.xchg.world > 0) q = exchange_dd(q, a.xchg);
+      finish_store<T>(q, a.flags, a.out);
+    }
+    return;
+  }
+  if (threadIdx.x == 0) {
+    a.group_partials[g] = q;
+    a.group_tickets[g] = 0u;  // every CTA of the group has arrived
+    stage = ticket_add(a.ticket) == ngroups - 1 ? 2 : 1;
+  }
+  __syncthreads();
+  if (stage != 2) return;
+  DD w; w.hi = 0.0; w.lo = 0.0;
+  for (unsigned int b = threadIdx.x; b < ngroups; b += BLOCK) {
+    DD p;
+    p.hi = __ldcg(&a.group_partials[b].hi);
+    p.lo = __ldcg(&a.group_partials[b].lo);
+    w = dd_add(w, p);
+  }
+  __syncthreads();
+  DD tot = block_reduce_dd<BLOCK>(w, smem);
+  if (threadIdx.x == 0) {
+    *a.ticket = 0u;  // ready for the next launch on this workspace
+    // Sharded reduction: trade this rank's total with the other ranks over
+    // NVLink peer memory inside this same kernel — no separate collective.
+    if (a.xchg.world > 0) tot = exchange_dd(tot, a.xchg);
+    finish_store<T>(tot, a.flags, a.out);
+  }
+}
+
 // ---------------------------------------------------------------- the kernel
 // MODE_ASSIGN:        dst[i] = EA(i)
 // MODE_REDUCE:        out    = sum_i ER(i)
@@ -556,114 +669,7 @@ __global__ void SALT_BOUNDS(BLOCK) fused_kernel(Args<T> a) {
     }
   }
 
-  if (REDUCE) {
-    // Two-level deterministic combine.  Every CTA publishes its partial; the
-    // last CTA to arrive in its group of a.group consecutive CTAs (GROUP, or
-    // the whole grid when it is a single group) folds the
-    // group's partials (thread t takes CTA t of the group, then a fixed
-    // shuffle/shared-memory tree); the last group to finish folds the group
-    // partials in group order.  Which CTA does the folding never changes
-    // the order, so the result depends only on n — not on scheduling, SM
-    // count or occupancy.
-    static_assert(MAX_ONE_GROUP % BLOCK == 0 && GROUP <= MAX_ONE_GROUP, "group fold layout");
-    __shared__ DD smem[BLOCK / 32];
-    __shared__ int stage;  // 0 done, 1 group finisher, 2 group + final finisher
-    DD part = block_reduce_dd<BLOCK>(acc.get(), smem);
-    if (gridDim.x == 1) {  // small n: no partials, no tickets, no fences
-      if (threadIdx.x == 0) {
-        if (a.xchg.world > 0) part = exchange_dd(part, a.xchg);
-        finish_store<T>(part, a.flags, a.out);
-      }
-      return;
-    }
-    if (a.cluster) {
-      // Small n: the whole grid is one cluster (<= 16 CTAs).  Partials meet
-      // in distributed shared memory behind one cluster barrier instead of
-      // global partials + ticket atomics.  CTA 0 folds them exactly like the
-      // single-group ticket path below (thread t takes CTA t, then the same
-      // block tree), so both paths give the same bits.
-      __shared__ DD cpart;
-      if (threadIdx.x == 0) cpart = part;
-      cluster_barrier();
-      DD v; v.hi = 0.0; v.lo = 0.0;
-      if (blockIdx.x == 0 && threadIdx.x < gridDim.x) {
-        DD p;
-        p.hi = ld_dsmem(&cpart.hi, threadIdx.x);
-        p.lo = ld_dsmem(&cpart.lo, threadIdx.x);
-        v = dd_add(v, p);
-      }
-      cluster_barrier();  // every CTA's shared memory stays alive until read
-      if (blockIdx.x != 0) return;
-      DD q = block_reduce_dd<BLOCK>(v, smem);
-      if (threadIdx.x == 0) {
-        if (a.xchg.world > 0) q = exchange_dd(q, a.xchg);
-        finish_store<T>(q, a.flags, a.out);
-      }
-      return;
-    }
-    const unsigned int G = (unsigned int)a.group;
-    const unsigned int g = blockIdx.x / G;
-    const unsigned int ngroups = (gridDim.x + G - 1) / G;
-    const unsigned int gsize = min(G, gridDim.x - g * G);
-    if (threadIdx.x == 0) {
-      a.partials[blockIdx.x] = part;
-      stage = ticket_add(&a.group_tickets[g]) == gsize - 1 ? 1 : 0;
-    }
-    __syncthreads();
-    if (stage == 0) return;
-    // Thread t folds CTAs t, t + BLOCK, ... of the group in that order (a
-    // group has at most MAX_ONE_GROUP = 4 * BLOCK CTAs); the loads (L2:
-    // other CTAs wrote these during this launch) are issued before the
-    // first add so they overlap.
-    DD v; v.hi = 0.0; v.lo = 0.0;
-    {
-      DD p[MAX_ONE_GROUP / BLOCK];
-#pragma unroll
-      for (int i = 0; i < MAX_ONE_GROUP / BLOCK; ++i) {
-        const unsigned int b = threadIdx.x + i * BLOCK;
-        if (b < gsize) {
-          p[i].hi = __ldcg(&a.partials[g * G + b].hi);
-          p[i].lo = __ldcg(&a.partials[g * G + b].lo);
-        }
-      }
-#pragma unroll
-      for (int i = 0; i < MAX_ONE_GROUP / BLOCK; ++i)
-        if (threadIdx.x + i * BLOCK < gsize) v = dd_add(v, p[i]);
-    }
-    __syncthreads();
-    DD q = block_reduce_dd<BLOCK>(v, smem);
-    if (ngroups == 1) {  // one group: its finisher holds the total
-      if (threadIdx.x == 0) {
-        a.group_tickets[g] = 0u;
-        if (a.xchg.world > 0) q = exchange_dd(q, a.xchg);
-        finish_store<T>(q, a.flags, a.out);
-      }
-      return;
-    }
-    if (threadIdx.x == 0) {
-      a.group_partials[g] = q;
-      a.group_tickets[g] = 0u;  // every CTA of the group has arrived
-      stage = ticket_add(a.ticket) == ngroups - 1 ? 2 : 1;
-    }
-    __syncthreads();
-    if (stage != 2) return;
-    DD w; w.hi = 0.0; w.lo = 0.0;
-    for (unsigned int b = threadIdx.x; b < ngroups; b += BLOCK) {
-      DD p;
-      p.hi = __ldcg(&a.group_partials[b].hi);
-      p.lo = __ldcg(&a.group_partials[b].lo);
-      w = dd_add(w, p);
-    }
-    __syncthreads();
-    DD tot = block_reduce_dd<BLOCK>(w, smem);
-    if (threadIdx.x == 0) {
-      *a.ticket = 0u;  // ready for the next launch on this workspace
-      // Sharded reduction: trade this rank's total with the other ranks over
-      // NVLink peer memory inside this same kernel — no separate collective.
-      if (a.xchg.world > 0) tot = exchange_dd(tot, a.xchg);
-      finish_store<T>(tot, a.flags, a.out);
-    }
-  }
+  if (REDUCE) reduce_epilogue<T, BLOCK>(acc.get(), a);
 }
 
 // Combine `count` partials (all-gathered per-device DD values, rank order).

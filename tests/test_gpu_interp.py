@@ -1,0 +1,143 @@
+"""The postfix interpreter kernel (csrc/salt_interp.cuh): the fallback for
+trees that are neither compiled in nor JIT-compilable (no NVRTC), forced
+here with salt_set_force_interp.  Elementwise results must be the
+reference's bits, exactly as from the template kernels; reductions within
+the BASELINE tolerance of the exact sum."""
+
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import paper_1109_1264_b200 as lv
+from conftest import NP, same_bits
+from oracle import restate
+from paper_1109_1264_b200 import _native
+from paper_1109_1264_b200.engine import execute_reduce
+from paper_1109_1264_b200.expressions import SumNode, as_node, lower
+from test_gpu_random_trees import random_tree
+
+pytestmark = pytest.mark.gpu
+ROOT = Path(__file__).resolve().parents[1]
+TOL = {"f32": 1e-5, "f64": 1e-12}
+
+
+@pytest.fixture
+def interp():
+    lib = _native.lib()
+    lib.salt_set_force_interp(1)
+    yield lib
+    lib.salt_set_force_interp(0)
+
+
+@pytest.mark.parametrize("dt", ["f32", "f64"])
+def test_interpreter_random_trees(interp, dt):
+    rng = np.random.default_rng(4242 if dt == "f32" else 4243)
+    before = interp.salt_interp_launch_count()
+    checked = 0
+    for case in range(24):
+        n = int(rng.choice([1, 7, 33, 1000, 4099, 65_537, 1 << 20]))
+        nv = int(rng.integers(1, 9))
+        host = [rng.uniform(-2, 2, n).astype(NP[dt]) for _ in range(nv)]
+        vecs = [lv.DenseVector.from_values(h, dt, device="cuda") for h in host]
+        expr = as_node(random_tree(rng, vecs, int(rng.integers(1, 7))))
+        lw = lower(expr)
+        idx = [next(i for i, v in enumerate(vecs) if v is u) for u in lw.vectors]
+        want = restate.eval_sig(" ".join(lw.tokens), [host[i] for i in idx], lw.scalars, dt)
+        out = lv.DenseVector.zeros(n, dt, device="cuda")
+        out.assign(expr)
+        assert same_bits(out.to_array(), want), (case, " ".join(lw.tokens))
+        r = execute_reduce(SumNode(expr))
+        exact = restate.exact_sum(want)
+        if exact != 0 and np.isfinite(exact):
+            scale = restate.exact_sum(np.abs(want))
+            assert abs(float(r) - exact) <= TOL[dt] * max(abs(exact), 1e-3 * scale), (case, float(r), exact)
+        checked += 1
+    assert checked == 24
+    assert interp.salt_interp_launch_count() - before >= 48
+
+
+@pytest.mark.parametrize("dt", ["f32", "f64"])
+def test_interpreter_baseline_trees_and_misaligned_views(interp, dt):
+    """Config 2's T2 and config 4's e-tree, on aligned vectors and on views
+    at every element offset of a 32-byte vector (head / V = 1 paths)."""
+    rng = np.random.default_rng(5)
+    n = 100_003
+    host = [rng.uniform(-1, 1, n + 8).astype(NP[dt]) for _ in range(4)]
+    base = [lv.DenseVector.from_values(h, dt, device="cuda") for h in host]
+    for off in range(0, 8 if dt == "f32" else 4):
+        a, b, c, d = (lv.DenseVector.from_tensor(v.tensor[off:off + n]) for v in base)
+        ha, hb, hc, hd = (h[off:off + n] for h in host)
+        out = lv.DenseVector.zeros(n, dt, device="cuda")
+        out.assign(1.25 * a + -0.75 * (b - c))
+        want = restate.eval_sig("S0 L0 * S1 L1 L2 - * +", [ha, hb, hc], [1.25, -0.75], dt)
+        assert same_bits(out.to_array(), want), off
+        out.assign(1.25 * (a + b) - 0.75 * (c - d) + 0.5 * a)
+        want = restate.eval_sig("S0 L0 L1 + * S1 L2 L3 - * - S2 L0 * +", [ha, hb, hc, hd],
+                                [1.25, 0.75, 0.5], dt)
+        assert same_bits(out.to_array(), want), off
+
+
+def test_interpreter_fused_statements_device_scalars_and_axpy_dot(interp):
+    n = 300_001
+    g = np.random.default_rng(9)
+    x, p, r, q = (g.standard_normal(n) for _ in range(4))
+    X, P, R, Q = (lv.DenseVector.from_values(v, "f64") for v in (x, p, r, q))
+    al = lv.DeviceScalar.full(0.375, "f64", device="cuda")
+    rr = lv.fused((X, X + al * P), (R, R - al * Q), R * R)
+    x1 = restate.eval_sig("L0 S0 L1 * +", [x, p], [0.375], "f64")
+    r1 = restate.eval_sig("L0 S0 L1 * -", [r, q], [0.375], "f64")
+    assert X.to_array().tobytes() == x1.tobytes() and R.to_array().tobytes() == r1.tobytes()
+    ex = restate.exact_sum(r1 * r1)
+    assert abs(float(rr) - ex) <= 1e-12 * abs(ex)
+    z = g.standard_normal(n)
+    Z = lv.DenseVector.from_values(z, "f64")
+    s = lv.axpy_dot(0.5, P, X, Z)
+    x2 = restate.eval_sig("L0 S0 L1 * +", [x1, p], [0.5], "f64")
+    assert X.to_array().tobytes() == x2.tobytes()
+    ex = restate.exact_sum(x2 * z)
+    assert abs(float(s) - ex) <= 1e-12 * abs(ex)
+    assert float(lv.dot(lv.DenseVector.zeros(0, "f64"), lv.DenseVector.zeros(0, "f64"))) == 0.0
+
+
+def test_interpreter_refuses_programs_beyond_its_shared_memory(interp):
+    import torch
+
+    deep = " ".join(["L0"] * 30) + " +" * 29   # 30-deep right-leaning stack
+    x = torch.ones(64, dtype=torch.float64, device="cuda")
+    out = torch.empty(64, dtype=torch.float64, device="cuda")
+    leaves, keep = _native.ptr_array([x.data_ptr()])
+    sc, keep2 = _native.double_array([])
+    rc = interp.salt_assign(1, deep.encode(), out.data_ptr(), leaves, 1, sc, 0, 64, None)
+    assert rc == -3 and b"interpreter slots" in interp.salt_last_error()
+
+
+def test_without_nvrtc_out_of_table_trees_fall_back_to_the_interpreter():
+    """SALT_NO_JIT=1 makes the library behave as if NVRTC were absent: an
+    out-of-table tree runs on the interpreter (same bits), an in-table tree
+    still on its compiled kernel."""
+    code = r"""
+import numpy as np, paper_1109_1264_b200 as lv
+from paper_1109_1264_b200 import _native
+from oracle import restate
+lib = _native.lib()
+g = np.random.default_rng(1)
+a, b, c = (g.uniform(-1, 1, 5000) for _ in range(3))
+A, B, C = (lv.DenseVector.from_values(v, "f64") for v in (a, b, c))
+D = lv.DenseVector.zeros(5000, "f64")
+k0 = lib.salt_interp_launch_count()
+D.assign(A * B + C * A - B)                       # not in the compiled-in table
+want = restate.eval_sig("L0 L1 * L2 L0 * + L1 -", [a, b, c], [], "f64")
+assert D.to_array().tobytes() == want.tobytes()
+k1 = lib.salt_interp_launch_count()
+D.assign(A + (B - C))                             # config 2 T1: compiled in
+assert lib.salt_interp_launch_count() == k1 and k1 == k0 + 1
+print("ok")
+"""
+    env = dict(os.environ, SALT_NO_JIT="1", PYTHONPATH=f"{ROOT}:{ROOT / 'tests'}")
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
+                         cwd=ROOT, timeout=300)
+    assert out.returncode == 0 and out.stdout.strip().endswith("ok"), out.stderr[-3000:]
