@@ -610,19 +610,24 @@ Kernel* get_kernel(int dtype, int mode, int vec, int nl, const std::string& ta,
 
 std::mutex g_dev_mu;
 
-// The interpreter kernels (one per element type and vector width).
-template <class T> Kernel* interp_kernel_for(int vec) {
-  static Kernel kv, k1;
+// The interpreter kernels: per element type, the vector width and unroll of
+// every compiled kernel (so the interpreter walks the same tiles and its
+// reductions add in the same order).
+template <class T> Kernel* interp_kernel_for(int vec, int unroll) {
+  static Kernel k2, k4, k1;
   static std::once_flag once;
   std::call_once(once, [] {
-    kv.aot = (const void*)&salt::interp_kernel<T, vec_of<T>(), kBlock>;
-    kv.vec = vec_of<T>();
-    k1.aot = (const void*)&salt::interp_kernel<T, 1, kBlock>;
+    k2.aot = (const void*)&salt::interp_kernel<T, vec_of<T>(), 2, kBlock>;
+    k4.aot = (const void*)&salt::interp_kernel<T, vec_of<T>(), 4, kBlock>;
+    k1.aot = (const void*)&salt::interp_kernel<T, 1, kUnrollScalar, kBlock>;
+    k2.vec = k4.vec = vec_of<T>();
     k1.vec = 1;
-    kv.unroll = k1.unroll = 1;
-    kv.interp = k1.interp = true;
+    k2.unroll = 2;
+    k4.unroll = 4;
+    k1.unroll = kUnrollScalar;
+    k2.interp = k4.interp = k1.interp = true;
   });
-  return vec == 1 ? &k1 : &kv;
+  return vec == 1 ? &k1 : unroll == 4 ? &k4 : &k2;
 }
 
 int current_device(int& dev) {
@@ -993,7 +998,7 @@ int run_fused(Plan& p, void* const* dsts, int ndst, const void* const* leaves, i
     // the postfix interpreter evaluates the same trees (salt_interp.cuh).
     if (!p.prog_ok)
       return fail(SALT_EJIT, (force_interp ? std::string() : g_err + "; ") + "interpreter: " + p.prog_err);
-    k = interp_kernel_for<T>(vec);
+    k = interp_kernel_for<T>(vec, unroll_for(p.mode, p.nl, (int)sizeof(T)));
   }
   int dev;
   int rc = current_device(dev);
@@ -1011,7 +1016,7 @@ int run_fused(Plan& p, void* const* dsts, int ndst, const void* const* leaves, i
   const i64 ntiles = (a.nvec + per_tile - 1) / per_tile;
   i64 K = assign_tiles_per_cta(), cap = i64(0x7fffffff);
   bool cluster = false, one_group = false;
-  if (reduce && !k->interp && ntiles > 2 && ntiles <= (i64)max_cluster() * cluster_tiles()) {
+  if (reduce && ntiles > 2 && ntiles <= (i64)max_cluster() * cluster_tiles()) {
     // Small n (3 .. 16 x 2 tiles; up to 2 tiles one CTA is quicker): one cluster
     // of <= 16 CTAs, partials combined in distributed shared memory — no
     // workspace round trip, no ticket atomics.  B200, back-to-back launches
@@ -1076,7 +1081,9 @@ int run_fused(Plan& p, void* const* dsts, int ndst, const void* const* leaves, i
       a.xchg.error = (unsigned int*)x->error;
     }
   }
-  a.cluster = cluster && grid > 1 && cluster_combine() ? 1 : 0;
+  // the interpreter keeps the cluster-sized grid but folds through the
+  // tickets (same bits, as SALT_CLUSTER_COMBINE=0 shows for compiled kernels)
+  a.cluster = cluster && grid > 1 && cluster_combine() && !k->interp ? 1 : 0;
   bool launched = false;
   if (a.cluster) {
     launched = launch_cluster<T>(k, dev, grid, a, st, rc);

@@ -8,9 +8,11 @@
 // first, no FMA), assignment roots are evaluated in order and a later root
 // reads an earlier root's value (D<r>), and reductions go through the same
 // compensated accumulator and the same deterministic CTA / group combine
-// (reduce_epilogue).  Reductions fold with one tile of BLOCK vectors per
-// step instead of the template kernel's BLOCK*UNR, so their last bits may
-// differ from the compiled kernels' (both stay within 1 ulp of exact).
+// (reduce_epilogue), over the same tiles of BLOCK*UNR vectors with the same
+// UNR as the compiled kernel of that tree: a thread adds its values in the
+// compiled kernel's order (head/tail elements, then per tile slot u = 0..UNR-1
+// lane by lane), so reductions are bit-identical to the compiled kernels too
+// — whichever kernel runs, a tree gives the same bits.
 //
 // The program comes in the kernel parameters (uniform across threads); the
 // evaluation stack and the loaded leaf vectors live in shared memory, one
@@ -111,7 +113,7 @@ __device__ __forceinline__ void interp_eval(const Prog& pg, const Args<T>& a, T*
   }
 }
 
-template <class T, int V, int BLOCK>
+template <class T, int V, int UNR, int BLOCK>
 __global__ void __launch_bounds__(BLOCK) interp_kernel(InterpArgs<T> ia) {
   asm volatile("griddepcontrol.wait;" ::: "memory");  // see fused_kernel
   const Args<T>& a = ia.a;
@@ -129,12 +131,15 @@ __global__ void __launch_bounds__(BLOCK) interp_kernel(InterpArgs<T> ia) {
       interp_eval<T, 1, BLOCK>(pg, a, sm, i, acc);
     }
   }
-  const i64 ntiles = (a.nvec + BLOCK - 1) / BLOCK;
+  const i64 ntiles = (a.nvec + (i64)BLOCK * UNR - 1) / ((i64)BLOCK * UNR);
   const i64 tile0 = (i64)blockIdx.x * a.tiles_per_cta;
   const i64 tile1 = tile0 + a.tiles_per_cta < ntiles ? tile0 + a.tiles_per_cta : ntiles;
   for (i64 t = tile0; t < tile1; ++t) {
-    const i64 j = t * BLOCK + threadIdx.x;
-    if (j < a.nvec) interp_eval<T, V, BLOCK>(pg, a, sm, a.head + j * V, acc);
+    const i64 base = t * BLOCK * UNR + threadIdx.x;
+    for (int u = 0; u < UNR; ++u) {
+      const i64 j = base + (i64)u * BLOCK;
+      if (j < a.nvec) interp_eval<T, V, BLOCK>(pg, a, sm, a.head + j * V, acc);
+    }
   }
   if (pg.reduce) reduce_epilogue<T, BLOCK>(acc.get(), a);
 }

@@ -55,6 +55,12 @@ def test_interpreter_random_trees(interp, dt):
         if exact != 0 and np.isfinite(exact):
             scale = restate.exact_sum(np.abs(want))
             assert abs(float(r) - exact) <= TOL[dt] * max(abs(exact), 1e-3 * scale), (case, float(r), exact)
+        # the interpreter walks the compiled kernel's tiles in its order:
+        # the reduction has the compiled (table or JIT) kernel's bits
+        interp.salt_set_force_interp(0)
+        r_compiled = execute_reduce(SumNode(expr))
+        interp.salt_set_force_interp(1)
+        assert same_bits(np.array([r]), np.array([r_compiled])), (case, float(r), float(r_compiled))
         checked += 1
     assert checked == 24
     assert interp.salt_interp_launch_count() - before >= 48
@@ -82,6 +88,10 @@ def test_interpreter_baseline_trees_and_misaligned_views(interp, dt):
 
 
 def test_interpreter_fused_statements_device_scalars_and_axpy_dot(interp):
+    _fused_sequence(interp, check=True)
+
+
+def _fused_sequence(lib, check):
     n = 300_001
     g = np.random.default_rng(9)
     x, p, r, q = (g.standard_normal(n) for _ in range(4))
@@ -101,6 +111,28 @@ def test_interpreter_fused_statements_device_scalars_and_axpy_dot(interp):
     ex = restate.exact_sum(x2 * z)
     assert abs(float(s) - ex) <= 1e-12 * abs(ex)
     assert float(lv.dot(lv.DenseVector.zeros(0, "f64"), lv.DenseVector.zeros(0, "f64"))) == 0.0
+    return float(rr), float(s)
+
+
+def test_interpreter_reductions_match_compiled_bits(interp):
+    """Fused statements + reduction and fused axpy->dot: the same bits on
+    the interpreter and on the compiled kernels."""
+    got = _fused_sequence(interp, check=True)
+    interp.salt_set_force_interp(0)
+    want = _fused_sequence(interp, check=True)
+    interp.salt_set_force_interp(1)
+    assert got == want
+    # sizes across every grid shape: one CTA, one cluster (3-32 tiles), one
+    # group, two ticket levels
+    for dt, n in (("f32", 1 << 22), ("f64", 1 << 22), ("f32", 12345), ("f64", 3), ("f64", 1 << 16),
+                  ("f32", 1 << 17), ("f64", 1 << 25)):
+        g = np.random.default_rng([n, len(dt)])
+        x, y = (lv.DenseVector.from_values(g.standard_normal(n), dt) for _ in range(2))
+        a = (lv.dot(x, y), lv.norm2(x), lv.sum(x))
+        interp.salt_set_force_interp(0)
+        b = (lv.dot(x, y), lv.norm2(x), lv.sum(x))
+        interp.salt_set_force_interp(1)
+        assert same_bits(np.array(a), np.array(b)), (dt, n, a, b)
 
 
 def test_interpreter_refuses_programs_beyond_its_shared_memory(interp):
