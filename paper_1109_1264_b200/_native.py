@@ -60,6 +60,8 @@ HEADER_SYMBOLS = (
     "salt_set_force_jit",
     "salt_set_force_interp",
     "salt_interp_launch_count",
+    "salt_set_jit_async",
+    "salt_jit_wait",
     "salt_launch_count",
     "salt_last_error",
     "salt_abi_version",
@@ -130,6 +132,8 @@ _SIGNATURES = {
     "salt_set_force_jit": (None, [_c_int]),
     "salt_set_force_interp": (None, [_c_int]),
     "salt_interp_launch_count": (ctypes.c_uint64, []),
+    "salt_set_jit_async": (None, [_c_int]),
+    "salt_jit_wait": (_c_int, []),
     "salt_launch_count": (ctypes.c_uint64, []),
     "salt_last_error": (_c_str, []),
     "salt_abi_version": (_c_int, []),

@@ -21,6 +21,9 @@
 #include <unistd.h>
 
 #include <atomic>
+#include <chrono>
+#include <condition_variable>
+#include <deque>
 #include <cstdio>
 #include <cstring>
 #include <fstream>
@@ -29,7 +32,9 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <unordered_map>
+#include <unordered_set>
 #include <vector>
 
 #include "../../include/salt.h"
@@ -401,8 +406,9 @@ std::unordered_map<std::string, std::unique_ptr<Kernel>>& table() {
   return t;
 }
 std::unordered_map<std::string, std::unique_ptr<Kernel>>& jit_table() {
-  static std::unordered_map<std::string, std::unique_ptr<Kernel>> t;
-  return t;
+  // leaked: the background JIT thread may insert while the process exits
+  static auto* t = new std::unordered_map<std::string, std::unique_ptr<Kernel>>;
+  return *t;
 }
 
 template <class T> constexpr int dtype_of();
@@ -519,8 +525,11 @@ void jit_cache_store(const std::string& dir, const std::string& path, const Kern
   rename(tmp.c_str(), path.c_str());
 }
 
-Kernel* jit_compile(int dtype, int mode, int vec, int nl, const std::string& ta,
-                    const std::string& tr, const std::string& key) {
+// Build (or load from the disk cache) the JIT kernel of a tree; nullptr +
+// g_err on failure.  cache_only: return nullptr on a cache miss instead of
+// compiling.  The caller inserts the result into jit_table().
+std::unique_ptr<Kernel> jit_build(int dtype, int mode, int vec, int nl, const std::string& ta,
+                                  const std::string& tr, bool cache_only) {
   Nvrtc& nv = nvrtc();
   if (!nv.ok) { g_err = "NVRTC unavailable: " + nv.why; return nullptr; }
   const char* tname = dtype == SALT_F32 ? "float" : "double";
@@ -551,11 +560,10 @@ Kernel* jit_compile(int dtype, int mode, int vec, int nl, const std::string& ta,
     if (jit_cache_load(cache_path, *k)) {
       k->vec = vec;
       k->unroll = unroll;
-      Kernel* raw = k.get();
-      jit_table()[key] = std::move(k);
-      return raw;
+      return k;
     }
   }
+  if (cache_only) return nullptr;
   void* prog = nullptr;
   if (nv.CreateProgram(&prog, kExprSource, "salt_expr_jit.cu", 0, nullptr, nullptr) != 0) {
     g_err = "nvrtcCreateProgram failed";
@@ -588,24 +596,129 @@ Kernel* jit_compile(int dtype, int mode, int vec, int nl, const std::string& ta,
     if (!parent.empty()) mkdir(parent.c_str(), 0755);
     jit_cache_store(cdir, cache_path, *k);
   }
-  Kernel* raw = k.get();
-  jit_table()[key] = std::move(k);
-  return raw;
+  return k;
 }
 
-// Look up (or JIT) the kernel; nullptr + g_err on failure.
+Kernel* jit_insert(const std::string& key, std::unique_ptr<Kernel> k) {
+  std::lock_guard<std::mutex> lk(g_table_mu);
+  auto& slot = jit_table()[key];
+  if (!slot) slot = std::move(k);  // a concurrent build of the same tree may have won
+  return slot.get();
+}
+
+// ---- tiered JIT: a tree outside the compiled-in table runs on the
+// interpreter (same bits, salt_interp.cuh) while a background thread
+// compiles it with NVRTC; later calls find the compiled kernel.  No call
+// waits ~0.4 s for NVRTC.  SALT_JIT_ASYNC=0 / salt_set_jit_async(0) compile
+// synchronously instead.
+struct JitJob {
+  int dtype, mode, vec, nl;
+  std::string ta, tr, key;
+};
+struct AsyncJit {
+  std::mutex mu;
+  std::condition_variable cv, idle;
+  std::deque<JitJob> queue;
+  std::unordered_set<std::string> pending, failed;
+  std::unordered_map<std::string, std::string> errors;
+  int active = 0;
+  bool started = false, stopping = false;
+};
+AsyncJit& async_jit() {
+  static AsyncJit* a = new AsyncJit;  // leaked: the worker may outlive static destructors
+  return *a;
+}
+std::atomic<int> g_jit_async{-1};  // -1: not yet read from SALT_JIT_ASYNC
+bool jit_async() {
+  int v = g_jit_async.load(std::memory_order_relaxed);
+  if (v < 0) {
+    const char* e = getenv("SALT_JIT_ASYNC");
+    v = e && atoi(e) == 0 ? 0 : 1;
+    g_jit_async.store(v);
+  }
+  return v == 1;
+}
+
+void jit_worker() {
+  AsyncJit& A = async_jit();
+  for (;;) {
+    JitJob j;
+    {
+      std::unique_lock<std::mutex> lk(A.mu);
+      A.cv.wait(lk, [&] { return !A.queue.empty() || A.stopping; });
+      if (A.stopping) return;
+      j = std::move(A.queue.front());
+      A.queue.pop_front();
+      ++A.active;
+    }
+    std::unique_ptr<Kernel> k = jit_build(j.dtype, j.mode, j.vec, j.nl, j.ta, j.tr, false);
+    std::string err = k ? std::string() : g_err;
+    if (k) jit_insert(j.key, std::move(k));
+    std::lock_guard<std::mutex> lk(A.mu);
+    A.pending.erase(j.key);
+    if (!err.empty()) {
+      A.failed.insert(j.key);
+      A.errors[j.key] = err;
+    }
+    --A.active;
+    if (A.queue.empty() && A.active == 0) A.idle.notify_all();
+  }
+}
+
+// At exit: let a compile in flight finish (NVRTC must not run while the
+// process tears its libraries down), then stop the worker.
+void jit_atexit() {
+  AsyncJit& A = async_jit();
+  std::unique_lock<std::mutex> lk(A.mu);
+  A.queue.clear();
+  A.idle.wait_for(lk, std::chrono::seconds(10), [&] { return A.active == 0; });
+  A.stopping = true;
+  A.cv.notify_all();
+}
+
+// Queue a background build; false if it failed before (g_err = why).
+bool jit_enqueue(JitJob j) {
+  AsyncJit& A = async_jit();
+  std::lock_guard<std::mutex> lk(A.mu);
+  if (A.failed.count(j.key)) {
+    g_err = A.errors[j.key];
+    return false;
+  }
+  if (A.pending.count(j.key)) return true;
+  if (!A.started) {
+    A.started = true;
+    std::thread(jit_worker).detach();
+    atexit(jit_atexit);
+  }
+  A.pending.insert(j.key);
+  A.queue.push_back(std::move(j));
+  A.cv.notify_one();
+  return true;
+}
+
+// Look up (or JIT) the kernel; nullptr + g_err on failure.  async: on a
+// miss (table, JIT table and disk cache) queue a background build and return
+// nullptr with *queued = true — the caller runs the interpreter meanwhile.
 Kernel* get_kernel(int dtype, int mode, int vec, int nl, const std::string& ta,
-                   const std::string& tr) {
+                   const std::string& tr, bool async = false, bool* queued = nullptr) {
   ensure_table();
   const std::string key = key_of(dtype, mode, vec, ta, tr);
-  std::lock_guard<std::mutex> lk(g_table_mu);
-  if (!g_force_jit.load() && tuning_unroll() <= 0 && tuning_minb() <= 0) {
-    auto it = table().find(key);
-    if (it != table().end()) return it->second.get();
+  {
+    std::lock_guard<std::mutex> lk(g_table_mu);
+    if (!g_force_jit.load() && tuning_unroll() <= 0 && tuning_minb() <= 0) {
+      auto it = table().find(key);
+      if (it != table().end()) return it->second.get();
+    }
+    auto jt = jit_table().find(key);
+    if (jt != jit_table().end()) return jt->second.get();
   }
-  auto jt = jit_table().find(key);
-  if (jt != jit_table().end()) return jt->second.get();
-  return jit_compile(dtype, mode, vec, nl, ta, tr, key);
+  if (async && nvrtc().ok) {
+    if (auto k = jit_build(dtype, mode, vec, nl, ta, tr, true)) return jit_insert(key, std::move(k));
+    if (queued) *queued = jit_enqueue(JitJob{dtype, mode, vec, nl, ta, tr, key});
+    return nullptr;
+  }
+  auto k = jit_build(dtype, mode, vec, nl, ta, tr, false);
+  return k ? jit_insert(key, std::move(k)) : nullptr;
 }
 
 std::mutex g_dev_mu;
@@ -990,7 +1103,13 @@ int run_fused(Plan& p, void* const* dsts, int ndst, const void* const* leaves, i
   const bool force_interp = g_force_interp.load(std::memory_order_relaxed) != 0;
   if (!force_interp) {
     Kernel*& slot = p.cached[g_force_jit.load(std::memory_order_relaxed)][vec == 1 ? 1 : 0];
-    if (!slot) slot = get_kernel(dtype_of<T>(), p.mode, vec, p.nl, p.sa.type, p.sr.type);
+    if (!slot) {
+      // tiered: trees the interpreter can run do not wait for NVRTC (unless
+      // the JIT itself is being tested: salt_set_force_jit)
+      const bool async = p.prog_ok && jit_async() && !g_force_jit.load(std::memory_order_relaxed);
+      bool queued = false;
+      slot = get_kernel(dtype_of<T>(), p.mode, vec, p.nl, p.sa.type, p.sr.type, async, &queued);
+    }
     k = slot;
   }
   if (!k) {
@@ -1379,6 +1498,15 @@ uint64_t salt_launch_count(void) { return g_launches.load(); }
 void salt_set_force_jit(int on) { g_force_jit.store(on ? 1 : 0); }
 
 void salt_set_force_interp(int on) { g_force_interp.store(on ? 1 : 0); }
+
+void salt_set_jit_async(int on) { g_jit_async.store(on ? 1 : 0); }
+
+int salt_jit_wait(void) {
+  AsyncJit& A = async_jit();
+  std::unique_lock<std::mutex> lk(A.mu);
+  A.idle.wait(lk, [&] { return A.queue.empty() && A.active == 0; });
+  return (int)A.failed.size();
+}
 
 uint64_t salt_interp_launch_count(void) { return g_interp_launches.load(); }
 

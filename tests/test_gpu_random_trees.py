@@ -10,6 +10,7 @@ import pytest
 import paper_1109_1264_b200 as lv
 from conftest import NP, same_bits
 from oracle import restate
+from paper_1109_1264_b200 import _native
 from paper_1109_1264_b200.engine import execute_reduce
 from paper_1109_1264_b200.expressions import SumNode, as_node, lower
 
@@ -51,6 +52,14 @@ def test_random_trees_bit_exact(dt):
         out.assign(expr)
         assert same_bits(out.to_array(), want), (case, " ".join(lw.tokens))
         r = execute_reduce(SumNode(expr))
+        # tiered JIT: the calls above may have run on the interpreter while
+        # NVRTC compiled in the background; once it is done, the compiled
+        # kernels must give the same bits
+        assert _native.lib().salt_jit_wait() == 0
+        out2 = lv.DenseVector.zeros(n, dt, device="cuda")
+        out2.assign(expr)
+        assert same_bits(out2.to_array(), want), (case, "compiled", " ".join(lw.tokens))
+        assert same_bits(np.array([execute_reduce(SumNode(expr))]), np.array([r])), case
         exact = restate.exact_sum(want)
         if exact != 0 and np.isfinite(exact):
             tol = {"f32": 1e-5, "f64": 1e-12}[dt]
@@ -141,6 +150,14 @@ def test_random_trees_with_device_scalars(dt):
         out.assign(expr)
         assert same_bits(out.to_array(), want), (case, " ".join(lw.tokens))
         r = execute_reduce(SumNode(expr))
+        # tiered JIT: the calls above may have run on the interpreter while
+        # NVRTC compiled in the background; once it is done, the compiled
+        # kernels must give the same bits
+        assert _native.lib().salt_jit_wait() == 0
+        out2 = lv.DenseVector.zeros(n, dt, device="cuda")
+        out2.assign(expr)
+        assert same_bits(out2.to_array(), want), (case, "compiled", " ".join(lw.tokens))
+        assert same_bits(np.array([execute_reduce(SumNode(expr))]), np.array([r])), case
         exact = restate.exact_sum(want)
         if exact != 0 and np.isfinite(exact):
             tol = {"f32": 1e-5, "f64": 1e-12}[dt]
