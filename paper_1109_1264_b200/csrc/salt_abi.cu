@@ -514,7 +514,9 @@ bool jit_cache_load(const std::string& path, Kernel& k) {
 
 void jit_cache_store(const std::string& dir, const std::string& path, const Kernel& k) {
   mkdir(dir.c_str(), 0755);  // parent of the default dir: ~/.cache
-  std::string tmp = path + ".tmp" + std::to_string(getpid());
+  // unique per process and thread (the background JIT thread may store too)
+  std::string tmp = path + ".tmp" + std::to_string(getpid()) + "." +
+                    std::to_string(std::hash<std::thread::id>()(std::this_thread::get_id()));
   {
     std::ofstream f(tmp, std::ios::binary);
     if (!f) return;
