@@ -55,6 +55,23 @@ int main() {
          per_call_us([&] { empty_kernel<<<1, 256, 0, s>>>(); }, calls));
   printf(" \"empty kernel with a 720-byte parameter block\": %.3f,\n",
          per_call_us([&] { big_kernel<<<1, 256, 0, s>>>(big); }, calls));
+  {
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.gridDim = dim3(1);
+    cfg.blockDim = dim3(256);
+    cfg.stream = s;
+    cfg.attrs = attr;
+    void* params[] = {&big};
+    cfg.numAttrs = 0;
+    printf(" \"720-byte kernel via cudaLaunchKernelExC, no attribute\": %.3f,\n",
+           per_call_us([&] { cudaLaunchKernelExC(&cfg, (const void*)big_kernel, params); }, calls));
+    cfg.numAttrs = 1;
+    printf(" \"720-byte kernel via cudaLaunchKernelExC, PDL attribute\": %.3f,\n",
+           per_call_us([&] { cudaLaunchKernelExC(&cfg, (const void*)big_kernel, params); }, calls));
+  }
   printf(" \"salt_assign T2 n=1024\": %.3f,\n",
          per_call_us([&] { salt_assign(SALT_F64, "S0 L0 * S1 L1 L2 - * +", d, leaves, 3, sc, 2, n, s); },
                      calls));
