@@ -1421,7 +1421,12 @@ int host_pipeline(int dtype, Plan& p, void* host_dst, const void* const* host_le
   if (staging_bytes <= fixed + 256) return fail(SALT_EWORKSPACE, "staging too small");
   i64 chunk = (i64)((staging_bytes - fixed) / (kNBuf * nbufs_per_set * esz));
   chunk = chunk / 64 * 64;
-  if (chunk > kMaxChunk) chunk = kMaxChunk;
+  static const i64 max_chunk = [] {  // SALT_HOST_CHUNK (elements; tuning only)
+    const char* e = getenv("SALT_HOST_CHUNK");
+    const long long v = e ? atoll(e) : 0;
+    return v >= 64 ? (i64)(v / 64 * 64) : kMaxChunk;
+  }();
+  if (chunk > max_chunk) chunk = max_chunk;
   if (chunk < 64) return fail(SALT_EWORKSPACE, "staging too small for one chunk");
   const i64 nchunks = (n + chunk - 1) / chunk;
   if (reduce && nchunks * (i64)sizeof(salt::DD) > 256 * 1024)
