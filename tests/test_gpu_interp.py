@@ -213,3 +213,48 @@ print("ok first_ms=%.1f" % first_ms)
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-3000:]
     first_ms = float(out.stdout.split("first_ms=")[1])
     assert first_ms < 300, first_ms   # a synchronous NVRTC build alone takes ~400 ms per tree
+
+
+def test_tiered_jit_under_concurrent_threads():
+    """Eight host threads evaluate fresh trees while the background JIT
+    compiles them: every result has the reference's bits, before and after
+    the compiled kernels take over."""
+    import threading
+
+    import torch
+
+    n = 50_003
+    g = np.random.default_rng(77)
+    host = [g.uniform(-1, 1, n) for _ in range(4)]
+    vecs = [lv.DenseVector.from_values(h, "f64") for h in host]
+    trees = []
+    for t in range(8):
+        c = 0.25 * (t + 1)
+        trees.append(((lambda c=c: (as_node(vecs[0]) * c - vecs[1]) * (as_node(vecs[2]) + vecs[3] * c)),
+                      f"L0 S0 * L1 - L2 L3 S1 * + *", [c, c]))
+    errors = []
+
+    def work(t):
+        try:
+            torch.cuda.set_device(0)
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                build, sig, sc = trees[t]
+                out = lv.DenseVector.zeros(n, "f64")
+                want = restate.eval_sig(sig, host, sc, "f64")
+                for _ in range(20):
+                    out.assign(build())
+                    s.synchronize()
+                    if out.to_array().tobytes() != want.tobytes():
+                        errors.append(t)
+                        return
+        except Exception as exc:  # pragma: no cover
+            errors.append(repr(exc))
+
+    threads = [threading.Thread(target=work, args=(t,)) for t in range(8)]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    assert not errors, errors
+    assert _native.lib().salt_jit_wait() == 0
