@@ -23,7 +23,8 @@ bench.py:9-15 / :49-50) and times on the device:
     sum norm2 t1 t2 etree axpy_dot       (BASELINE configs; --op extended)
 
 --flush-l2 overwrites a 256 MiB buffer (> 126 MB L2) between reps, outside
-the timed region, for HBM claims.  --extended adds pct_hbm and device
+the timed region, for HBM claims.  --extended adds pct_hbm (of the
+measured copy peak), device, gpus, bytes and pct_hbm_nominal (of 8 TB/s)
 columns.
 """
 
@@ -44,7 +45,10 @@ OPS = ("dot", "scal", "axpy", "scaled_copy")
 EXTENDED_OPS = OPS + ("sum", "norm2", "t1", "t2", "etree", "axpy_dot")
 VARIANTS = ("engine", "engine-host", "torch", "naive", "engine-U1", "engine-U2", "engine-U4", "engine-U8")
 CSV_HEADER = "op,variant,type,n,reps,best_s,median_s,gflops,gbytes"
-EXT_HEADER = CSV_HEADER + ",pct_hbm,device"
+# + gpus, bytes (algorithmic, per call), % of the
+# measured and of the nominal (8 TB/s) HBM peak, device
+EXT_HEADER = CSV_HEADER + ",pct_hbm,device,gpus,bytes,pct_hbm_nominal"
+NOMINAL_HBM_GBS = 8000.0
 
 # per element: (flops, distinct vectors read + written)
 _ACCOUNT = {
@@ -67,6 +71,9 @@ class BenchRecord:
     gbytes: float
     pct_hbm: float = float("nan")
     device: str = ""
+    gpus: int = 1
+    bytes: int = 0
+    pct_hbm_nominal: float = float("nan")
 
 
 def default_sizes() -> list:
@@ -235,7 +242,8 @@ def measure(op, variant, n, dtype="f32", reps=25, warmup=5, seed=0, packages=Non
     med = statistics.median(times)
     gbytes = bytes_moved(op, n, dt) / best / 1e9
     return BenchRecord(op, variant, dtype_name(dt), n, reps, best, med, flop_count(op, n) / best / 1e9,
-                       gbytes, gbytes / _hbm_peak(), torch.cuda.get_device_name())
+                       gbytes, gbytes / _hbm_peak(), torch.cuda.get_device_name(), 1,
+                       bytes_moved(op, n, dt), gbytes / NOMINAL_HBM_GBS)
 
 
 def run_sweep(ops, variants, sizes, dtype="f32", reps=25, warmup=5, seed=0, packages=None, flush_l2=False):
@@ -254,7 +262,7 @@ def _lines(records, extended):
     for r in records:
         vals = [r.op, r.variant, r.type, r.n, r.reps, r.best_s, r.median_s, r.gflops, r.gbytes]
         if extended:
-            vals += [r.pct_hbm, r.device.replace(",", " ")]
+            vals += [r.pct_hbm, r.device.replace(",", " "), r.gpus, r.bytes, r.pct_hbm_nominal]
         yield ",".join(repr(v) if isinstance(v, float) else str(v) for v in vals)
 
 
@@ -282,8 +290,9 @@ def parse_csv(text: str) -> list:
     out = []
     for ln in lines[1:]:
         p = ln.split(",")
+        extra = [float(p[9]), p[10], int(p[11]), int(p[12]), float(p[13])] if ext else []
         rec = BenchRecord(p[0], p[1], p[2], int(p[3]), int(p[4]), float(p[5]), float(p[6]),
-                          float(p[7]), float(p[8]), *( [float(p[9]), p[10]] if ext else []))
+                          float(p[7]), float(p[8]), *extra)
         out.append(rec)
     return out
 

@@ -24,7 +24,8 @@ def test_accounting_matches_reference_for_shared_ops():
 
 def test_csv_round_trip_and_header(tmp_path):
     recs = [sb.BenchRecord("dot", "engine", "f32", 64, 3, 1e-6, 2e-6, 0.128, 0.512),
-            sb.BenchRecord("t2", "torch", "f64", 1024, 3, 2e-6, 3e-6, 2.048, 16.384, 0.0025, "B200")]
+            sb.BenchRecord("t2", "torch", "f64", 1024, 3, 2e-6, 3e-6, 2.048, 16.384, 0.0025, "B200", 1,
+                           32768, 0.002048)]
     p = tmp_path / "a.csv"
     sb.emit_csv(recs[:1], str(p))
     lines = p.read_text().splitlines()
@@ -33,6 +34,8 @@ def test_csv_round_trip_and_header(tmp_path):
     sb.emit_csv(recs, str(p), extended=True)
     back = sb.parse_csv(p.read_text())
     assert back[1].pct_hbm == recs[1].pct_hbm and back[1].device == "B200"
+    assert back[1] == recs[1]
+    assert p.read_text().splitlines()[0].endswith(",pct_hbm,device,gpus,bytes,pct_hbm_nominal")
     with pytest.raises(ValueError):
         sb.parse_csv("bad,header\n")
 
