@@ -11,6 +11,7 @@ NCCL communicators from ncclCommInitAll.  This module is the second:
         for g in range(dg.size):                  # elementwise: no exchange,
             ys[g].assign(ys[g] + 0.5 * xs[g])     # launches run concurrently
         r = dg.reduce([y * x for y, x in zip(ys, xs)])   # dot over all blocks
+        r = dg.axpy_dot(0.5, xs, ys, zs)                 # config 5's fused step
 
 Blocks follow the same partition as ShardedVector (shard_bounds: 64-element
 aligned bases).  A reduction runs one fused kernel per device writing its
@@ -27,7 +28,7 @@ import numpy as np
 import torch
 
 from . import _native
-from .expressions import Expression, lower
+from .expressions import AssignNode, Expression, FusedNode, SumNode, as_node, lower
 from .lanes import as_dtype
 from .runtime import _dtype_code, _OnDevice, _raw_stream, _require_cuda, _workspace
 from .sharding import shard_bounds
@@ -129,10 +130,74 @@ class DeviceGroup:
             parts.append(part)
             streams.append(stream)
             keep += [k1, k2]
+        return self._allreduce(parts, streams, dt, _native.SALT_SQRT if sqrt else 0, lazy)
+
+    def fused(self, statements, *, lazy=False):
+        """statements[g] holds the `lv.fused` arguments for device g —
+        `(dest, expression)` assignments, then one final expression to sum —
+        run as ONE kernel per device (the assignments and the device's
+        partial sum in one pass); the partials combine across devices with
+        salt_allreduce_sum.  Returns the sum (per-device DeviceScalars with
+        lazy=True).  Config 5's step: `fused([((y, y + a * x), y * z)
+        for x, y, z in zip(xs, ys, zs)])`."""
+        statements = list(statements)
+        if len(statements) != self.size:
+            raise ValueError(f"need one statement list per device ({self.size}), got {len(statements)}")
+        lib = _native.lib()
+        parts, streams, keep, dts = [], [], [], set()
+        for g, (sts, d) in enumerate(zip(statements, self.devices)):
+            sts = list(sts)
+            if len(sts) < 2 or isinstance(sts[-1], tuple) or not all(
+                    isinstance(s, tuple) and len(s) == 2 for s in sts[:-1]):
+                raise TypeError("statements: (dest, expression) pairs, then one expression to sum")
+            node = FusedNode([AssignNode(as_node(dst), as_node(e)) for dst, e in sts[:-1]],
+                             SumNode(as_node(sts[-1])))
+            asig, rsig, lw, dests = node.lower()
+            dev = torch.device("cuda", d)
+            vecs = list(lw.vectors) + list(dests)
+            for v in vecs:
+                if not isinstance(v, DenseVector) or v.tensor.device != dev:
+                    raise ValueError(f"statements {g}: every operand must be a DenseVector on cuda:{d}")
+            for ds in lw.pscalars:
+                if ds.tensor.device != dev:
+                    raise ValueError(f"statements {g}: device scalars must live on cuda:{d}")
+            lengths = {len(v) for v in vecs}
+            if len(lengths) != 1:
+                raise ValueError(f"statements {g}: operands of different lengths {sorted(lengths)}")
+            n = lengths.pop()
+            dt = as_dtype(node.dtype)
+            dts.add(dt)
+            with _OnDevice(d):
+                stream = _raw_stream(d)
+                ws = _workspace(d, stream)
+                part = torch.empty(2, dtype=torch.float64, device=dev)
+                leaves, k1 = _native.ptr_array([v.tensor.data_ptr() for v in lw.vectors])
+                dsts, k2 = _native.ptr_array([v.tensor.data_ptr() for v in dests])
+                scal, k3 = _native.double_array(lw.scalars)
+                pscal, k4 = _native.ptr_array([ds.tensor.data_ptr() for ds in lw.pscalars])
+                _native.check(lib.salt_fused(_dtype_code(dt), asig.encode(), rsig.encode(), dsts, len(dests),
+                                             leaves, len(lw.vectors), scal, len(lw.scalars), pscal,
+                                             len(lw.pscalars), n, _native.SALT_PARTIAL, ws.data_ptr(),
+                                             ws.numel(), part.data_ptr(), None, stream))
+            parts.append(part)
+            streams.append(stream)
+            keep += [k1, k2, k3, k4]
+        if len(dts) != 1:
+            raise TypeError("all devices' statements must have one element type")
+        return self._allreduce(parts, streams, dts.pop(), 0, lazy)
+
+    def axpy_dot(self, alpha, xs, ys, zs, **kw):
+        """y_g = y_g + alpha*x_g on every device, then dot(y, z) over all
+        blocks — one fused kernel per device plus one all-reduce (config 5)."""
+        return self.fused([((y, as_node(y) + alpha * as_node(x)), as_node(y) * as_node(z))
+                           for x, y, z in zip(xs, ys, zs)], **kw)
+
+    def _allreduce(self, parts, streams, dt, flags, lazy):
+        lib = _native.lib()
         outs, k3 = _native.ptr_array([p.data_ptr() for p in parts])
         strs, k4 = _native.ptr_array(streams)
-        _native.check(lib.salt_allreduce_sum_flags(outs, self.size, code, ctypes.addressof(self._comms),
-                                                   strs, _native.SALT_SQRT if sqrt else 0))
+        _native.check(lib.salt_allreduce_sum_flags(outs, self.size, _dtype_code(dt),
+                                                   ctypes.addressof(self._comms), strs, flags))
         scalars = [DeviceScalar(p.view(torch.float32)[:1] if dt.itemsize == 4 else p[:1], dt) for p in parts]
         return scalars if lazy else scalars[0].item()
 

@@ -118,3 +118,27 @@ def test_devicegroup_all_devices_agree():
         assert len(set(vals)) == 1
         ex = restate.exact_sum(x * y)
         assert abs(vals[0] - ex) <= 1e-12 * abs(ex)
+
+
+@pytest.mark.parametrize("dt", ["f64", "f32"])
+def test_devicegroup_fused_axpy_dot_and_cg_update(dt):
+    """Config 5's fused step and a CG update through DeviceGroup: the same
+    bits as lv.axpy_dot / lv.fused on one device (partial + all-reduce of
+    one partial == the direct finish)."""
+    n = 1 << 20 | 5
+    x, y, z = _vals(12, n), _vals(13, n), _vals(14, n)
+    with lv.DeviceGroup([0]) as dg:
+        xs, ys, zs = dg.scatter(x, dt), dg.scatter(y, dt), dg.scatter(z, dt)
+        X, Y, Z = (lv.DenseVector.from_values(v, dt) for v in (x, y, z))
+        for k in range(3):
+            r = dg.axpy_dot(0.5, xs, ys, zs)
+            q = lv.axpy_dot(0.5, X, Y, Z)
+            assert r.dtype == q.dtype and r == q, (k, r, q)
+            assert ys[0].to_array().tobytes() == Y.to_array().tobytes()
+        a = lv.DeviceScalar.full(0.125, dt, device="cuda")
+        rr = dg.fused([((xs[0], xs[0] + a * zs[0]), (ys[0], ys[0] - a * xs[0]), ys[0] * ys[0])], lazy=True)
+        qq = lv.fused((X, X + a * Z), (Y, Y - a * X), Y * Y, lazy=True)
+        assert rr[0].item() == qq.item()
+        assert xs[0].to_array().tobytes() == X.to_array().tobytes()
+        with pytest.raises(TypeError, match="expression to sum"):
+            dg.fused([((xs[0], xs[0] + ys[0]),)])
