@@ -142,3 +142,17 @@ def test_devicegroup_fused_axpy_dot_and_cg_update(dt):
         assert xs[0].to_array().tobytes() == X.to_array().tobytes()
         with pytest.raises(TypeError, match="expression to sum"):
             dg.fused([((xs[0], xs[0] + ys[0]),)])
+
+
+def test_config5_example_runs_and_checks():
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parents[1]
+    out = subprocess.run([sys.executable, str(root / "examples" / "c5_devicegroup.py"), "--n", str(1 << 22),
+                          "--iters", "5", "--check"], capture_output=True, text=True, timeout=300, cwd=root)
+    assert out.returncode == 0, out.stderr[-3000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert line["checked"] is True and line["gpus"] == torch.cuda.device_count()
