@@ -2,8 +2,10 @@
 
 CPU restatements of the reference's evaluation of BLAS-1 expression trees
 (/root/reference/pkg/src/lanevec), used as the parity checker by tests/,
-by `__graft_entry__.smoke()`, and by bench.py's cpu_baseline and
-`--impl reference` legs (CPU timing of the reference algorithm).
+by `__graft_entry__.smoke()`, by bench.py's cpu_baseline and
+`--impl reference` legs (CPU timing of the reference algorithm), and by the
+measurement tools tools/config_sweep.py, tools/reference_engine_timing.py
+(CPU timing legs) and tools/dist_check.py (checker).
 
 Nothing in paper_1109_1264_b200/ imports this package: the product has no
 CPU evaluation path.
