@@ -258,3 +258,21 @@ def test_tiered_jit_under_concurrent_threads():
         th.join()
     assert not errors, errors
     assert _native.lib().salt_jit_wait() == 0
+
+
+def test_interpreter_on_pinned_host_vectors(interp):
+    """Host vectors stream through the GPU in chunks (salt_*_host); the
+    interpreter runs each chunk with the same bits."""
+    n = (1 << 21) + 3
+    g = np.random.default_rng(21)
+    a, b, c = (g.uniform(-1, 1, n) for _ in range(3))
+    A, B, C = (lv.DenseVector.from_values(v, "f64", device="cpu") for v in (a, b, c))
+    D = lv.DenseVector.zeros(n, "f64", device="cpu")
+    k0 = interp.salt_interp_launch_count()
+    D.assign(1.25 * A + -0.75 * (B - C))
+    want = restate.eval_sig("S0 L0 * S1 L1 L2 - * +", [a, b, c], [1.25, -0.75], "f64")
+    assert D.to_array().tobytes() == want.tobytes()
+    r = lv.dot(A, B)
+    ex = restate.exact_sum(a * b)
+    assert abs(float(r) - ex) <= 1e-12 * abs(ex)
+    assert interp.salt_interp_launch_count() > k0
