@@ -353,3 +353,19 @@ def test_dlpack_round_trip_is_zero_copy():
     assert back[3] == 42.0
     with pytest.raises(AttributeError):
         v.__cuda_array_interface__
+
+
+def test_no_cuda_fails_loudly():
+    """Without a CUDA device the product has no path: evaluation and the
+    single-process device group raise instead of computing on the CPU."""
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("this process has a GPU")
+    x, y = hv(np.arange(8.0)), hv(np.arange(8.0))
+    with pytest.raises(RuntimeError):
+        lv.DeviceGroup([0])
+    with pytest.raises(RuntimeError):
+        lv.dot(x, y)
+    with pytest.raises(RuntimeError):
+        y.assign(as_node(x) + as_node(y))
