@@ -214,6 +214,19 @@ int salt_allreduce_sum_flags(void* out_dev_per_gpu[], int G, int dtype, void* co
 int salt_nccl_comm_init_all(int G, const int* devices, void** comms_out);
 int salt_nccl_comm_destroy(int G, void** comms);
 
+/* Batched assignments: `count` independent evaluations of ONE tree shape
+ * `sig` (single root, no device scalars) over different vectors, scalars
+ * and lengths, in ONE kernel launch per up to 96 problems (the problem table
+ * travels in the kernel parameters) — for launch-bound sizes, where a launch
+ * per tree costs more than its work.  leaves: count x nleaves pointers
+ * (problem-major); scalars: count x nscalars; ns: count lengths.  Problems
+ * must not overlap each other's destinations (they run concurrently); each
+ * result has the bits of its own salt_assign.  Trees with more than 8 leaves
+ * or 8 scalars run one launch per problem. */
+int salt_assign_batch(int dtype, const char* sig, int count, void* const* dsts,
+                      const void* const* leaves, int nleaves, const double* scalars, int nscalars,
+                      const int64_t* ns, void* stream);
+
 /* Host-buffer (end-to-end) variants: leaves / dst are HOST pointers (pinned
  * memory for full speed).  Chunks are streamed H2D -> fused kernel -> D2H
  * through `staging` (device memory, caller-owned) on three caller streams

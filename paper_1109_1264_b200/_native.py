@@ -42,6 +42,7 @@ HEADER_SYMBOLS = (
     "salt_reduce",
     "salt_assign_reduce",
     "salt_fused",
+    "salt_assign_batch",
     "salt_reduce_finish",
     "salt_assign_host",
     "salt_reduce_host",
@@ -94,6 +95,7 @@ _SIGNATURES = {
          _c_i64, _c_int, _c_vp, _c_size, _c_vp, _c_vp, _c_vp],
     ),
     "salt_reduce_finish": (_c_int, [_c_int, _c_vp, _c_int, _c_int, _c_vp, _c_vp, _c_vp]),
+    "salt_assign_batch": (_c_int, [_c_int, _c_str, _c_int, _c_vpp, _c_vpp, _c_int, _c_dp, _c_int, _c_vp, _c_vp]),
     "salt_assign_host": (
         _c_int, [_c_int, _c_str, _c_vp, _c_vpp, _c_int, _c_dp, _c_int, _c_i64, _c_vp, _c_size, _c_vpp]
     ),
@@ -214,6 +216,7 @@ def fastpath():
                     # raw C getters: CUDA is initialised once a device vector exists
                     torch._C._cuda_getCurrentRawStream, torch._C._cuda_getDevice,
                     runtime._workspace, np.float32, np.float64, runtime._lazy_out,
+                    addr(h.salt_assign_batch),
                 )
                 _fast = _fastpath
             except (ImportError, AttributeError):

@@ -20,6 +20,7 @@
 #define PY_SSIZE_T_CLEAN
 #include <Python.h>
 #include <stdint.h>
+#include <stdlib.h>
 #include <stdio.h>
 #include <string.h>
 
@@ -39,12 +40,15 @@ typedef int (*assign_reduce_fn)(int, const char*, const char*, void*, const void
 typedef int (*fused_fn)(int, const char*, const char*, void* const*, int, const void* const*, int,
                         const double*, int, const void* const*, int, int64_t, int, void*, size_t,
                         void*, void*, void*);
+typedef int (*assign_batch_fn)(int, const char*, int, void* const*, const void* const*, int,
+                               const double*, int, const int64_t*, void*);
 typedef const char* (*last_error_fn)(void);
 
 static assign_fn p_assign;
 static reduce_fn p_reduce;
 static assign_reduce_fn p_assign_reduce;
 static fused_fn p_fused;
+static assign_batch_fn p_assign_batch;
 static last_error_fn p_last_error;
 static size_t ws_bytes;
 
@@ -510,13 +514,173 @@ static PyObject* fp_op(PyObject* self, PyObject* args) {
   return launch_reduce(&w, NULL, NULL, 0, flags, lazy, ws, slot, stream);
 }
 
+/* ---- assign_batch(statements): lv.assign_batch's common case in C.
+ * Every statement (dest, source) must be eligible for fp_assign (plain
+ * device vectors on the current device, no device scalars); statements are
+ * grouped by (element type, signature) and each group is ONE
+ * salt_assign_batch call.  A destination used by another statement (as its
+ * destination or a leaf) makes the whole batch ineligible, so the Python
+ * path raises the error.  Returns the statement count, or None. */
+typedef struct {
+  int code, nl, nsc;
+  char* sig;
+  Py_ssize_t count, cap;
+  void** dsts;
+  void** leaves;   /* count x nl */
+  double* sc;      /* count x nsc */
+  int64_t* ns;
+} Group;
+
+static int ptr_cmp(const void* a, const void* b) {
+  uintptr_t x = *(const uintptr_t*)a, y = *(const uintptr_t*)b;
+  return x < y ? -1 : x > y;
+}
+
+static int group_push(Group* g, void* dptr, const Walk* w) {
+  if (g->count == g->cap) {
+    Py_ssize_t cap = g->cap ? 2 * g->cap : 16;
+    void** d = PyMem_Realloc(g->dsts, cap * sizeof(void*));
+    if (d) g->dsts = d;
+    void** l = PyMem_Realloc(g->leaves, cap * (g->nl ? g->nl : 1) * sizeof(void*));
+    if (l) g->leaves = l;
+    double* c = PyMem_Realloc(g->sc, cap * (g->nsc ? g->nsc : 1) * sizeof(double));
+    if (c) g->sc = c;
+    int64_t* n = PyMem_Realloc(g->ns, cap * sizeof(int64_t));
+    if (n) g->ns = n;
+    if (!d || !l || !c || !n) { PyErr_NoMemory(); return -1; }
+    g->cap = cap;
+  }
+  g->dsts[g->count] = dptr;
+  for (int k = 0; k < g->nl; ++k) g->leaves[g->count * g->nl + k] = w->ptrs[k];
+  for (int k = 0; k < g->nsc; ++k) g->sc[g->count * g->nsc + k] = w->sc[k];
+  g->ns[g->count] = (int64_t)w->n;
+  ++g->count;
+  return 1;
+}
+
+static void groups_free(Group* gs, int ng) {
+  for (int i = 0; i < ng; ++i) {
+    PyMem_Free(gs[i].sig);
+    PyMem_Free(gs[i].dsts);
+    PyMem_Free(gs[i].leaves);
+    PyMem_Free(gs[i].sc);
+    PyMem_Free(gs[i].ns);
+  }
+  PyMem_Free(gs);
+}
+
+static PyObject* fp_assign_batch(PyObject* self, PyObject* args) {
+  PyObject* list;
+  if (!PyArg_ParseTuple(args, "O!", &PyList_Type, &list)) return NULL;
+  if (!p_assign_batch) Py_RETURN_NONE;
+  const Py_ssize_t m = PyList_GET_SIZE(list);
+  if (m == 0) return PyLong_FromLong(0);
+  Group* gs = NULL;
+  int ng = 0, capg = 0, dev = -1;
+  uintptr_t* dests = PyMem_Malloc(m * sizeof(uintptr_t));
+  if (!dests) return PyErr_NoMemory();
+  PyObject* result = NULL;
+  int eligible = 1;
+  Py_ssize_t empties = 0;
+  Walk w;
+  /* pass 1: walk every statement, collect destinations */
+  for (Py_ssize_t i = 0; i < m && eligible; ++i) {
+    PyObject* st = PyList_GET_ITEM(list, i);
+    if (!PyTuple_Check(st) || PyTuple_GET_SIZE(st) != 2) { eligible = 0; break; }
+    void* dptr;
+    int rc = start(&w, PyTuple_GET_ITEM(st, 0), &dptr);
+    if (rc > 0) rc = walk(&w, PyTuple_GET_ITEM(st, 1));
+    if (rc < 0) goto done;
+    if (rc == 0 || w.nps || w.nvec == 0 || (dev >= 0 && w.dev != dev)) { eligible = 0; break; }
+    dev = w.dev;
+    dests[i] = w.n ? (uintptr_t)dptr : 0; /* empty statements write nothing */
+  }
+  if (eligible) {  /* no destination shared with another statement */
+    uintptr_t* sorted = PyMem_Malloc(m * sizeof(uintptr_t));
+    if (!sorted) { PyErr_NoMemory(); goto done; }
+    memcpy(sorted, dests, m * sizeof(uintptr_t));
+    qsort(sorted, (size_t)m, sizeof(uintptr_t), ptr_cmp);
+    for (Py_ssize_t i = 1; i < m; ++i)
+      if (sorted[i] && sorted[i] == sorted[i - 1]) eligible = 0;
+    /* pass 2: leaves vs other statements' destinations, and grouping */
+    for (Py_ssize_t i = 0; i < m && eligible; ++i) {
+      PyObject* st = PyList_GET_ITEM(list, i);
+      void* dptr;
+      int rc = start(&w, PyTuple_GET_ITEM(st, 0), &dptr);
+      if (rc > 0) rc = walk(&w, PyTuple_GET_ITEM(st, 1));
+      if (rc <= 0) { eligible = 0; if (rc < 0) { PyMem_Free(sorted); goto done; } break; }
+      for (int k = 0; k < w.nvec && eligible; ++k) {
+        uintptr_t p = (uintptr_t)w.ptrs[k];
+        if (p != dests[i] && w.n > 0 &&
+            bsearch(&p, sorted, (size_t)m, sizeof(uintptr_t), ptr_cmp))
+          eligible = 0;
+      }
+      if (!eligible) continue;
+      if (w.n == 0) { ++empties; continue; }
+      int gi = 0;
+      for (; gi < ng; ++gi)
+        if (gs[gi].code == w.code && gs[gi].nl == w.nvec && gs[gi].nsc == w.nsc &&
+            strcmp(gs[gi].sig, w.sig) == 0)
+          break;
+      if (gi == ng) {
+        if (ng == capg) {
+          int cap = capg ? 2 * capg : 4;
+          Group* n = PyMem_Realloc(gs, cap * sizeof(Group));
+          if (!n) { PyErr_NoMemory(); PyMem_Free(sorted); goto done; }
+          gs = n;
+          capg = cap;
+        }
+        memset(&gs[ng], 0, sizeof(Group));
+        gs[ng].code = w.code;
+        gs[ng].nl = w.nvec;
+        gs[ng].nsc = w.nsc;
+        gs[ng].sig = PyMem_Malloc((size_t)w.len + 1);
+        if (!gs[ng].sig) { PyErr_NoMemory(); PyMem_Free(sorted); goto done; }
+        memcpy(gs[ng].sig, w.sig, (size_t)w.len + 1);
+        ++ng;
+      }
+      if (group_push(&gs[gi], dptr, &w) < 0) { PyMem_Free(sorted); goto done; }
+    }
+    PyMem_Free(sorted);
+  }
+  if (!eligible) {
+    Py_INCREF(Py_None);
+    result = Py_None;
+    goto done;
+  }
+  {
+    void* stream;
+    w.dev = dev;
+    int rc = stream_for(&w, &stream);
+    if (rc < 0) goto done;
+    if (rc == 0) { Py_INCREF(Py_None); result = Py_None; goto done; }
+    Py_ssize_t launched = empties;
+    for (int gi = 0; gi < ng; ++gi) {
+      Group* g = &gs[gi];
+      int e = p_assign_batch(g->code, g->sig, (int)g->count, g->dsts, (const void* const*)g->leaves,
+                             g->nl, g->sc, g->nsc, g->ns, stream);
+      if (e != 0) {
+        PyErr_Format(PyExc_RuntimeError, "libsalt error %d: %s", e, p_last_error());
+        goto done;
+      }
+      launched += g->count;
+    }
+    result = PyLong_FromSsize_t(launched);
+  }
+done:
+  PyMem_Free(dests);
+  groups_free(gs, ng);
+  return result;
+}
+
 static PyObject* fp_init(PyObject* self, PyObject* args) {
-  unsigned long long a, r, ar, fu, le;
+  unsigned long long a, r, ar, fu, le, ab;
   Py_ssize_t wsb;
-  if (!PyArg_ParseTuple(args, "KKKKKnOOOOOOOOOOOOO", &a, &r, &ar, &fu, &le, &wsb, &T_Leaf, &T_Add,
+  if (!PyArg_ParseTuple(args, "KKKKKnOOOOOOOOOOOOOK", &a, &r, &ar, &fu, &le, &wsb, &T_Leaf, &T_Add,
                         &T_Sub, &T_Mul, &T_Scale, &T_Dense, &T_DevScalar, &get_stream,
-                        &current_device, &workspace_fn, &np_f32, &np_f64, &lazy_out))
+                        &current_device, &workspace_fn, &np_f32, &np_f64, &lazy_out, &ab))
     return NULL;
+  p_assign_batch = (assign_batch_fn)(uintptr_t)ab;
   PyObject* keep[] = {T_Leaf, T_Add, T_Sub, T_Mul, T_Scale, T_Dense, T_DevScalar, get_stream,
                       current_device, workspace_fn, np_f32, np_f64, lazy_out};
   for (size_t i = 0; i < sizeof keep / sizeof keep[0]; ++i) Py_INCREF(keep[i]);
@@ -537,6 +701,8 @@ static PyMethodDef methods[] = {
      "assign_reduce(dest, source, child, flags, lazy=False) -> scalar or None"},
     {"op", fp_op, METH_VARARGS,
      "op(sig, dest_or_None, leaves, alpha_or_None, flags, lazy=False) -> True / result, or None"},
+    {"assign_batch", fp_assign_batch, METH_VARARGS,
+     "assign_batch([(dest, source), ...]) -> statements launched, or None"},
     {"fused", fp_fused, METH_VARARGS,
      "fused(((dest, source), ...), total_child_or_None, flags, lazy=False) -> (result,) or None"},
     {NULL, NULL, 0, NULL}};

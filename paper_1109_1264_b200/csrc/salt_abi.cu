@@ -434,9 +434,29 @@ void reg_one(const char* asig, const char* rsig) {
   table()[key_of(dtype_of<T>(), MODE, 1, ta, tr)] = std::move(k2);
 }
 
+// Batch kernels (salt_assign_batch) of a single-root assignment tree.
+constexpr int kBatchKind = 3;  // table key "mode" of batch kernels
+template <class T, class EA> void reg_batch_one(const char* asig) {
+  Sig sa;
+  parse_assign(asig, sa);
+  constexpr int V = vec_of<T>();
+  constexpr int U = unroll_for(salt::MODE_ASSIGN, EA::NL, (int)sizeof(T));
+  auto k = std::make_unique<Kernel>();
+  k->aot = (const void*)&salt::batch_kernel<T, EA, V, U, kBlock>;
+  k->vec = V;
+  k->unroll = U;
+  table()[key_of(dtype_of<T>(), kBatchKind, V, sa.type, "batch")] = std::move(k);
+}
+
 template <class EA, class ER, int MODE> void reg(const char* asig, const char* rsig) {
   reg_one<float, EA, ER, MODE>(asig, rsig);
   reg_one<double, EA, ER, MODE>(asig, rsig);
+  if constexpr (MODE == salt::MODE_ASSIGN) {
+    if constexpr (EA::NL <= salt::BATCH_LEAVES && EA::NS <= salt::BATCH_SCALARS) {
+      reg_batch_one<float, EA>(asig);
+      reg_batch_one<double, EA>(asig);
+    }
+  }
 }
 
 using namespace salt;
@@ -535,12 +555,16 @@ std::unique_ptr<Kernel> jit_build(int dtype, int mode, int vec, int nl, const st
   Nvrtc& nv = nvrtc();
   if (!nv.ok) { g_err = "NVRTC unavailable: " + nv.why; return nullptr; }
   const char* tname = dtype == SALT_F32 ? "float" : "double";
+  const bool batch = mode == kBatchKind;
   const int unroll = vec == 1 ? kUnrollScalar
                      : tuning_unroll() > 0 ? tuning_unroll()
-                                             : unroll_for(mode, nl, dtype == SALT_F32 ? 4 : 8);
-  std::string expr = std::string("salt::fused_kernel<") + tname + "," + ta + "," + tr + "," +
-                     std::to_string(mode) + "," + std::to_string(vec) + "," +
-                     std::to_string(unroll) + "," + std::to_string(kBlock) + ">";
+                     : unroll_for(batch ? salt::MODE_ASSIGN : mode, nl, dtype == SALT_F32 ? 4 : 8);
+  std::string expr =
+      batch ? std::string("salt::batch_kernel<") + tname + "," + ta + "," + std::to_string(vec) + "," +
+                  std::to_string(unroll) + "," + std::to_string(kBlock) + ">"
+            : std::string("salt::fused_kernel<") + tname + "," + ta + "," + tr + "," +
+                  std::to_string(mode) + "," + std::to_string(vec) + "," + std::to_string(unroll) +
+                  "," + std::to_string(kBlock) + ">";
   const std::string minb = "-DSALT_MIN_BLOCKS=" + std::to_string(tuning_minb());
   const char* opts[8] = {"--gpu-architecture=sm_100a", "-fmad=false", "--std=c++17",
                          "-lineinfo", "-default-device"};
@@ -1249,6 +1273,87 @@ int dispatch(int dtype, Plan& p, void* const* dsts, int ndst, const void* const*
                            ws_bytes, out_dev, out_host, st, x, pscalars, npscalars);
 }
 
+// Batched assignments: problem table in the kernel parameters, up to
+// BATCH_MAX problems (and < 2^31 tiles) per launch; trees beyond the batch
+// limits, or without a kernel (no JIT), run one launch per problem.
+template <class T>
+int run_batch(Plan& p, int count, void* const* dsts, const void* const* leaves, int nleaves,
+              const double* scalars, int nscalars, const int64_t* ns, cudaStream_t st) {
+  if (count < 0 || (count > 0 && (!dsts || !ns || (nleaves > 0 && !leaves))))
+    return fail(SALT_EINVAL, "bad batch arguments");
+  for (int q = 0; q < count; ++q) {
+    if (ns[q] < 0) return fail(SALT_EINVAL, "negative length");
+    if (ns[q] == 0) continue;
+    if (!dsts[q]) return fail(SALT_EINVAL, "NULL destination");
+    for (int l = 0; l < p.nl; ++l)
+      if (!leaves[(size_t)q * nleaves + l]) return fail(SALT_EINVAL, "NULL leaf pointer");
+  }
+  Kernel* k = nullptr;
+  const bool batchable = p.sa.nroots == 1 && p.np == 0 && p.nl <= salt::BATCH_LEAVES &&
+                         p.ns <= salt::BATCH_SCALARS;
+  if (batchable) k = get_kernel(dtype_of<T>(), kBatchKind, vec_of<T>(), p.nl, p.sa.type, "batch");
+  if (!k) {  // one fused launch per problem (table, JIT or interpreter kernel)
+    for (int q = 0; q < count; ++q) {
+      if (ns[q] == 0) continue;
+      void* d = dsts[q];
+      int rc = run_fused<T>(p, &d, 1, leaves + (size_t)q * nleaves, nleaves, scalars + (size_t)q * nscalars,
+                            nscalars, ns[q], 0, nullptr, 0, nullptr, nullptr, st, nullptr, nullptr, 0);
+      if (rc) return rc;
+    }
+    return 0;
+  }
+  int dev;
+  int rc = current_device(dev);
+  if (rc) return rc;
+  rc = prepare(k, dev);
+  if (rc) return rc;
+  constexpr int V = vec_of<T>();
+  const i64 per_tile = (i64)kBlock * k->unroll;
+  auto args = std::make_unique<salt::BatchArgs<T>>();  // ~17 KB: not on the stack
+  auto flush = [&]() -> int {
+    if (args->count == 0) return 0;
+    const salt::BatchProblem<T>& last = args->p[args->count - 1];
+    const i64 tiles = last.tile0 + last.nst + (last.nvec + per_tile - 1) / per_tile;
+    int r = launch_raw(k, dev, (int)tiles, args.get(), 0, st);
+    args->count = 0;
+    return r;
+  };
+  memset(args.get(), 0, sizeof(salt::BatchArgs<T>));
+  i64 tile = 0;
+  for (int q = 0; q < count; ++q) {
+    const i64 n = ns[q];
+    if (n == 0) continue;
+    const void* const* lq = leaves + (size_t)q * nleaves;
+    void* dq = dsts[q];
+    int vec;
+    i64 head, nvec;
+    geometry<T>(&dq, 1, lq, p.nl, n, vec, head, nvec);
+    if (vec == 1) {  // operands not sharing one 32-byte alignment: all scalar
+      head = n;
+      nvec = 0;
+    }
+    const i64 nscalar = head + (n - head - nvec * V);
+    const i64 nst = (nscalar + kBlock - 1) / kBlock;
+    const i64 ntiles = nst + (nvec + per_tile - 1) / per_tile;
+    if (args->count == salt::BATCH_MAX || (args->count > 0 && tile + ntiles > i64(0x7fffffff))) {
+      if ((rc = flush())) return rc;
+      tile = 0;
+    }
+    if (ntiles > i64(0x7fffffff)) return fail(SALT_EINVAL, "batch problem too large for one launch");
+    salt::BatchProblem<T>& P = args->p[args->count++];
+    P.dst = (T*)dq;
+    for (int l = 0; l < p.nl; ++l) P.leaf[l] = (const T*)lq[l];
+    for (int c = 0; c < p.ns; ++c) P.sc[c] = (T)scalars[(size_t)q * nscalars + c];
+    P.n = n;
+    P.head = head;
+    P.nvec = nvec;
+    P.tile0 = tile;
+    P.nst = nst;
+    tile += ntiles;
+  }
+  return flush();
+}
+
 template <class T>
 int finish(const void* parts, int count, int flags, void* out_dev, void* out_host,
            cudaStream_t st) {
@@ -1660,6 +1765,17 @@ int salt_reduce_finish(int dtype, const void* partials_dev, int count, int flags
   if (dtype == SALT_F64)
     return finish<double>(partials_dev, count, flags, out_dev, out_host, (cudaStream_t)stream);
   return fail(SALT_EINVAL, "dtype must be SALT_F32 or SALT_F64");
+}
+
+int salt_assign_batch(int dtype, const char* sig, int count, void* const* dsts,
+                      const void* const* leaves, int nleaves, const double* scalars, int nscalars,
+                      const int64_t* ns, void* stream) {
+  Plan* p;
+  int rc = make_plan(dtype, sig, nullptr, salt::MODE_ASSIGN, nleaves, nscalars, p);
+  if (rc) return rc;
+  if (dtype == SALT_F32)
+    return run_batch<float>(*p, count, dsts, leaves, nleaves, scalars, nscalars, ns, (cudaStream_t)stream);
+  return run_batch<double>(*p, count, dsts, leaves, nleaves, scalars, nscalars, ns, (cudaStream_t)stream);
 }
 
 int salt_assign_host(int dtype, const char* sig, void* host_dst, const void* const* host_leaves,

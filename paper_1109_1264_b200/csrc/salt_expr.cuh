@@ -672,6 +672,82 @@ __global__ void SALT_BOUNDS(BLOCK) fused_kernel(Args<T> a) {
   if (REDUCE) reduce_epilogue<T, BLOCK>(acc.get(), a);
 }
 
+// ---------------------------------------------------------------- batches
+// Many independent assignments of ONE tree shape (different vectors,
+// scalars and lengths) in ONE launch — for launch-bound sizes, where a
+// launch per tree costs more than its work.  The problem table travels in
+// the kernel parameters (CUDA >= 12.1 allows 32 KiB).  Problem q owns the
+// global tiles [tile0, tile0 + nst + vector tiles): its first nst tiles are
+// its head / tail elements (BLOCK per tile, scalar; all of it when its
+// operands do not share one 32-byte alignment), the rest BLOCK*UNR-vector
+// tiles exactly as in fused_kernel.  Same arithmetic per element, so the
+// same bits as one fused_kernel launch per problem.
+enum { BATCH_MAX = 96, BATCH_LEAVES = 8, BATCH_SCALARS = 8 };
+template <class T> struct BatchProblem {
+  T* dst;
+  const T* leaf[BATCH_LEAVES];
+  T sc[BATCH_SCALARS];
+  i64 n, head, nvec;  // as Args
+  i64 tile0;          // first global tile
+  i64 nst;            // scalar tiles
+};
+template <class T> struct BatchArgs {
+  int count;
+  BatchProblem<T> p[BATCH_MAX];
+};
+
+template <class T, class EA, int V, int UNR, int BLOCK>
+__global__ void SALT_BOUNDS(BLOCK) batch_kernel(BatchArgs<T> a) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // see fused_kernel
+  constexpr int NL = EA::NL, NS = EA::NS;
+  static_assert(NL <= BATCH_LEAVES && NS <= BATCH_SCALARS && EA::NP == 0, "batch tree limits");
+  typedef Env<T, NL, NS, 0, 1, V> E1;
+  typedef Env<T, NL, NS, 0, 1, 1> ES;
+  int lo = 0, hi = a.count - 1;  // the problem owning this CTA: last tile0 <= blockIdx.x
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (a.p[mid].tile0 <= (i64)blockIdx.x) lo = mid;
+    else hi = mid - 1;
+  }
+  const BatchProblem<T>& P = a.p[lo];
+  T* const dst[1] = {P.dst};
+  const i64 local = (i64)blockIdx.x - P.tile0;
+  if (local < P.nst) {  // head / tail elements of this problem
+    const i64 tail0 = P.head + P.nvec * V;
+    const i64 nscalar = P.head + (P.n - tail0);
+    const i64 t = local * BLOCK + threadIdx.x;
+    if (t < nscalar) {
+      const i64 i = t < P.head ? t : tail0 + (t - P.head);
+      ES e;
+#pragma unroll
+      for (int l = 0; l < NL; ++l) e.x[l][0] = P.leaf[l][i];
+#pragma unroll
+      for (int s = 0; s < NS; ++s) e.s[s] = P.sc[s];
+      AssignRoots<EA, 0, 1>::template one<T>(e, dst, i);
+    }
+    return;
+  }
+  const i64 base = (local - P.nst) * BLOCK * UNR + threadIdx.x;
+  E1 e[UNR];
+#pragma unroll
+  for (int u = 0; u < UNR; ++u) {
+    const i64 j = base + (i64)u * BLOCK;
+    if (j < P.nvec) {
+#pragma unroll
+      for (int l = 0; l < NL; ++l) VecIO<T, V>::load(e[u].x[l], P.leaf[l] + P.head + j * V);
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < UNR; ++u) {
+    const i64 j = base + (i64)u * BLOCK;
+    if (j < P.nvec) {
+#pragma unroll
+      for (int s = 0; s < NS; ++s) e[u].s[s] = P.sc[s];
+      AssignRoots<EA, 0, 1>::template vec<T>(e[u], dst, P.head + j * V);
+    }
+  }
+}
+
 // Combine `count` partials (all-gathered per-device DD values, rank order).
 // Up to XCHG_MAX_RANKS partials are folded sequentially in rank order — the
 // same arithmetic as exchange_dd, so the NCCL all-gather path and the NVLink

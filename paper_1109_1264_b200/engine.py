@@ -34,6 +34,7 @@ from .expressions import (
     Leaf,
     ScaleNode,
     SumNode,
+    as_node,
     common_length,
     lower,
 )
@@ -259,6 +260,41 @@ def _reduce(root: SumNode, length: int, flags: int = 0, lazy: bool = False):
     if not _fits(lw):
         lw = lower(_fit(root.child, length))
     return runtime.run_reduce(lw, root.dtype, length, flags=flags, lazy=lazy)
+
+
+def _check_assign_batch(statements) -> list:
+    """Validate a batch of independent assignments (ops.assign_batch) as
+    execute_assign would, all before anything runs; returns [(lowering,
+    dest, dtype, length)].  A destination may alias its own statement's
+    leaves but no other statement's operands (identity or same storage)."""
+    items, dest_owner, users = [], {}, []
+    for k, st in enumerate(statements):
+        if not (isinstance(st, tuple) and len(st) == 2):
+            raise TypeError("assign_batch takes (dest, expression) pairs")
+        root = AssignNode(as_node(st[0]), as_node(st[1]))
+        length = common_length(root)
+        lw = lower(root.source)
+        if not _fits(lw):
+            lw = lower(_fit(root.source, length))
+        dest = root.dest.vector
+        items.append((lw, dest, root.dtype, length))
+        dest_owner.setdefault(_storage_key(dest), k)
+        if dest_owner[_storage_key(dest)] != k:
+            raise ValueError(f"assign_batch: statements {dest_owner[_storage_key(dest)]} and {k} "
+                             "write the same destination")
+        users.append({_storage_key(v) for v in lw.vectors})
+    for k, keys in enumerate(users):
+        for key in keys:
+            owner = dest_owner.get(key)
+            if owner is not None and owner != k:
+                raise ValueError(f"assign_batch: statement {k} reads the destination of statement {owner} "
+                                 "(statements of a batch run concurrently)")
+    return items
+
+
+def _storage_key(v):
+    t = getattr(v, "_data", None)
+    return ("ptr", t.get_device(), t.data_ptr()) if t is not None and t.numel() else ("id", id(v))
 
 
 def execute_assign(root, plan: UnrollPlan = None, *, backend: LaneBackend = None,

@@ -27,7 +27,7 @@ from .expressions import (
     as_node,
 )
 
-__all__ = ["dot", "scal", "axpy", "scaled_copy", "sum", "norm2", "axpy_dot", "fused"]
+__all__ = ["dot", "scal", "axpy", "scaled_copy", "sum", "norm2", "axpy_dot", "fused", "assign_batch"]
 
 
 def _op(sig, dest, leaves, alpha=None, flags=0, lazy=False):
@@ -125,3 +125,28 @@ def fused(*statements, lazy=False):
         else:
             raise TypeError("only the last statement may be a bare expression (the sum)")
     return execute_fused(FusedNode(assigns, total), lazy=lazy)
+
+
+def assign_batch(statements) -> int:
+    """Evaluate many INDEPENDENT assignments `(dest, expression)` at once.
+    Statements whose operands are device vectors and share a tree shape and
+    element type run as ONE kernel launch per up to 96 of them
+    (salt_assign_batch) — for launch-bound sizes, where one launch per tree
+    costs more than the work; each result has the bits of its own
+    `dest.assign(expression)`.  Every statement is validated like `assign`
+    (dtype, lengths) before anything runs.  A destination may alias its own
+    statement's operands (as in axpy) but must not be used by any other
+    statement of the batch (ValueError): the statements run concurrently.
+    Returns how many statements went through a batched launch."""
+    statements = list(statements)
+    fast = _native.fastpath()
+    if fast is not None:
+        r = fast.assign_batch(statements)  # C: walk, check, group, launch
+        if r is not None:
+            return r
+    from .engine import _check_assign_batch
+
+    items = _check_assign_batch(statements)
+    from .runtime import run_assign_batch
+
+    return run_assign_batch(items)

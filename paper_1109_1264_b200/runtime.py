@@ -22,6 +22,7 @@ local block of a ShardedVector, or — for any other duck-typed vector
 read_block/write_block protocol.
 """
 
+import array
 import ctypes
 import threading
 
@@ -32,7 +33,7 @@ from . import _native
 from .lanes import as_dtype
 from .vectors import DenseVector, DeviceScalar
 
-__all__ = ["run_assign", "run_reduce", "run_assign_reduce", "run_fused", "Placement"]
+__all__ = ["run_assign", "run_reduce", "run_assign_reduce", "run_fused", "run_assign_batch", "Placement"]
 
 _ws_lock = threading.Lock()
 _workspaces = {}
@@ -300,6 +301,37 @@ def run_assign(lw, dest, dtype, n):
                                           _raw_stream(pl.device.index)))
     pl.finish()
     _record_counts(lw, dest, n)
+
+
+def run_assign_batch(items):
+    """items: [(lowering, dest, dtype, n)] of validated assignments.  Those
+    whose operands are plain device DenseVectors are grouped by (device,
+    element type, signature) and each group goes to salt_assign_batch (one
+    launch per up to 96 problems); the rest run one by one.  Returns the
+    number of statements that went through a batch."""
+    groups, rest = {}, []
+    for lw, dest, dtype, n in items:
+        fast = None if lw.pscalars else _fast(lw.vectors, dest)
+        if fast is None:
+            rest.append((lw, dest, dtype, n))
+            continue
+        dev, ptrs, dptr = fast
+        key = (dev, _dtype_code(dtype), " ".join(lw.tokens), len(lw.vectors), len(lw.scalars))
+        groups.setdefault(key, []).append((ptrs, dptr, lw.scalars, n))
+    lib = _native.lib()
+    batched = 0
+    for (dev, code, sig, nl, ns), probs in groups.items():
+        leaves, k1 = _native.ptr_array([p for ptrs, _, _, _ in probs for p in ptrs])
+        dsts, k2 = _native.ptr_array([d for _, d, _, _ in probs])
+        scal, k3 = _native.double_array([c for _, _, sc, _ in probs for c in sc])
+        lens = array.array("q", [n for _, _, _, n in probs])
+        with _OnDevice(dev):
+            _native.check(lib.salt_assign_batch(code, sig.encode(), len(probs), dsts, leaves, nl, scal, ns,
+                                                lens.buffer_info()[0], _raw_stream(dev)))
+        batched += len(probs)
+    for lw, dest, dtype, n in rest:
+        run_assign(lw, dest, dtype, n)
+    return batched
 
 
 # ---------------------------------------------------------------- reduce
