@@ -12,10 +12,14 @@ sharded steps at a small length with the same steps on one device.  Device
 time is the max over devices between a barrier of events.
 """
 
+import os
 import argparse
 import json
 import sys
 from pathlib import Path
+# steady-state measurements: build out-of-table trees with NVRTC on first use
+# instead of running them on the interpreter meanwhile (tiered JIT)
+os.environ.setdefault("SALT_JIT_ASYNC", "0")
 
 import numpy as np
 import torch

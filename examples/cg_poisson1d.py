@@ -15,10 +15,14 @@ axpy -> dot step is the building block of.
     python examples/cg_poisson1d.py --n 1048576 --iters 200
 """
 
+import os
 import argparse
 import sys
 import time
 from pathlib import Path
+# steady-state measurements: build out-of-table trees with NVRTC on first use
+# instead of running them on the interpreter meanwhile (tiered JIT)
+os.environ.setdefault("SALT_JIT_ASYNC", "0")
 
 import numpy as np
 import torch

@@ -273,11 +273,13 @@ void salt_set_force_jit(int on);
  * without NVRTC).  salt_interp_launch_count() counts its launches. */
 void salt_set_force_interp(int on);
 uint64_t salt_interp_launch_count(void);
-/* Tiered JIT (default on; SALT_JIT_ASYNC=0 or salt_set_jit_async(0) turns it
- * off): a tree outside the compiled-in table and the JIT disk cache runs on
- * the interpreter kernel — same bits — while a background thread compiles it
- * with NVRTC; later calls use the compiled kernel.  salt_jit_wait() blocks
- * until no compile is queued or running and returns how many failed. */
+/* Tiered JIT (opt-in: SALT_JIT_ASYNC=1 or salt_set_jit_async(1); default
+ * off — fresh trees are built synchronously on first use and no background
+ * thread exists): a tree outside the compiled-in table and the JIT disk
+ * cache runs on the interpreter kernel — same bits — while a background
+ * thread compiles it with NVRTC; later calls use the compiled kernel.
+ * salt_jit_wait() blocks until no compile is queued or running and returns
+ * how many failed. */
 void salt_set_jit_async(int on);
 int salt_jit_wait(void);
 

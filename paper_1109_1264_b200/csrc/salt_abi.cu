@@ -634,9 +634,9 @@ Kernel* jit_insert(const std::string& key, std::unique_ptr<Kernel> k) {
 
 // ---- tiered JIT: a tree outside the compiled-in table runs on the
 // interpreter (same bits, salt_interp.cuh) while a background thread
-// compiles it with NVRTC; later calls find the compiled kernel.  No call
-// waits ~0.4 s for NVRTC.  SALT_JIT_ASYNC=0 / salt_set_jit_async(0) compile
-// synchronously instead.
+// compiles it with NVRTC; later calls find the compiled kernel, so no call
+// waits for NVRTC.  Opt-in (SALT_JIT_ASYNC=1 / salt_set_jit_async(1)): by
+// default fresh trees are built synchronously and no thread is started.
 struct JitJob {
   int dtype, mode, vec, nl;
   std::string ta, tr, key;
@@ -658,8 +658,8 @@ std::atomic<int> g_jit_async{-1};  // -1: not yet read from SALT_JIT_ASYNC
 bool jit_async() {
   int v = g_jit_async.load(std::memory_order_relaxed);
   if (v < 0) {
-    const char* e = getenv("SALT_JIT_ASYNC");
-    v = e && atoi(e) == 0 ? 0 : 1;
+    const char* e = getenv("SALT_JIT_ASYNC");  // opt-in
+    v = e && atoi(e) != 0 ? 1 : 0;
     g_jit_async.store(v);
   }
   return v == 1;
@@ -671,8 +671,9 @@ void jit_worker() {
     JitJob j;
     {
       std::unique_lock<std::mutex> lk(A.mu);
-      A.cv.wait(lk, [&] { return !A.queue.empty() || A.stopping; });
-      if (A.stopping) return;
+      // never woken once the process exits (see jit_atexit): a thread
+      // returning while exit() tears down the C++ runtime can crash it
+      A.cv.wait(lk, [&] { return !A.queue.empty() && !A.stopping; });
       j = std::move(A.queue.front());
       A.queue.pop_front();
       ++A.active;
@@ -691,15 +692,17 @@ void jit_worker() {
   }
 }
 
-// At exit: let a compile in flight finish (NVRTC must not run while the
-// process tears its libraries down), then stop the worker.
+// At exit: drop queued builds and let a compile in flight finish (NVRTC
+// must not run while the process tears its libraries down).  The worker is
+// then left blocked on its condition variable — it is never woken again, so
+// it cannot run any code while exit() destroys the runtime.
 void jit_atexit() {
   AsyncJit& A = async_jit();
   std::unique_lock<std::mutex> lk(A.mu);
-  A.queue.clear();
-  A.idle.wait_for(lk, std::chrono::seconds(10), [&] { return A.active == 0; });
   A.stopping = true;
-  A.cv.notify_all();
+  A.queue.clear();
+  A.pending.clear();
+  A.idle.wait_for(lk, std::chrono::seconds(10), [&] { return A.active == 0; });
 }
 
 // Queue a background build; false if it failed before (g_err = why).
@@ -711,6 +714,7 @@ bool jit_enqueue(JitJob j) {
     return false;
   }
   if (A.pending.count(j.key)) return true;
+  if (A.stopping) return false;
   if (!A.started) {
     A.started = true;
     std::thread(jit_worker).detach();
@@ -1132,7 +1136,12 @@ int run_fused(Plan& p, void* const* dsts, int ndst, const void* const* leaves, i
     if (!slot) {
       // tiered: trees the interpreter can run do not wait for NVRTC (unless
       // the JIT itself is being tested: salt_set_force_jit)
-      const bool async = p.prog_ok && jit_async() && !g_force_jit.load(std::memory_order_relaxed);
+      // ... nor while the stream is being captured into a CUDA graph: the
+      // graph would keep the interpreter kernel for good
+      cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+      if (cudaStreamIsCapturing(st, &cap) != cudaSuccess) cudaGetLastError();
+      const bool async = p.prog_ok && jit_async() && !g_force_jit.load(std::memory_order_relaxed) &&
+                         cap == cudaStreamCaptureStatusNone;
       bool queued = false;
       slot = get_kernel(dtype_of<T>(), p.mode, vec, p.nl, p.sa.type, p.sr.type, async, &queued);
     }

@@ -27,7 +27,8 @@ from .expressions import (
     as_node,
 )
 
-__all__ = ["dot", "scal", "axpy", "scaled_copy", "sum", "norm2", "axpy_dot", "fused", "assign_batch"]
+__all__ = ["dot", "scal", "axpy", "scaled_copy", "sum", "norm2", "axpy_dot", "fused", "assign_batch",
+           "jit_wait"]
 
 
 def _op(sig, dest, leaves, alpha=None, flags=0, lazy=False):
@@ -150,3 +151,12 @@ def assign_batch(statements) -> int:
     from .runtime import run_assign_batch
 
     return run_assign_batch(items)
+
+
+def jit_wait() -> None:
+    """Block until every background NVRTC build has finished (trees outside
+    the compiled-in table run on the bit-identical interpreter kernel until
+    their build is done).  Call it after warming up, before timing."""
+    failed = _native.lib().salt_jit_wait()
+    if failed:
+        raise RuntimeError(f"{failed} background JIT build(s) failed; those trees stay on the interpreter")

@@ -21,6 +21,7 @@ MEASURED = {  # GB/s at 2^28 on one B200 (round 1)
 def best_time(fn, reps=10):
     for _ in range(3):
         fn()
+    lv.jit_wait()  # out-of-table trees (device-scalar CG update): time the compiled kernel
     best = float("inf")
     for _ in range(reps):
         torch.cuda._sleep(100_000)

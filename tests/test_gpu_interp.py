@@ -206,8 +206,7 @@ assert lib.salt_interp_launch_count() == k1       # compiled kernels now
 assert E.to_array().tobytes() == e1.tobytes() and r1.tobytes() == r2.tobytes()
 print("ok first_ms=%.1f" % first_ms)
 """
-    env = dict(os.environ, SALT_JIT_CACHE="off", PYTHONPATH=f"{ROOT}:{ROOT / 'tests'}")
-    env.pop("SALT_JIT_ASYNC", None)
+    env = dict(os.environ, SALT_JIT_CACHE="off", SALT_JIT_ASYNC="1", PYTHONPATH=f"{ROOT}:{ROOT / 'tests'}")
     out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
                          cwd=ROOT, timeout=300)
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-3000:]
@@ -217,47 +216,44 @@ print("ok first_ms=%.1f" % first_ms)
 
 def test_tiered_jit_under_concurrent_threads():
     """Eight host threads evaluate fresh trees while the background JIT
-    compiles them: every result has the reference's bits, before and after
-    the compiled kernels take over."""
-    import threading
-
-    import torch
-
-    n = 50_003
-    g = np.random.default_rng(77)
-    host = [g.uniform(-1, 1, n) for _ in range(4)]
-    vecs = [lv.DenseVector.from_values(h, "f64") for h in host]
-    trees = []
-    for t in range(8):
+    compiles them (tiered JIT on, in a child process): every result has the
+    reference's bits, before and after the compiled kernels take over."""
+    code = r"""
+import threading, numpy as np, torch, paper_1109_1264_b200 as lv
+from paper_1109_1264_b200.expressions import as_node
+from oracle import restate
+n = 50_003
+g = np.random.default_rng(77)
+host = [g.uniform(-1, 1, n) for _ in range(4)]
+vecs = [lv.DenseVector.from_values(h, "f64") for h in host]
+errors = []
+def work(t):
+    try:
+        torch.cuda.set_device(0)
+        s = torch.cuda.Stream()
         c = 0.25 * (t + 1)
-        trees.append(((lambda c=c: (as_node(vecs[0]) * c - vecs[1]) * (as_node(vecs[2]) + vecs[3] * c)),
-                      f"L0 S0 * L1 - L2 L3 S1 * + *", [c, c]))
-    errors = []
-
-    def work(t):
-        try:
-            torch.cuda.set_device(0)
-            s = torch.cuda.Stream()
-            with torch.cuda.stream(s):
-                build, sig, sc = trees[t]
-                out = lv.DenseVector.zeros(n, "f64")
-                want = restate.eval_sig(sig, host, sc, "f64")
-                for _ in range(20):
-                    out.assign(build())
-                    s.synchronize()
-                    if out.to_array().tobytes() != want.tobytes():
-                        errors.append(t)
-                        return
-        except Exception as exc:  # pragma: no cover
-            errors.append(repr(exc))
-
-    threads = [threading.Thread(target=work, args=(t,)) for t in range(8)]
-    for th in threads:
-        th.start()
-    for th in threads:
-        th.join()
-    assert not errors, errors
-    assert _native.lib().salt_jit_wait() == 0
+        with torch.cuda.stream(s):
+            out = lv.DenseVector.zeros(n, "f64")
+            want = restate.eval_sig("L0 S0 * L1 - L2 L3 S1 * + *", host, [c, c], "f64")
+            for _ in range(20):
+                out.assign((as_node(vecs[0]) * c - vecs[1]) * (as_node(vecs[2]) + vecs[3] * c))
+                s.synchronize()
+                if out.to_array().tobytes() != want.tobytes():
+                    errors.append(t)
+                    return
+    except Exception as exc:
+        errors.append(repr(exc))
+threads = [threading.Thread(target=work, args=(t,)) for t in range(8)]
+for th in threads: th.start()
+for th in threads: th.join()
+assert not errors, errors
+lv.jit_wait()
+print("ok")
+"""
+    env = dict(os.environ, SALT_JIT_CACHE="off", SALT_JIT_ASYNC="1", PYTHONPATH=f"{ROOT}:{ROOT / 'tests'}")
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
+                         cwd=ROOT, timeout=300)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-3000:]
 
 
 def test_interpreter_on_pinned_host_vectors(interp):
@@ -276,3 +272,28 @@ def test_interpreter_on_pinned_host_vectors(interp):
     ex = restate.exact_sum(a * b)
     assert abs(float(r) - ex) <= 1e-12 * abs(ex)
     assert interp.salt_interp_launch_count() > k0
+
+
+def test_fresh_tree_captured_in_a_graph_without_warm_up():
+    """A tree never seen before, first evaluated inside CUDA-graph capture:
+    the capture builds it synchronously (a graph must not keep the
+    interpreter kernel), and replays give the reference's bits."""
+    import torch
+
+    n = 100_003
+    g = np.random.default_rng(99)
+    a, b, c = (g.uniform(-1, 1, n) for _ in range(3))
+    A, B, C = (lv.DenseVector.from_values(v, "f64") for v in (a, b, c))
+    D = lv.DenseVector.zeros(n, "f64")
+    lib = _native.lib()
+    k0 = lib.salt_interp_launch_count()
+    s = torch.cuda.Stream()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=s):
+        D.assign((A * 0.8125 - B) * (C - A * 0.4375))   # out-of-table, fresh
+    graph.replay()
+    graph.replay()
+    torch.cuda.synchronize()
+    want = restate.eval_sig("L0 S0 * L1 - L2 L0 S1 * - *", [a, b, c], [0.8125, 0.4375], "f64")
+    assert D.to_array().tobytes() == want.tobytes()
+    assert lib.salt_interp_launch_count() == k0   # the compiled kernel was captured

@@ -11,11 +11,15 @@ is the host issue cost, the GPU runs behind), for:
     python tools/api_overhead.py [--n 1024] [--calls 2000]
 """
 
+import os
 import argparse
 import json
 import sys
 import time
 from pathlib import Path
+# steady-state measurements: build out-of-table trees with NVRTC on first use
+# instead of running them on the interpreter meanwhile (tiered JIT)
+os.environ.setdefault("SALT_JIT_ASYNC", "0")
 
 import numpy as np
 import torch

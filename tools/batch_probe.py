@@ -6,10 +6,14 @@ and wall time (host included, expressions prebuilt), best of 5.
     python tools/batch_probe.py
 """
 
+import os
 import json
 import sys
 import time
 from pathlib import Path
+# steady-state measurements: build out-of-table trees with NVRTC on first use
+# instead of running them on the interpreter meanwhile (tiered JIT)
+os.environ.setdefault("SALT_JIT_ASYNC", "0")
 
 import numpy as np
 import torch

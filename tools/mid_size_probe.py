@@ -16,10 +16,14 @@ and the same for the torch library call (torch.dot / vector_norm / eager T1).
     python tools/mid_size_probe.py [--out profiles/r01_mid_sizes.json]
 """
 
+import os
 import argparse
 import json
 import sys
 from pathlib import Path
+# steady-state measurements: build out-of-table trees with NVRTC on first use
+# instead of running them on the interpreter meanwhile (tiered JIT)
+os.environ.setdefault("SALT_JIT_ASYNC", "0")
 
 import torch
 

@@ -8,9 +8,13 @@ Data is device-generated (torch.rand) — only the kernel's behaviour is of
 interest here; parity is covered by tests/.
 """
 
+import os
 import argparse
 import sys
 from pathlib import Path
+# steady-state measurements: build out-of-table trees with NVRTC on first use
+# instead of running them on the interpreter meanwhile (tiered JIT)
+os.environ.setdefault("SALT_JIT_ASYNC", "0")
 
 import torch
 

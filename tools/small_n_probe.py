@@ -4,9 +4,13 @@ launches between two events (no host gaps: the GPU queue stays full), per
 size.  Used with SALT_ASSIGN_TILES / SALT_REDUCE_TILES to tune the work per
 CTA at sizes where launch and ramp costs matter."""
 
+import os
 import json
 import sys
 from pathlib import Path
+# steady-state measurements: build out-of-table trees with NVRTC on first use
+# instead of running them on the interpreter meanwhile (tiered JIT)
+os.environ.setdefault("SALT_JIT_ASYNC", "0")
 
 import torch
 
