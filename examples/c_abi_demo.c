@@ -8,6 +8,7 @@
  *   2. r = dot(d, a)                     salt_reduce   (one kernel, device workspace)
  *   3. y = y + alpha*x ; r = dot(y, z)   salt_assign_reduce (one pass)
  *   4. the same axpy on HOST buffers     salt_assign_host (chunked PCIe pipeline)
+ *   5. 64 small independent axpys         salt_assign_batch (one launch)
  *
  * Elementwise results are compared bit for bit with a plain C loop in the
  * reference's operation order (expressions.py:248-249, :320: left operand
@@ -156,6 +157,50 @@ int main(int argc, char** argv) {
   SK(salt_assign_host(SALT_F64, "L0 S0 L1 * +", pb, hba, 2, &alpha, 1, n, staging, staging_bytes,
                       (void* const*)st));
   ok &= same_bits(pb, want, n, "salt_assign_host  y += alpha*x (pinned)");
+
+  /* 5. 64 independent axpys y_k += alpha_k * x_k of ragged small lengths,
+   *    one batched launch; each must equal its own salt_assign */
+  {
+    enum { M = 64 };
+    int64_t ns[M], off[M + 1];
+    off[0] = 0;
+    for (int k = 0; k < M; ++k) {
+      ns[k] = 100 + 97 * k;
+      off[k + 1] = off[k] + ns[k] + 3; /* +3: later problems start misaligned */
+    }
+    const size_t tb = (size_t)off[M] * sizeof(double);
+    double *hx = malloc(tb), *hy = malloc(tb), *hy1 = malloc(tb), *hy2 = malloc(tb);
+    for (int64_t i = 0; i < off[M]; ++i) {
+      hx[i] = uniform();
+      hy[i] = uniform();
+    }
+    double *x, *y1, *y2;
+    CK(cudaMalloc((void**)&x, tb));
+    CK(cudaMalloc((void**)&y1, tb));
+    CK(cudaMalloc((void**)&y2, tb));
+    CK(cudaMemcpy(x, hx, tb, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(y1, hy, tb, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(y2, hy, tb, cudaMemcpyHostToDevice));
+    void* dsts[M];
+    const void* lv[2 * M];
+    double sc[M];
+    for (int k = 0; k < M; ++k) {
+      dsts[k] = y1 + off[k];
+      lv[2 * k] = y1 + off[k];
+      lv[2 * k + 1] = x + off[k];
+      sc[k] = 0.125 * (k + 1);
+    }
+    SK(salt_assign_batch(SALT_F64, "L0 S0 L1 * +", M, dsts, lv, 2, sc, 1, ns, s));
+    for (int k = 0; k < M; ++k) {
+      const void* l2[2] = {y2 + off[k], x + off[k]};
+      SK(salt_assign(SALT_F64, "L0 S0 L1 * +", y2 + off[k], l2, 2, &sc[k], 1, ns[k], s));
+    }
+    CK(cudaMemcpyAsync(hy1, y1, tb, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(hy2, y2, tb, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    ok &= same_bits(hy1, hy2, off[M], "salt_assign_batch  64 axpys == 64 salt_assign");
+    free(hx); free(hy); free(hy1); free(hy2);
+  }
 
   /* error path: a bad signature is refused before any launch */
   int rc = salt_assign(SALT_F64, "L0 +", d, abc, 3, NULL, 0, n, s);

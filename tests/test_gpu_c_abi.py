@@ -1,7 +1,7 @@
 """The C ABI used from plain C (examples/c_abi_demo.c): no Python in the
 process — cudaMalloc'd vectors, salt_assign / salt_reduce /
-salt_assign_reduce / salt_assign_host, results checked in C (bit-exact
-elementwise, 1e-12 for reductions)."""
+salt_assign_reduce / salt_assign_host / salt_assign_batch, results checked
+in C (bit-exact elementwise, 1e-12 for reductions)."""
 
 import subprocess
 from pathlib import Path
