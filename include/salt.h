@@ -227,6 +227,18 @@ int salt_assign_batch(int dtype, const char* sig, int count, void* const* dsts,
                       const void* const* leaves, int nleaves, const double* scalars, int nscalars,
                       const int64_t* ns, void* stream);
 
+/* Batched small reductions: `count` independent sums of ONE reduce tree
+ * `sig` over different vectors / scalars / lengths.  Problems of at most two
+ * tiles (a few thousand elements) whose operands share one 32-byte
+ * alignment run as ONE launch per up to 96 of them, one CTA each; the rest
+ * run as ordinary reductions (workspace: salt_reduce_workspace_bytes(), used
+ * only by those).  outs[q]: device pointer receiving problem q's result
+ * (element type, or the {hi, lo} partial with SALT_PARTIAL; SALT_SQRT as in
+ * salt_reduce).  Every result has the bits of its own salt_reduce. */
+int salt_reduce_batch(int dtype, const char* sig, int count, const void* const* leaves, int nleaves,
+                      const double* scalars, int nscalars, const int64_t* ns, int flags,
+                      void* const* outs, void* workspace, size_t workspace_bytes, void* stream);
+
 /* Host-buffer (end-to-end) variants: leaves / dst are HOST pointers (pinned
  * memory for full speed).  Chunks are streamed H2D -> fused kernel -> D2H
  * through `staging` (device memory, caller-owned) on three caller streams

@@ -43,6 +43,7 @@ HEADER_SYMBOLS = (
     "salt_assign_reduce",
     "salt_fused",
     "salt_assign_batch",
+    "salt_reduce_batch",
     "salt_reduce_finish",
     "salt_assign_host",
     "salt_reduce_host",
@@ -96,6 +97,8 @@ _SIGNATURES = {
     ),
     "salt_reduce_finish": (_c_int, [_c_int, _c_vp, _c_int, _c_int, _c_vp, _c_vp, _c_vp]),
     "salt_assign_batch": (_c_int, [_c_int, _c_str, _c_int, _c_vpp, _c_vpp, _c_int, _c_dp, _c_int, _c_vp, _c_vp]),
+    "salt_reduce_batch": (_c_int, [_c_int, _c_str, _c_int, _c_vpp, _c_int, _c_dp, _c_int, _c_vp, _c_int, _c_vpp,
+                                   _c_vp, _c_size, _c_vp]),
     "salt_assign_host": (
         _c_int, [_c_int, _c_str, _c_vp, _c_vpp, _c_int, _c_dp, _c_int, _c_i64, _c_vp, _c_size, _c_vpp]
     ),

@@ -448,6 +448,20 @@ template <class T, class EA> void reg_batch_one(const char* asig) {
   table()[key_of(dtype_of<T>(), kBatchKind, V, sa.type, "batch")] = std::move(k);
 }
 
+// Batched small-reduction kernels (salt_reduce_batch) of a reduce tree.
+constexpr int kBatchReduceKind = 4;
+template <class T, class ER> void reg_batch_reduce_one(const char* rsig) {
+  Sig sr;
+  parse_sig(rsig, 0, sr);
+  constexpr int V = vec_of<T>();
+  constexpr int U = unroll_for(salt::MODE_REDUCE, ER::NL, (int)sizeof(T));
+  auto k = std::make_unique<Kernel>();
+  k->aot = (const void*)&salt::batch_reduce_kernel<T, ER, V, U, kBlock>;
+  k->vec = V;
+  k->unroll = U;
+  table()[key_of(dtype_of<T>(), kBatchReduceKind, V, "batch", sr.type)] = std::move(k);
+}
+
 template <class EA, class ER, int MODE> void reg(const char* asig, const char* rsig) {
   reg_one<float, EA, ER, MODE>(asig, rsig);
   reg_one<double, EA, ER, MODE>(asig, rsig);
@@ -455,6 +469,12 @@ template <class EA, class ER, int MODE> void reg(const char* asig, const char* r
     if constexpr (EA::NL <= salt::BATCH_LEAVES && EA::NS <= salt::BATCH_SCALARS) {
       reg_batch_one<float, EA>(asig);
       reg_batch_one<double, EA>(asig);
+    }
+  }
+  if constexpr (MODE == salt::MODE_REDUCE) {
+    if constexpr (ER::NL <= salt::BATCH_LEAVES && ER::NS <= salt::BATCH_SCALARS) {
+      reg_batch_reduce_one<float, ER>(rsig);
+      reg_batch_reduce_one<double, ER>(rsig);
     }
   }
 }
@@ -555,16 +575,18 @@ std::unique_ptr<Kernel> jit_build(int dtype, int mode, int vec, int nl, const st
   Nvrtc& nv = nvrtc();
   if (!nv.ok) { g_err = "NVRTC unavailable: " + nv.why; return nullptr; }
   const char* tname = dtype == SALT_F32 ? "float" : "double";
-  const bool batch = mode == kBatchKind;
+  const bool batch = mode == kBatchKind, batch_reduce = mode == kBatchReduceKind;
+  const int kmode = batch ? salt::MODE_ASSIGN : batch_reduce ? salt::MODE_REDUCE : mode;
   const int unroll = vec == 1 ? kUnrollScalar
                      : tuning_unroll() > 0 ? tuning_unroll()
-                     : unroll_for(batch ? salt::MODE_ASSIGN : mode, nl, dtype == SALT_F32 ? 4 : 8);
+                     : unroll_for(kmode, nl, dtype == SALT_F32 ? 4 : 8);
+  const std::string tail = std::to_string(vec) + "," + std::to_string(unroll) + "," +
+                           std::to_string(kBlock) + ">";
   std::string expr =
-      batch ? std::string("salt::batch_kernel<") + tname + "," + ta + "," + std::to_string(vec) + "," +
-                  std::to_string(unroll) + "," + std::to_string(kBlock) + ">"
-            : std::string("salt::fused_kernel<") + tname + "," + ta + "," + tr + "," +
-                  std::to_string(mode) + "," + std::to_string(vec) + "," + std::to_string(unroll) +
-                  "," + std::to_string(kBlock) + ">";
+      batch ? std::string("salt::batch_kernel<") + tname + "," + ta + "," + tail
+      : batch_reduce ? std::string("salt::batch_reduce_kernel<") + tname + "," + tr + "," + tail
+                     : std::string("salt::fused_kernel<") + tname + "," + ta + "," + tr + "," +
+                           std::to_string(mode) + "," + tail;
   const std::string minb = "-DSALT_MIN_BLOCKS=" + std::to_string(tuning_minb());
   const char* opts[8] = {"--gpu-architecture=sm_100a", "-fmad=false", "--std=c++17",
                          "-lineinfo", "-default-device"};
@@ -1363,6 +1385,95 @@ int run_batch(Plan& p, int count, void* const* dsts, const void* const* leaves, 
   return flush();
 }
 
+// Batched small reductions: problems of <= 2 tiles whose operands share the
+// 32-byte alignment go into batch_reduce_kernel launches (one CTA each, the
+// one-CTA fused order: same bits); the others run as ordinary reductions.
+template <class T>
+int run_reduce_batch(Plan& p, int count, const void* const* leaves, int nleaves, const double* scalars,
+                     int nscalars, const int64_t* ns, int flags, void* const* outs, void* ws,
+                     size_t ws_bytes, cudaStream_t st) {
+  if (count < 0 || (count > 0 && (!ns || !outs || (nleaves > 0 && !leaves))))
+    return fail(SALT_EINVAL, "bad batch arguments");
+  if (flags & ~(SALT_SQRT | SALT_PARTIAL)) return fail(SALT_EINVAL, "reduce flags: SALT_SQRT, SALT_PARTIAL");
+  for (int q = 0; q < count; ++q) {
+    if (ns[q] < 0) return fail(SALT_EINVAL, "negative length");
+    if (!outs[q]) return fail(SALT_EINVAL, "NULL reduction output");
+    for (int l = 0; ns[q] > 0 && l < p.nl; ++l)
+      if (!leaves[(size_t)q * nleaves + l]) return fail(SALT_EINVAL, "NULL leaf pointer");
+  }
+  Kernel* k = nullptr;
+  if (p.np == 0 && p.nl <= salt::BATCH_LEAVES && p.ns <= salt::BATCH_SCALARS)
+    k = get_kernel(dtype_of<T>(), kBatchReduceKind, vec_of<T>(), p.nl, "batch", p.sr.type);
+  int dev, rc;
+  if (k) {
+    if ((rc = current_device(dev)) || (rc = prepare(k, dev))) return rc;
+  }
+  constexpr int V = vec_of<T>();
+  const i64 per_tile = k ? (i64)kBlock * k->unroll : 0;
+  auto args = std::make_unique<salt::BatchArgs<T>>();
+  memset(args.get(), 0, sizeof(salt::BatchArgs<T>));
+  auto flush = [&]() -> int {
+    if (args->count == 0) return 0;
+    void* params[] = {args.get(), &flags};
+    const bool pdl = use_pdl();
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.gridDim = dim3(args->count);
+    cfg.blockDim = dim3(kBlock);
+    cfg.stream = st;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    if (k->aot) {
+      cudaError_t e = cudaLaunchKernelExC(&cfg, k->aot, params);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaLaunchKernelExC(batch reduce)");
+    } else {
+      CUlaunchConfig c = {};
+      CUlaunchAttribute at[1];
+      at[0].id = CU_LAUNCH_ATTRIBUTE_PROGRAMMATIC_STREAM_SERIALIZATION;
+      at[0].value.programmaticStreamSerializationAllowed = 1;
+      c.gridDimX = (unsigned)args->count;
+      c.gridDimY = c.gridDimZ = 1;
+      c.blockDimX = kBlock;
+      c.blockDimY = c.blockDimZ = 1;
+      c.hStream = (CUstream)st;
+      c.attrs = at;
+      c.numAttrs = pdl && driver().LaunchKernelEx ? 1 : 0;
+      CUresult r = driver().LaunchKernelEx
+                       ? driver().LaunchKernelEx(&c, k->jit_fn[dev], params, nullptr)
+                       : driver().LaunchKernel(k->jit_fn[dev], args->count, 1, 1, kBlock, 1, 1, 0,
+                                               (CUstream)st, params, nullptr);
+      if (r != CUDA_SUCCESS) return fail(SALT_ECUDA, "cuLaunchKernel(batch reduce) failed");
+    }
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    args->count = 0;
+    return 0;
+  };
+  for (int q = 0; q < count; ++q) {
+    const i64 n = ns[q];
+    const void* const* lq = leaves + (size_t)q * nleaves;
+    int vec = V;
+    i64 head = 0, nvec = 0;
+    if (n > 0) geometry<T>(nullptr, 0, lq, p.nl, n, vec, head, nvec);
+    if (k && vec == V && (nvec + per_tile - 1) / per_tile <= 2) {
+      if (args->count == salt::BATCH_MAX && (rc = flush())) return rc;
+      salt::BatchProblem<T>& P = args->p[args->count++];
+      P.dst = (T*)outs[q];
+      for (int l = 0; l < p.nl; ++l) P.leaf[l] = (const T*)lq[l];
+      for (int c = 0; c < p.ns; ++c) P.sc[c] = (T)scalars[(size_t)q * nscalars + c];
+      P.n = n;
+      P.head = head;
+      P.nvec = nvec;
+      continue;
+    }
+    if ((rc = run_fused<T>(p, nullptr, 0, lq, nleaves, scalars + (size_t)q * nscalars, nscalars, n,
+                           flags, ws, ws_bytes, outs[q], nullptr, st, nullptr, nullptr, 0)))
+      return rc;
+  }
+  return k ? flush() : 0;
+}
+
 template <class T>
 int finish(const void* parts, int count, int flags, void* out_dev, void* out_host,
            cudaStream_t st) {
@@ -1785,6 +1896,19 @@ int salt_assign_batch(int dtype, const char* sig, int count, void* const* dsts,
   if (dtype == SALT_F32)
     return run_batch<float>(*p, count, dsts, leaves, nleaves, scalars, nscalars, ns, (cudaStream_t)stream);
   return run_batch<double>(*p, count, dsts, leaves, nleaves, scalars, nscalars, ns, (cudaStream_t)stream);
+}
+
+int salt_reduce_batch(int dtype, const char* sig, int count, const void* const* leaves, int nleaves,
+                      const double* scalars, int nscalars, const int64_t* ns, int flags,
+                      void* const* outs, void* workspace, size_t workspace_bytes, void* stream) {
+  Plan* p;
+  int rc = make_plan(dtype, nullptr, sig, salt::MODE_REDUCE, nleaves, nscalars, p);
+  if (rc) return rc;
+  if (dtype == SALT_F32)
+    return run_reduce_batch<float>(*p, count, leaves, nleaves, scalars, nscalars, ns, flags, outs, workspace,
+                                   workspace_bytes, (cudaStream_t)stream);
+  return run_reduce_batch<double>(*p, count, leaves, nleaves, scalars, nscalars, ns, flags, outs, workspace,
+                                  workspace_bytes, (cudaStream_t)stream);
 }
 
 int salt_assign_host(int dtype, const char* sig, void* host_dst, const void* const* host_leaves,

@@ -748,6 +748,61 @@ __global__ void SALT_BOUNDS(BLOCK) batch_kernel(BatchArgs<T> a) {
   }
 }
 
+// Batched small reductions: CTA q sums problem q entirely — its head/tail
+// elements, then its <= 2 tiles in order — and rounds it (flags: sqrt,
+// partial) into P.dst, exactly the order of a one-CTA fused_kernel launch
+// (which every reduction of <= 2 tiles is), so each result has the bits of
+// its own salt_reduce.  Problems with more tiles are not batched.
+template <class T, class ER, int V, int UNR, int BLOCK>
+__global__ void SALT_BOUNDS(BLOCK) batch_reduce_kernel(BatchArgs<T> a, int flags) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // see fused_kernel
+  constexpr int NL = ER::NL, NS = ER::NS;
+  static_assert(NL <= BATCH_LEAVES && NS <= BATCH_SCALARS && ER::NP == 0, "batch tree limits");
+  typedef Env<T, NL, NS, 0, 1, V> E1;
+  typedef Env<T, NL, NS, 0, 1, 1> ES;
+  const BatchProblem<T>& P = a.p[blockIdx.x];
+  Acc<T> acc;
+  {
+    const i64 tail0 = P.head + P.nvec * V;
+    const i64 nscalar = P.head + (P.n - tail0);
+    for (i64 t = threadIdx.x; t < nscalar; t += BLOCK) {
+      const i64 i = t < P.head ? t : tail0 + (t - P.head);
+      ES e;
+#pragma unroll
+      for (int l = 0; l < NL; ++l) e.x[l][0] = P.leaf[l][i];
+#pragma unroll
+      for (int s = 0; s < NS; ++s) e.s[s] = P.sc[s];
+      acc.add(ER::ev(e, 0));
+    }
+  }
+  const i64 ntiles = (P.nvec + (i64)BLOCK * UNR - 1) / ((i64)BLOCK * UNR);
+  for (i64 t = 0; t < ntiles; ++t) {
+    const i64 base = t * BLOCK * UNR + threadIdx.x;
+    E1 e[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const i64 j = base + (i64)u * BLOCK;
+      if (j < P.nvec) {
+#pragma unroll
+        for (int l = 0; l < NL; ++l) VecIO<T, V>::load(e[u].x[l], P.leaf[l] + P.head + j * V);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const i64 j = base + (i64)u * BLOCK;
+      if (j < P.nvec) {
+#pragma unroll
+        for (int s = 0; s < NS; ++s) e[u].s[s] = P.sc[s];
+#pragma unroll
+        for (int k = 0; k < V; ++k) acc.add(ER::ev(e[u], k));
+      }
+    }
+  }
+  __shared__ DD smem[BLOCK / 32];
+  DD part = block_reduce_dd<BLOCK>(acc.get(), smem);
+  if (threadIdx.x == 0) finish_store<T>(part, flags, P.dst);
+}
+
 // Combine `count` partials (all-gathered per-device DD values, rank order).
 // Up to XCHG_MAX_RANKS partials are folded sequentially in rank order — the
 // same arithmetic as exchange_dd, so the NCCL all-gather path and the NVLink

@@ -292,6 +292,17 @@ def _check_assign_batch(statements) -> list:
     return items
 
 
+def _lower_sum(expression):
+    """(lowering, dtype, length) of sum(expression), validated as
+    execute_reduce validates it (reduce_batch)."""
+    root = SumNode(as_node(expression))
+    length = common_length(root)
+    lw = lower(root.child)
+    if not _fits(lw):
+        lw = lower(_fit(root.child, length))
+    return lw, root.dtype, length
+
+
 def _storage_key(v):
     t = getattr(v, "_data", None)
     return ("ptr", t.get_device(), t.data_ptr()) if t is not None and t.numel() else ("id", id(v))

@@ -28,7 +28,7 @@ from .expressions import (
 )
 
 __all__ = ["dot", "scal", "axpy", "scaled_copy", "sum", "norm2", "axpy_dot", "fused", "assign_batch",
-           "jit_wait"]
+           "reduce_batch", "dot_batch", "jit_wait"]
 
 
 def _op(sig, dest, leaves, alpha=None, flags=0, lazy=False):
@@ -160,3 +160,33 @@ def jit_wait() -> None:
     failed = _native.lib().salt_jit_wait()
     if failed:
         raise RuntimeError(f"{failed} background JIT build(s) failed; those trees stay on the interpreter")
+
+
+def reduce_batch(expressions, *, sqrt=False, lazy=False) -> list:
+    """Sums of many INDEPENDENT expressions (the reduce counterpart of
+    assign_batch): small ones (at most two tiles, a few thousand elements)
+    sharing a tree shape and element type run as ONE launch per up to 96,
+    and all of a group's results return to the host in one copy; each result
+    has the bits of its own `execute_reduce(SumNode(expression))` (sqrt=True:
+    of `norm2`).  lazy=True returns DeviceScalars."""
+    from .engine import _lower_sum
+    from .runtime import run_reduce_batch
+
+    items = [_lower_sum(e) for e in expressions]
+    return run_reduce_batch(items, flags=_native.SALT_SQRT if sqrt else 0, lazy=lazy)
+
+
+def dot_batch(pairs, *, lazy=False) -> list:
+    """[dot(x, y) for x, y in pairs] through reduce_batch (same bits).
+    Pairs of plain DenseVectors of one element type and equal lengths skip
+    the node objects; anything else goes through the full validation."""
+    from .runtime import _PairLowering, run_reduce_batch
+    from .vectors import DenseVector
+
+    pairs = list(pairs)
+    items = []
+    for x, y in pairs:
+        if type(x) is not DenseVector or type(y) is not DenseVector or x.dtype != y.dtype or len(x) != len(y):
+            return reduce_batch([MulNode(as_node(a), as_node(b)) for a, b in pairs], lazy=lazy)
+        items.append((_PairLowering(x, y), x.dtype, len(x)))
+    return run_reduce_batch(items, lazy=lazy)

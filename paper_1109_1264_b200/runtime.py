@@ -33,7 +33,8 @@ from . import _native
 from .lanes import as_dtype
 from .vectors import DenseVector, DeviceScalar
 
-__all__ = ["run_assign", "run_reduce", "run_assign_reduce", "run_fused", "run_assign_batch", "Placement"]
+__all__ = ["run_assign", "run_reduce", "run_assign_reduce", "run_fused", "run_assign_batch", "run_reduce_batch",
+           "Placement"]
 
 _ws_lock = threading.Lock()
 _workspaces = {}
@@ -332,6 +333,64 @@ def run_assign_batch(items):
     for lw, dest, dtype, n in rest:
         run_assign(lw, dest, dtype, n)
     return batched
+
+
+class _PairLowering:
+    """The lowering of x*y (or x*x) for plain device vectors, without node
+    objects (ops.dot_batch's fast path): same signature and leaves as
+    expressions.lower(MulNode(x, y))."""
+
+    __slots__ = ("tokens", "vectors", "scalars", "pscalars")
+
+    def __init__(self, x, y):
+        same = x is y
+        self.tokens = ["L0", "L0", "*"] if same else ["L0", "L1", "*"]
+        self.vectors = [x] if same else [x, y]
+        self.scalars = []
+        self.pscalars = []
+
+
+def run_reduce_batch(items, flags=0, lazy=False):
+    """items: [(lowering, dtype, n)] of validated sums.  Plain-device ones
+    are grouped by (device, element type, signature) and each group is one
+    salt_reduce_batch call writing into one device buffer; the results then
+    come back to the host in ONE copy per group (or stay on the device as
+    DeviceScalars with lazy=True).  Others run one by one."""
+    results = [None] * len(items)
+    groups = {}
+    for i, (lw, dtype, n) in enumerate(items):
+        fast = None if lw.pscalars else _fast(lw.vectors, None)
+        if fast is None:
+            results[i] = run_reduce(lw, dtype, n, flags=flags, lazy=lazy)
+            continue
+        dev, ptrs, _ = fast
+        key = (dev, _dtype_code(dtype), " ".join(lw.tokens), len(lw.vectors), len(lw.scalars))
+        groups.setdefault(key, []).append((i, ptrs, lw.scalars, n, as_dtype(dtype)))
+    lib = _native.lib()
+    for (dev, code, sig, nl, ns), probs in groups.items():
+        device = torch.device("cuda", dev)
+        out = torch.empty(2 * len(probs), dtype=torch.float64, device=device)
+        base = out.data_ptr()
+        outs, k0 = _native.ptr_array([base + 16 * q for q in range(len(probs))])
+        leaves, k1 = _native.ptr_array([p for _, ptrs, _, _, _ in probs for p in ptrs])
+        scal, k2 = _native.double_array([c for _, _, sc, _, _ in probs for c in sc])
+        lens = array.array("q", [n for _, _, _, n, _ in probs])
+        with _OnDevice(dev):
+            stream = _raw_stream(dev)
+            ws = _workspace(dev, stream)
+            _native.check(lib.salt_reduce_batch(code, sig.encode(), len(probs), leaves, nl, scal, ns,
+                                                lens.buffer_info()[0], flags, outs, ws.data_ptr(),
+                                                ws.numel(), stream))
+        dt = probs[0][4]
+        if lazy:
+            for q, (i, *_rest) in enumerate(probs):
+                slot = out[2 * q:2 * q + 2]
+                results[i] = DeviceScalar(slot.view(torch.float32)[:1] if dt.itemsize == 4 else slot[:1], dt)
+        else:
+            host = out.cpu().numpy().view(np.uint8).reshape(len(probs), 16)
+            for q, (i, *_rest) in enumerate(probs):
+                results[i] = np.frombuffer(host[q, :dt.itemsize].tobytes(), dtype=dt)[0]
+    return results
 
 
 # ---------------------------------------------------------------- reduce

@@ -124,3 +124,41 @@ def test_batch_is_one_launch_for_many_small_trees():
     w_loop = min(wall(lambda: [y.assign(st) for y, st in sts]) for _ in range(5))
     assert w_batch < w_loop, (w_batch, w_loop)
     print(f"256 axpys n=4096: device {t_batch:.0f} vs {t_loop:.0f} us; wall {w_batch:.0f} vs {w_loop:.0f} us")
+
+
+@pytest.mark.parametrize("dt", ["f64", "f32"])
+def test_reduce_batch_bits_equal_individual_reductions(dt):
+    npdt = np.float64 if dt == "f64" else np.float32
+    g = np.random.default_rng([41, len(dt)])
+    pairs, xs = [], []
+    for k in range(180):
+        n = int(g.integers(0, 4000)) if k % 30 else (1 << 20) + int(g.integers(0, 9))  # a few large ones
+        x, y = (g.standard_normal(n).astype(npdt) for _ in range(2))
+        off = int(g.integers(1, 4)) if k % 7 == 0 else 0
+        X = lv.DenseVector.from_tensor(torch.from_numpy(np.concatenate([np.zeros(off, npdt), x])).cuda()[off:])
+        Y = lv.DenseVector.from_tensor(torch.from_numpy(np.concatenate([np.zeros(off, npdt), y])).cuda()[off:])
+        pairs.append((X, Y))
+        xs.append(X)
+    l0 = _launches()
+    got = lv.dot_batch(pairs)
+    launches = _launches() - l0
+    assert launches <= 10, launches   # 174 small ones: 2 batched launches; 6 large: one each
+    want = [lv.dot(x, y) for x, y in pairs]
+    assert all(a.dtype == npdt for a in got)
+    assert np.array(got).tobytes() == np.array(want).tobytes()
+    nr = lv.reduce_batch([lv.expressions.as_node(x) * x for x in xs], sqrt=True)
+    assert np.array(nr).tobytes() == np.array([lv.norm2(x) for x in xs]).tobytes()
+    lazy = lv.dot_batch(pairs[:40], lazy=True)
+    assert np.array([d.item() for d in lazy]).tobytes() == np.array(want[:40]).tobytes()
+    ex = restate.exact_sum(pairs[1][0].to_array().astype(np.float64) * pairs[1][1].to_array())
+    assert abs(float(got[1]) - ex) <= (1e-12 if dt == "f64" else 1e-5) * max(abs(ex), 1e-30)
+
+
+def test_reduce_batch_one_launch_for_many_small_dots():
+    n, m = 2048, 192
+    g = np.random.default_rng(9)
+    pairs = [tuple(lv.DenseVector.from_values(g.uniform(-1, 1, n), "f64") for _ in range(2)) for _ in range(m)]
+    lv.dot_batch(pairs)
+    l0 = _launches()
+    lv.dot_batch(pairs, lazy=True)
+    assert _launches() - l0 == 2   # 192 problems = 2 launches of 96

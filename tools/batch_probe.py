@@ -59,8 +59,20 @@ def main():
                  "loop_wall_us": round(min(wall_us(loop) for _ in range(5)), 1)}
             rows.append(r)
             print(json.dumps(r), flush=True)
+    for n in (1024, 4096):
+        for m in (16, 256, 1024):
+            P = [tuple(lv.DenseVector.from_values(g.uniform(-1, 1, n), "f64") for _ in range(2))
+                 for _ in range(m)]
+            batch = lambda: lv.dot_batch(P)  # noqa: E731   one launch per 96 + ONE copy back
+            loop = lambda: [lv.dot(x, y) for x, y in P]  # noqa: E731   a sync per dot
+            batch(), loop()
+            r = {"op": "dot", "n": n, "m": m,
+                 "batch_wall_us": round(min(wall_us(batch) for _ in range(5)), 1),
+                 "loop_wall_us": round(min(wall_us(loop) for _ in range(5)), 1)}
+            rows.append(r)
+            print(json.dumps(r), flush=True)
     print(json.dumps({"gpu": torch.cuda.get_device_name(), "what": "m axpys of n f64 elements: "
-                      "lv.assign_batch vs one assign per tree"}))
+                      "lv.assign_batch vs one assign per tree; m dots: lv.dot_batch vs lv.dot each"}))
 
 
 if __name__ == "__main__":
