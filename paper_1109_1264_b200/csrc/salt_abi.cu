@@ -1,16 +1,23 @@
 // salt_abi.cu — libsalt.so: the C ABI declared in include/salt.h.
 //
-// Host runtime around the fused kernels of salt_expr.cuh:
-//   * signature parsing / validation (postfix, see salt.h),
-//   * the kernel table: compiled-in (AOT, sm_100a) instantiations for the
-//     trees the reference's named ops and the BASELINE configs use, plus an
-//     NVRTC JIT that instantiates the SAME template for any other tree and
-//     caches the cubin per signature and the module per device,
-//   * launch geometry (persistent grid = SMs x resident CTAs),
-//   * deterministic reductions (per-CTA double-double partials, last-CTA
-//     combine) and the multi-device finish,
-//   * the host-buffer streaming path (H2D / kernel / D2H pipelined over
-//     three streams) used for end-to-end evaluation of host vectors.
+// Host runtime around the kernels of salt_expr.cuh / salt_interp.cuh, one
+// translation unit in six parts:
+//   salt_abi_signatures.inc  postfix signature parsing / validation (salt.h)
+//   salt_abi_jit.inc         driver / NVRTC loading; the kernel table —
+//                            compiled-in (AOT, sm_100a) instantiations for
+//                            the reference's named ops and the BASELINE
+//                            trees — plus the NVRTC JIT that instantiates the
+//                            SAME templates for any other tree (disk cache,
+//                            module per device, opt-in tiered build)
+//   this file                launch geometry (tiles per CTA, reduction
+//                            groups, one-cluster small reductions), PDL
+//                            launches, plans, the interpreter fallback,
+//                            run_fused / dispatch
+//   salt_abi_batch.inc       batched assignments and small reductions
+//   salt_abi_nccl.inc        single-process multi-GPU all-reduce (NCCL)
+//   salt_abi_host.inc        host-buffer streaming (H2D / kernel / D2H on
+//                            three streams) for end-to-end evaluation
+// followed by the extern "C" entry points.
 //
 // Reference anchors (pkg/src/lanevec/): engine.py:243-264 (assign loop),
 // :267-292 (reduce loop), expressions.py:392-395 (commit), :457-480 (sum).
@@ -158,620 +165,9 @@ int cuda_fail(cudaError_t e, const char* what) {
     if (e_ != cudaSuccess) return cuda_fail(e_, #call);  \
   } while (0)
 
-// ------------------------------------------------------------------ signatures
-struct Sig {
-  std::string canon;  // tokens joined by single spaces (roots joined by " ; ")
-  std::string type;   // C++ type of the tree, e.g. salt::Add<salt::L<0>,salt::L<1>>
-  int nl = 0, ns = 0, np = 0;
-  int nroots = 0;     // assignment roots (Multi<...> when > 1)
-  bool uses_d = false;
-};
+#include "salt_abi_signatures.inc"
 
-bool parse_index(const std::string& t, size_t from, int& k) {
-  if (t.size() <= from || t.size() > from + 2) return false;
-  k = 0;
-  for (size_t i = from; i < t.size(); ++i) {
-    if (t[i] < '0' || t[i] > '9') return false;
-    k = k * 10 + (t[i] - '0');
-  }
-  return true;
-}
-
-// One postfix tree.  `d_limit` = how many earlier roots' values (D0 ..) it
-// may read; "D" is D0.  Returns "" on success, else an error message.
-std::string parse_tree(const std::string& s, int d_limit, Sig& out) {
-  std::vector<std::string> toks;
-  std::string cur;
-  for (size_t i = 0; i <= s.size(); ++i) {
-    char c = i < s.size() ? s[i] : '\0';
-    if (c == ' ' || c == '\t' || c == '\0') {
-      if (!cur.empty()) toks.push_back(cur), cur.clear();
-    } else {
-      cur.push_back(c);
-    }
-  }
-  if (toks.empty()) return "empty signature";
-  if (toks.size() > 256) return "signature too long";
-  std::vector<std::string> st;
-  for (const auto& t : toks) {
-    int k = 0;
-    if (t == "+" || t == "-" || t == "*") {
-      if (st.size() < 2) return "operator '" + t + "' needs two operands in '" + s + "'";
-      std::string b = st.back(); st.pop_back();
-      std::string a = st.back(); st.pop_back();
-      const char* node = t == "+" ? "salt::Add<" : t == "-" ? "salt::Sub<" : "salt::Mul<";
-      st.push_back(std::string(node) + a + "," + b + ">");
-    } else if (t[0] == 'L' && parse_index(t, 1, k)) {
-      if (k >= salt::MAX_LEAVES) return "leaf index out of range: " + t;
-      out.nl = std::max(out.nl, k + 1);
-      st.push_back("salt::L<" + std::to_string(k) + ">");
-    } else if (t[0] == 'S' && parse_index(t, 1, k)) {
-      if (k >= salt::MAX_SCALARS) return "scalar index out of range: " + t;
-      out.ns = std::max(out.ns, k + 1);
-      st.push_back("salt::S<" + std::to_string(k) + ">");
-    } else if (t[0] == 'P' && parse_index(t, 1, k)) {
-      if (k >= salt::MAX_PSCALARS) return "device scalar index out of range: " + t;
-      out.np = std::max(out.np, k + 1);
-      st.push_back("salt::P<" + std::to_string(k) + ">");
-    } else if (t[0] == 'D' && (t.size() == 1 || parse_index(t, 1, k)) && d_limit > 0) {
-      if (t.size() == 1) k = 0;
-      if (k >= d_limit) return "'" + t + "' reads a root that is not computed before it";
-      out.uses_d = true;
-      st.push_back("salt::Dk<" + std::to_string(k) + ">");
-    } else {
-      return "bad token '" + t + "' in signature '" + s + "'";
-    }
-    if (!out.canon.empty()) out.canon.push_back(' ');
-    out.canon += t;
-  }
-  if (st.size() != 1) return std::string("signature leaves ") + std::to_string(st.size()) +
-                            " values on the stack: '" + s + "'";
-  out.type = st.back();
-  return "";
-}
-
-// A reduce tree (d_limit = roots of the fused assignment, 0 for none).
-std::string parse_sig(const char* s, int d_limit, Sig& out) {
-  if (!s) return "signature is NULL";
-  out = Sig();
-  return parse_tree(s, d_limit, out);
-}
-
-// Assignment roots separated by ';'; root r may read D0 .. D(r-1).
-std::string parse_assign(const char* s, Sig& out) {
-  if (!s) return "signature is NULL";
-  out = Sig();
-  std::string all(s);
-  std::vector<std::string> types;
-  size_t pos = 0;
-  while (true) {
-    size_t semi = all.find(';', pos);
-    std::string part = all.substr(pos, semi == std::string::npos ? std::string::npos : semi - pos);
-    if ((int)types.size() == salt::MAX_ROOTS)
-      return "more than " + std::to_string((int)salt::MAX_ROOTS) + " assignment roots";
-    Sig r;
-    std::string err = parse_tree(part, (int)types.size(), r);
-    if (!err.empty()) return err;
-    out.nl = std::max(out.nl, r.nl);
-    out.ns = std::max(out.ns, r.ns);
-    out.np = std::max(out.np, r.np);
-    out.uses_d = out.uses_d || r.uses_d;
-    if (!out.canon.empty()) out.canon += " ; ";
-    out.canon += r.canon;
-    types.push_back(r.type);
-    if (semi == std::string::npos) break;
-    pos = semi + 1;
-  }
-  out.nroots = (int)types.size();
-  if (types.size() == 1) {
-    out.type = types[0];
-  } else {
-    out.type = "salt::Multi<";
-    for (size_t i = 0; i < types.size(); ++i) out.type += (i ? "," : "") + types[i];
-    out.type += ">";
-  }
-  return "";
-}
-
-// ------------------------------------------------------------------ driver / NVRTC
-struct Driver {
-  bool ok = false;
-  std::string why;
-  CUresult (*ModuleLoadData)(CUmodule*, const void*) = nullptr;
-  CUresult (*ModuleGetFunction)(CUfunction*, CUmodule, const char*) = nullptr;
-  CUresult (*LaunchKernel)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned,
-                           unsigned, CUstream, void**, void**) = nullptr;
-  CUresult (*GetErrorString)(CUresult, const char**) = nullptr;
-  // optional (cluster launches of JIT kernels)
-  CUresult (*LaunchKernelEx)(const CUlaunchConfig*, CUfunction, void**, void**) = nullptr;
-  CUresult (*FuncSetAttribute)(CUfunction, CUfunction_attribute, int) = nullptr;
-};
-
-template <class F> bool entry(const char* name, F& fp, std::string& why) {
-  void* p = nullptr;
-  cudaDriverEntryPointQueryResult q;
-  if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess || !p) {
-    why = std::string("driver entry point missing: ") + name;
-    return false;
-  }
-  fp = reinterpret_cast<F>(p);
-  return true;
-}
-
-Driver& driver() {
-  static Driver d;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    d.ok = entry("cuModuleLoadData", d.ModuleLoadData, d.why) &&
-           entry("cuModuleGetFunction", d.ModuleGetFunction, d.why) &&
-           entry("cuLaunchKernel", d.LaunchKernel, d.why) &&
-           entry("cuGetErrorString", d.GetErrorString, d.why);
-    std::string ignore;
-    if (!entry("cuLaunchKernelEx", d.LaunchKernelEx, ignore) ||
-        !entry("cuFuncSetAttribute", d.FuncSetAttribute, ignore))
-      d.LaunchKernelEx = nullptr;
-  });
-  return d;
-}
-
-typedef int nvrtcResult_t;
-struct Nvrtc {
-  bool ok = false;
-  std::string why;
-  void* h = nullptr;
-  nvrtcResult_t (*CreateProgram)(void**, const char*, const char*, int, const char* const*,
-                                 const char* const*) = nullptr;
-  nvrtcResult_t (*AddNameExpression)(void*, const char*) = nullptr;
-  nvrtcResult_t (*CompileProgram)(void*, int, const char* const*) = nullptr;
-  nvrtcResult_t (*GetProgramLogSize)(void*, size_t*) = nullptr;
-  nvrtcResult_t (*GetProgramLog)(void*, char*) = nullptr;
-  nvrtcResult_t (*GetCUBINSize)(void*, size_t*) = nullptr;
-  nvrtcResult_t (*GetCUBIN)(void*, char*) = nullptr;
-  nvrtcResult_t (*GetLoweredName)(void*, const char*, const char**) = nullptr;
-  nvrtcResult_t (*DestroyProgram)(void**) = nullptr;
-  nvrtcResult_t (*Version)(int*, int*) = nullptr;
-  bool has_256bit = false;  // NVRTC >= 12.9 accepts .v8.f32 / .v4.f64
-};
-
-Nvrtc& nvrtc() {
-  static Nvrtc n;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    // Prefer the toolkit's NVRTC (12.9, PTX ISA 8.8: 256-bit ld/st) by full
-    // path: a bare soname would return torch's already-loaded 12.8 copy.
-    const char* off = getenv("SALT_NO_JIT");  // test hook: behave as if NVRTC were absent
-    if (off && atoi(off) != 0) {
-      n.why = "JIT disabled (SALT_NO_JIT)";
-      return;
-    }
-    const char* env = getenv("SALT_NVRTC_LIB");
-    const char* cands[] = {env, "/usr/local/cuda/lib64/libnvrtc.so.12", "libnvrtc.so.12",
-                           "libnvrtc.so"};
-    for (const char* c : cands) {
-      if (!c) continue;
-      n.h = dlopen(c, RTLD_NOW | RTLD_LOCAL);
-      if (n.h) break;
-    }
-    if (!n.h) {
-      n.why = "libnvrtc.so.12 not found (set SALT_NVRTC_LIB)";
-      return;
-    }
-#define SYM(F, NAME)                                               \
-  n.F = reinterpret_cast<decltype(n.F)>(dlsym(n.h, NAME));         \
-  if (!n.F) { n.why = std::string("nvrtc symbol missing: ") + NAME; return; }
-    SYM(CreateProgram, "nvrtcCreateProgram");
-    SYM(AddNameExpression, "nvrtcAddNameExpression");
-    SYM(CompileProgram, "nvrtcCompileProgram");
-    SYM(GetProgramLogSize, "nvrtcGetProgramLogSize");
-    SYM(GetProgramLog, "nvrtcGetProgramLog");
-    SYM(GetCUBINSize, "nvrtcGetCUBINSize");
-    SYM(GetCUBIN, "nvrtcGetCUBIN");
-    SYM(GetLoweredName, "nvrtcGetLoweredName");
-    SYM(DestroyProgram, "nvrtcDestroyProgram");
-    SYM(Version, "nvrtcVersion");
-#undef SYM
-    int major = 0, minor = 0;
-    n.Version(&major, &minor);
-    n.has_256bit = major > 12 || (major == 12 && minor >= 9);
-    n.ok = true;
-  });
-  return n;
-}
-
-const char* kExprSource =
-#include "salt_expr_src.inc"
-    ;
-
-// ------------------------------------------------------------------ kernel table
-struct Kernel {
-  const void* aot = nullptr;                 // compiled-in kernel
-  std::string cubin, lowered;                // JIT kernel (device independent)
-  CUfunction jit_fn[kMaxDevices] = {};       // JIT module per device
-  int vec = 1;                               // lanes per vector access
-  int unroll = 1;
-  // cluster launches (reductions at small n): 0 unknown, 1 ok, -1 refused
-  std::atomic<int> cluster_ok[kMaxDevices] = {};
-  bool interp = false;                       // salt::interp_kernel (program in the parameters)
-  std::atomic<int> smem_limit[kMaxDevices] = {};  // 1: dynamic shared memory cap raised on the device
-};
-
-std::string key_of(int dtype, int mode, int vec, const std::string& ta, const std::string& tr) {
-  return std::to_string(dtype) + "|" + std::to_string(mode) + "|" + std::to_string(vec) + "|" +
-         ta + "|" + tr;
-}
-
-std::mutex g_table_mu;
-std::unordered_map<std::string, std::unique_ptr<Kernel>>& table() {
-  static std::unordered_map<std::string, std::unique_ptr<Kernel>> t;
-  return t;
-}
-std::unordered_map<std::string, std::unique_ptr<Kernel>>& jit_table() {
-  // leaked: the background JIT thread may insert while the process exits
-  static auto* t = new std::unordered_map<std::string, std::unique_ptr<Kernel>>;
-  return *t;
-}
-
-template <class T> constexpr int dtype_of();
-template <> constexpr int dtype_of<float>() { return SALT_F32; }
-template <> constexpr int dtype_of<double>() { return SALT_F64; }
-template <class T> constexpr int vec_of() { return 32 / (int)sizeof(T); }
-
-template <class T, class EA, class ER, int MODE>
-void reg_one(const char* asig, const char* rsig) {
-  Sig sa, sr;
-  std::string ta = "salt::None", tr = "salt::None";
-  if (asig) { parse_assign(asig, sa); ta = sa.type; }
-  if (rsig) { parse_sig(rsig, MODE == salt::MODE_ASSIGN_REDUCE ? sa.nroots : 0, sr); tr = sr.type; }
-  constexpr int V = vec_of<T>();
-  constexpr int U = unroll_for(MODE, salt::cmax(EA::NL, ER::NL), (int)sizeof(T));
-  auto k1 = std::make_unique<Kernel>();
-  k1->aot = (const void*)&salt::fused_kernel<T, EA, ER, MODE, V, U, kBlock>;
-  k1->vec = V; k1->unroll = U;
-  table()[key_of(dtype_of<T>(), MODE, V, ta, tr)] = std::move(k1);
-  auto k2 = std::make_unique<Kernel>();
-  k2->aot = (const void*)&salt::fused_kernel<T, EA, ER, MODE, 1, kUnrollScalar, kBlock>;
-  k2->vec = 1; k2->unroll = kUnrollScalar;
-  table()[key_of(dtype_of<T>(), MODE, 1, ta, tr)] = std::move(k2);
-}
-
-// Batch kernels (salt_assign_batch) of a single-root assignment tree.
-constexpr int kBatchKind = 3;  // table key "mode" of batch kernels
-template <class T, class EA> void reg_batch_one(const char* asig) {
-  Sig sa;
-  parse_assign(asig, sa);
-  constexpr int V = vec_of<T>();
-  constexpr int U = unroll_for(salt::MODE_ASSIGN, EA::NL, (int)sizeof(T));
-  auto k = std::make_unique<Kernel>();
-  k->aot = (const void*)&salt::batch_kernel<T, EA, V, U, kBlock>;
-  k->vec = V;
-  k->unroll = U;
-  table()[key_of(dtype_of<T>(), kBatchKind, V, sa.type, "batch")] = std::move(k);
-}
-
-// Batched small-reduction kernels (salt_reduce_batch) of a reduce tree.
-constexpr int kBatchReduceKind = 4;
-template <class T, class ER> void reg_batch_reduce_one(const char* rsig) {
-  Sig sr;
-  parse_sig(rsig, 0, sr);
-  constexpr int V = vec_of<T>();
-  constexpr int U = unroll_for(salt::MODE_REDUCE, ER::NL, (int)sizeof(T));
-  auto k = std::make_unique<Kernel>();
-  k->aot = (const void*)&salt::batch_reduce_kernel<T, ER, V, U, kBlock>;
-  k->vec = V;
-  k->unroll = U;
-  table()[key_of(dtype_of<T>(), kBatchReduceKind, V, "batch", sr.type)] = std::move(k);
-}
-
-template <class EA, class ER, int MODE> void reg(const char* asig, const char* rsig) {
-  reg_one<float, EA, ER, MODE>(asig, rsig);
-  reg_one<double, EA, ER, MODE>(asig, rsig);
-  if constexpr (MODE == salt::MODE_ASSIGN) {
-    if constexpr (EA::NL <= salt::BATCH_LEAVES && EA::NS <= salt::BATCH_SCALARS) {
-      reg_batch_one<float, EA>(asig);
-      reg_batch_one<double, EA>(asig);
-    }
-  }
-  if constexpr (MODE == salt::MODE_REDUCE) {
-    if constexpr (ER::NL <= salt::BATCH_LEAVES && ER::NS <= salt::BATCH_SCALARS) {
-      reg_batch_reduce_one<float, ER>(rsig);
-      reg_batch_reduce_one<double, ER>(rsig);
-    }
-  }
-}
-
-using namespace salt;
-// Trees of the reference's named ops (ops.py:18-55) and of BASELINE.json's
-// configs.  The sig string and the C++ type on each line must agree; the GPU
-// tests prove it by comparing every entry against the JIT build of its sig.
-void register_aot() {
-  constexpr int A = MODE_ASSIGN, R = MODE_REDUCE, AR = MODE_ASSIGN_REDUCE;
-  // --- assignments
-  reg<L<0>, None, A>("L0", nullptr);                                      // copy
-  reg<Mul<S<0>, L<0>>, None, A>("S0 L0 *", nullptr);                      // scal / scaled_copy
-  reg<Add<L<0>, Mul<S<0>, L<1>>>, None, A>("L0 S0 L1 * +", nullptr);      // axpy  y + a*x
-  reg<Add<Mul<S<0>, L<0>>, L<1>>, None, A>("S0 L0 * L1 +", nullptr);      // a*x + y
-  reg<Add<L<0>, L<1>>, None, A>("L0 L1 +", nullptr);
-  reg<Sub<L<0>, L<1>>, None, A>("L0 L1 -", nullptr);
-  reg<Mul<L<0>, L<1>>, None, A>("L0 L1 *", nullptr);
-  reg<Add<L<0>, Sub<L<1>, L<2>>>, None, A>("L0 L1 L2 - +", nullptr);      // C2 T1
-  reg<Add<Mul<S<0>, L<0>>, Mul<S<1>, Sub<L<1>, L<2>>>>, None, A>(         // C2 T2
-      "S0 L0 * S1 L1 L2 - * +", nullptr);
-  reg<Add<Sub<Mul<S<0>, Add<L<0>, L<1>>>, Mul<S<1>, Sub<L<2>, L<3>>>>, Mul<S<2>, L<0>>>, None,
-      A>("S0 L0 L1 + * S1 L2 L3 - * - S2 L0 * +", nullptr);               // C4 e-tree
-  reg<Add<Mul<S<0>, L<0>>, Mul<S<1>, L<1>>>, None, A>("S0 L0 * S1 L1 * +", nullptr);  // axpby
-  reg<Sub<L<0>, Mul<S<0>, L<1>>>, None, A>("L0 S0 L1 * -", nullptr);      // y - a*x (CG residual)
-  // --- reductions
-  reg<None, L<0>, R>(nullptr, "L0");                                      // sum
-  reg<None, Mul<L<0>, L<1>>, R>(nullptr, "L0 L1 *");                      // dot
-  reg<None, Mul<L<0>, L<0>>, R>(nullptr, "L0 L0 *");                      // dot(x,x) / nrm2
-  reg<None, Mul<Sub<L<0>, L<1>>, Sub<L<0>, L<1>>>, R>(nullptr, "L0 L1 - L0 L1 - *");  // ||x-y||^2
-  reg<None, Mul<Mul<L<0>, L<1>>, L<2>>, R>(nullptr, "L0 L1 * L2 *");       // weighted dot
-  // --- fused assign + reduce (C5: y = y + a*x ; r = dot(y, z))
-  reg<Add<L<0>, Mul<S<0>, L<1>>>, Mul<D, L<2>>, AR>("L0 S0 L1 * +", "D L2 *");
-  reg<Add<L<0>, Mul<S<0>, L<1>>>, Mul<D, D>, AR>("L0 S0 L1 * +", "D D *");
-  reg<Sub<L<0>, Mul<S<0>, L<1>>>, Mul<D, D>, AR>("L0 S0 L1 * -", "D D *");  // CG: r -= a*q; r.r
-  // CG iteration body in one pass: x += a*p ; r -= a*q ; rr = r.r
-  reg<Multi<Add<L<0>, Mul<S<0>, L<1>>>, Sub<L<2>, Mul<S<1>, L<3>>>>, Mul<Dk<1>, Dk<1>>, AR>(
-      "L0 S0 L1 * + ; L2 S1 L3 * -", "D1 D1 *");
-}
-
-void ensure_table() {
-  static std::once_flag once;
-  std::call_once(once, [] { register_aot(); });
-}
-
-// Compile the tree with NVRTC; returns nullptr + g_err on failure.
-// On-disk cubin cache for JIT kernels: $SALT_JIT_CACHE (default
-// ~/.cache/salt_jit; "off" disables), one file per (source, options, kernel)
-// hash holding the lowered name and the cubin.  Only a start-up cost saver:
-// a miss simply compiles.
-std::string jit_cache_dir() {
-  const char* e = getenv("SALT_JIT_CACHE");
-  if (e && std::string(e) == "off") return "";
-  if (e && *e) return e;
-  const char* home = getenv("HOME");
-  return home ? std::string(home) + "/.cache/salt_jit" : "";
-}
-
-uint64_t fnv1a(const std::string& s, uint64_t h = 1469598103934665603ull) {
-  for (unsigned char c : s) h = (h ^ c) * 1099511628211ull;
-  return h;
-}
-
-bool jit_cache_load(const std::string& path, Kernel& k) {
-  std::ifstream f(path, std::ios::binary);
-  if (!f) return false;
-  std::string name;
-  if (!std::getline(f, name) || name.empty()) return false;
-  std::stringstream ss;
-  ss << f.rdbuf();
-  std::string bin = ss.str();
-  if (bin.size() < 16) return false;
-  k.lowered = name;
-  k.cubin = bin;
-  return true;
-}
-
-void jit_cache_store(const std::string& dir, const std::string& path, const Kernel& k) {
-  mkdir(dir.c_str(), 0755);  // parent of the default dir: ~/.cache
-  // unique per process and thread (the background JIT thread may store too)
-  std::string tmp = path + ".tmp" + std::to_string(getpid()) + "." +
-                    std::to_string(std::hash<std::thread::id>()(std::this_thread::get_id()));
-  {
-    std::ofstream f(tmp, std::ios::binary);
-    if (!f) return;
-    f << k.lowered << "\n";
-    f.write(k.cubin.data(), (std::streamsize)k.cubin.size());
-    if (!f) return;
-  }
-  rename(tmp.c_str(), path.c_str());
-}
-
-// Build (or load from the disk cache) the JIT kernel of a tree; nullptr +
-// g_err on failure.  cache_only: return nullptr on a cache miss instead of
-// compiling.  The caller inserts the result into jit_table().
-std::unique_ptr<Kernel> jit_build(int dtype, int mode, int vec, int nl, const std::string& ta,
-                                  const std::string& tr, bool cache_only) {
-  Nvrtc& nv = nvrtc();
-  if (!nv.ok) { g_err = "NVRTC unavailable: " + nv.why; return nullptr; }
-  const char* tname = dtype == SALT_F32 ? "float" : "double";
-  const bool batch = mode == kBatchKind, batch_reduce = mode == kBatchReduceKind;
-  const int kmode = batch ? salt::MODE_ASSIGN : batch_reduce ? salt::MODE_REDUCE : mode;
-  const int unroll = vec == 1 ? kUnrollScalar
-                     : tuning_unroll() > 0 ? tuning_unroll()
-                     : unroll_for(kmode, nl, dtype == SALT_F32 ? 4 : 8);
-  const std::string tail = std::to_string(vec) + "," + std::to_string(unroll) + "," +
-                           std::to_string(kBlock) + ">";
-  std::string expr =
-      batch ? std::string("salt::batch_kernel<") + tname + "," + ta + "," + tail
-      : batch_reduce ? std::string("salt::batch_reduce_kernel<") + tname + "," + tr + "," + tail
-                     : std::string("salt::fused_kernel<") + tname + "," + ta + "," + tr + "," +
-                           std::to_string(mode) + "," + tail;
-  const std::string minb = "-DSALT_MIN_BLOCKS=" + std::to_string(tuning_minb());
-  const char* opts[8] = {"--gpu-architecture=sm_100a", "-fmad=false", "--std=c++17",
-                         "-lineinfo", "-default-device"};
-  int nopts = 5;
-  if (!nv.has_256bit) opts[nopts++] = "-DSALT_NO_256BIT";
-  if (tuning_minb() > 0 && vec != 1) opts[nopts++] = minb.c_str();
-  std::string cache_path;
-  const std::string cdir = jit_cache_dir();
-  if (!cdir.empty()) {
-    std::string id = expr;
-    for (int i = 0; i < nopts; ++i) id += std::string("|") + opts[i];
-    int maj = 0, min = 0;
-    nv.Version(&maj, &min);
-    id += "|nvrtc" + std::to_string(maj) + "." + std::to_string(min);
-    char hex[32];
-    snprintf(hex, sizeof hex, "%016llx", (unsigned long long)fnv1a(id, fnv1a(kExprSource)));
-    cache_path = cdir + "/" + hex + ".salt";
-    auto k = std::make_unique<Kernel>();
-    if (jit_cache_load(cache_path, *k)) {
-      k->vec = vec;
-      k->unroll = unroll;
-      return k;
-    }
-  }
-  if (cache_only) return nullptr;
-  void* prog = nullptr;
-  if (nv.CreateProgram(&prog, kExprSource, "salt_expr_jit.cu", 0, nullptr, nullptr) != 0) {
-    g_err = "nvrtcCreateProgram failed";
-    return nullptr;
-  }
-  nv.AddNameExpression(prog, expr.c_str());
-  int rc = nv.CompileProgram(prog, nopts, opts);
-  if (rc != 0) {
-    size_t ls = 0;
-    nv.GetProgramLogSize(prog, &ls);
-    std::string log(ls, '\0');
-    nv.GetProgramLog(prog, &log[0]);
-    nv.DestroyProgram(&prog);
-    g_err = "NVRTC compile failed for " + expr + ":\n" + log;
-    return nullptr;
-  }
-  auto k = std::make_unique<Kernel>();
-  size_t cs = 0;
-  nv.GetCUBINSize(prog, &cs);
-  k->cubin.resize(cs);
-  nv.GetCUBIN(prog, &k->cubin[0]);
-  const char* low = nullptr;
-  nv.GetLoweredName(prog, expr.c_str(), &low);
-  k->lowered = low ? low : "";
-  nv.DestroyProgram(&prog);
-  k->vec = vec;
-  k->unroll = unroll;
-  if (!cache_path.empty()) {
-    std::string parent = cdir.substr(0, cdir.find_last_of('/'));
-    if (!parent.empty()) mkdir(parent.c_str(), 0755);
-    jit_cache_store(cdir, cache_path, *k);
-  }
-  return k;
-}
-
-Kernel* jit_insert(const std::string& key, std::unique_ptr<Kernel> k) {
-  std::lock_guard<std::mutex> lk(g_table_mu);
-  auto& slot = jit_table()[key];
-  if (!slot) slot = std::move(k);  // a concurrent build of the same tree may have won
-  return slot.get();
-}
-
-// ---- tiered JIT: a tree outside the compiled-in table runs on the
-// interpreter (same bits, salt_interp.cuh) while a background thread
-// compiles it with NVRTC; later calls find the compiled kernel, so no call
-// waits for NVRTC.  Opt-in (SALT_JIT_ASYNC=1 / salt_set_jit_async(1)): by
-// default fresh trees are built synchronously and no thread is started.
-struct JitJob {
-  int dtype, mode, vec, nl;
-  std::string ta, tr, key;
-};
-struct AsyncJit {
-  std::mutex mu;
-  std::condition_variable cv, idle;
-  std::deque<JitJob> queue;
-  std::unordered_set<std::string> pending, failed;
-  std::unordered_map<std::string, std::string> errors;
-  int active = 0;
-  bool started = false, stopping = false;
-};
-AsyncJit& async_jit() {
-  static AsyncJit* a = new AsyncJit;  // leaked: the worker may outlive static destructors
-  return *a;
-}
-std::atomic<int> g_jit_async{-1};  // -1: not yet read from SALT_JIT_ASYNC
-bool jit_async() {
-  int v = g_jit_async.load(std::memory_order_relaxed);
-  if (v < 0) {
-    const char* e = getenv("SALT_JIT_ASYNC");  // opt-in
-    v = e && atoi(e) != 0 ? 1 : 0;
-    g_jit_async.store(v);
-  }
-  return v == 1;
-}
-
-void jit_worker() {
-  AsyncJit& A = async_jit();
-  for (;;) {
-    JitJob j;
-    {
-      std::unique_lock<std::mutex> lk(A.mu);
-      // never woken once the process exits (see jit_atexit): a thread
-      // returning while exit() tears down the C++ runtime can crash it
-      A.cv.wait(lk, [&] { return !A.queue.empty() && !A.stopping; });
-      j = std::move(A.queue.front());
-      A.queue.pop_front();
-      ++A.active;
-    }
-    std::unique_ptr<Kernel> k = jit_build(j.dtype, j.mode, j.vec, j.nl, j.ta, j.tr, false);
-    std::string err = k ? std::string() : g_err;
-    if (k) jit_insert(j.key, std::move(k));
-    std::lock_guard<std::mutex> lk(A.mu);
-    A.pending.erase(j.key);
-    if (!err.empty()) {
-      A.failed.insert(j.key);
-      A.errors[j.key] = err;
-    }
-    --A.active;
-    if (A.queue.empty() && A.active == 0) A.idle.notify_all();
-  }
-}
-
-// At exit: drop queued builds and let a compile in flight finish (NVRTC
-// must not run while the process tears its libraries down).  The worker is
-// then left blocked on its condition variable — it is never woken again, so
-// it cannot run any code while exit() destroys the runtime.
-void jit_atexit() {
-  AsyncJit& A = async_jit();
-  std::unique_lock<std::mutex> lk(A.mu);
-  A.stopping = true;
-  A.queue.clear();
-  A.pending.clear();
-  A.idle.wait_for(lk, std::chrono::seconds(10), [&] { return A.active == 0; });
-}
-
-// Queue a background build; false if it failed before (g_err = why).
-bool jit_enqueue(JitJob j) {
-  AsyncJit& A = async_jit();
-  std::lock_guard<std::mutex> lk(A.mu);
-  if (A.failed.count(j.key)) {
-    g_err = A.errors[j.key];
-    return false;
-  }
-  if (A.pending.count(j.key)) return true;
-  if (A.stopping) return false;
-  if (!A.started) {
-    A.started = true;
-    std::thread(jit_worker).detach();
-    atexit(jit_atexit);
-  }
-  A.pending.insert(j.key);
-  A.queue.push_back(std::move(j));
-  A.cv.notify_one();
-  return true;
-}
-
-// Look up (or JIT) the kernel; nullptr + g_err on failure.  async: on a
-// miss (table, JIT table and disk cache) queue a background build and return
-// nullptr with *queued = true — the caller runs the interpreter meanwhile.
-Kernel* get_kernel(int dtype, int mode, int vec, int nl, const std::string& ta,
-                   const std::string& tr, bool async = false, bool* queued = nullptr) {
-  ensure_table();
-  const std::string key = key_of(dtype, mode, vec, ta, tr);
-  {
-    std::lock_guard<std::mutex> lk(g_table_mu);
-    if (!g_force_jit.load() && tuning_unroll() <= 0 && tuning_minb() <= 0) {
-      auto it = table().find(key);
-      if (it != table().end()) return it->second.get();
-    }
-    auto jt = jit_table().find(key);
-    if (jt != jit_table().end()) return jt->second.get();
-  }
-  if (async && nvrtc().ok) {
-    if (auto k = jit_build(dtype, mode, vec, nl, ta, tr, true)) return jit_insert(key, std::move(k));
-    if (queued) *queued = jit_enqueue(JitJob{dtype, mode, vec, nl, ta, tr, key});
-    return nullptr;
-  }
-  auto k = jit_build(dtype, mode, vec, nl, ta, tr, false);
-  return k ? jit_insert(key, std::move(k)) : nullptr;
-}
+#include "salt_abi_jit.inc"
 
 std::mutex g_dev_mu;
 
@@ -1304,175 +700,7 @@ int dispatch(int dtype, Plan& p, void* const* dsts, int ndst, const void* const*
                            ws_bytes, out_dev, out_host, st, x, pscalars, npscalars);
 }
 
-// Batched assignments: problem table in the kernel parameters, up to
-// BATCH_MAX problems (and < 2^31 tiles) per launch; trees beyond the batch
-// limits, or without a kernel (no JIT), run one launch per problem.
-template <class T>
-int run_batch(Plan& p, int count, void* const* dsts, const void* const* leaves, int nleaves,
-              const double* scalars, int nscalars, const int64_t* ns, cudaStream_t st) {
-  if (count < 0 || (count > 0 && (!dsts || !ns || (nleaves > 0 && !leaves))))
-    return fail(SALT_EINVAL, "bad batch arguments");
-  for (int q = 0; q < count; ++q) {
-    if (ns[q] < 0) return fail(SALT_EINVAL, "negative length");
-    if (ns[q] == 0) continue;
-    if (!dsts[q]) return fail(SALT_EINVAL, "NULL destination");
-    for (int l = 0; l < p.nl; ++l)
-      if (!leaves[(size_t)q * nleaves + l]) return fail(SALT_EINVAL, "NULL leaf pointer");
-  }
-  Kernel* k = nullptr;
-  const bool batchable = p.sa.nroots == 1 && p.np == 0 && p.nl <= salt::BATCH_LEAVES &&
-                         p.ns <= salt::BATCH_SCALARS;
-  if (batchable) k = get_kernel(dtype_of<T>(), kBatchKind, vec_of<T>(), p.nl, p.sa.type, "batch");
-  if (!k) {  // one fused launch per problem (table, JIT or interpreter kernel)
-    for (int q = 0; q < count; ++q) {
-      if (ns[q] == 0) continue;
-      void* d = dsts[q];
-      int rc = run_fused<T>(p, &d, 1, leaves + (size_t)q * nleaves, nleaves, scalars + (size_t)q * nscalars,
-                            nscalars, ns[q], 0, nullptr, 0, nullptr, nullptr, st, nullptr, nullptr, 0);
-      if (rc) return rc;
-    }
-    return 0;
-  }
-  int dev;
-  int rc = current_device(dev);
-  if (rc) return rc;
-  rc = prepare(k, dev);
-  if (rc) return rc;
-  constexpr int V = vec_of<T>();
-  const i64 per_tile = (i64)kBlock * k->unroll;
-  auto args = std::make_unique<salt::BatchArgs<T>>();  // ~17 KB: not on the stack
-  auto flush = [&]() -> int {
-    if (args->count == 0) return 0;
-    const salt::BatchProblem<T>& last = args->p[args->count - 1];
-    const i64 tiles = last.tile0 + last.nst + (last.nvec + per_tile - 1) / per_tile;
-    int r = launch_raw(k, dev, (int)tiles, args.get(), 0, st);
-    args->count = 0;
-    return r;
-  };
-  memset(args.get(), 0, sizeof(salt::BatchArgs<T>));
-  i64 tile = 0;
-  for (int q = 0; q < count; ++q) {
-    const i64 n = ns[q];
-    if (n == 0) continue;
-    const void* const* lq = leaves + (size_t)q * nleaves;
-    void* dq = dsts[q];
-    int vec;
-    i64 head, nvec;
-    geometry<T>(&dq, 1, lq, p.nl, n, vec, head, nvec);
-    if (vec == 1) {  // operands not sharing one 32-byte alignment: all scalar
-      head = n;
-      nvec = 0;
-    }
-    const i64 nscalar = head + (n - head - nvec * V);
-    const i64 nst = (nscalar + kBlock - 1) / kBlock;
-    const i64 ntiles = nst + (nvec + per_tile - 1) / per_tile;
-    if (args->count == salt::BATCH_MAX || (args->count > 0 && tile + ntiles > i64(0x7fffffff))) {
-      if ((rc = flush())) return rc;
-      tile = 0;
-    }
-    if (ntiles > i64(0x7fffffff)) return fail(SALT_EINVAL, "batch problem too large for one launch");
-    salt::BatchProblem<T>& P = args->p[args->count++];
-    P.dst = (T*)dq;
-    for (int l = 0; l < p.nl; ++l) P.leaf[l] = (const T*)lq[l];
-    for (int c = 0; c < p.ns; ++c) P.sc[c] = (T)scalars[(size_t)q * nscalars + c];
-    P.n = n;
-    P.head = head;
-    P.nvec = nvec;
-    P.tile0 = tile;
-    P.nst = nst;
-    tile += ntiles;
-  }
-  return flush();
-}
-
-// Batched small reductions: problems of <= 2 tiles whose operands share the
-// 32-byte alignment go into batch_reduce_kernel launches (one CTA each, the
-// one-CTA fused order: same bits); the others run as ordinary reductions.
-template <class T>
-int run_reduce_batch(Plan& p, int count, const void* const* leaves, int nleaves, const double* scalars,
-                     int nscalars, const int64_t* ns, int flags, void* const* outs, void* ws,
-                     size_t ws_bytes, cudaStream_t st) {
-  if (count < 0 || (count > 0 && (!ns || !outs || (nleaves > 0 && !leaves))))
-    return fail(SALT_EINVAL, "bad batch arguments");
-  if (flags & ~(SALT_SQRT | SALT_PARTIAL)) return fail(SALT_EINVAL, "reduce flags: SALT_SQRT, SALT_PARTIAL");
-  for (int q = 0; q < count; ++q) {
-    if (ns[q] < 0) return fail(SALT_EINVAL, "negative length");
-    if (!outs[q]) return fail(SALT_EINVAL, "NULL reduction output");
-    for (int l = 0; ns[q] > 0 && l < p.nl; ++l)
-      if (!leaves[(size_t)q * nleaves + l]) return fail(SALT_EINVAL, "NULL leaf pointer");
-  }
-  Kernel* k = nullptr;
-  if (p.np == 0 && p.nl <= salt::BATCH_LEAVES && p.ns <= salt::BATCH_SCALARS)
-    k = get_kernel(dtype_of<T>(), kBatchReduceKind, vec_of<T>(), p.nl, "batch", p.sr.type);
-  int dev, rc;
-  if (k) {
-    if ((rc = current_device(dev)) || (rc = prepare(k, dev))) return rc;
-  }
-  constexpr int V = vec_of<T>();
-  const i64 per_tile = k ? (i64)kBlock * k->unroll : 0;
-  auto args = std::make_unique<salt::BatchArgs<T>>();
-  memset(args.get(), 0, sizeof(salt::BatchArgs<T>));
-  auto flush = [&]() -> int {
-    if (args->count == 0) return 0;
-    void* params[] = {args.get(), &flags};
-    const bool pdl = use_pdl();
-    cudaLaunchConfig_t cfg = {};
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.gridDim = dim3(args->count);
-    cfg.blockDim = dim3(kBlock);
-    cfg.stream = st;
-    cfg.attrs = attr;
-    cfg.numAttrs = pdl ? 1 : 0;
-    if (k->aot) {
-      cudaError_t e = cudaLaunchKernelExC(&cfg, k->aot, params);
-      if (e != cudaSuccess) return cuda_fail(e, "cudaLaunchKernelExC(batch reduce)");
-    } else {
-      CUlaunchConfig c = {};
-      CUlaunchAttribute at[1];
-      at[0].id = CU_LAUNCH_ATTRIBUTE_PROGRAMMATIC_STREAM_SERIALIZATION;
-      at[0].value.programmaticStreamSerializationAllowed = 1;
-      c.gridDimX = (unsigned)args->count;
-      c.gridDimY = c.gridDimZ = 1;
-      c.blockDimX = kBlock;
-      c.blockDimY = c.blockDimZ = 1;
-      c.hStream = (CUstream)st;
-      c.attrs = at;
-      c.numAttrs = pdl && driver().LaunchKernelEx ? 1 : 0;
-      CUresult r = driver().LaunchKernelEx
-                       ? driver().LaunchKernelEx(&c, k->jit_fn[dev], params, nullptr)
-                       : driver().LaunchKernel(k->jit_fn[dev], args->count, 1, 1, kBlock, 1, 1, 0,
-                                               (CUstream)st, params, nullptr);
-      if (r != CUDA_SUCCESS) return fail(SALT_ECUDA, "cuLaunchKernel(batch reduce) failed");
-    }
-    g_launches.fetch_add(1, std::memory_order_relaxed);
-    args->count = 0;
-    return 0;
-  };
-  for (int q = 0; q < count; ++q) {
-    const i64 n = ns[q];
-    const void* const* lq = leaves + (size_t)q * nleaves;
-    int vec = V;
-    i64 head = 0, nvec = 0;
-    if (n > 0) geometry<T>(nullptr, 0, lq, p.nl, n, vec, head, nvec);
-    if (k && vec == V && (nvec + per_tile - 1) / per_tile <= 2) {
-      if (args->count == salt::BATCH_MAX && (rc = flush())) return rc;
-      salt::BatchProblem<T>& P = args->p[args->count++];
-      P.dst = (T*)outs[q];
-      for (int l = 0; l < p.nl; ++l) P.leaf[l] = (const T*)lq[l];
-      for (int c = 0; c < p.ns; ++c) P.sc[c] = (T)scalars[(size_t)q * nscalars + c];
-      P.n = n;
-      P.head = head;
-      P.nvec = nvec;
-      continue;
-    }
-    if ((rc = run_fused<T>(p, nullptr, 0, lq, nleaves, scalars + (size_t)q * nscalars, nscalars, n,
-                           flags, ws, ws_bytes, outs[q], nullptr, st, nullptr, nullptr, 0)))
-      return rc;
-  }
-  return k ? flush() : 0;
-}
+#include "salt_abi_batch.inc"
 
 template <class T>
 int finish(const void* parts, int count, int flags, void* out_dev, void* out_host,
@@ -1490,231 +718,9 @@ int finish(const void* parts, int count, int flags, void* out_dev, void* out_hos
   return 0;
 }
 
-// ------------------------------------------------------------------ single-process multi-GPU
-// NCCL is loaded at run time (no link-time dependency): $SALT_NCCL_LIB, else
-// the soname libnccl.so.2 — which resolves to the copy torch already loaded
-// when torch is in the process — else the system library.
-typedef int ncclResult_v;
-struct Nccl {
-  bool ok = false;
-  std::string why;
-  ncclResult_v (*CommInitAll)(void** comms, int ndev, const int* devlist) = nullptr;
-  ncclResult_v (*CommDestroy)(void* comm) = nullptr;
-  ncclResult_v (*CommCuDevice)(void* comm, int* device) = nullptr;
-  ncclResult_v (*CommCount)(void* comm, int* count) = nullptr;
-  ncclResult_v (*CommUserRank)(void* comm, int* rank) = nullptr;
-  ncclResult_v (*GroupStart)() = nullptr;
-  ncclResult_v (*GroupEnd)() = nullptr;
-  ncclResult_v (*AllGather)(const void* send, void* recv, size_t count, int datatype, void* comm,
-                            cudaStream_t stream) = nullptr;
-  const char* (*GetErrorString)(ncclResult_v) = nullptr;
-};
-constexpr int kNcclFloat64 = 8;  // ncclFloat64 (nccl.h)
+#include "salt_abi_nccl.inc"
 
-Nccl& nccl() {
-  static Nccl n;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    const char* env = getenv("SALT_NCCL_LIB");
-    const char* cands[] = {env, "libnccl.so.2", "/usr/lib/x86_64-linux-gnu/libnccl.so.2"};
-    void* h = nullptr;
-    for (const char* c : cands) {
-      if (!c) continue;
-      h = dlopen(c, RTLD_NOW | RTLD_LOCAL);
-      if (h) break;
-    }
-    if (!h) {
-      n.why = "libnccl.so.2 not found (set SALT_NCCL_LIB)";
-      return;
-    }
-#define SYM(F, NAME)                                        \
-  n.F = reinterpret_cast<decltype(n.F)>(dlsym(h, NAME));    \
-  if (!n.F) { n.why = std::string("nccl symbol missing: ") + NAME; return; }
-    SYM(CommInitAll, "ncclCommInitAll");
-    SYM(CommDestroy, "ncclCommDestroy");
-    SYM(CommCuDevice, "ncclCommCuDevice");
-    SYM(CommCount, "ncclCommCount");
-    SYM(CommUserRank, "ncclCommUserRank");
-    SYM(GroupStart, "ncclGroupStart");
-    SYM(GroupEnd, "ncclGroupEnd");
-    SYM(AllGather, "ncclAllGather");
-    SYM(GetErrorString, "ncclGetErrorString");
-#undef SYM
-    n.ok = true;
-  });
-  return n;
-}
-
-int nccl_fail(ncclResult_v r, const char* what) {
-  return fail(SALT_ECUDA, std::string(what) + ": " + (nccl().GetErrorString ? nccl().GetErrorString(r) : "nccl error"));
-}
-
-// Restores the caller's current device on scope exit.
-struct DeviceGuard {
-  int dev = -1;
-  DeviceGuard() { cudaGetDevice(&dev); }
-  ~DeviceGuard() { if (dev >= 0) cudaSetDevice(dev); }
-};
-
-// G per-device {hi, lo} partials -> every device holds the rank-ordered fold
-// (finish_kernel: the same arithmetic as salt_reduce_finish and the NVLink
-// exchange, so all three multi-GPU paths give identical bits).  One group of
-// G all-gathers of 16 bytes, then one finish kernel per device, all
-// enqueued on the callers' streams; gathered partials live in stream-ordered
-// allocations freed on the same streams.
-int allreduce_sum(void* const* out_dev, int G, int dtype, void* const* comms, void* const* streams,
-                  int flags) {
-  if (G < 1 || !out_dev || !comms || !streams) return fail(SALT_EINVAL, "bad allreduce arguments");
-  if (dtype != SALT_F32 && dtype != SALT_F64) return fail(SALT_EINVAL, "dtype must be SALT_F32 or SALT_F64");
-  if (flags & ~SALT_SQRT) return fail(SALT_EINVAL, "allreduce flags: only SALT_SQRT");
-  Nccl& nc = nccl();
-  if (!nc.ok) return fail(SALT_ECUDA, nc.why);
-  DeviceGuard guard;
-  std::vector<int> devs(G);
-  std::vector<void*> gathered(G, nullptr);
-  auto release = [&]() {
-    for (int g = 0; g < G; ++g)
-      if (gathered[g]) {
-        cudaSetDevice(devs[g]);
-        cudaFreeAsync(gathered[g], (cudaStream_t)streams[g]);
-      }
-  };
-  for (int g = 0; g < G; ++g) {
-    if (!out_dev[g] || !comms[g]) return fail(SALT_EINVAL, "NULL partial or communicator");
-    int count = 0, rank = -1;
-    ncclResult_v r = nc.CommCuDevice(comms[g], &devs[g]);
-    if (!r) r = nc.CommCount(comms[g], &count);
-    if (!r) r = nc.CommUserRank(comms[g], &rank);
-    if (r) return nccl_fail(r, "ncclComm query");
-    if (count != G || rank != g) return fail(SALT_EINVAL, "comms[g] must be rank g of a G-rank communicator");
-  }
-  for (int g = 0; g < G; ++g) {
-    cudaError_t e = cudaSetDevice(devs[g]);
-    if (e == cudaSuccess) e = cudaMallocAsync(&gathered[g], (size_t)G * sizeof(salt::DD), (cudaStream_t)streams[g]);
-    if (e != cudaSuccess) { release(); return cuda_fail(e, "cudaMallocAsync(gathered partials)"); }
-  }
-  ncclResult_v r = nc.GroupStart();
-  for (int g = 0; g < G && !r; ++g)
-    r = nc.AllGather(out_dev[g], gathered[g], 2, kNcclFloat64, comms[g], (cudaStream_t)streams[g]);
-  ncclResult_v r2 = nc.GroupEnd();
-  if (r || r2) { release(); return nccl_fail(r ? r : r2, "ncclAllGather"); }
-  int rc = 0;
-  for (int g = 0; g < G && !rc; ++g) {
-    cudaError_t e = cudaSetDevice(devs[g]);
-    if (e != cudaSuccess) { rc = cuda_fail(e, "cudaSetDevice"); break; }
-    rc = dtype == SALT_F32 ? finish<float>(gathered[g], G, flags, out_dev[g], nullptr, (cudaStream_t)streams[g])
-                           : finish<double>(gathered[g], G, flags, out_dev[g], nullptr, (cudaStream_t)streams[g]);
-  }
-  release();
-  return rc;
-}
-
-// ------------------------------------------------------------------ host streaming
-struct Events {
-  std::vector<cudaEvent_t> ev;
-  ~Events() { for (auto e : ev) cudaEventDestroy(e); }
-  int make(int count) {
-    ev.resize(count, nullptr);
-    for (auto& e : ev) SALT_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    return 0;
-  }
-};
-
-constexpr int kNBuf = 3;
-constexpr i64 kMaxChunk = i64(1) << 23;
-
-// Shared by assign (reduce == false) and reduce: stream chunk c of every
-// operand through buffer c % 3; the fused kernel runs on streams[1].
-int host_pipeline(int dtype, Plan& p, void* host_dst, const void* const* host_leaves,
-                  int nleaves, const double* scalars, int nscalars, i64 n, int flags,
-                  void* staging, size_t staging_bytes, void* const* streams3, void* out_host) {
-  const bool reduce = p.mode != salt::MODE_ASSIGN;   // produces a sum
-  const bool has_dst = p.mode != salt::MODE_REDUCE;  // streams a destination back
-  const size_t esz = dtype == SALT_F32 ? 4 : 8;
-  if (n < 0) return fail(SALT_EINVAL, "negative length");
-  if (!streams3 || !staging) return fail(SALT_EINVAL, "NULL staging or streams");
-  if (!reduce && n == 0) return 0;
-  cudaStream_t sh = (cudaStream_t)streams3[0], sc = (cudaStream_t)streams3[1],
-               sd = (cudaStream_t)streams3[2];
-  if (has_dst && p.sa.nroots != 1)
-    return fail(SALT_EINVAL, "host streaming takes exactly one assignment root");
-  const int nl = p.nl;
-  const int nbufs_per_set = nl + (has_dst ? 1 : 0);
-  // staging: [reduce workspace][chunk partials][result 256B][kNBuf x (nl leaves + dst)]
-  size_t ws = reduce ? salt_reduce_workspace_bytes() : 0;
-  size_t fixed = ws + (reduce ? 256 * 1024 : 0) + 256;
-  if (staging_bytes <= fixed + 256) return fail(SALT_EWORKSPACE, "staging too small");
-  i64 chunk = (i64)((staging_bytes - fixed) / (kNBuf * nbufs_per_set * esz));
-  chunk = chunk / 64 * 64;
-  static const i64 max_chunk = [] {  // SALT_HOST_CHUNK (elements; tuning only)
-    const char* e = getenv("SALT_HOST_CHUNK");
-    const long long v = e ? atoll(e) : 0;
-    return v >= 64 ? (i64)(v / 64 * 64) : kMaxChunk;
-  }();
-  if (chunk > max_chunk) chunk = max_chunk;
-  if (chunk < 64) return fail(SALT_EWORKSPACE, "staging too small for one chunk");
-  const i64 nchunks = (n + chunk - 1) / chunk;
-  if (reduce && nchunks * (i64)sizeof(salt::DD) > 256 * 1024)
-    return fail(SALT_EWORKSPACE, "too many chunks for the partial buffer; enlarge staging");
-  char* base = (char*)staging;
-  void* wsp = base;
-  salt::DD* parts = (salt::DD*)(base + ws);
-  void* result = base + ws + (reduce ? 256 * 1024 : 0);
-  char* bufs = base + fixed;
-  auto buf = [&](int b, int i) -> void* {
-    return bufs + ((size_t)b * nbufs_per_set + i) * chunk * esz;
-  };
-  if (reduce) SALT_CUDA(cudaMemsetAsync(wsp, 0, SALT_WORKSPACE_TICKET_BYTES, sc));
-  Events h2d, comp, d2h;
-  int rc = h2d.make(kNBuf);
-  if (!rc) rc = comp.make(kNBuf);
-  if (!rc) rc = d2h.make(kNBuf);
-  if (rc) return rc;
-  for (i64 c = 0; c < nchunks; ++c) {
-    const int b = (int)(c % kNBuf);
-    const i64 off = c * chunk;
-    const i64 m = std::min(chunk, n - off);
-    if (c >= kNBuf) SALT_CUDA(cudaStreamWaitEvent(sh, comp.ev[b], 0));
-    const void* dleaves[salt::MAX_LEAVES];
-    for (int l = 0; l < nl; ++l) {
-      SALT_CUDA(cudaMemcpyAsync(buf(b, l), (const char*)host_leaves[l] + off * esz, m * esz,
-                                cudaMemcpyHostToDevice, sh));
-      dleaves[l] = buf(b, l);
-    }
-    SALT_CUDA(cudaEventRecord(h2d.ev[b], sh));
-    SALT_CUDA(cudaStreamWaitEvent(sc, h2d.ev[b], 0));
-    if (has_dst && c >= kNBuf) SALT_CUDA(cudaStreamWaitEvent(sc, d2h.ev[b], 0));
-    void* ddst = has_dst ? buf(b, nl) : nullptr;
-    rc = dispatch(dtype, p, &ddst, has_dst ? 1 : 0, dleaves, nleaves, scalars, nscalars, m,
-                  reduce ? SALT_PARTIAL : 0, wsp, ws, reduce ? (void*)(parts + c) : nullptr,
-                  nullptr, sc);
-    if (rc) return rc;
-    SALT_CUDA(cudaEventRecord(comp.ev[b], sc));
-    if (has_dst) {
-      SALT_CUDA(cudaStreamWaitEvent(sd, comp.ev[b], 0));
-      SALT_CUDA(cudaMemcpyAsync((char*)host_dst + off * esz, ddst, m * esz,
-                                cudaMemcpyDeviceToHost, sd));
-      SALT_CUDA(cudaEventRecord(d2h.ev[b], sd));
-    }
-  }
-  if (reduce) {
-    if (nchunks == 0) {
-      // zero length: the sum is dtype(0) (test_engine.py:147-153)
-      void* hdst = host_dst;
-      rc = dispatch(dtype, p, &hdst, has_dst ? 1 : 0, host_leaves, nleaves, scalars, nscalars, 0, flags, wsp, ws,
-                    result, out_host, sc);
-      if (rc) return rc;
-    } else {
-      rc = dtype == SALT_F32 ? finish<float>(parts, (int)nchunks, flags, result, out_host, sc)
-                             : finish<double>(parts, (int)nchunks, flags, result, out_host, sc);
-      if (rc) return rc;
-    }
-  }
-  SALT_CUDA(cudaStreamSynchronize(sh));
-  SALT_CUDA(cudaStreamSynchronize(sc));
-  SALT_CUDA(cudaStreamSynchronize(sd));
-  return 0;
-}
+#include "salt_abi_host.inc"
 
 }  // namespace
 
