@@ -33,6 +33,7 @@ import torch
 import torch.distributed as dist
 
 from .lanes import as_dtype
+from .sugar import VectorOps
 from .vectors import DenseVector
 
 __all__ = ["shard_bounds", "ShardedVector", "SHARD_ALIGN"]
@@ -124,7 +125,7 @@ def _world(group):
     return 1, 0
 
 
-class ShardedVector:
+class ShardedVector(VectorOps):
     """A global vector of `global_len` elements; this rank holds `local`."""
 
     __slots__ = ("local", "global_len", "lo", "hi", "group", "world", "rank")
@@ -210,30 +211,6 @@ class ShardedVector:
 
         execute_assign(AssignNode(Leaf(self), as_node(expression)), **options)
 
-    def __add__(self, other):
-        from .expressions import add_nodes
-
-        return add_nodes(self, other)
-
-    def __sub__(self, other):
-        from .expressions import sub_nodes
-
-        return sub_nodes(self, other)
-
-    def __mul__(self, other):
-        from .expressions import mul_nodes
-
-        return mul_nodes(self, other)
-
-    def __rmul__(self, other):
-        from .expressions import scale_node
-
-        return scale_node(other, self)
-
-    def __neg__(self):
-        from .expressions import negate_node
-
-        return negate_node(self)
 
     def __repr__(self):
         return (

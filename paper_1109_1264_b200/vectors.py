@@ -22,6 +22,7 @@ import numpy as np
 import torch
 
 from .lanes import DEVICE_ALIGNMENT, as_dtype
+from .sugar import VectorOps
 
 __all__ = ["DenseVector", "DeviceScalar", "default_device", "torch_dtype"]
 
@@ -67,7 +68,7 @@ def _aligned_empty(n: int, dt: np.dtype, device: torch.device) -> torch.Tensor:
     return raw[start : start + n]
 
 
-class DenseVector:
+class DenseVector(VectorOps):
     """Fixed-length contiguous f32/f64 vector (reference vectors.py:18-31)."""
 
     # _ptr/_dev/_n/_code cache what the C fast path (csrc/fastpath.c) reads
@@ -208,31 +209,7 @@ class DenseVector:
 
         execute_assign(AssignNode(Leaf(self), as_node(expression)), **plan_kwargs)
 
-    # Arithmetic builds lazy nodes (reference vectors.py:109-138).
-    def __add__(self, other):
-        from .expressions import add_nodes
-
-        return add_nodes(self, other)
-
-    def __sub__(self, other):
-        from .expressions import sub_nodes
-
-        return sub_nodes(self, other)
-
-    def __mul__(self, other):
-        from .expressions import mul_nodes
-
-        return mul_nodes(self, other)
-
-    def __rmul__(self, other):
-        from .expressions import scale_node
-
-        return scale_node(other, self)
-
-    def __neg__(self):
-        from .expressions import negate_node
-
-        return negate_node(self)
+    # Arithmetic builds lazy nodes: sugar.VectorOps (reference vectors.py:109-138).
 
     __array_ufunc__ = None
 
