@@ -23,6 +23,7 @@ vector up to the ≤ 1 ulp compensated-sum bound (expressions.py:401-480).
 """
 
 import ctypes
+import sys
 
 import numpy as np
 import torch
@@ -66,6 +67,10 @@ class DeviceGroup:
         self.close()
 
     def __del__(self):
+        # not during interpreter shutdown: CUDA / NCCL may already be torn
+        # down, and the process is about to release everything anyway
+        if sys.is_finalizing():
+            return
         try:
             self.close()
         except Exception:
