@@ -219,7 +219,7 @@ def fastpath():
                     # raw C getters: CUDA is initialised once a device vector exists
                     torch._C._cuda_getCurrentRawStream, torch._C._cuda_getDevice,
                     runtime._workspace, np.float32, np.float64, runtime._lazy_out,
-                    addr(h.salt_assign_batch),
+                    addr(h.salt_assign_batch), addr(h.salt_reduce_batch), runtime._batch_out,
                 )
                 _fast = _fastpath
             except (ImportError, AttributeError):

@@ -42,6 +42,8 @@ typedef int (*fused_fn)(int, const char*, const char*, void* const*, int, const 
                         void*, void*, void*);
 typedef int (*assign_batch_fn)(int, const char*, int, void* const*, const void* const*, int,
                                const double*, int, const int64_t*, void*);
+typedef int (*reduce_batch_fn)(int, const char*, int, const void* const*, int, const double*, int,
+                               const int64_t*, int, void* const*, void*, size_t, void*);
 typedef const char* (*last_error_fn)(void);
 
 static assign_fn p_assign;
@@ -49,6 +51,8 @@ static reduce_fn p_reduce;
 static assign_reduce_fn p_assign_reduce;
 static fused_fn p_fused;
 static assign_batch_fn p_assign_batch;
+static reduce_batch_fn p_reduce_batch;
+static PyObject* batch_out; /* runtime._batch_out(device, count) -> (tensor, data_ptr) */
 static last_error_fn p_last_error;
 static size_t ws_bytes;
 
@@ -673,14 +677,134 @@ done:
   return result;
 }
 
+/* Walk one reduction child: the first leaf fixes device / dtype / length
+ * (as fp_reduce).  1 ok, 0 not eligible, -1 error. */
+static int walk_child(Walk* w, PyObject* child) {
+  memset(w, 0, sizeof *w);
+  PyObject* first = child;
+  while ((PyObject*)Py_TYPE(first) != T_Leaf && (PyObject*)Py_TYPE(first) != T_Dense) {
+    PyObject* t = (PyObject*)Py_TYPE(first);
+    if (t != T_Scale && t != T_Add && t != T_Sub && t != T_Mul) return 0;
+    PyObject* nxt = PyObject_GetAttr(first, t == T_Scale ? s_child : s_left);
+    if (!nxt) { PyErr_Clear(); return 0; }
+    Py_DECREF(nxt); /* nodes are kept alive by their parents */
+    first = nxt;
+  }
+  PyObject* v0 = (PyObject*)Py_TYPE(first) == T_Leaf ? PyObject_GetAttr(first, s_vector) : (Py_INCREF(first), first);
+  if (!v0) return -1;
+  int rc = start(w, v0, NULL);
+  Py_DECREF(v0);
+  if (rc <= 0) return rc;
+  return walk(w, child);
+}
+
+/* reduce_batch([child, ...], flags) -> (out_tensor, [slot index per child])
+ * or None: lv.reduce_batch's common case in C — every child eligible for
+ * fp_reduce and on the current device, no device scalars; grouped by
+ * (element type, signature), one salt_reduce_batch call per group, result
+ * q in 16-byte slot q of out_tensor (element type at its start). */
+static PyObject* fp_reduce_batch(PyObject* self, PyObject* args) {
+  PyObject* list;
+  int flags;
+  if (!PyArg_ParseTuple(args, "O!i", &PyList_Type, &list, &flags)) return NULL;
+  if (!p_reduce_batch || !batch_out) Py_RETURN_NONE;
+  const Py_ssize_t m = PyList_GET_SIZE(list);
+  if (m == 0) Py_RETURN_NONE;
+  Group* gs = NULL;
+  int ng = 0, capg = 0, dev = -1;
+  int* gid = PyMem_Malloc(m * sizeof(int));
+  Py_ssize_t* pos = PyMem_Malloc(m * sizeof(Py_ssize_t));
+  PyObject *result = NULL, *out = NULL, *slots = NULL;
+  if (!gid || !pos) { PyErr_NoMemory(); goto done; }
+  Walk w;
+  for (Py_ssize_t i = 0; i < m; ++i) {
+    int rc = walk_child(&w, PyList_GET_ITEM(list, i));
+    if (rc < 0) goto done;
+    if (rc == 0 || w.nps || w.nvec == 0 || (dev >= 0 && w.dev != dev)) { Py_INCREF(Py_None); result = Py_None; goto done; }
+    dev = w.dev;
+    int g = 0;
+    for (; g < ng; ++g)
+      if (gs[g].code == w.code && gs[g].nl == w.nvec && gs[g].nsc == w.nsc && strcmp(gs[g].sig, w.sig) == 0)
+        break;
+    if (g == ng) {
+      if (ng == capg) {
+        int cap = capg ? 2 * capg : 4;
+        Group* n = PyMem_Realloc(gs, cap * sizeof(Group));
+        if (!n) { PyErr_NoMemory(); goto done; }
+        gs = n;
+        capg = cap;
+      }
+      memset(&gs[ng], 0, sizeof(Group));
+      gs[ng].code = w.code;
+      gs[ng].nl = w.nvec;
+      gs[ng].nsc = w.nsc;
+      gs[ng].sig = PyMem_Malloc((size_t)w.len + 1);
+      if (!gs[ng].sig) { PyErr_NoMemory(); goto done; }
+      memcpy(gs[ng].sig, w.sig, (size_t)w.len + 1);
+      ++ng;
+    }
+    gid[i] = g;
+    pos[i] = gs[g].count;
+    if (group_push(&gs[g], NULL, &w) < 0) goto done;
+  }
+  {
+    void* stream;
+    w.dev = dev;
+    int rc = stream_for(&w, &stream);
+    if (rc < 0) goto done;
+    if (rc == 0) { Py_INCREF(Py_None); result = Py_None; goto done; }
+    PyObject* r = PyObject_CallFunction(batch_out, "in", dev, m);
+    if (!r) goto done;
+    out = PyTuple_GetItem(r, 0);
+    void* base = PyLong_AsVoidPtr(PyTuple_GetItem(r, 1));
+    Py_XINCREF(out);
+    Py_DECREF(r);
+    if (!out || PyErr_Occurred()) goto done;
+    void *ws, *slot;
+    if (workspace(&w, stream, &ws, &slot) < 0) goto done;
+    /* slot of child i: groups are laid out one after another */
+    Py_ssize_t off = 0;
+    for (int g = 0; g < ng; ++g) {
+      for (Py_ssize_t q = 0; q < gs[g].count; ++q) gs[g].dsts[q] = (char*)base + 16 * (off + q);
+      int e = p_reduce_batch(gs[g].code, gs[g].sig, (int)gs[g].count, (const void* const*)gs[g].leaves,
+                             gs[g].nl, gs[g].sc, gs[g].nsc, gs[g].ns, flags, gs[g].dsts, ws, ws_bytes,
+                             stream);
+      if (e != 0) {
+        PyErr_Format(PyExc_RuntimeError, "libsalt error %d: %s", e, p_last_error());
+        goto done;
+      }
+      gs[g].cap = off; /* reuse: group start slot */
+      off += gs[g].count;
+    }
+    slots = PyList_New(m);
+    if (!slots) goto done;
+    for (Py_ssize_t i = 0; i < m; ++i) {
+      PyObject* v = PyLong_FromSsize_t(gs[gid[i]].cap + pos[i]);
+      if (!v) goto done;
+      PyList_SET_ITEM(slots, i, v);
+    }
+    result = PyTuple_Pack(2, out, slots);
+  }
+done:
+  Py_XDECREF(out);
+  Py_XDECREF(slots);
+  PyMem_Free(gid);
+  PyMem_Free(pos);
+  groups_free(gs, ng);
+  return result;
+}
+
 static PyObject* fp_init(PyObject* self, PyObject* args) {
-  unsigned long long a, r, ar, fu, le, ab;
+  unsigned long long a, r, ar, fu, le, ab, rb;
   Py_ssize_t wsb;
-  if (!PyArg_ParseTuple(args, "KKKKKnOOOOOOOOOOOOOK", &a, &r, &ar, &fu, &le, &wsb, &T_Leaf, &T_Add,
+  if (!PyArg_ParseTuple(args, "KKKKKnOOOOOOOOOOOOOKKO", &a, &r, &ar, &fu, &le, &wsb, &T_Leaf, &T_Add,
                         &T_Sub, &T_Mul, &T_Scale, &T_Dense, &T_DevScalar, &get_stream,
-                        &current_device, &workspace_fn, &np_f32, &np_f64, &lazy_out, &ab))
+                        &current_device, &workspace_fn, &np_f32, &np_f64, &lazy_out, &ab, &rb,
+                        &batch_out))
     return NULL;
   p_assign_batch = (assign_batch_fn)(uintptr_t)ab;
+  p_reduce_batch = (reduce_batch_fn)(uintptr_t)rb;
+  Py_INCREF(batch_out);
   PyObject* keep[] = {T_Leaf, T_Add, T_Sub, T_Mul, T_Scale, T_Dense, T_DevScalar, get_stream,
                       current_device, workspace_fn, np_f32, np_f64, lazy_out};
   for (size_t i = 0; i < sizeof keep / sizeof keep[0]; ++i) Py_INCREF(keep[i]);
@@ -703,6 +827,8 @@ static PyMethodDef methods[] = {
      "op(sig, dest_or_None, leaves, alpha_or_None, flags, lazy=False) -> True / result, or None"},
     {"assign_batch", fp_assign_batch, METH_VARARGS,
      "assign_batch([(dest, source), ...]) -> statements launched, or None"},
+    {"reduce_batch", fp_reduce_batch, METH_VARARGS,
+     "reduce_batch([child, ...], flags) -> (out_tensor, slots), or None"},
     {"fused", fp_fused, METH_VARARGS,
      "fused(((dest, source), ...), total_child_or_None, flags, lazy=False) -> (result,) or None"},
     {NULL, NULL, 0, NULL}};

@@ -170,23 +170,25 @@ def reduce_batch(expressions, *, sqrt=False, lazy=False) -> list:
     has the bits of its own `execute_reduce(SumNode(expression))` (sqrt=True:
     of `norm2`).  lazy=True returns DeviceScalars."""
     from .engine import _lower_sum
-    from .runtime import run_reduce_batch
+    from .runtime import batch_results, run_reduce_batch
 
+    expressions = list(expressions)
+    flags = _native.SALT_SQRT if sqrt else 0
+    fast = _native.fastpath()
+    if fast is not None and expressions:
+        roots = [SumNode(as_node(e)) for e in expressions]  # validates dtypes
+        dts = {r.dtype for r in roots}
+        if len(dts) == 1:
+            r = fast.reduce_batch([root.child for root in roots], flags)  # C: walk, group, launch
+            if r is not None:
+                return batch_results(r[0], r[1], dts.pop(), lazy)
     items = [_lower_sum(e) for e in expressions]
-    return run_reduce_batch(items, flags=_native.SALT_SQRT if sqrt else 0, lazy=lazy)
+    return run_reduce_batch(items, flags=flags, lazy=lazy)
 
 
 def dot_batch(pairs, *, lazy=False) -> list:
     """[dot(x, y) for x, y in pairs] through reduce_batch (same bits).
     Pairs of plain DenseVectors of one element type and equal lengths skip
     the node objects; anything else goes through the full validation."""
-    from .runtime import _PairLowering, run_reduce_batch
-    from .vectors import DenseVector
-
     pairs = list(pairs)
-    items = []
-    for x, y in pairs:
-        if type(x) is not DenseVector or type(y) is not DenseVector or x.dtype != y.dtype or len(x) != len(y):
-            return reduce_batch([MulNode(as_node(a), as_node(b)) for a, b in pairs], lazy=lazy)
-        items.append((_PairLowering(x, y), x.dtype, len(x)))
-    return run_reduce_batch(items, lazy=lazy)
+    return reduce_batch([MulNode(as_node(x), as_node(y)) for x, y in pairs], lazy=lazy)

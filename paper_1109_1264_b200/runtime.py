@@ -335,19 +335,26 @@ def run_assign_batch(items):
     return batched
 
 
-class _PairLowering:
-    """The lowering of x*y (or x*x) for plain device vectors, without node
-    objects (ops.dot_batch's fast path): same signature and leaves as
-    expressions.lower(MulNode(x, y))."""
+def _batch_out(index: int, count: int):
+    """(tensor, data pointer) of count 16-byte result slots on a device (the
+    C fast path's reduce_batch)."""
+    t = torch.empty(2 * count, dtype=torch.float64, device=torch.device("cuda", index))
+    return t, t.data_ptr()
 
-    __slots__ = ("tokens", "vectors", "scalars", "pscalars")
 
-    def __init__(self, x, y):
-        same = x is y
-        self.tokens = ["L0", "L0", "*"] if same else ["L0", "L1", "*"]
-        self.vectors = [x] if same else [x, y]
-        self.scalars = []
-        self.pscalars = []
+def batch_results(out, slots, dt, lazy):
+    """Element-typed results from the 16-byte slots of `out` (one copy to
+    the host unless lazy)."""
+    dt = as_dtype(dt)
+    if lazy:
+        return [DeviceScalar(out[2 * q:2 * q + 1].view(torch.float32)[:1] if dt.itemsize == 4
+                             else out[2 * q:2 * q + 1], dt) for q in slots]
+    host = out.cpu().numpy()
+    if dt.itemsize == 8:
+        vals = host[0::2]
+    else:
+        vals = host.view(np.float32)[0::4]
+    return [vals[q] for q in slots]
 
 
 def run_reduce_batch(items, flags=0, lazy=False):

@@ -32,6 +32,9 @@ def test_fast_path_keeps_reference_counts_and_memory_flat():
         lv.axpy_dot(0.25, A, B, C, lazy=True)
         lv.fused((B, B - al * A), (C, C + al * A), C * C, lazy=True)
         D.assign(al * A + B)
+        lv.assign_batch([(D, A + C), (B, B * 0.5)])
+        lv.dot_batch([(A, B), (C, C)])
+        lv.reduce_batch([A - C, B * 2.0], lazy=True)
 
     for _ in range(2000):  # warm: JIT, workspaces, allocator pools
         calls()
