@@ -25,6 +25,14 @@ __device__ __forceinline__ void ld4_ef(double (&r)[4], const double* p) {
   asm volatile("ld.global.L1::no_allocate.L2::evict_first.v4.f64 {%0,%1,%2,%3}, [%4];"
                : "=d"(r[0]), "=d"(r[1]), "=d"(r[2]), "=d"(r[3]) : "l"(p));
 }
+__device__ __forceinline__ void ld4_pf(double (&r)[4], const double* p) {
+  asm volatile("ld.global.L1::no_allocate.L2::256B.v4.f64 {%0,%1,%2,%3}, [%4];"
+               : "=d"(r[0]), "=d"(r[1]), "=d"(r[2]), "=d"(r[3]) : "l"(p));
+}
+__device__ __forceinline__ void ld4_nc(double (&r)[4], const double* p) {
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f64 {%0,%1,%2,%3}, [%4];"
+               : "=d"(r[0]), "=d"(r[1]), "=d"(r[2]), "=d"(r[3]) : "l"(p));
+}
 __device__ __forceinline__ void st4(double* p, const double (&r)[4]) {
   asm volatile("st.global.L1::no_allocate.v4.f64 [%0], {%1,%2,%3,%4};"
                :: "l"(p), "d"(r[0]), "d"(r[1]), "d"(r[2]), "d"(r[3]) : "memory");
@@ -107,6 +115,32 @@ __global__ void __launch_bounds__(BLOCK) kC(double* d, const double* a, const do
   for (int u = 0; u < UNR; ++u) {
     i64 j = base + (i64)u * BLOCK;
     if (j < nvec) { ld4(x[u], a + 4 * j); ld4(y[u], b + 4 * j); ld4(z[u], c + 4 * j); }
+  }
+#pragma unroll
+  for (int u = 0; u < UNR; ++u) {
+    i64 j = base + (i64)u * BLOCK;
+    if (j < nvec) {
+      double r[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) r[k] = f(x[u][k], y[u][k], z[u][k], al, be);
+      st4(d + 4 * j, r);
+    }
+  }
+}
+
+// Variant E: variant C with a load hint: 1 = L2::256B prefetch, 2 = ld.global.nc.
+template <int UNR, int BLOCK, int LH>
+__global__ void __launch_bounds__(BLOCK) kE(double* d, const double* a, const double* b,
+                                            const double* c, double al, double be, i64 nvec) {
+  i64 base = (i64)blockIdx.x * BLOCK * UNR + threadIdx.x;
+  double x[UNR][4], y[UNR][4], z[UNR][4];
+#pragma unroll
+  for (int u = 0; u < UNR; ++u) {
+    i64 j = base + (i64)u * BLOCK;
+    if (j < nvec) {
+      if (LH == 1) { ld4_pf(x[u], a + 4 * j); ld4_pf(y[u], b + 4 * j); ld4_pf(z[u], c + 4 * j); }
+      else { ld4_nc(x[u], a + 4 * j); ld4_nc(y[u], b + 4 * j); ld4_nc(z[u], c + 4 * j); }
+    }
   }
 #pragma unroll
   for (int u = 0; u < UNR; ++u) {
@@ -281,6 +315,14 @@ int main() {
     run("C one-tile-per-CTA unr2 blk256", [&] { k<<<(unsigned)g, 256>>>(d, a, b, c, 1.25, -0.75, nvec); }); }
   { auto k = kC<1, 256>; i64 g = (nvec + 255) / 256;
     run("C one-tile-per-CTA unr1 blk256", [&] { k<<<(unsigned)g, 256>>>(d, a, b, c, 1.25, -0.75, nvec); }); }
+  { auto k = kE<2, 256, 1>; i64 g = (nvec + 511) / 512;
+    run("E one-tile unr2 L2::256B prefetch", [&] { k<<<(unsigned)g, 256>>>(d, a, b, c, 1.25, -0.75, nvec); }); }
+  { auto k = kE<2, 256, 2>; i64 g = (nvec + 511) / 512;
+    run("E one-tile unr2 ld.global.nc", [&] { k<<<(unsigned)g, 256>>>(d, a, b, c, 1.25, -0.75, nvec); }); }
+  { auto k = kC<2, 512>; i64 g = (nvec + 1023) / 1024;
+    run("C one-tile-per-CTA unr2 blk512", [&] { k<<<(unsigned)g, 512>>>(d, a, b, c, 1.25, -0.75, nvec); }); }
+  { auto k = kC<4, 128>; i64 g = (nvec + 511) / 512;
+    run("C one-tile-per-CTA unr4 blk128", [&] { k<<<(unsigned)g, 128>>>(d, a, b, c, 1.25, -0.75, nvec); }); }
   { auto k = kD<2, 256>; int o = occ((const void*)k, 256, 0); int g = sms * o; char nm[96];
     snprintf(nm, 96, "D persistent+prefetch unr2 occ%d", o);
     run(nm, [&] { k<<<g, 256>>>(d, a, b, c, 1.25, -0.75, nvec); }); }
