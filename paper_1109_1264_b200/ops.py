@@ -117,6 +117,17 @@ def fused(*statements, lazy=False):
 
     Same results as running them one after another (later statements see
     earlier assignments); returns the sum, or None without one."""
+    # common case straight to the C fast path, without node objects (it
+    # declines anything unusual; the node path below then validates/raises)
+    pairs = statements if statements and isinstance(statements[-1], tuple) else statements[:-1]
+    if 1 <= len(pairs) <= _native.SALT_MAX_ROOTS and all(
+            isinstance(st, tuple) and len(st) == 2 for st in pairs):
+        fast = _native.fastpath()
+        if fast is not None:
+            total = None if pairs is statements else statements[-1]
+            r = fast.fused(pairs, total, 0, lazy)
+            if r is not None:
+                return r[0]
     assigns, total = [], None
     for k, st in enumerate(statements):
         if isinstance(st, tuple) and len(st) == 2:
