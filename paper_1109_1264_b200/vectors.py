@@ -204,6 +204,12 @@ class DenseVector(VectorOps):
     # ------------------------------------------------------------ evaluation
     def assign(self, expression, **plan_kwargs) -> None:
         """Evaluate a lazy expression into this vector in one fused pass."""
+        if not plan_kwargs:  # the C fast path first: no AssignNode / Leaf objects
+            from ._native import fastpath
+
+            fast = fastpath()
+            if fast is not None and fast.assign(self, expression):
+                return
         from .engine import execute_assign
         from .expressions import AssignNode, Leaf, as_node
 
