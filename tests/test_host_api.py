@@ -369,3 +369,24 @@ def test_no_cuda_fails_loudly():
         lv.dot(x, y)
     with pytest.raises(RuntimeError):
         y.assign(as_node(x) + as_node(y))
+
+
+def test_assign_batch_validation_on_the_host():
+    """assign_batch validates every statement before anything runs: pair
+    shape, element types, lengths, and no destination shared with another
+    statement (engine._check_assign_batch; no GPU needed)."""
+    from paper_1109_1264_b200.engine import _check_assign_batch
+
+    x, y, z = hv(np.arange(4.0)), hv(np.arange(4.0)), hv(np.zeros(4))
+    items = _check_assign_batch([(y, as_node(y) + x), (z, as_node(x) * 2.0)])
+    assert [" ".join(lw.tokens) for lw, *_ in items] == ["L0 L1 +", "S0 L0 *"]
+    with pytest.raises(ValueError, match="reads the destination"):
+        _check_assign_batch([(y, as_node(y) + x), (z, as_node(y) - x)])
+    with pytest.raises(ValueError, match="same destination"):
+        _check_assign_batch([(z, as_node(x) + y), (z, as_node(y) + x)])
+    with pytest.raises(LengthMismatchError):
+        _check_assign_batch([(z, as_node(x) + hv(np.arange(3.0)))])
+    with pytest.raises(TypeError):
+        _check_assign_batch([(z, as_node(x) + hv(np.arange(4.0), "f64"))])
+    with pytest.raises(TypeError):
+        _check_assign_batch([z])
