@@ -162,3 +162,36 @@ def test_reduce_batch_one_launch_for_many_small_dots():
     l0 = _launches()
     lv.dot_batch(pairs, lazy=True)
     assert _launches() - l0 == 2   # 192 problems = 2 launches of 96
+
+
+def test_batches_with_special_values_match_single_calls():
+    """±0, ±inf, NaN, subnormals and huge values: batched results have the
+    bits of the single calls (NaN positions for NaN)."""
+    specials = np.array([0.0, -0.0, np.inf, -np.inf, np.nan, 5e-324, 1e308, -1e308, 1.0, -2.5])
+    g = np.random.default_rng(13)
+    for dt in ("f64", "f32"):
+        npdt = np.float64 if dt == "f64" else np.float32
+        pairs, sts, outs_b, outs_s = [], [], [], []
+        for k in range(40):
+            n = int(g.integers(1, 3000))
+            x = g.uniform(-1, 1, n)
+            y = g.uniform(-1, 1, n)
+            if k % 3 == 0:
+                idx = g.integers(0, n, size=min(n, 4))
+                x[idx] = g.choice(specials, size=len(idx))
+            X = lv.DenseVector.from_values(x.astype(npdt), dt)
+            Y = lv.DenseVector.from_values(y.astype(npdt), dt)
+            pairs.append((X, Y))
+            ob, os_ = lv.DenseVector.zeros(n, dt), lv.DenseVector.zeros(n, dt)
+            sts.append((ob, 0.75 * lv.expressions.as_node(X) - Y))
+            outs_b.append(ob)
+            outs_s.append((os_, X, Y))
+        got = lv.dot_batch(pairs)
+        want = [lv.dot(x, y) for x, y in pairs]
+        for a, b in zip(got, want):
+            assert (np.isnan(a) and np.isnan(b)) or a.tobytes() == b.tobytes(), (dt, a, b)
+        lv.assign_batch(sts)
+        for ob, (os_, X, Y) in zip(outs_b, outs_s):
+            os_.assign(0.75 * X - Y)
+            a, b = ob.to_array(), os_.to_array()
+            assert np.array_equal(a, b, equal_nan=True) and np.array_equal(np.signbit(a), np.signbit(b))
