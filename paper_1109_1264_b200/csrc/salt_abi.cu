@@ -581,7 +581,7 @@ int run_fused(Plan& p, void* const* dsts, int ndst, const void* const* leaves, i
   // assignments take one BLOCK*UNR tile per CTA — the block scheduler
   // refills an SM the moment a CTA retires, which keeps loads in flight
   // (7.29 TB/s vs 7.06 for a persistent grid-stride loop); reductions take
-  // kReduceTilesPerCta tiles per CTA and combine per-CTA partials in two
+  // reduce_tiles_per_cta() tiles per CTA and combine per-CTA partials in two
   // deterministic ticket levels (7.25 vs 6.88 TB/s persistent, fused
   // axpy->dot f64 2^28).  Both grids depend only on n.
   const i64 per_tile = (i64)kBlock * k->unroll;
