@@ -36,6 +36,10 @@ CASES = {
     # BASELINE config 3 at its smaller size (one combine group of 512 CTAs)
     "nrm2_64_mid": (torch.float64, 1 << 24, 1),
     "dot64_mid": (torch.float64, 1 << 24, 2),
+    # the interpreter fallback on config 2's tree (salt_set_force_interp)
+    "interp_t2": (torch.float64, 1 << 28, 4),
+    # 256 axpys of 4096 elements in one batched launch (lv.assign_batch)
+    "batch_axpy": (torch.float64, 4096, 512),
 }
 
 
@@ -64,12 +68,21 @@ def main():
         "daxpy20": lambda: lv.axpy(0.5, v[0], v[1]),
         "nrm2_64_mid": lambda: lv.norm2(v[0], lazy=True),
         "dot64_mid": lambda: lv.dot(v[0], v[1], lazy=True),
+        "interp_t2": lambda: v[3].assign(1.25 * v[0] + -0.75 * (v[1] - v[2])),
+        "batch_axpy": lambda: lv.assign_batch(batch),
     }
+    batch = [(v[2 * i + 1], lv.expressions.as_node(v[2 * i + 1]) + 0.5 * v[2 * i]) for i in range(k // 2)] \
+        if a.case == "batch_axpy" else []
+    if a.case == "interp_t2":
+        from paper_1109_1264_b200 import _native
+
+        _native.lib().salt_set_force_interp(1)
     if a.time:
         import json
 
         per = {"t2": 4, "t1": 4, "dot64": 2, "dot32": 2, "nrm2_32": 1, "nrm2_64": 1, "cgupdate": 6,
-               "etree32": 5, "axpydot": 4, "daxpy20": 3, "nrm2_64_mid": 1, "dot64_mid": 2}[a.case]
+               "etree32": 5, "axpydot": 4, "daxpy20": 3, "nrm2_64_mid": 1, "dot64_mid": 2,
+               "interp_t2": 4, "batch_axpy": 3 * 256}[a.case]
         nbytes = per * n * torch.empty(0, dtype=dt).element_size()
         for _ in range(3):
             calls[a.case]()
