@@ -28,7 +28,7 @@ from .expressions import (
 )
 
 __all__ = ["dot", "scal", "axpy", "scaled_copy", "sum", "norm2", "axpy_dot", "fused", "assign_batch",
-           "reduce_batch", "dot_batch", "jit_wait"]
+           "reduce_batch", "dot_batch", "norm2_batch", "jit_wait"]
 
 
 def _op(sig, dest, leaves, alpha=None, flags=0, lazy=False):
@@ -203,3 +203,8 @@ def dot_batch(pairs, *, lazy=False) -> list:
     the node objects; anything else goes through the full validation."""
     pairs = list(pairs)
     return reduce_batch([MulNode(as_node(x), as_node(y)) for x, y in pairs], lazy=lazy)
+
+
+def norm2_batch(vectors, *, lazy=False) -> list:
+    """[norm2(x) for x in vectors] through reduce_batch (same bits)."""
+    return reduce_batch([MulNode(as_node(x), as_node(x)) for x in vectors], sqrt=True, lazy=lazy)

@@ -148,6 +148,7 @@ def test_reduce_batch_bits_equal_individual_reductions(dt):
     assert np.array(got).tobytes() == np.array(want).tobytes()
     nr = lv.reduce_batch([lv.expressions.as_node(x) * x for x in xs], sqrt=True)
     assert np.array(nr).tobytes() == np.array([lv.norm2(x) for x in xs]).tobytes()
+    assert np.array(lv.norm2_batch(xs)).tobytes() == np.array(nr).tobytes()
     lazy = lv.dot_batch(pairs[:40], lazy=True)
     assert np.array([d.item() for d in lazy]).tobytes() == np.array(want[:40]).tobytes()
     ex = restate.exact_sum(pairs[1][0].to_array().astype(np.float64) * pairs[1][1].to_array())
