@@ -217,7 +217,11 @@ def measure(op, variant, n, dtype="f32", reps=25, warmup=5, seed=0, packages=Non
     # Device variants without an L2 flush: below 64 MB of traffic a call
     # lasts a few microseconds, close to the ~1-2 us tick of the event
     # clock, so one rep times `inner` back-to-back calls and divides.
-    inner = 1 if host or flush is not None or bytes_moved(op, n, dt) >= (64 << 20) else 16
+    # In-place ops (scal, axpy, axpy_dot) keep one call per rep, so every
+    # call starts from the restored operand, as in the reference
+    # (bench.py:156-170).
+    inner = 1 if host or flush is not None or mutated is not None or bytes_moved(op, n, dt) >= (64 << 20) \
+        else 16
     times = []
     for _ in range(reps):
         restore()

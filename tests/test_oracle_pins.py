@@ -139,3 +139,61 @@ def test_default_plans_match_survey_table():
         restate.footprint_of("S0 L0 L1 + * S1 L2 L3 - * - S2 L0 * +", "assign"), "f32") == (1, 16)
     assert restate.default_plan(restate.footprint_of("L0 L1 *", "sum"), "f32") == (4, 16)
     assert restate.default_plan(restate.footprint_of("L0", "sum"), "f64") == (8, 8)
+
+
+# ---- the reference's scalar-loop oracles (oracle.py:26-69), restated in
+# oracle/restate.py as test infrastructure: the reference's test names, our
+# own cases
+def test_oracle_dot():
+    from oracle import restate
+
+    assert restate.oracle_dot([1.0, -2.0, 0.5], [4.0, 0.25, 8.0]) == 7.5
+
+
+def test_oracle_sum():
+    from oracle import restate
+
+    assert restate.oracle_sum(np.arange(1.0, 11.0)) == 55.0
+
+
+def test_oracle_scal():
+    from oracle import restate
+
+    assert list(restate.oracle_scal(-0.5, [2.0, 4.0, -6.0])) == [-1.0, -2.0, 3.0]
+
+
+def test_oracle_axpy():
+    from oracle import restate
+
+    assert list(restate.oracle_axpy(2.0, [1.0, 2.0], [10.0, 20.0])) == [12.0, 24.0]
+
+
+def test_oracle_scaled_copy():
+    from oracle import restate
+
+    assert list(restate.oracle_scaled_copy(3.0, [1.5, -1.0])) == [4.5, -3.0]
+
+
+def test_oracles_preserve_element_type():
+    from oracle import restate
+
+    x32 = np.array([1.0, 2.0], np.float32)
+    assert type(restate.oracle_dot(x32, x32)) is np.float32
+    assert all(type(v) is np.float32 for v in restate.oracle_scal(np.float32(2), x32))
+
+
+def test_kahan_sum_trivia():
+    from oracle import restate
+
+    assert restate.kahan_sum([]) == 0 and restate.kahan_sum([2.5]) == 2.5
+
+
+def test_kahan_sum_beats_naive_summation():
+    from oracle import restate
+
+    vals = np.array([1.0] + [1e-16] * 10_000, dtype=np.float64)
+    naive = 0.0
+    for v in vals:
+        naive += v
+    exact = 1.0 + 1e-12
+    assert abs(restate.kahan_sum(vals) - exact) < abs(naive - exact)
