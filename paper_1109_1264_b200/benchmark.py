@@ -314,6 +314,9 @@ def main(argv=None) -> int:
     ap.add_argument("--csv", default="-")
     ap.add_argument("--packages", type=int, default=None,
                     help="accepted and validated like the reference's (bench.py:294-295)")
+    ap.add_argument("--cache-sizes", default=None,
+                    help="comma list of cache sizes in bytes, written to <csv>.meta for plotting "
+                         "(reference bench.py:295-297; ignored on stdout)")
     ap.add_argument("--flush-l2", action="store_true")
     ap.add_argument("--extended", action="store_true")
     a = ap.parse_args(argv)
@@ -336,6 +339,12 @@ def main(argv=None) -> int:
             ap.error("--sizes expects non-negative integers")
     if a.reps < 1 or a.warmup < 0:
         ap.error("--reps must be >= 1 and --warmup >= 0")
+    caches = None
+    if a.cache_sizes is not None:
+        try:
+            caches = [int(c) for c in a.cache_sizes.split(",") if c]
+        except ValueError:
+            ap.error(f"--cache-sizes expects integers, got {a.cache_sizes!r}")
     records = run_sweep(ops, variants, sizes, a.type, a.reps, a.warmup, a.seed, packages=a.packages,
                         flush_l2=a.flush_l2)
     try:
@@ -343,6 +352,15 @@ def main(argv=None) -> int:
     except OSError as exc:
         print(f"error: cannot write CSV to {a.csv}: {exc}", file=sys.stderr)
         return 1
+    if caches is not None:
+        if a.csv == "-":
+            print("note: --cache-sizes ignored when the CSV goes to stdout", file=sys.stderr)
+            return 0
+        try:
+            Path(a.csv + ".meta").write_text("cache_sizes_bytes," + ",".join(map(str, caches)) + "\n")
+        except OSError as exc:
+            print(f"error: cannot write {a.csv}.meta: {exc}", file=sys.stderr)
+            return 1
     return 0
 
 

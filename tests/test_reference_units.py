@@ -439,3 +439,16 @@ def test_cli_writes_csv(tmp_path, monkeypatch):
 
 def test_simd_available_reports_backend_capability():
     assert sb.simd_available("f32") == default_backend("f32").caps.specialized
+
+
+def test_cli_cache_sizes_sidecar(tmp_path, monkeypatch):
+    monkeypatch.setattr(sb, "run_sweep", lambda *a, **k: [])
+    f = tmp_path / "c.csv"
+    assert sb.main(["--op", "dot", "--sizes", "8", "--csv", str(f), "--cache-sizes", "49152,2097152"]) == 0
+    assert (tmp_path / "c.csv.meta").read_text() == "cache_sizes_bytes,49152,2097152\n"
+
+
+def test_cli_cache_sizes_ignored_on_stdout(capsys, monkeypatch):
+    monkeypatch.setattr(sb, "run_sweep", lambda *a, **k: [])
+    assert sb.main(["--op", "dot", "--sizes", "8", "--cache-sizes", "1024"]) == 0
+    assert "ignored" in capsys.readouterr().err
