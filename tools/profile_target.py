@@ -36,6 +36,12 @@ CASES = {
     # BASELINE config 3 at its smaller size (one combine group of 512 CTAs)
     "nrm2_64_mid": (torch.float64, 1 << 24, 1),
     "dot64_mid": (torch.float64, 1 << 24, 2),
+    "nrm2_32_mid": (torch.float32, 1 << 24, 1),
+    "dot32_mid": (torch.float32, 1 << 24, 2),
+    # config 2 at the small end of its sweep (L2-resident sizes)
+    "t1_20": (torch.float64, 1 << 20, 4),
+    "t2_20": (torch.float64, 1 << 20, 4),
+    "t2_22": (torch.float64, 1 << 22, 4),
     # the interpreter fallback on config 2's tree (salt_set_force_interp)
     "interp_t2": (torch.float64, 1 << 28, 4),
     # 256 axpys of 4096 elements in one batched launch (lv.assign_batch)
@@ -68,6 +74,11 @@ def main():
         "daxpy20": lambda: lv.axpy(0.5, v[0], v[1]),
         "nrm2_64_mid": lambda: lv.norm2(v[0], lazy=True),
         "dot64_mid": lambda: lv.dot(v[0], v[1], lazy=True),
+        "nrm2_32_mid": lambda: lv.norm2(v[0], lazy=True),
+        "dot32_mid": lambda: lv.dot(v[0], v[1], lazy=True),
+        "t1_20": lambda: v[3].assign(v[0] + (v[1] - v[2])),
+        "t2_20": lambda: v[3].assign(1.25 * v[0] + -0.75 * (v[1] - v[2])),
+        "t2_22": lambda: v[3].assign(1.25 * v[0] + -0.75 * (v[1] - v[2])),
         "interp_t2": lambda: v[3].assign(1.25 * v[0] + -0.75 * (v[1] - v[2])),
         "batch_axpy": lambda: lv.assign_batch(batch),
     }
@@ -82,6 +93,7 @@ def main():
 
         per = {"t2": 4, "t1": 4, "dot64": 2, "dot32": 2, "nrm2_32": 1, "nrm2_64": 1, "cgupdate": 6,
                "etree32": 5, "axpydot": 4, "daxpy20": 3, "nrm2_64_mid": 1, "dot64_mid": 2,
+               "nrm2_32_mid": 1, "dot32_mid": 2, "t1_20": 4, "t2_20": 4, "t2_22": 4,
                "interp_t2": 4, "batch_axpy": 3 * 256}[a.case]
         nbytes = per * n * torch.empty(0, dtype=dt).element_size()
         for _ in range(3):
