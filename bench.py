@@ -18,6 +18,22 @@ Arms
                      same per-element IEEE ops) with all host threads, each
                      step a bounded sample of the workload; rank 0 only.
 
+Multi-GPU block (every line of the default arm, unless --no-multi): the
+north_star's multi-GPU claims, measured at the run's N:
+  config4   e = alpha*(a + b) - beta*(c - d) + gamma*a, f32, 2^30 elements
+            GLOBAL, block-sharded over the N ranks (strong scaling), no
+            communication; max-over-ranks device time, aggregate GB/s and the
+            fraction of N x the measured HBM peak;
+  config5   y = alpha*x + y; r = dot(y, z), f64, 2^31 elements GLOBAL,
+            block-sharded, 100 fused axpy->dot steps on ShardedVectors with
+            the cross-rank reduction of every step inside the timed region;
+            ms/step, the exchange route that ran, and whether r_100 is
+            bit-identical on every rank.
+
+--gpus is authoritative: under torchrun WORLD_SIZE must equal it (else exit
+2); without torchrun, --gpus N > 1 re-executes this script under
+torch.distributed.run with N ranks (exit 2 if fewer than N GPUs exist).
+
 Output: one JSON line on rank 0 (see the keys below).
 """
 
@@ -83,8 +99,10 @@ def _traffic():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled every 25 ms (about ten
-    samples inside the default ~240 ms timed region)."""
+    """nvidia-smi clocks / throttle reasons sampled every 10 ms.  Windows are
+    delimited by mark() pairs; the headline region of a short run (the
+    driver's --steps 20 is ~24 ms) holds only a few samples, so the line
+    also carries the window over the multi-GPU block (about a second)."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -100,7 +118,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-i", str(self.index), "-lms", "25"],
+                 "-i", str(self.index), "-lms", "10"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except FileNotFoundError:
             self.proc = None
@@ -123,11 +141,16 @@ class ClockSampler:
             except Exception:
                 self.proc.kill()
 
-    def summary(self):
+    def summary(self, window=0):
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        t0, t1 = (self.marks + [0, 0])[:2] if len(self.marks) >= 2 else (0, float("inf"))
-        inside = [s for t, s in self.samples if t0 <= t <= t1] or [s for _, s in self.samples]
+        if len(self.marks) >= 2 * window + 2:
+            t0, t1 = self.marks[2 * window], self.marks[2 * window + 1]
+        else:
+            t0, t1 = 0, float("inf")
+        inside = [s for t, s in self.samples if t0 <= t <= t1]
+        if not inside:  # region shorter than the sampling period: nearest sample
+            inside = [min(self.samples, key=lambda ts: abs(ts[0] - t0))[1]]
         sm, smax, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for s in inside:
@@ -195,6 +218,49 @@ def cpu_reference_gbs(n_sample, steps, warmup, threads, seconds_cap=None):
     return 32.0 * n_sample / per / 1e9, per, len(t)
 
 
+LANEVEC_SNIPPET = r"""
+import json, os, sys, time
+import numpy as np
+sys.path.insert(0, sys.argv[1])
+sys.path.insert(1, sys.argv[2])
+os.sched_setaffinity(0, {min(os.sched_getaffinity(0))})
+import lanevec as lv
+from paper_1109_1264_b200 import synth
+n = int(sys.argv[3])
+al, be = synth.scalars(2, 2)
+a, b, c = (lv.DenseVector.from_values(synth.block(2, k, 0, n, np.float64), "f64") for k in range(3))
+d = lv.DenseVector.zeros(n, "f64")
+d.assign(al * a + be * (b - c))
+ts = []
+for _ in range(3):
+    t0 = time.perf_counter()
+    d.assign(al * a + be * (b - c))
+    ts.append(time.perf_counter() - t0)
+print(json.dumps({"best_s": min(ts), "n": n}))
+"""
+
+
+def lanevec_1core(n=1 << 20):
+    """The UNMODIFIED reference engine (lanevec, pip-installed into
+    baseline/_ref) on one host core: config 2's tree at n = 2^20 through its
+    own public API (DenseVector / operator tree / assign, default plan) —
+    BASELINE.md §3's CPU plan, reference bench.py:144-192.  None when
+    baseline/_ref is absent."""
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "lanevec").exists():
+        return None
+    try:
+        r = subprocess.run([sys.executable, "-c", LANEVEC_SNIPPET, str(ref), str(ROOT), str(n)],
+                           capture_output=True, text=True, timeout=300)
+        d = json.loads(r.stdout.strip().splitlines()[-1])
+    except Exception as exc:  # reported, not fatal: the port is the arm's number
+        return {"error": f"{type(exc).__name__}: {exc}"[:200]}
+    return {"value": round(32.0 * n / d["best_s"] / 1e9, 4), "unit": "GB/s", "cores": 1,
+            "kind": "reference",
+            "sample": f"best of 3 lanevec DenseVector assigns of config 2's tree at n = {n} f64 "
+                      "(unmodified reference engine from baseline/_ref, default plan, one core)"}
+
+
 def run_reference(args, world, rank):
     if rank != 0:
         return
@@ -224,6 +290,7 @@ def run_reference(args, world, rank):
         "e2e": {"value": round(gbs, 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
+    line["cpu_baseline"]["lanevec_1core"] = lanevec_1core()
     print(json.dumps(line), flush=True)
 
 
@@ -282,8 +349,7 @@ def run_gpu(args, world, rank, local):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     elapsed_max = float(t.item())
-    sampler.stop()
-    clocks = sampler.summary()
+    clocks = sampler.summary(0)
 
     bytes_step = 32.0 * n
     value = world * bytes_step * args.steps / (elapsed_max / 1e3) / 1e9
@@ -334,6 +400,17 @@ def run_gpu(args, world, rank, local):
         }
         del hv, hd, ha, hb, hc
 
+    del vecs, a, b, c, d
+    torch.cuda.empty_cache()
+    multi = None
+    if not args.no_multi:
+        sampler.mark()
+        multi = {"config4": run_config4(world, rank, dev, peak),
+                 "config5": run_config5(world, rank, dev)}
+        sampler.mark()
+        multi["clocks"] = sampler.summary(1)
+    sampler.stop()
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         threads = _host_threads()
@@ -341,7 +418,8 @@ def run_gpu(args, world, rank, local):
         gbs, per, done = cpu_reference_gbs(n_sample, 1000, 1, threads, seconds_cap=15)
         cpu = {"value": round(gbs, 3), "unit": "GB/s", "cores": threads, "kind": "port",
                "sample": f"{done} evaluations of the tree on {n_sample} f64 elements "
-                         "(oracle/salt_oracle.c, reference per-node tile evaluation)"}
+                         "(oracle/salt_oracle.c, reference per-node tile evaluation)",
+               "lanevec_1core": lanevec_1core()}
 
     if rank == 0:
         line = {
@@ -383,8 +461,159 @@ def run_gpu(args, world, rank, local):
             "e2e": e2e,
             "gpu_launches": int(launches),
             "clocks": clocks,
+            "multi_gpu": multi,
         }
         print(json.dumps(line), flush=True)
+
+
+def _timed_region(world, dev, fn, steps, warmup):
+    """warmup untimed calls, then `steps` calls between a barrier +
+    synchronize on both sides; (device time in ms — CUDA events on the
+    launching stream, max over ranks — and libsalt launches in the region)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1109_1264_b200 import _native
+
+    for _ in range(warmup):
+        fn(True)
+    stream = torch.cuda.current_stream(dev)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    l0 = _native.lib().salt_launch_count()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        fn(False)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    launches = _native.lib().salt_launch_count() - l0
+    if world > 1:
+        dist.barrier()
+    t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item()), launches
+
+
+def run_config4(world, rank, dev, peak, steps=20, warmup=3):
+    """BASELINE config 4: strong scaling of a global 2^30 f32 e-tree."""
+    import torch
+
+    import paper_1109_1264_b200 as lv
+    from paper_1109_1264_b200 import synth
+    from paper_1109_1264_b200.sharding import shard_bounds
+
+    n = 1 << 30
+    lo, hi = shard_bounds(n, world, rank)
+    al, be, ga = synth.scalars(4, 3)
+    ops = []
+    for k in range(4):
+        v = lv.DenseVector.empty(hi - lo, "f32", device=dev)
+        synth.fill_device_philox(v.tensor, 4, k, lo)
+        ops.append(lv.ShardedVector(v, n))
+    a, b, c, d = ops
+    e = lv.ShardedVector(lv.DenseVector.empty(hi - lo, "f32", device=dev), n)
+    torch.cuda.synchronize(dev)
+    ms, launches = _timed_region(world, dev, lambda _w: e.assign(al * (a + b) - be * (c - d) + ga * a),
+                                 steps, warmup)
+    nbytes = 20.0 * n  # 4 distinct f32 reads + 1 write per element, global
+    value = nbytes * steps / (ms / 1e3) / 1e9
+    del ops, a, b, c, d, e
+    torch.cuda.empty_cache()
+    return {
+        "workload": "config4: e = alpha*(a + b) - beta*(c - d) + gamma*a, f32, n = 2^30 GLOBAL, "
+                    "block-sharded over the ranks",
+        "scaling": "strong", "collective": "none",
+        "n_global": n, "n_per_rank": hi - lo if world == 1 else shard_bounds(n, world, 0)[1],
+        "steps": steps, "warmup": warmup,
+        "ms_per_step": round(ms / steps, 5),
+        "value": round(value, 3), "unit": "GB/s",
+        "algorithmic_bytes_per_step": int(nbytes),
+        "frac_of_aggregate_peak": round(value / (world * peak), 4),
+        "gpu_launches": int(launches),
+        "data": "synthetic, device Philox streams keyed per global 2^24 chunk (synth.fill_device_philox)",
+    }
+
+
+def run_config5(world, rank, dev, iters=100, warmup=3):
+    """BASELINE config 5: 100 fused axpy->dot steps on a global 2^31 f64
+    vector triple, block-sharded, with a cross-rank reduction per step."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1109_1264_b200 as lv
+    from paper_1109_1264_b200 import sharding, synth
+    from paper_1109_1264_b200.sharding import shard_bounds
+
+    n = 1 << 31
+    lo, hi = shard_bounds(n, world, rank)
+    alpha = synth.scalars(5, 1)[0]
+    vecs = []
+    for k in range(3):
+        v = lv.DenseVector.empty(hi - lo, "f64", device=dev)
+        synth.fill_device_philox(v.tensor, 5, k, lo)
+        vecs.append(lv.ShardedVector(v, n))
+    X, Y, Z = vecs
+    torch.cuda.synchronize(dev)
+    out = {}
+
+    def step(warm):
+        # warm-up steps use alpha = 0: y + 0*x == y bit for bit, so the timed
+        # 100 iterations start from the generated y
+        out["r"] = lv.axpy_dot(0.0 if warm else alpha, X, Y, Z, lazy=True)
+
+    ms, launches = _timed_region(world, dev, step, iters, warmup)
+    r100 = float(out["r"].item())
+    bits = torch.tensor([np.float64(r100).view(np.int64)], dtype=torch.int64, device=dev)
+    same = True
+    if world > 1:
+        allb = [torch.empty_like(bits) for _ in range(world)]
+        dist.all_gather(allb, bits)
+        same = all(int(b.item()) == int(bits.item()) for b in allb)
+    route = sharding.exchange_route()
+    peer = any(x is not None for x in sharding._exchanges.values())
+    nbytes = 32.0 * n  # x, y, z read + y written, f64, global
+    del vecs, X, Y, Z
+    torch.cuda.empty_cache()
+    return {
+        "workload": "config5: y = alpha*x + y; r = dot(y, z), f64, n = 2^31 GLOBAL, block-sharded, "
+                    "100 fused axpy->dot steps (lv.axpy_dot on ShardedVectors, lazy results)",
+        "scaling": "strong",
+        "collective": ("in-kernel NVLink peer exchange" if peer else
+                       "NCCL all-gather of per-rank double-double partials + salt_reduce_finish")
+                      + " per step, inside the timed region",
+        "exchange_route": "peer" if peer else route,
+        "n_global": n, "iterations": iters, "warmup": warmup,
+        "ms_per_step": round(ms / iters, 5),
+        "value": round(nbytes * iters / (ms / 1e3) / 1e9, 3), "unit": "GB/s",
+        "algorithmic_bytes_per_step": int(nbytes),
+        "r_100": r100.hex(),
+        "r_100_identical_on_all_ranks": bool(same),
+        "gpu_launches": int(launches),
+        "data": "synthetic, device Philox streams keyed per global 2^24 chunk (synth.fill_device_philox)",
+    }
+
+
+def _launch_ranks(args, argv):
+    """--gpus N > 1 without torchrun: re-run this script as N ranks."""
+    import socket
+
+    import torch
+
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but this host has {have} GPU(s)", file=sys.stderr)
+        sys.exit(2)
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve())] + list(argv)
+    sys.exit(subprocess.run(cmd).returncode)
 
 
 def main(argv=None):
@@ -396,12 +625,24 @@ def main(argv=None):
     ap.add_argument("--n", type=int, default=1 << 28)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-multi", action="store_true",
+                    help="skip the config-4 / config-5 multi-GPU block")
     ap.add_argument("--n-sample", type=int, default=1 << 25,
                     help="elements per step of the --impl reference CPU sample")
-    args = ap.parse_args(argv)
+    raw_argv = list(sys.argv[1:] if argv is None else argv)
+    args = ap.parse_args(raw_argv)
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus < 1:
+        ap.error("--gpus must be >= 1")
+    under_torchrun = "WORLD_SIZE" in os.environ
+    if under_torchrun and int(os.environ["WORLD_SIZE"]) != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but torchrun started WORLD_SIZE="
+              f"{os.environ['WORLD_SIZE']} ranks", file=sys.stderr)
+        sys.exit(2)
     _ensure_built()
+    if args.impl == "salt" and not under_torchrun and args.gpus > 1:
+        _launch_ranks(args, raw_argv)
     if args.impl == "reference":
         world = int(os.environ.get("WORLD_SIZE", "1"))
         rank = int(os.environ.get("RANK", "0"))

@@ -375,6 +375,10 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
 // each does only after finishing its epoch-e reads, so a slot is never
 // overwritten while it is still being read.
 __device__ DD exchange_dd(DD mine, const Xchg& x) {
+  DD nan; nan.hi = __longlong_as_double(0x7ff8000000000000ll); nan.lo = 0.0;
+  // A previous exchange of this rank timed out: the protocol's epochs are
+  // out of step, so touch no slot (a late peer may have reused it) — NaN.
+  if (x.error && *(volatile unsigned int*)x.error) return nan;
   const int par = (int)(x.epoch & 1ull);
   for (int p = 0; p < x.world; ++p) {
     volatile DD* dst = (volatile DD*)(x.slots[p] + par * XCHG_MAX_RANKS + x.rank);
@@ -389,9 +393,7 @@ __device__ DD exchange_dd(DD mine, const Xchg& x) {
     while (ld_acquire_sys(x.flags[x.rank] + q) < x.epoch) {
       if (x.timeout_ns && globaltimer_ns() - t0 > x.timeout_ns) {
         if (x.error) *x.error = 1u;
-        acc.hi = __longlong_as_double(0x7ff8000000000000ll);  // NaN: the peer never arrived
-        acc.lo = 0.0;
-        return acc;
+        return nan;  // the peer never arrived
       }
     }
     volatile DD* src = (volatile DD*)(x.slots[x.rank] + par * XCHG_MAX_RANKS + q);

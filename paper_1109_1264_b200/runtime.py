@@ -431,6 +431,12 @@ def _device_reduce(dev, dt, call, flags, lazy, sharded=None, xcall=None):
         desc = xchg.next()
         _native.check(xcall(flags, ws.data_ptr(), ws.numel(), ctypes.addressof(desc),
                             out.data_ptr(), hptr, stream))
+        if lazy:
+            return DeviceScalar(out.view(torch.float32)[:1] if dt.itemsize == 4 else out, dt,
+                                guard=xchg.check)
+        result = _result(dt, out, host, lazy)
+        xchg.check(result)  # NaN + the error word: a peer never arrived
+        return result
     else:
         part = torch.empty(2, dtype=torch.float64, device=out.device)
         _native.check(call(flags | _native.SALT_PARTIAL, ws.data_ptr(), ws.numel(), part.data_ptr(),

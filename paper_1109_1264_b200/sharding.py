@@ -12,17 +12,30 @@ communication.  Reductions exchange one double-double total per rank and
 every rank folds them in rank order — deterministic and identical on all
 ranks — by one of two routes:
 
-  peer  (default on GPUs with symmetric memory): the reduction kernel's last
-        CTA writes its total straight into every peer's symmetric buffer
-        over NVLink, raises a flag there, waits for all peers' flags and
-        folds — the collective happens inside the reduction kernel
-        (salt_reduce_exchange), no NCCL launch, no host involvement;
-  nccl  (fallback, and gloo on CPU): the kernel writes its partial
+  nccl  (default, and gloo on CPU): the kernel writes its partial
         (SALT_PARTIAL), a 16-byte all-gather collects them, and
-        salt_reduce_finish folds them.
+        salt_reduce_finish folds them;
+  peer  (opt-in: SALT_EXCHANGE=peer, GPUs with symmetric memory): the
+        reduction kernel's last CTA writes its total straight into every
+        peer's symmetric buffer over NVLink, raises a flag there, waits for
+        all peers' flags and folds — the collective happens inside the
+        reduction kernel (salt_reduce_exchange), no NCCL launch, no host
+        involvement.
 
 Both fold the same values in the same order, so they give identical bits.
-SALT_EXCHANGE=nccl forces the fallback.
+
+Failure behaviour of the peer route (it must never return a wrong number):
+  * the ranks agree on the route: after building its buffers every rank
+    contributes an ok flag to one all_reduce(MIN); if any rank failed, every
+    rank falls back to the all-gather;
+  * a peer that does not arrive within the timeout (SALT_PEER_TIMEOUT_MS,
+    default 60 s) makes the kernel write NaN and set a sticky error word;
+    the host sees the NaN, reads the word and raises RuntimeError — at once
+    for host results, at DeviceScalar.item() for lazy ones;
+  * the error word poisons the exchange on the device: every later
+    exchange kernel of that rank returns NaN at once without touching the
+    peer slots (no read of a slot a later epoch has overwritten), and the
+    host refuses further exchanges on that group.
 """
 
 import os
@@ -36,7 +49,7 @@ from .lanes import as_dtype
 from .sugar import VectorOps
 from .vectors import DenseVector
 
-__all__ = ["shard_bounds", "ShardedVector", "SHARD_ALIGN"]
+__all__ = ["shard_bounds", "ShardedVector", "SHARD_ALIGN", "exchange_route"]
 
 SHARD_ALIGN = 64
 
@@ -60,7 +73,7 @@ class PeerExchange:
 
     TIMEOUT_NS = 60_000_000_000  # a peer that never arrives yields NaN, not a hang
 
-    def __init__(self, group, device):
+    def __init__(self, group, device, timeout_ns=None):
         import torch.distributed._symmetric_memory as symm_mem
 
         from ._native import XCHG_BUFFER_BYTES, XCHG_MAX_RANKS, Exchange
@@ -84,28 +97,59 @@ class PeerExchange:
         self.desc = Exchange()
         self.desc.rank = self.rank
         self.desc.world = self.world
-        self.desc.timeout_ns = self.TIMEOUT_NS
+        if timeout_ns is None:
+            ms = os.environ.get("SALT_PEER_TIMEOUT_MS")
+            timeout_ns = int(float(ms) * 1e6) if ms else self.TIMEOUT_NS
+        self.desc.timeout_ns = int(timeout_ns)
         self.desc.error = self.error.data_ptr()
         for p, base in enumerate(ptrs):
             self.desc.slots[p] = base                     # DD[2][8]
             self.desc.flags[p] = base + 2 * XCHG_MAX_RANKS * 16  # u64[8]
         self.epoch = 0
+        self.failed = False
 
     def next(self):
         """Descriptor for the next exchange (epochs advance in SPMD order)."""
+        if self.failed:
+            raise RuntimeError(self._message())
         self.epoch += 1
         self.desc.epoch = self.epoch
         return self.desc
+
+    def _message(self):
+        return (f"NVLink peer exchange of rank {self.rank}/{self.world} failed: a peer did not "
+                f"arrive within {self.desc.timeout_ns / 1e6:.0f} ms (epoch {self.epoch}); the "
+                "exchange is disabled for this group — rerun with SALT_EXCHANGE=nccl")
+
+    def check(self, value=None):
+        """Raise if the exchange timed out.  `value` is the reduction result
+        (host scalar): the kernel writes NaN on a timeout, so only a NaN
+        result costs a read of the device error word."""
+        if value is not None and value == value:  # not NaN: cannot be a timeout
+            return
+        if self.failed or int(self.error.item()) != 0:
+            self.failed = True
+            raise RuntimeError(self._message())
 
 
 _exchanges = {}
 _exchange_lock = threading.Lock()
 
 
+def exchange_route() -> str:
+    """'nccl' (default) or 'peer' (SALT_EXCHANGE=peer)."""
+    route = os.environ.get("SALT_EXCHANGE", "nccl")
+    if route not in ("nccl", "peer"):
+        raise ValueError(f"SALT_EXCHANGE must be 'nccl' or 'peer', got {route!r}")
+    return route
+
+
 def peer_exchange(group, device):
     """The PeerExchange of (group, device), or None when peer exchange is
-    unavailable or disabled (then reductions use the NCCL all-gather)."""
-    if os.environ.get("SALT_EXCHANGE", "peer") != "peer" or device.type != "cuda":
+    disabled (the default) or unavailable on any rank of the group (then
+    reductions use the NCCL all-gather).  Collective on first use: every
+    rank of the group must reach it (they do — reductions are SPMD)."""
+    if exchange_route() != "peer" or device.type != "cuda":
         return None
     if not (dist.is_available() and dist.is_initialized()):
         return None
@@ -113,9 +157,13 @@ def peer_exchange(group, device):
     with _exchange_lock:
         if key not in _exchanges:
             try:
-                _exchanges[key] = PeerExchange(group, device)
+                xchg = PeerExchange(group, device)
             except Exception:
-                _exchanges[key] = None
+                xchg = None
+            # one route for the whole group: peer only if every rank built it
+            ok = torch.tensor([1 if xchg is not None else 0], dtype=torch.int32, device=device)
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)
+            _exchanges[key] = xchg if int(ok.item()) == 1 else None
         return _exchanges[key]
 
 

@@ -11,7 +11,7 @@ alpha, beta, gamma.
 
 import numpy as np
 
-__all__ = ["SEED", "CHUNK", "CONFIGS", "block", "scalars", "fill_device"]
+__all__ = ["SEED", "CHUNK", "CONFIGS", "block", "scalars", "fill_device", "fill_device_philox"]
 
 SEED = 1109_1264
 CHUNK = 1 << 24
@@ -65,4 +65,36 @@ def fill_device(tensor, cfg: int, operand: int, lo: int = 0):
     for s in range(0, n, CHUNK):
         e = min(n, s + CHUNK)
         tensor[s:e].copy_(torch.from_numpy(block(cfg, operand, lo + s, lo + e, dt)))
+    return tensor
+
+
+def fill_device_philox(tensor, cfg: int, operand: int, lo: int = 0):
+    """Fill a device tensor with elements [lo, lo + len) of a DEVICE-generated
+    stream: torch's Philox generator seeded per global chunk
+    (SEED, cfg, operand, chunk), drawn in float64 with the config's
+    distribution, then cast.  Chunk keying makes the global vector independent
+    of the sharding, like block().  Used for the multi-GiB operands of the
+    bench's multi-GPU block (config 5 is 3 x 16 GiB at one GPU), where the
+    NumPy streams would cost a minute of host time; these values are NOT the
+    NumPy streams' values (parity tests use block())."""
+    import torch
+
+    n = tensor.shape[0]
+    dev = tensor.device
+    normal = CONFIGS[cfg][0] == "normal"
+    g = torch.Generator(device=dev)
+    pos = 0
+    while pos < n:
+        c = (lo + pos) // CHUNK
+        c_lo = c * CHUNK
+        take = min(n - pos, c_lo + CHUNK - (lo + pos))
+        g.manual_seed(((SEED * 16 + cfg) * 256 + operand) * (1 << 20) + c)
+        full = torch.empty(CHUNK, dtype=torch.float64, device=dev)
+        if normal:
+            full.normal_(generator=g)
+        else:
+            full.uniform_(-1.0, 1.0, generator=g)
+        off = lo + pos - c_lo
+        tensor[pos:pos + take].copy_(full[off:off + take])
+        pos += take
     return tensor

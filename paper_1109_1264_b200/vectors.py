@@ -241,13 +241,16 @@ class DeviceScalar:
     element-typed NumPy scalar the reference returns (test_ops.py:29-31).
     """
 
-    __slots__ = ("tensor", "dtype")
+    __slots__ = ("tensor", "dtype", "guard")
 
     __array_ufunc__ = None
 
-    def __init__(self, tensor: torch.Tensor, dtype):
+    def __init__(self, tensor: torch.Tensor, dtype, guard=None):
         self.tensor = tensor
         self.dtype = as_dtype(dtype)
+        # guard(value): raises if the producing collective failed (a peer
+        # exchange that timed out writes NaN; see sharding.PeerExchange.check)
+        self.guard = guard
 
     @classmethod
     def full(cls, value, dtype="f64", device=None) -> "DeviceScalar":
@@ -260,7 +263,10 @@ class DeviceScalar:
         return self.tensor.data_ptr()
 
     def item(self):
-        return self.dtype.type(self.tensor.item())
+        v = self.dtype.type(self.tensor.item())
+        if self.guard is not None:
+            self.guard(v)
+        return v
 
     def __float__(self):
         return float(self.item())

@@ -30,7 +30,7 @@ def test_reference_arm_non_zero_ranks_print_nothing():
     import os
 
     env = {**os.environ, **env}
-    r = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--impl", "reference", "--steps", "3",
-                        "--n-sample", "4096"], capture_output=True, text=True, timeout=300, cwd=ROOT,
+    r = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--impl", "reference", "--gpus", "2",
+                        "--steps", "3", "--n-sample", "4096"], capture_output=True, text=True, timeout=300, cwd=ROOT,
                        env=env)
     assert r.returncode == 0 and r.stdout.strip() == ""
