@@ -214,6 +214,30 @@ int salt_allreduce_sum_flags(void* out_dev_per_gpu[], int G, int dtype, void* co
 int salt_nccl_comm_init_all(int G, const int* devices, void** comms_out);
 int salt_nccl_comm_destroy(int G, void** comms);
 
+/* Concurrent issue on the devices of one process (single-process multi-GPU,
+ * devicegroup.py).  A group keeps one persistent host thread per member
+ * device; salt_group_fused hands every member its own salt_fused call at
+ * the same moment, so device g does not start g launch costs after device 0
+ * (the serial issue loop the reference-side FFI would otherwise run).
+ * Arguments are salt_fused's with per-member arrays (member-major):
+ *   dsts      G x ndst        leaves    G x nleaves    pscalars G x npscalars
+ *   ns[G]     lengths         ws[G]     workspaces (reduce modes)
+ *   out_dev[G] results / SALT_PARTIAL partials     streams[G] per member
+ * scalars are shared.  Enqueues only; returns after every member issued,
+ * with the first failing member's code and message.  Members may repeat a
+ * device (several streams of one GPU).  salt_group_issue_times reports, for
+ * the last call, each member's issue start / end in ns after the job was
+ * published (the cross-device issue skew). */
+int salt_group_create(int G, const int* devices, void** group_out);
+int salt_group_destroy(void* group);
+int salt_group_size(void* group);
+int salt_group_fused(void* group, int dtype, const char* assign_sigs, const char* reduce_sig,
+                     void* const* dsts, int ndst, const void* const* leaves, int nleaves,
+                     const double* scalars, int nscalars, const void* const* pscalars, int npscalars,
+                     const int64_t* ns, int flags, void* const* ws, size_t ws_bytes,
+                     void* const* out_dev, void* const* streams);
+int salt_group_issue_times(void* group, int64_t* start_ns, int64_t* end_ns);
+
 /* Batched assignments: `count` independent evaluations of ONE tree shape
  * `sig` (single root, no device scalars) over different vectors, scalars
  * and lengths, in ONE kernel launch per up to 96 problems (the problem table

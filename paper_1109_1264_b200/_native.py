@@ -57,6 +57,11 @@ HEADER_SYMBOLS = (
     "salt_allreduce_sum_flags",
     "salt_nccl_comm_init_all",
     "salt_nccl_comm_destroy",
+    "salt_group_create",
+    "salt_group_destroy",
+    "salt_group_size",
+    "salt_group_fused",
+    "salt_group_issue_times",
     "salt_signature_kind",
     "salt_prepare",
     "salt_set_force_jit",
@@ -132,6 +137,15 @@ _SIGNATURES = {
     "salt_allreduce_sum_flags": (_c_int, [_c_vpp, _c_int, _c_int, _c_vpp, _c_vpp, _c_int]),
     "salt_nccl_comm_init_all": (_c_int, [_c_int, _c_vp, _c_vpp]),
     "salt_nccl_comm_destroy": (_c_int, [_c_int, _c_vpp]),
+    "salt_group_create": (_c_int, [_c_int, _c_vp, _c_vp]),
+    "salt_group_destroy": (_c_int, [_c_vp]),
+    "salt_group_size": (_c_int, [_c_vp]),
+    "salt_group_fused": (
+        _c_int,
+        [_c_vp, _c_int, _c_str, _c_str, _c_vpp, _c_int, _c_vpp, _c_int, _c_dp, _c_int, _c_vpp, _c_int,
+         _c_vp, _c_int, _c_vpp, _c_size, _c_vpp, _c_vpp],
+    ),
+    "salt_group_issue_times": (_c_int, [_c_vp, _c_vp, _c_vp]),
     "salt_signature_kind": (_c_int, [_c_int, _c_str, _c_str, _c_int]),
     "salt_prepare": (_c_int, [_c_int, _c_str, _c_str, _c_int]),
     "salt_set_force_jit": (None, [_c_int]),
@@ -236,6 +250,12 @@ def check(rc: int) -> None:
 
 _EMPTY_Q = array.array("Q", [0])
 _EMPTY_D = array.array("d", [0.0])
+
+
+def i64_array(values):
+    """(address, keep-alive) of an int64 array holding `values`."""
+    arr = array.array("q", values) if values else array.array("q", [0])
+    return arr.buffer_info()[0], arr
 
 
 def ptr_array(ptrs):

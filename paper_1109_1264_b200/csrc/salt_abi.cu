@@ -1006,3 +1006,5 @@ int salt_allreduce_sum_flags(void* out_dev_per_gpu[], int G, int dtype, void* co
 }
 
 }  // extern "C"
+
+#include "salt_abi_group.inc"

@@ -13,6 +13,14 @@ NCCL communicators from ncclCommInitAll.  This module is the second:
         r = dg.reduce([y * x for y, x in zip(ys, xs)])   # dot over all blocks
         r = dg.axpy_dot(0.5, xs, ys, zs)                 # config 5's fused step
 
+Launches on the G devices are issued CONCURRENTLY: the group owns a native
+salt_group (csrc/salt_abi_group.inc) with one persistent host thread per
+device, and each call lowers every device's tree first, then hands all G
+launches to those threads at once — device g does not wait for g launch
+costs of the devices before it (tools/group_issue_probe.py measures the
+skew).  Trees whose signature or scalars differ between devices are issued
+one device after the other instead.
+
 Blocks follow the same partition as ShardedVector (shard_bounds: 64-element
 aligned bases).  A reduction runs one fused kernel per device writing its
 double-double partial (SALT_PARTIAL), then salt_allreduce_sum — one NCCL
@@ -50,8 +58,14 @@ class DeviceGroup:
             raise ValueError(f"need distinct devices, got {devices}")
         self.devices = devices
         self.size = len(devices)
-        self._comms = (ctypes.c_void_p * self.size)()
+        self._comms = None
+        self._group = None
         devs = (ctypes.c_int * self.size)(*devices)
+        group = ctypes.c_void_p()
+        _native.check(_native.lib().salt_group_create(self.size, ctypes.addressof(devs),
+                                                      ctypes.addressof(group)))
+        self._group = group
+        self._comms = (ctypes.c_void_p * self.size)()
         _native.check(_native.lib().salt_nccl_comm_init_all(self.size, ctypes.addressof(devs),
                                                             ctypes.addressof(self._comms)))
 
@@ -59,6 +73,53 @@ class DeviceGroup:
         if self._comms is not None:
             _native.check(_native.lib().salt_nccl_comm_destroy(self.size, ctypes.addressof(self._comms)))
             self._comms = None
+        if self._group is not None:
+            _native.check(_native.lib().salt_group_destroy(self._group))
+            self._group = None
+
+    def issue_times(self):
+        """[(start_ns, end_ns)] of every device's issue in the last group
+        call, relative to the moment the job was published."""
+        st = (ctypes.c_int64 * self.size)()
+        en = (ctypes.c_int64 * self.size)()
+        _native.check(_native.lib().salt_group_issue_times(self._group, ctypes.addressof(st),
+                                                           ctypes.addressof(en)))
+        return list(zip(st, en))
+
+    def _issue(self, code, asig, rsig, members, flags):
+        """members[g] = (dst ptrs, leaf ptrs, scalars, pscalar ptrs, n, ws, out ptr, stream):
+        one salt_fused per device, all issued at once when the scalars agree
+        (the signature is the caller's, shared by construction)."""
+        lib = _native.lib()
+        scal0 = members[0][2]
+        if all(m[2] == scal0 for m in members):
+            nd, nl, npq = len(members[0][0]), len(members[0][1]), len(members[0][3])
+            if any(len(m[0]) != nd or len(m[1]) != nl or len(m[3]) != npq for m in members):
+                raise ValueError("every device's tree must have the same shape")
+            keep = []
+            arr = lambda xs, f=_native.ptr_array: keep.append(f(xs)) or keep[-1][0]  # noqa: E731
+            dsts = arr([p for m in members for p in m[0]])
+            leaves = arr([p for m in members for p in m[1]])
+            psc = arr([p for m in members for p in m[3]])
+            scal = arr(list(scal0), _native.double_array)
+            ns = arr([m[4] for m in members], _native.i64_array)
+            wss = arr([m[5] for m in members])
+            outs = arr([m[6] for m in members])
+            strs = arr([m[7] for m in members])
+            _native.check(lib.salt_group_fused(
+                self._group, code, asig.encode() if asig else None, rsig.encode() if rsig else None,
+                dsts, nd, leaves, nl, scal, len(scal0), psc, npq, ns, flags, wss,
+                lib.salt_reduce_workspace_bytes() if rsig else 0, outs, strs))
+            return
+        for g, (dst, lv_, sc, pq, n, ws, out, stream) in enumerate(members):
+            keep = [_native.ptr_array(dst), _native.ptr_array(lv_), _native.double_array(sc),
+                    _native.ptr_array(pq)]
+            with _OnDevice(self.devices[g]):
+                _native.check(lib.salt_fused(code, asig.encode() if asig else None,
+                                             rsig.encode() if rsig else None, keep[0][0], len(dst),
+                                             keep[1][0], len(lv_), keep[2][0], len(sc), keep[3][0],
+                                             len(pq), n, flags, ws, lib.salt_reduce_workspace_bytes()
+                                             if rsig else 0, out, None, stream))
 
     def __enter__(self):
         return self
@@ -95,6 +156,43 @@ class DeviceGroup:
     def gather(blocks) -> np.ndarray:
         return np.concatenate([b.to_array() for b in blocks])
 
+    # ---- elementwise
+    def assign(self, pairs) -> None:
+        """pairs[g] = (dest, expression) over device g's vectors: one fused
+        kernel per device, all issued at once, no communication (config 4's
+        step: `assign([(e[g], al*(a[g] + b[g]) - be*(c[g] - d[g]) + ga*a[g])
+        for g in range(G)])`)."""
+        pairs = list(pairs)
+        if len(pairs) != self.size:
+            raise ValueError(f"need one (dest, expression) per device ({self.size}), got {len(pairs)}")
+        members, dts, sigs = [], set(), set()
+        for g, ((dst, expr), d) in enumerate(zip(pairs, self.devices)):
+            node = FusedNode([AssignNode(as_node(dst), as_node(expr))], None)
+            asig, _rsig, lw, dests = node.lower()
+            dev = torch.device("cuda", d)
+            vecs = list(lw.vectors) + list(dests)
+            for v in vecs:
+                if not isinstance(v, DenseVector) or v.tensor.device != dev:
+                    raise ValueError(f"pair {g}: every operand must be a DenseVector on cuda:{d}")
+            for ds in lw.pscalars:
+                if ds.tensor.device != dev:
+                    raise ValueError(f"pair {g}: device scalars must live on cuda:{d}")
+            lengths = {len(v) for v in vecs}
+            if len(lengths) != 1:
+                raise ValueError(f"pair {g}: operands of different lengths {sorted(lengths)}")
+            dts.add(as_dtype(node.dtype))
+            sigs.add(asig)
+            with _OnDevice(d):
+                stream = _raw_stream(d)
+            members.append(([v.tensor.data_ptr() for v in dests], [v.tensor.data_ptr() for v in lw.vectors],
+                            list(lw.scalars), [ds.tensor.data_ptr() for ds in lw.pscalars], lengths.pop(),
+                            0, 0, stream))
+        if len(dts) != 1:
+            raise TypeError("all devices' trees must have one element type")
+        if len(sigs) != 1:
+            raise ValueError(f"every device's tree must have the same shape, got {sorted(sigs)}")
+        self._issue(_dtype_code(dts.pop()), sigs.pop(), None, members, 0)
+
     # ---- reductions
     def reduce(self, summands, *, sqrt=False, lazy=False):
         """Sum over every device's block of summands[g] (an elementwise tree
@@ -104,13 +202,12 @@ class DeviceGroup:
         summands = list(summands)
         if len(summands) != self.size:
             raise ValueError(f"need one summand per device ({self.size}), got {len(summands)}")
-        lib = _native.lib()
         dts = {s.dtype for s in summands}
         if len(dts) != 1 or not all(isinstance(s, Expression) for s in summands):
             raise TypeError("summands must be expressions of one element type")
         dt = as_dtype(dts.pop())
         code = _dtype_code(dt)
-        parts, streams, keep = [], [], []
+        parts, streams, members, sigs = [], [], [], set()
         for g, (expr, d) in enumerate(zip(summands, self.devices)):
             lw = lower(expr)
             if lw.pscalars:
@@ -123,18 +220,18 @@ class DeviceGroup:
                 if not isinstance(v, DenseVector) or v.tensor.device != torch.device("cuda", d):
                     raise ValueError(f"summand {g}: every operand must be a DenseVector on cuda:{d}")
             n = lengths.pop()
+            sigs.add(" ".join(lw.tokens))
             with _OnDevice(d):
                 stream = _raw_stream(d)
                 ws = _workspace(d, stream)
                 part = torch.empty(2, dtype=torch.float64, device=torch.device("cuda", d))
-                leaves, k1 = _native.ptr_array([v.tensor.data_ptr() for v in vecs])
-                scal, k2 = _native.double_array(lw.scalars)
-                _native.check(lib.salt_reduce(code, " ".join(lw.tokens).encode(), leaves, len(vecs), scal,
-                                              len(lw.scalars), n, _native.SALT_PARTIAL, ws.data_ptr(),
-                                              ws.numel(), part.data_ptr(), None, stream))
+            members.append(([], [v.tensor.data_ptr() for v in vecs], list(lw.scalars), [], n,
+                            ws.data_ptr(), part.data_ptr(), stream))
             parts.append(part)
             streams.append(stream)
-            keep += [k1, k2]
+        if len(sigs) != 1:
+            raise ValueError(f"every device's summand must have the same tree shape, got {sorted(sigs)}")
+        self._issue(code, None, sigs.pop(), members, _native.SALT_PARTIAL)
         return self._allreduce(parts, streams, dt, _native.SALT_SQRT if sqrt else 0, lazy)
 
     def fused(self, statements, *, lazy=False):
@@ -148,8 +245,7 @@ class DeviceGroup:
         statements = list(statements)
         if len(statements) != self.size:
             raise ValueError(f"need one statement list per device ({self.size}), got {len(statements)}")
-        lib = _native.lib()
-        parts, streams, keep, dts = [], [], [], set()
+        parts, streams, members, dts, sigs = [], [], [], set(), set()
         for g, (sts, d) in enumerate(zip(statements, self.devices)):
             sts = list(sts)
             if len(sts) < 2 or isinstance(sts[-1], tuple) or not all(
@@ -172,23 +268,21 @@ class DeviceGroup:
             n = lengths.pop()
             dt = as_dtype(node.dtype)
             dts.add(dt)
+            sigs.add((asig, rsig))
             with _OnDevice(d):
                 stream = _raw_stream(d)
                 ws = _workspace(d, stream)
                 part = torch.empty(2, dtype=torch.float64, device=dev)
-                leaves, k1 = _native.ptr_array([v.tensor.data_ptr() for v in lw.vectors])
-                dsts, k2 = _native.ptr_array([v.tensor.data_ptr() for v in dests])
-                scal, k3 = _native.double_array(lw.scalars)
-                pscal, k4 = _native.ptr_array([ds.tensor.data_ptr() for ds in lw.pscalars])
-                _native.check(lib.salt_fused(_dtype_code(dt), asig.encode(), rsig.encode(), dsts, len(dests),
-                                             leaves, len(lw.vectors), scal, len(lw.scalars), pscal,
-                                             len(lw.pscalars), n, _native.SALT_PARTIAL, ws.data_ptr(),
-                                             ws.numel(), part.data_ptr(), None, stream))
+            members.append(([v.tensor.data_ptr() for v in dests], [v.tensor.data_ptr() for v in lw.vectors],
+                            list(lw.scalars), [ds.tensor.data_ptr() for ds in lw.pscalars], n,
+                            ws.data_ptr(), part.data_ptr(), stream))
             parts.append(part)
             streams.append(stream)
-            keep += [k1, k2, k3, k4]
         if len(dts) != 1:
             raise TypeError("all devices' statements must have one element type")
+        if len(sigs) != 1:
+            raise ValueError(f"every device's statements must have the same tree shape, got {sorted(sigs)}")
+        self._issue(_dtype_code(next(iter(dts))), *sigs.pop(), members, _native.SALT_PARTIAL)
         return self._allreduce(parts, streams, dts.pop(), 0, lazy)
 
     def axpy_dot(self, alpha, xs, ys, zs, **kw):
