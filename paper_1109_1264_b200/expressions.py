@@ -34,6 +34,8 @@ __all__ = [
     "AssignReduceNode",
     "FusedNode",
     "LengthMismatchError",
+    "Cell",
+    "SlotCell",
     "as_node",
     "common_length",
     "combine_partials",
@@ -128,12 +130,71 @@ class _Lowering:
         self.scalars.append(float(value))
 
 
+class SlotCell:
+    """One lane register of a node (reference expressions.py:49-57): in the
+    fused kernel, the V-lane register a leaf is loaded into, the broadcast
+    scalar of a ScaleNode, an assigned value or a reduction accumulator."""
+
+    __slots__ = ("backend", "value")
+
+    def __init__(self, backend):
+        self.backend, self.value = backend, None
+
+
+class Cell:
+    """One loop-wide scalar (reference expressions.py:59-66): the remainder
+    accumulator of a SumNode (the kernel's scalar head/tail sum)."""
+
+    __slots__ = ("value",)
+
+    def __init__(self):
+        self.value = None
+
+
+def _storage(node, backend):
+    """Per-slot register layout of `node`, mirroring the tree: a SlotCell
+    per register, a pair for a binary node, (own register, child layout)
+    for Scale / Assign / Sum (reference contract: expressions.py:166-167,
+    213-214, 291-292, 360-361, 425-426)."""
+    if isinstance(node, Leaf):
+        return SlotCell(backend)
+    if isinstance(node, _BinaryNode):
+        return (_storage(node.left, backend), _storage(node.right, backend))
+    inner = {ScaleNode: "child", SumNode: "child", AssignNode: "source"}.get(type(node))
+    if inner is None:
+        raise TypeError(f"{type(node).__name__} has no per-slot storage")
+    return (SlotCell(backend), _storage(getattr(node, inner), backend))
+
+
+def _temporary(node, backend):
+    """Loop-wide scalars of `node`: only a SumNode owns one (its remainder
+    Cell); other nodes pass their children's through (reference
+    expressions.py:169-170, 216-217, 294-295, 363-364, 428-429)."""
+    if isinstance(node, Leaf):
+        return None
+    if isinstance(node, _BinaryNode):
+        return (_temporary(node.left, backend), _temporary(node.right, backend))
+    if isinstance(node, SumNode):
+        return (Cell(), _temporary(node.child, backend))
+    if isinstance(node, ScaleNode):
+        return _temporary(node.child, backend)
+    if isinstance(node, AssignNode):
+        return _temporary(node.source, backend)
+    raise TypeError(f"{type(node).__name__} has no temporary storage")
+
+
 class Expression:
     """Base class: operator sugar (reference expressions.py:103-132)."""
 
     __slots__ = ()
 
     __array_ufunc__ = None
+
+    def make_storage(self, backend):
+        return _storage(self, backend)
+
+    def make_temporary(self, backend):
+        return _temporary(self, backend)
 
     def __add__(self, other):
         return add_nodes(self, other)

@@ -1,0 +1,61 @@
+"""Run the reference's OWN unit tests (pkg/tests/*.py) against this package.
+
+build() copies /root/reference/pkg/tests/test_*.py, unmodified, into
+tests/reference_suite/_vendored/ (git-ignored: reference sources stay out of
+this repository's history; the copy travels to the GPU box with the
+snapshot like the built .so files).  This conftest makes `import lanevec`
+resolve to paper_1109_1264_b200 — the drop-in claim of SURVEY.md §8(b) —
+before those modules are imported:
+
+    lanevec              -> paper_1109_1264_b200
+    lanevec.vectors      -> .vectors        lanevec.expressions -> .expressions
+    lanevec.lanes        -> .lanes          lanevec.engine      -> .engine
+    lanevec.ops          -> .ops            lanevec.bench       -> .benchmark
+    lanevec.oracle       -> .checks (CountingVector + the scalar loops)
+
+Every collected test is marked `gpu` (the package evaluates on the GPU
+only), except test_lanes.py, which never evaluates a tree and also runs in
+the CPU suite.  XFAIL lists the tests
+whose reference contract this package deliberately does not keep, each with
+its reason.
+"""
+
+import sys
+from pathlib import Path
+
+import pytest
+
+import paper_1109_1264_b200 as _pkg
+from paper_1109_1264_b200 import benchmark, checks, engine, expressions, lanes, ops, vectors
+
+VENDORED = Path(__file__).resolve().parent / "_vendored"
+
+ALIASES = {
+    "lanevec": _pkg,
+    "lanevec.vectors": vectors,
+    "lanevec.expressions": expressions,
+    "lanevec.lanes": lanes,
+    "lanevec.engine": engine,
+    "lanevec.ops": ops,
+    "lanevec.bench": benchmark,
+    "lanevec.oracle": checks,
+}
+for _name, _mod in ALIASES.items():
+    sys.modules[_name] = _mod
+
+CPU_FILES = {"test_lanes.py"}
+
+# test node id (file::name, parametrisation stripped) -> reason
+XFAIL = {}
+
+
+def pytest_collection_modifyitems(config, items):
+    for item in items:
+        path = Path(str(item.fspath))
+        if VENDORED not in path.parents:
+            continue
+        if path.name not in CPU_FILES:
+            item.add_marker(pytest.mark.gpu)
+        key = f"{path.name}::{item.originalname if hasattr(item, 'originalname') else item.name}"
+        if key in XFAIL:
+            item.add_marker(pytest.mark.xfail(reason=XFAIL[key], strict=True))
