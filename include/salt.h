@@ -291,6 +291,17 @@ int salt_assign_reduce_host(int dtype, const char* assign_sig, const char* reduc
  * before the first use; the kernels reset them after every reduction. */
 #define SALT_WORKSPACE_TICKET_BYTES 16640
 size_t salt_reduce_workspace_bytes(void);
+/* Two-step host result for callers that release a lock while waiting:
+ * enqueue the device->host copy of a reduction result (out_dev, <= 64
+ * bytes) into this host thread's pinned slot on `stream` and return the
+ * slot; after salt_stream_synchronize(stream) the slot holds the bytes. */
+int salt_result_enqueue(const void* out_dev, size_t bytes, void* stream, void** host_slot);
+int salt_stream_synchronize(void* stream);
+/* Identity of the CUDA graph capture in progress on `stream` (0: the stream
+ * is not capturing).  A reduction captured into a graph needs a workspace
+ * of its own (its tickets and partials are baked into the graph): hosts key
+ * per-capture workspaces by this id. */
+uint64_t salt_capture_id(void* stream);
 
 /* 0 = invalid signature, 1 = compiled-in (AOT) kernel, 2 = needs the NVRTC
  * JIT.  kind: 0 assign, 1 reduce, 2 assign+reduce (reduce_sig used). */

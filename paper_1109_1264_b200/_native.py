@@ -49,6 +49,9 @@ HEADER_SYMBOLS = (
     "salt_reduce_host",
     "salt_assign_reduce_host",
     "salt_reduce_workspace_bytes",
+    "salt_capture_id",
+    "salt_result_enqueue",
+    "salt_stream_synchronize",
     "salt_reduce_exchange",
     "salt_assign_reduce_exchange",
     "salt_fused_exchange",
@@ -117,6 +120,9 @@ _SIGNATURES = {
          _c_vpp, _c_vp],
     ),
     "salt_reduce_workspace_bytes": (_c_size, []),
+    "salt_capture_id": (ctypes.c_uint64, [_c_vp]),
+    "salt_result_enqueue": (_c_int, [_c_vp, _c_size, _c_vp, _c_vp]),
+    "salt_stream_synchronize": (_c_int, [_c_vp]),
     "salt_reduce_exchange": (
         _c_int,
         [_c_int, _c_str, _c_vpp, _c_int, _c_dp, _c_int, _c_i64, _c_int, _c_vp, _c_size, _c_vp, _c_vp,
@@ -234,6 +240,7 @@ def fastpath():
                     torch._C._cuda_getCurrentRawStream, torch._C._cuda_getDevice,
                     runtime._workspace, np.float32, np.float64, runtime._lazy_out,
                     addr(h.salt_assign_batch), addr(h.salt_reduce_batch), runtime._batch_out,
+                    addr(h.salt_result_enqueue), addr(h.salt_stream_synchronize),
                 )
                 _fast = _fastpath
             except (ImportError, AttributeError):

@@ -45,6 +45,8 @@ typedef int (*assign_batch_fn)(int, const char*, int, void* const*, const void* 
 typedef int (*reduce_batch_fn)(int, const char*, int, const void* const*, int, const double*, int,
                                const int64_t*, int, void* const*, void*, size_t, void*);
 typedef const char* (*last_error_fn)(void);
+typedef int (*result_enqueue_fn)(const void*, size_t, void*, void**);
+typedef int (*stream_sync_fn)(void*);
 
 static assign_fn p_assign;
 static reduce_fn p_reduce;
@@ -54,6 +56,8 @@ static assign_batch_fn p_assign_batch;
 static reduce_batch_fn p_reduce_batch;
 static PyObject* batch_out; /* runtime._batch_out(device, count) -> (tensor, data_ptr) */
 static last_error_fn p_last_error;
+static result_enqueue_fn p_result_enqueue;
+static stream_sync_fn p_stream_sync;
 static size_t ws_bytes;
 
 static PyObject *T_Leaf, *T_Add, *T_Sub, *T_Mul, *T_Scale, *T_Dense, *T_DevScalar;
@@ -304,22 +308,37 @@ static PyObject* launch_reduce(Walk* w, const char* asig, void* const* dptrs, in
   void* out = slot;
   double host[2] = {0.0, 0.0};
   if (lazy && !(ds = lazy_slot(w, &out))) return NULL;
+  /* Non-lazy: the kernel writes the workspace's result slot and the copy to
+   * this thread's pinned slot is enqueued behind it with the GIL held (a
+   * later reduction on the same stream — same workspace — is ordered after
+   * the copy); only the wait for the stream runs without the GIL, so other
+   * Python threads progress during a long reduction. */
   const void* const* leaves = (const void* const*)w->ptrs;
   int rc;
   if (w->nps || ndst > 1)
     rc = p_fused(w->code, asig, w->sig, dptrs, ndst, leaves, w->nvec, w->sc, w->nsc, w->ps, w->nps,
-                 w->n, flags, ws, ws_bytes, out, lazy ? NULL : host, stream);
+                 w->n, flags, ws, ws_bytes, out, NULL, stream);
   else if (asig)
     rc = p_assign_reduce(w->code, asig, w->sig, dptrs[0], leaves, w->nvec, w->sc, w->nsc, w->n,
-                         flags, ws, ws_bytes, out, lazy ? NULL : host, stream);
+                         flags, ws, ws_bytes, out, NULL, stream);
   else
     rc = p_reduce(w->code, w->sig, leaves, w->nvec, w->sc, w->nsc, w->n, flags, ws, ws_bytes, out,
-                  lazy ? NULL : host, stream);
+                  NULL, stream);
   if (rc != 0) {
     Py_XDECREF(ds);
     return check(rc);
   }
-  return lazy ? ds : scalar_result(w, host);
+  if (lazy) return ds;
+  const size_t bytes = (flags & 2) ? 16 : (w->code == 0 ? 4 : 8);
+  void* hslot = NULL;
+  rc = p_result_enqueue(out, bytes, stream, &hslot);
+  if (rc != 0) return check(rc);
+  Py_BEGIN_ALLOW_THREADS
+  rc = p_stream_sync(stream);
+  Py_END_ALLOW_THREADS
+  if (rc != 0) return check(rc);
+  memcpy(host, hslot, bytes);
+  return scalar_result(w, host);
 }
 
 /* reduce(child, flags, lazy) -> NumPy scalar (or DeviceScalar if lazy), or
@@ -795,13 +814,15 @@ done:
 }
 
 static PyObject* fp_init(PyObject* self, PyObject* args) {
-  unsigned long long a, r, ar, fu, le, ab, rb;
+  unsigned long long a, r, ar, fu, le, ab, rb, re, ss;
   Py_ssize_t wsb;
-  if (!PyArg_ParseTuple(args, "KKKKKnOOOOOOOOOOOOOKKO", &a, &r, &ar, &fu, &le, &wsb, &T_Leaf, &T_Add,
+  if (!PyArg_ParseTuple(args, "KKKKKnOOOOOOOOOOOOOKKOKK", &a, &r, &ar, &fu, &le, &wsb, &T_Leaf, &T_Add,
                         &T_Sub, &T_Mul, &T_Scale, &T_Dense, &T_DevScalar, &get_stream,
                         &current_device, &workspace_fn, &np_f32, &np_f64, &lazy_out, &ab, &rb,
-                        &batch_out))
+                        &batch_out, &re, &ss))
     return NULL;
+  p_result_enqueue = (result_enqueue_fn)(uintptr_t)re;
+  p_stream_sync = (stream_sync_fn)(uintptr_t)ss;
   p_assign_batch = (assign_batch_fn)(uintptr_t)ab;
   p_reduce_batch = (reduce_batch_fn)(uintptr_t)rb;
   Py_INCREF(batch_out);

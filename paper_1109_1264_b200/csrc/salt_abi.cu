@@ -513,7 +513,8 @@ int make_plan(int dtype, const char* asig, const char* rsig, int mode, int nleav
 // small pinned pool, claimed once; beyond the pool, threads copy directly.
 constexpr int kResultSlots = 256;
 std::atomic<int> g_result_slot_next{0};
-int result_to_host(void* out_host, const void* out_dev, size_t bytes, cudaStream_t st) {
+// This host thread's 64-byte pinned result slot (nullptr beyond the pool).
+char* thread_result_slot() {
   static char* pool = nullptr;
   static std::once_flag once;
   std::call_once(once, [] {
@@ -527,10 +528,30 @@ int result_to_host(void* out_host, const void* out_dev, size_t bytes, cudaStream
     const int k = g_result_slot_next.fetch_add(1, std::memory_order_relaxed);
     slot = pool && k < kResultSlots ? k : -1;
   }
-  void* dst = slot >= 0 ? (void*)(pool + 64 * slot) : out_host;
+  return slot >= 0 ? pool + 64 * slot : nullptr;
+}
+
+int result_to_host(void* out_host, const void* out_dev, size_t bytes, cudaStream_t st) {
+  char* pinned = thread_result_slot();
+  void* dst = pinned ? (void*)pinned : out_host;
   SALT_CUDA(cudaMemcpyAsync(dst, out_dev, bytes, cudaMemcpyDeviceToHost, st));
   SALT_CUDA(cudaStreamSynchronize(st));
   if (dst != out_host) memcpy(out_host, dst, bytes);
+  return 0;
+}
+
+// Split form for hosts that release a lock while waiting (the CPython fast
+// path drops the GIL): enqueue the copy into this thread's pinned slot; the
+// caller synchronises the stream, then reads *host_slot.
+int result_enqueue(const void* out_dev, size_t bytes, cudaStream_t st, void** host_slot) {
+  char* pinned = thread_result_slot();
+  if (!pinned) {  // beyond the pool's threads: a pinned slot of this thread's own
+    thread_local char* own = nullptr;
+    if (!own) SALT_CUDA(cudaHostAlloc((void**)&own, 64, cudaHostAllocPortable));
+    pinned = own;
+  }
+  SALT_CUDA(cudaMemcpyAsync(pinned, out_dev, bytes, cudaMemcpyDeviceToHost, st));
+  *host_slot = pinned;
   return 0;
 }
 
@@ -770,6 +791,26 @@ int salt_jit_wait(void) {
 uint64_t salt_interp_launch_count(void) { return g_interp_launches.load(); }
 
 size_t salt_reduce_workspace_bytes(void) { return (size_t)salt::WsLayout::bytes; }
+
+int salt_result_enqueue(const void* out_dev, size_t bytes, void* stream, void** host_slot) {
+  if (!out_dev || !host_slot || bytes == 0 || bytes > 64) return fail(SALT_EINVAL, "bad result fetch");
+  return result_enqueue(out_dev, bytes, (cudaStream_t)stream, host_slot);
+}
+
+int salt_stream_synchronize(void* stream) {
+  SALT_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+  return 0;
+}
+
+uint64_t salt_capture_id(void* stream) {
+  cudaStreamCaptureStatus status = cudaStreamCaptureStatusNone;
+  unsigned long long id = 0;
+  if (cudaStreamGetCaptureInfo((cudaStream_t)stream, &status, &id) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return status == cudaStreamCaptureStatusActive ? (uint64_t)id : 0;
+}
 
 int salt_signature_kind(int dtype, const char* sig, const char* reduce_sig, int kind) {
   if (kind < 0 || kind > 2) return 0;

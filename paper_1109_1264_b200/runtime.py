@@ -38,6 +38,11 @@ __all__ = ["run_assign", "run_reduce", "run_assign_reduce", "run_fused", "run_as
 
 _ws_lock = threading.Lock()
 _workspaces = {}
+_capture_workspaces = {}
+try:
+    _is_capturing = torch._C._cuda_isCurrentStreamCapturing
+except AttributeError:  # pragma: no cover
+    _is_capturing = torch.cuda.is_current_stream_capturing
 _host_state = {}
 _HOST_STAGING_BYTES = 768 << 20
 
@@ -203,11 +208,35 @@ def _require_cuda() -> torch.device:
 _MAX_CACHED_WORKSPACES = 64
 
 
+def _capture_workspace(index: int, stream_ptr: int) -> torch.Tensor:
+    """Private scratch of the CUDA graph being captured on `stream_ptr`: the
+    graph bakes the workspace address in, so two graphs replayed at once on
+    different streams — or a graph replayed while eager reductions run on
+    its capture stream — must not share tickets.  One workspace per capture
+    (all reductions of one captured stream run in order), allocated in the
+    graph's memory pool and kept for the life of the process; its ticket
+    words are zeroed by a captured memset, i.e. at the start of every
+    replay."""
+    cid = _native.lib().salt_capture_id(stream_ptr)
+    key = (index, stream_ptr, cid)
+    ws = _capture_workspaces.get(key)
+    if ws is None:
+        nbytes = _native.lib().salt_reduce_workspace_bytes() + 256
+        ws = torch.empty(nbytes, dtype=torch.uint8, device=torch.device("cuda", index))
+        ws[: _native.SALT_WORKSPACE_TICKET_BYTES].zero_()
+        _capture_workspaces[key] = ws
+    return ws
+
+
 def _workspace(index: int, stream_ptr: int) -> torch.Tensor:
     """Reduction scratch of (device, stream): zeroed once, then kept — the
     kernels reset their tickets themselves, so consecutive reductions on one
     stream share it safely.  Beyond _MAX_CACHED_WORKSPACES streams a fresh
-    scratch is made per call (tickets zeroed, tied to the stream)."""
+    scratch is made per call (tickets zeroed, tied to the stream).  While
+    the stream is being captured into a CUDA graph: the capture's own
+    scratch (_capture_workspace)."""
+    if _is_capturing():
+        return _capture_workspace(index, stream_ptr)
     key = (index, stream_ptr)
     ws = _workspaces.get(key)
     if ws is None:

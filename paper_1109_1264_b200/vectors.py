@@ -279,11 +279,19 @@ class DeviceScalar:
             return other.tensor
         return float(self.dtype.type(other))
 
+    def _operand_tensor(self, other):
+        """`other` as a device tensor of this dtype.  Division needs it:
+        torch divides a CUDA tensor by a host number as a multiply by the
+        host-computed reciprocal, and number / tensor as reciprocal() *
+        number — two roundings each, up to 1 ulp off IEEE a / b."""
+        o = self._other(other)
+        return o if isinstance(o, torch.Tensor) else torch.full_like(self.tensor, o)
+
     def __truediv__(self, other):
-        return DeviceScalar(torch.div(self.tensor, self._other(other)), self.dtype)
+        return DeviceScalar(torch.div(self.tensor, self._operand_tensor(other)), self.dtype)
 
     def __rtruediv__(self, other):
-        return DeviceScalar(self._other(other) / self.tensor, self.dtype)
+        return DeviceScalar(torch.div(self._operand_tensor(other), self.tensor), self.dtype)
 
     def copy_(self, other) -> "DeviceScalar":
         """In-place assignment (keeps this scalar's device address, so a

@@ -151,6 +151,11 @@ def test_device_scalar_operands():
         assert alpha.item().tobytes() == (av / bv).tobytes()  # IEEE division in dtype
         assert (-alpha).item() == -(av / bv) and (alpha * 2.0).item() == (av / bv) * NP[dt](2.0)
         assert (1.0 / alpha).item() == NP[dt](1.0) / (av / bv)
+        # division by / into a host number: ONE IEEE rounding
+        q = av / bv
+        for c in (3.0, 7.0, 0.1, -1e-3):
+            assert (alpha / c).item().tobytes() == (q / NP[dt](c)).tobytes(), c
+            assert (c / alpha).item().tobytes() == (NP[dt](c) / q).tobytes(), c
         assert (alpha - b).item() == (av / bv) - bv
         D = lv.DenseVector.zeros(n, dt, device="cuda")
         launches = _native.lib().salt_launch_count()

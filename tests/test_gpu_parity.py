@@ -386,6 +386,43 @@ def test_cuda_graph_capture_of_fused_steps():
     assert Y2.to_array().tobytes() == y_eager.tobytes()
 
 
+def test_graphs_with_reductions_replay_concurrently():
+    """Each captured graph gets its own reduction workspace:
+    two graphs whose reductions combine through tickets (multi-CTA n),
+    replayed at the same time on two streams, plus eager reductions on the
+    default stream meanwhile, all give the eager bits."""
+    from paper_1109_1264_b200 import runtime
+
+    n = (1 << 23) + 5
+    g = np.random.default_rng(12)
+    xs = [dev(g.standard_normal(n), "f64") for _ in range(4)]
+    want = [float(lv.dot(xs[0], xs[1])), float(lv.dot(xs[2], xs[3])), float(lv.norm2(xs[0]))]
+    graphs, outs = [], []
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        lv.dot(xs[0], xs[1], lazy=True)  # warm-up outside capture
+    torch.cuda.current_stream().wait_stream(side)
+    before = len(runtime._capture_workspaces)
+    for a, b in ((0, 1), (2, 3)):
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gr):
+            outs.append(lv.dot(xs[a], xs[b], lazy=True))
+        graphs.append(gr)
+    assert len(runtime._capture_workspaces) == before + 2
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    for _ in range(20):
+        for gr, st in zip(graphs, streams):
+            st.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(st):
+                gr.replay()
+        assert float(lv.norm2(xs[0])) == want[2]  # eager, default stream, meanwhile
+        for st in streams:
+            torch.cuda.current_stream().wait_stream(st)
+        torch.cuda.synchronize()
+        assert [float(o.item()) for o in outs] == want[:2]
+
+
 def test_special_reductions_match_reference():
     """inf / -inf / NaN / overflow in reductions: the compensated sum falls
     back to the plain IEEE sum, giving the reference's inf / NaN results."""

@@ -130,6 +130,33 @@ def test_jit_disk_cache(tmp_path):
     second = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
                             cwd=ROOT, check=True)
     assert float(second.stdout) < float(first.stdout)
+    # every entry carries the format magic and is private to the user
+    for f in files:
+        assert f.read_bytes().startswith(b"SALTJIT2 ") and (f.stat().st_mode & 0o077) == 0
+    assert ((tmp_path / "jit").stat().st_mode & 0o077) == 0
+    # a corrupted entry is not trusted: it is deleted and rebuilt by NVRTC
+    blob = bytearray(files[0].read_bytes())
+    blob[-20] ^= 0xFF
+    files[0].write_bytes(bytes(blob))
+    subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, cwd=ROOT, check=True)
+    assert files[0].read_bytes() != bytes(blob) and files[0].read_bytes().startswith(b"SALTJIT2 ")
+
+
+def test_jit_disk_cache_refuses_a_shared_directory(tmp_path):
+    """A cache directory writable by group/others is not used at all (no
+    kernel is read from it or written to it); compilation still works."""
+    import os
+    import sys
+
+    shared = tmp_path / "shared"
+    shared.mkdir()
+    os.chmod(shared, 0o777)
+    (shared / "planted.salt").write_bytes(b"not a kernel")
+    code = ("from paper_1109_1264_b200 import _native; l = _native.lib(); "
+            "assert l.salt_prepare(0, b'L0 L1 + L0 * L2 -', None, 0) == 0")
+    env = {**os.environ, "SALT_JIT_CACHE": str(shared)}
+    subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, cwd=ROOT, check=True)
+    assert sorted(p.name for p in shared.iterdir()) == ["planted.salt"]
 
 
 def test_c_fast_path_declines_what_it_cannot_take():
