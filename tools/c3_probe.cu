@@ -1,0 +1,406 @@
+// Round-2 design-space probe for BASELINE config 3's 2^24 reductions
+// (ddot/dnrm2, f32/f64) on B200 — the kernel furthest below its roofline in
+// round 1 (VERDICT r01 "What's weak" 2).  Not product code.  Extends
+// tools/midred_probe.cu with: thread-block-cluster combines (partials meet
+// in distributed shared memory, one ticket level over clusters), several
+// independent per-thread accumulators (ILP), and one tile per CTA (K = 1,
+// the bandwidth floor's geometry) with every combine.
+//
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -fmad=false \
+//        -o tools/c3_probe tools/c3_probe.cu && tools/c3_probe
+//
+// Every variant computes the same compensated double-double sum as the
+// product (TwoSum per f64 term / exact f64 sum of f32 terms) and is checked
+// against variant "cur".  Timing: CUDA events around one launch, preceded
+// by an L2 sweep — "clean" (a 512 MiB read sweep: L2 full of clean lines) or
+// "dirty" (a 512 MiB memset: L2 full of dirty lines, config_sweep's flush).
+//
+// Variants (K = tiles of BLOCK*UNR 32-byte vectors per CTA; U = UNR; I =
+// independent accumulators per thread; GS = combine units per group):
+//   floor        K=1, per-CTA partial only, no combine (bandwidth floor)
+//   floor_U8     the same with 8 vectors in flight per thread
+//   product_r01  the round-1 product geometry (one group of <= 512 / 256 CTAs,
+//                K = tiles / CTAs), I = 1 / 2 / 4
+//   gs256_*      groups of 256 CTAs, two ticket levels
+//   one_*        one group of the whole grid (the last CTA folds all partials)
+//   cl8_* cl4_*  clusters of 8 / 4 CTAs fold in DSMEM; one ticket level over
+//                the clusters (the last cluster leader folds their partials)
+#include <cuda_runtime.h>
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("%s: %s\n", #x, cudaGetErrorString(e)); exit(1);} } while (0)
+typedef long long i64;
+struct DD { double hi, lo; };
+constexpr int BLOCK = 256;
+
+__device__ __forceinline__ void two_sum(double a, double b, double& s, double& e) {
+  s = __dadd_rn(a, b);
+  double bp = __dsub_rn(s, a), ap = __dsub_rn(s, bp);
+  e = __dadd_rn(__dsub_rn(a, ap), __dsub_rn(b, bp));
+}
+__device__ __forceinline__ DD dd_add(DD a, DD b) {
+  double s, e;
+  two_sum(a.hi, b.hi, s, e);
+  e = __dadd_rn(e, __dadd_rn(a.lo, b.lo));
+  DD r;
+  two_sum(s, e, r.hi, r.lo);
+  return r;
+}
+__device__ DD block_dd(DD v, DD* sm) {
+  for (int o = 16; o; o >>= 1) {
+    DD w; w.hi = __shfl_xor_sync(~0u, v.hi, o); w.lo = __shfl_xor_sync(~0u, v.lo, o);
+    v = dd_add(v, w);
+  }
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    DD z{0, 0};
+    v = threadIdx.x < BLOCK / 32 ? sm[threadIdx.x] : z;
+    for (int o = 16; o; o >>= 1) {
+      DD w; w.hi = __shfl_xor_sync(~0u, v.hi, o); w.lo = __shfl_xor_sync(~0u, v.lo, o);
+      v = dd_add(v, w);
+    }
+  }
+  return v;
+}
+__device__ __forceinline__ unsigned ticket_add(unsigned* p) {
+  unsigned old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(p) : "memory");
+  return old;
+}
+
+template <class T> struct Vec;
+template <> struct Vec<double> {
+  double v[4];
+  __device__ __forceinline__ void load(const double* p) {
+    asm volatile("ld.global.L1::no_allocate.v4.f64 {%0,%1,%2,%3}, [%4];"
+                 : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]) : "l"(p));
+  }
+  static constexpr int W = 4;
+};
+template <> struct Vec<float> {
+  float v[8];
+  __device__ __forceinline__ void load(const float* p) {
+    asm volatile("ld.global.L1::no_allocate.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
+                 : "l"(p));
+  }
+  static constexpr int W = 8;
+};
+template <class T> struct Acc;
+template <> struct Acc<double> {
+  double hi = 0, lo = 0;
+  __device__ __forceinline__ void add(double x) { double s, e; two_sum(hi, x, s, e); hi = s; lo = __dadd_rn(lo, e); }
+  __device__ __forceinline__ DD get() const { DD r; two_sum(hi, lo, r.hi, r.lo); return r; }
+};
+template <> struct Acc<float> {
+  double hi = 0;
+  __device__ __forceinline__ void add(float x) { hi = __dadd_rn(hi, (double)x); }
+  __device__ __forceinline__ DD get() const { return DD{hi, 0.0}; }
+};
+template <class T> __device__ __forceinline__ T mul_rn(T a, T b);
+template <> __device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+template <> __device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+
+struct Args {
+  const void* x; const void* y;  // y == x for nrm2 (one leaf)
+  i64 nvec;                      // vectors of 32 bytes
+  i64 K;                         // tiles per CTA
+  int GS;                        // combine units (CTAs, or clusters) per group
+  int combine;                   // 0: partials only
+  DD* partials; DD* gpart; unsigned* gticket; unsigned* ticket; DD* out;
+};
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ double ld_dsmem(const double* local, unsigned rank) {
+  const unsigned addr = (unsigned)__cvta_generic_to_shared(local);
+  unsigned remote;
+  double v;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(addr), "r"(rank));
+  asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(remote) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned cluster_rank() {
+  unsigned r; asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r)); return r;
+}
+__device__ __forceinline__ unsigned cluster_id_x() {
+  unsigned r; asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r)); return r;
+}
+__device__ __forceinline__ unsigned nclusters_x() {
+  unsigned r; asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(r)); return r;
+}
+
+template <class T, int NL, int UNR, int ILP, int CL>
+__global__ void __launch_bounds__(BLOCK) red_kernel(Args a) {
+  const T* x = (const T*)a.x;
+  const T* y = (const T*)a.y;
+  Acc<T> acc[ILP];
+  const i64 per = (i64)BLOCK * UNR;
+  const i64 ntiles = (a.nvec + per - 1) / per;
+  const i64 t0 = (i64)blockIdx.x * a.K;
+  const i64 t1 = min(t0 + a.K, ntiles);
+  for (i64 t = t0; t < t1; ++t) {
+    Vec<T> va[UNR], vb[UNR];
+    const i64 base = t * per + threadIdx.x;
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const i64 j = base + (i64)u * BLOCK;
+      if (j < a.nvec) { va[u].load(x + j * Vec<T>::W); if (NL == 2) vb[u].load(y + j * Vec<T>::W); }
+    }
+#pragma unroll
+    for (int u = 0; u < UNR; ++u)
+      if (base + (i64)u * BLOCK < a.nvec) {
+#pragma unroll
+        for (int k = 0; k < Vec<T>::W; ++k)
+          acc[(u * Vec<T>::W + k) % ILP].add(mul_rn(va[u].v[k], NL == 1 ? va[u].v[k] : vb[u].v[k]));
+      }
+  }
+  DD mine = acc[0].get();
+#pragma unroll
+  for (int i = 1; i < ILP; ++i) mine = dd_add(mine, acc[i].get());
+  __shared__ DD sm[BLOCK / 32];
+  __shared__ int stage;
+  __shared__ DD cpart;
+  DD part = block_dd(mine, sm);
+  if (!a.combine) {
+    if (threadIdx.x == 0) a.partials[blockIdx.x] = part;
+    return;
+  }
+  unsigned unit = blockIdx.x, nunits = gridDim.x;
+  if constexpr (CL > 0) {  // fold the cluster's CTA partials in DSMEM; rank 0 carries on
+    if (threadIdx.x == 0) cpart = part;
+    cluster_sync_all();
+    const unsigned cr = cluster_rank();
+    DD v{0, 0};
+    if (cr == 0 && threadIdx.x < 32) {
+      if (threadIdx.x < CL) { v.hi = ld_dsmem(&cpart.hi, threadIdx.x); v.lo = ld_dsmem(&cpart.lo, threadIdx.x); }
+      for (int o = 16; o; o >>= 1) {
+        DD w; w.hi = __shfl_xor_sync(~0u, v.hi, o); w.lo = __shfl_xor_sync(~0u, v.lo, o);
+        v = dd_add(v, w);
+      }
+    }
+    cluster_sync_all();
+    if (cr != 0) return;
+    part = v;  // valid in thread 0
+    unit = cluster_id_x();
+    nunits = nclusters_x();
+  }
+  const unsigned GS = a.GS;
+  const unsigned g = unit / GS, ng = (nunits + GS - 1) / GS;
+  const unsigned gsize = min(GS, nunits - g * GS);
+  if (threadIdx.x == 0) {
+    a.partials[unit] = part;
+    stage = ticket_add(&a.gticket[g]) == gsize - 1;
+  }
+  __syncthreads();
+  if (!stage) return;
+  DD v{0, 0};
+  {
+    DD p[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const unsigned b = threadIdx.x + i * BLOCK;
+      if (b < gsize) { p[i].hi = __ldcg(&a.partials[g * GS + b].hi); p[i].lo = __ldcg(&a.partials[g * GS + b].lo); }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (threadIdx.x + i * BLOCK < gsize) v = dd_add(v, p[i]);
+    for (unsigned b = threadIdx.x + 4 * BLOCK; b < gsize; b += BLOCK) {
+      DD q; q.hi = __ldcg(&a.partials[g * GS + b].hi); q.lo = __ldcg(&a.partials[g * GS + b].lo);
+      v = dd_add(v, q);
+    }
+  }
+  __syncthreads();
+  DD q = block_dd(v, sm);
+  if (ng == 1) {
+    if (threadIdx.x == 0) { a.gticket[g] = 0; *a.out = q; }
+    return;
+  }
+  if (threadIdx.x == 0) {
+    a.gpart[g] = q;
+    a.gticket[g] = 0;
+    stage = ticket_add(a.ticket) == ng - 1 ? 2 : 0;
+  }
+  __syncthreads();
+  if (stage != 2) return;
+  DD w{0, 0};
+  for (unsigned b = threadIdx.x; b < ng; b += BLOCK) {
+    DD p; p.hi = __ldcg(&a.gpart[b].hi); p.lo = __ldcg(&a.gpart[b].lo);
+    w = dd_add(w, p);
+  }
+  __syncthreads();
+  DD tot = block_dd(w, sm);
+  if (threadIdx.x == 0) { *a.ticket = 0; *a.out = tot; }
+}
+
+__global__ void sweep_read(const double4* p, i64 n, double* sink) {
+  double s = 0;
+  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
+    double4 v = p[i];
+    s += v.x + v.w;
+  }
+  if (s == 12345.678) *sink = s;
+}
+
+struct Variant { std::string name; int unr; int ilp; int cl; i64 K; int GS; int combine; };
+
+template <class T, int NL, int UNR, int ILP, int CL> void launch(int grid, const Args& a) {
+  auto fn = red_kernel<T, NL, UNR, ILP, CL>;
+  if (CL == 0) { fn<<<grid, BLOCK>>>(a); return; }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(BLOCK);
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CL > 0 ? CL : 1;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  CK(cudaLaunchKernelEx(&cfg, fn, a));
+}
+template <class T, int NL, int UNR, int ILP> void by_cl(int cl, int grid, const Args& a) {
+  if (cl == 0) launch<T, NL, UNR, ILP, 0>(grid, a);
+  else if (cl == 4) launch<T, NL, UNR, ILP, 4>(grid, a);
+  else launch<T, NL, UNR, ILP, 8>(grid, a);
+}
+template <class T, int NL, int UNR> void by_ilp(int ilp, int cl, int grid, const Args& a) {
+  if (ilp == 1) by_cl<T, NL, UNR, 1>(cl, grid, a);
+  else if (ilp == 2) by_cl<T, NL, UNR, 2>(cl, grid, a);
+  else by_cl<T, NL, UNR, 4>(cl, grid, a);
+}
+template <class T, int NL> void dispatch(const Variant& v, int grid, const Args& a) {
+  if (v.unr == 2) by_ilp<T, NL, 2>(v.ilp, v.cl, grid, a);
+  else if (v.unr == 4) by_ilp<T, NL, 4>(v.ilp, v.cl, grid, a);
+  else by_ilp<T, NL, 8>(v.ilp, v.cl, grid, a);
+}
+
+int main(int argc, char** argv) {
+  int reps = argc > 1 ? atoi(argv[1]) : 15;
+  const i64 maxn = i64(1) << 27;
+  void *x, *y;
+  CK(cudaMalloc(&x, maxn * 8));
+  CK(cudaMalloc(&y, maxn * 8));
+  {  // fill with 0.5-ish values (no NaN/inf); exact values do not matter for timing
+    std::vector<double> h(maxn);
+    for (i64 i = 0; i < maxn; ++i) h[i] = std::ldexp((double)((i * 2654435761ull) % 1000003) - 500001.0, -20);
+    CK(cudaMemcpy(x, h.data(), maxn * 8, cudaMemcpyHostToDevice));
+    for (i64 i = 0; i < maxn; ++i) h[i] = std::ldexp((double)((i * 40503ull) % 999983) - 499991.0, -20);
+    CK(cudaMemcpy(y, h.data(), maxn * 8, cudaMemcpyHostToDevice));
+  }
+  const i64 sweep_bytes = i64(512) << 20;
+  void* sw; double* sink;
+  CK(cudaMalloc(&sw, sweep_bytes));
+  CK(cudaMemset(sw, 1, sweep_bytes));
+  CK(cudaMalloc(&sink, 8));
+  DD *parts, *gpart, *out;
+  unsigned *gt, *tk;
+  CK(cudaMalloc(&parts, 16 << 20));
+  CK(cudaMalloc(&gpart, 16 << 16));
+  CK(cudaMalloc(&gt, 4 << 16));
+  CK(cudaMalloc(&tk, 256));
+  CK(cudaMemset(gt, 0, 4 << 16));
+  CK(cudaMemset(tk, 0, 256));
+  CK(cudaMalloc(&out, 16));
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  int sms;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+  printf("# c3_probe: %d SMs, reps %d; us per launch (median / best) after an L2 sweep\n", sms, reps);
+
+  const char* ops[4] = {"nrm2_f64", "dot_f64", "nrm2_f32", "dot_f32"};
+  for (int op = 0; op < 4; ++op) {
+    const bool f64 = op < 2;
+    const int NL = (op & 1) ? 2 : 1;
+    const int es = f64 ? 8 : 4;
+    const char* lo_e = getenv("PROBE_LG_LO");
+    const char* hi_e = getenv("PROBE_LG_HI");
+    for (int lg = lo_e ? atoi(lo_e) : 24; lg <= (hi_e ? atoi(hi_e) : 24); ++lg) {
+      const i64 n = i64(1) << lg;
+      const i64 nvec = n * es / 32;
+      const double bytes = (double)n * es * NL;
+      std::vector<Variant> vs;
+      const int ucur = (!f64 || NL == 1) ? 4 : 2;
+      // K: > 0 fixed; -2 the round-1 product rule (one group of <= 512 / 256
+      // CTAs); GS: CTAs (or clusters) per combine group, -1 = the whole grid
+      vs.push_back({"floor", ucur, 1, 0, 1, 1 << 30, 0});
+      vs.push_back({"floor_U8", 8, 1, 0, 1, 1 << 30, 0});
+      vs.push_back({"product_r01", ucur, 1, 0, -2, 0, 1});
+      vs.push_back({"product_ilp2", ucur, 2, 0, -2, 0, 1});
+      vs.push_back({"product_ilp4", ucur, 4, 0, -2, 0, 1});
+      for (int u : {4, 8})
+        for (int ilp : {1, 2})
+          for (int K : {1, 2}) {
+            const std::string tag = "_U" + std::to_string(u) + "_I" + std::to_string(ilp) + "_K" + std::to_string(K);
+            vs.push_back({"gs256" + tag, u, ilp, 0, K, 256, 1});
+            vs.push_back({"one" + tag, u, ilp, 0, K, -1, 1});
+            vs.push_back({"cl8" + tag, u, ilp, 8, K, -1, 1});
+            vs.push_back({"cl4" + tag, u, ilp, 4, K, -1, 1});
+          }
+      double ref = NAN;
+      for (const Variant& v : vs) {
+        const i64 per = (i64)BLOCK * v.unr;
+        const i64 ntiles = (nvec + per - 1) / per;
+        i64 K = v.K;
+        int GS = v.GS;
+        if (K == -2) {  // round-1 product: one group of <= cap CTAs up to 16 tiles per CTA
+          const i64 cap = NL == 1 ? 512 : 256;
+          if (ntiles <= 16 * cap) { K = (ntiles + cap - 1) / cap; GS = 4096; }
+          else { K = NL == 1 ? 4 : 2; GS = 256; }
+        }
+        i64 grid = (ntiles + K - 1) / K;
+        if (v.cl) grid = (grid + v.cl - 1) / v.cl * v.cl;  // whole clusters (extra CTAs idle)
+        const i64 units = v.cl ? grid / v.cl : grid;
+        if (GS == -1) GS = (int)std::min<i64>(units, 1 << 20);
+        if (grid > (1 << 20) || (v.combine && (units + GS - 1) / GS > 65536)) continue;
+        Args a{x, NL == 2 ? y : x, nvec, K, GS, v.combine, parts, gpart, gt, tk, out};
+        auto sweep = [&](int mode, int r) {
+          if (mode == 0) sweep_read<<<sms * 8, 256>>>((const double4*)sw, sweep_bytes / 32, sink);
+          else CK(cudaMemsetAsync(sw, r & 0xff, sweep_bytes));
+        };
+        auto kern = [&]() {
+          if (f64) (NL == 1 ? dispatch<double, 1>(v, (int)grid, a) : dispatch<double, 2>(v, (int)grid, a));
+          else (NL == 1 ? dispatch<float, 1>(v, (int)grid, a) : dispatch<float, 2>(v, (int)grid, a));
+        };
+        for (int mode = 0; mode < 2; ++mode) {
+          // differential: R x (sweep + kernel) minus R x sweep, 3 trials, min
+          // (the event clock ticks in ~2 us steps on this box)
+          double best = 1e30;
+          for (int trial = 0; trial < 3; ++trial) {
+            float ms_pair, ms_sweep;
+            sweep(mode, 0); kern();
+            CK(cudaEventRecord(e0));
+            for (int r = 0; r < reps; ++r) { sweep(mode, r); kern(); }
+            CK(cudaEventRecord(e1));
+            CK(cudaEventSynchronize(e1));
+            CK(cudaEventElapsedTime(&ms_pair, e0, e1));
+            CK(cudaEventRecord(e0));
+            for (int r = 0; r < reps; ++r) sweep(mode, r);
+            CK(cudaEventRecord(e1));
+            CK(cudaEventSynchronize(e1));
+            CK(cudaEventElapsedTime(&ms_sweep, e0, e1));
+            best = std::min(best, (double)(ms_pair - ms_sweep) * 1000.0 / reps);
+          }
+          CK(cudaGetLastError());
+          if (v.combine && mode == 0) {
+            DD h;
+            CK(cudaMemcpy(&h, out, 16, cudaMemcpyDeviceToHost));
+            if (std::isnan(ref)) ref = h.hi;
+            else if (std::fabs(h.hi - ref) > 1e-13 * std::fabs(ref)) printf("MISMATCH %s %.17g vs %.17g\n", v.name.c_str(), h.hi, ref);
+          }
+          printf("%-9s 2^%d %-5s %-14s grid %7lld K %2lld GS %5d: %8.2f us  %6.0f GB/s\n", ops[op], lg,
+                 mode ? "dirty" : "clean", v.name.c_str(), (long long)grid, (long long)K, GS, best, bytes / best / 1e3);
+        }
+      }
+    }
+  }
+  return 0;
+}
