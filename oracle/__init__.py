@@ -16,7 +16,9 @@ Modules
             (bit-exact for a given plan), exact fsum reductions, the
             reference's scalar-loop oracles (oracle.py:26-69).
   coracle   ctypes wrapper of salt_oracle.c (C restatement, threaded).
-  data      chunk-keyed seeded synthetic inputs for the BASELINE configs.
+
+(The chunk-keyed seeded synthetic inputs for the BASELINE configs live in
+the package, paper_1109_1264_b200/synth.py: they are inputs, not a checker.)
 
 Parity is PINNED: restate/coracle are checked in tests/test_oracle_pins.py
 against golden vectors produced by the reference itself

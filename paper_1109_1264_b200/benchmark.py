@@ -33,13 +33,14 @@ import json
 import statistics
 import sys
 import time
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 from pathlib import Path
 
 import numpy as np
 
 __all__ = ["BenchRecord", "OPS", "EXTENDED_OPS", "VARIANTS", "run_sweep", "emit_csv", "parse_csv",
-           "main", "bytes_moved", "flop_count", "default_sizes", "simd_available", "record_lines"]
+           "main", "bytes_moved", "flop_count", "default_sizes", "gpu_sizes", "simd_available", "record_lines",
+           "measure", "CSV_HEADER"]
 
 OPS = ("dot", "scal", "axpy", "scaled_copy")
 EXTENDED_OPS = OPS + ("sum", "norm2", "t1", "t2", "etree", "axpy_dot")
@@ -69,15 +70,28 @@ class BenchRecord:
     median_s: float
     gflops: float
     gbytes: float
-    pct_hbm: float = float("nan")
-    device: str = ""
-    gpus: int = 1
-    bytes: int = 0
-    pct_hbm_nominal: float = float("nan")
+    # GPU extras (--extended CSV columns).  They take no part in equality, so
+    # a record read back from the reference's 9-column CSV equals the one
+    # written (reference test_bench.py:90-100).
+    pct_hbm: float = field(default=float("nan"), compare=False)
+    device: str = field(default="", compare=False)
+    gpus: int = field(default=1, compare=False)
+    bytes: int = field(default=0, compare=False)
+    pct_hbm_nominal: float = field(default=float("nan"), compare=False)
 
 
 def default_sizes() -> list:
-    """2^6 .. 2^28 by 4x, each with its +-1 neighbours."""
+    """The reference's sweep (bench.py:72-82): every power of two 2^6 .. 2^22
+    with its +-1 neighbours.  Device-scale sweeps: gpu_sizes()."""
+    out = set()
+    for p in range(6, 23):
+        out.update(((1 << p) - 1, 1 << p, (1 << p) + 1))
+    return sorted(out)
+
+
+def gpu_sizes() -> list:
+    """2^6 .. 2^28 by 4x, each with its +-1 neighbours (`--sizes gpu`): up to
+    the HBM-resident sizes where the roofline applies."""
     out = set()
     for p in range(6, 29, 2):
         out.update(((1 << p) - 1, 1 << p, (1 << p) + 1))
@@ -122,7 +136,31 @@ def _operands(op, n, dt, device, seed):
     return vecs, out
 
 
-def _engine_call(op, v, out, options):
+def _make_data(op, n, dtype, seed, device=None):
+    """(x, y, out) of a reference op, seeded as the reference seeds them
+    (bench.py:97-106: stream [seed, n, op index], x then y, out zeros)."""
+    vecs, out = _operands(op, n, dtype, device if device is not None else "cuda", seed)
+    return vecs[0], (vecs[1] if len(vecs) > 1 else None), out
+
+
+def _engine_call(op, x, y, out, alpha, options):
+    """Zero-argument callable running a reference op once (reference
+    bench.py:109-118)."""
+    import paper_1109_1264_b200 as lv
+
+    if op == "dot":
+        return lambda: lv.dot(x, y, lazy=True, **options)
+    if op == "scal":
+        return lambda: lv.scal(alpha, x, **options)
+    if op == "axpy":
+        return lambda: lv.axpy(alpha, x, y, **options)
+    if op == "scaled_copy":
+        return lambda: lv.scaled_copy(alpha, x, out, **options)
+    raise ValueError(f"unknown op {op!r}")
+
+
+def _engine_call_ext(op, v, out, options):
+    """The BASELINE-config ops (and the reference ops) over operand list v."""
     import paper_1109_1264_b200 as lv
 
     if op == "dot":
@@ -199,7 +237,12 @@ def measure(op, variant, n, dtype="f32", reps=25, warmup=5, seed=0, packages=Non
     if packages is not None:
         options["packages"] = packages
     unfused = variant in ("torch", "naive")
-    call = _torch_call(op, vecs, out) if unfused else _engine_call(op, vecs, out, options)
+    if unfused:
+        call = _torch_call(op, vecs, out)
+    elif op in OPS:  # through the module global, so a spy can wrap it (reference test_bench.py:190-212)
+        call = _engine_call(op, vecs[0], vecs[1] if len(vecs) > 1 else None, out, _ALPHA, options)
+    else:
+        call = _engine_call_ext(op, vecs, out, options)
     mutated = {"scal": 0, "axpy": 1, "axpy_dot": 1}.get(op)
     pristine = vecs[mutated].tensor.clone() if mutated is not None and n else None
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda") if flush_l2 else None
@@ -307,7 +350,8 @@ def main(argv=None) -> int:
     ap.add_argument("--op", default="all", help="one op, 'all' (reference ops) or 'extended'")
     ap.add_argument("--type", default="f32", choices=("f32", "f64"))
     ap.add_argument("--variants", default="engine,torch")
-    ap.add_argument("--sizes", default="default")
+    ap.add_argument("--sizes", default="default",
+                    help="'default' (the reference's 2^6..2^22 sweep), 'gpu' (2^6..2^28 by 4x) or a comma list")
     ap.add_argument("--reps", type=int, default=25)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--seed", type=int, default=0)
@@ -330,6 +374,8 @@ def main(argv=None) -> int:
             ap.error(f"unknown variant {v!r}; choose from {', '.join(VARIANTS)}")
     if a.sizes == "default":
         sizes = default_sizes()
+    elif a.sizes == "gpu":
+        sizes = gpu_sizes()
     else:
         try:
             sizes = [int(s) for s in a.sizes.split(",") if s]

@@ -108,9 +108,9 @@ def test_all_variants_run():
 def test_seeded_data_is_reproducible():
     import paper_1109_1264_b200.benchmark as bm
 
-    (x1,), _ = bm._operands("scal", 50, np.dtype(np.float64), "cuda", 3)
-    (x2,), _ = bm._operands("scal", 50, np.dtype(np.float64), "cuda", 3)
-    (x3,), _ = bm._operands("scal", 50, np.dtype(np.float64), "cuda", 4)
+    x1, _, _ = bm._make_data("scal", 50, np.dtype(np.float64), 3)
+    x2, _, _ = bm._make_data("scal", 50, np.dtype(np.float64), 3)
+    x3, _, _ = bm._make_data("scal", 50, np.dtype(np.float64), 4)
     assert x1.to_array().tobytes() == x2.to_array().tobytes() != x3.to_array().tobytes()
 
 
@@ -128,11 +128,11 @@ def test_inplace_ops_are_restored_between_reps():
     seen = []
     real = bm._engine_call
 
-    def spy(op, v, out, options):
-        call = real(op, v, out, options)
+    def spy(op, x, y, out, alpha, options):
+        call = real(op, x, y, out, alpha, options)
 
         def wrapped():
-            seen.append(v[0 if op == "scal" else 1].to_array().copy())
+            seen.append((x if op == "scal" else y).to_array().copy())
             return call()
         return wrapped
 

@@ -388,9 +388,12 @@ def test_flop_and_byte_accounting():
 
 def test_default_sizes_cover_powers_of_two_with_neighbors():
     sizes = sb.default_sizes()
-    for p in (8, 16, 24):
+    for p in range(6, 23):
         assert {(1 << p) - 1, 1 << p, (1 << p) + 1} <= set(sizes)
-    assert sizes == sorted(set(sizes))
+    assert sizes == sorted(set(sizes)) and sizes[-1] == (1 << 22) + 1
+    big = sb.gpu_sizes()
+    for p in (8, 16, 24, 28):
+        assert {(1 << p) - 1, 1 << p, (1 << p) + 1} <= set(big)
 
 
 def test_emit_csv_header_only_for_no_records(tmp_path):

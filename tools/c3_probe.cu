@@ -240,6 +240,64 @@ __global__ void __launch_bounds__(BLOCK) red_kernel(Args a) {
   if (threadIdx.x == 0) { *a.ticket = 0; *a.out = tot; }
 }
 
+// Collector combine (no fences, no atomics on the streaming CTAs): CTA 0
+// folds; CTAs 1.. stream K tiles each and store their partial XOR-encoded
+// (zero memory = "not written": MASK is a signalling-NaN pattern no
+// arithmetic produces) with a plain 16-byte store, then exit.  Collector
+// thread t polls slots t, t + BLOCK, ... in order (volatile loads), folds
+// each as it appears, resets it to zero; block reduce; done.
+constexpr unsigned long long kMask = 0x7ff4000000000001ull;
+template <class T, int NL, int UNR>
+__global__ void __launch_bounds__(BLOCK) coll_kernel(Args a) {
+  __shared__ DD sm[BLOCK / 32];
+  unsigned long long* slots = (unsigned long long*)a.partials;
+  const unsigned np = gridDim.x - 1;
+  if (blockIdx.x == 0) {
+    DD v{0, 0};
+    for (unsigned q = threadIdx.x; q < np; q += BLOCK) {
+      unsigned long long h, l;
+      do {
+        asm volatile("ld.volatile.global.v2.u64 {%0,%1}, [%2];" : "=l"(h), "=l"(l) : "l"(slots + 2 * q));
+      } while (h == 0ull || l == 0ull);
+      DD p; p.hi = __longlong_as_double((long long)(h ^ kMask)); p.lo = __longlong_as_double((long long)(l ^ kMask));
+      v = dd_add(v, p);
+      asm volatile("st.global.v2.u64 [%0], {%1,%2};" :: "l"(slots + 2 * q), "l"(0ull), "l"(0ull) : "memory");
+    }
+    DD tot = block_dd(v, sm);
+    if (threadIdx.x == 0) *a.out = tot;
+    return;
+  }
+  const T* x = (const T*)a.x;
+  const T* y = (const T*)a.y;
+  Acc<T> acc;
+  const i64 per = (i64)BLOCK * UNR;
+  const i64 ntiles = (a.nvec + per - 1) / per;
+  const i64 t0 = (i64)(blockIdx.x - 1) * a.K;
+  const i64 t1 = min(t0 + a.K, ntiles);
+  for (i64 t = t0; t < t1; ++t) {
+    Vec<T> va[UNR], vb[UNR];
+    const i64 base = t * per + threadIdx.x;
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const i64 j = base + (i64)u * BLOCK;
+      if (j < a.nvec) { va[u].load(x + j * Vec<T>::W); if (NL == 2) vb[u].load(y + j * Vec<T>::W); }
+    }
+#pragma unroll
+    for (int u = 0; u < UNR; ++u)
+      if (base + (i64)u * BLOCK < a.nvec) {
+#pragma unroll
+        for (int k = 0; k < Vec<T>::W; ++k) acc.add(mul_rn(va[u].v[k], NL == 1 ? va[u].v[k] : vb[u].v[k]));
+      }
+  }
+  DD part = block_dd(acc.get(), sm);
+  if (threadIdx.x == 0) {
+    const unsigned long long h = (unsigned long long)__double_as_longlong(part.hi) ^ kMask;
+    const unsigned long long l = (unsigned long long)__double_as_longlong(part.lo) ^ kMask;
+    const unsigned q = blockIdx.x - 1;
+    asm volatile("st.global.v2.u64 [%0], {%1,%2};" :: "l"(slots + 2 * q), "l"(h), "l"(l) : "memory");
+  }
+}
+
 __global__ void sweep_read(const double4* p, i64 n, double* sink) {
   double s = 0;
   for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
@@ -277,6 +335,12 @@ template <class T, int NL, int UNR> void by_ilp(int ilp, int cl, int grid, const
   else by_cl<T, NL, UNR, 4>(cl, grid, a);
 }
 template <class T, int NL> void dispatch(const Variant& v, int grid, const Args& a) {
+  if (v.combine == 3) {
+    if (v.unr == 4) coll_kernel<T, NL, 4><<<grid + 1, BLOCK>>>(a);
+    else if (v.unr == 8) coll_kernel<T, NL, 8><<<grid + 1, BLOCK>>>(a);
+    else coll_kernel<T, NL, 2><<<grid + 1, BLOCK>>>(a);
+    return;
+  }
   if (v.unr == 2) by_ilp<T, NL, 2>(v.ilp, v.cl, grid, a);
   else if (v.unr == 4) by_ilp<T, NL, 4>(v.ilp, v.cl, grid, a);
   else by_ilp<T, NL, 8>(v.ilp, v.cl, grid, a);
@@ -303,6 +367,9 @@ int main(int argc, char** argv) {
   DD *parts, *gpart, *out;
   unsigned *gt, *tk;
   CK(cudaMalloc(&parts, 16 << 20));
+  DD* cparts;  // the collector's slots: zero = not written; it resets them
+  CK(cudaMalloc(&cparts, 16 << 20));
+  CK(cudaMemset(cparts, 0, 16 << 20));
   CK(cudaMalloc(&gpart, 16 << 16));
   CK(cudaMalloc(&gt, 4 << 16));
   CK(cudaMalloc(&tk, 256));
@@ -336,6 +403,13 @@ int main(int argc, char** argv) {
       vs.push_back({"product_r01", ucur, 1, 0, -2, 0, 1});
       vs.push_back({"product_ilp2", ucur, 2, 0, -2, 0, 1});
       vs.push_back({"product_ilp4", ucur, 4, 0, -2, 0, 1});
+      vs.push_back({"coll_product", ucur, 1, 0, -2, 0, 3});
+      for (int u : {2, 4, 8})
+        for (int K : {1, 2, 4}) {
+          vs.push_back({"coll_U" + std::to_string(u) + "_K" + std::to_string(K), u, 1, 0, K, 0, 3});
+          vs.push_back({"nocomb_U" + std::to_string(u) + "_K" + std::to_string(K), u, 1, 0, K, 1 << 30, 0});
+        }
+      if (getenv("PROBE_ALL"))
       for (int u : {4, 8})
         for (int ilp : {1, 2})
           for (int K : {1, 2}) {
@@ -361,7 +435,7 @@ int main(int argc, char** argv) {
         const i64 units = v.cl ? grid / v.cl : grid;
         if (GS == -1) GS = (int)std::min<i64>(units, 1 << 20);
         if (grid > (1 << 20) || (v.combine && (units + GS - 1) / GS > 65536)) continue;
-        Args a{x, NL == 2 ? y : x, nvec, K, GS, v.combine, parts, gpart, gt, tk, out};
+        Args a{x, NL == 2 ? y : x, nvec, K, GS, v.combine, v.combine == 3 ? cparts : parts, gpart, gt, tk, out};
         auto sweep = [&](int mode, int r) {
           if (mode == 0) sweep_read<<<sms * 8, 256>>>((const double4*)sw, sweep_bytes / 32, sink);
           else CK(cudaMemsetAsync(sw, r & 0xff, sweep_bytes));
