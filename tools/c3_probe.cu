@@ -348,6 +348,7 @@ template <class T, int NL> void dispatch(const Variant& v, int grid, const Args&
 
 int main(int argc, char** argv) {
   int reps = argc > 1 ? atoi(argv[1]) : 15;
+  setvbuf(stdout, nullptr, _IOLBF, 0);
   const i64 maxn = i64(1) << 27;
   void *x, *y;
   CK(cudaMalloc(&x, maxn * 8));
@@ -403,10 +404,10 @@ int main(int argc, char** argv) {
       vs.push_back({"product_r01", ucur, 1, 0, -2, 0, 1});
       vs.push_back({"product_ilp2", ucur, 2, 0, -2, 0, 1});
       vs.push_back({"product_ilp4", ucur, 4, 0, -2, 0, 1});
-      vs.push_back({"coll_product", ucur, 1, 0, -2, 0, 3});
+      vs.push_back({"coll_product", ucur, 1, 0, -2, 1 << 30, 3});
       for (int u : {2, 4, 8})
         for (int K : {1, 2, 4}) {
-          vs.push_back({"coll_U" + std::to_string(u) + "_K" + std::to_string(K), u, 1, 0, K, 0, 3});
+          vs.push_back({"coll_U" + std::to_string(u) + "_K" + std::to_string(K), u, 1, 0, K, 1 << 30, 3});
           vs.push_back({"nocomb_U" + std::to_string(u) + "_K" + std::to_string(K), u, 1, 0, K, 1 << 30, 0});
         }
       if (getenv("PROBE_ALL"))
