@@ -247,11 +247,47 @@ __global__ void __launch_bounds__(BLOCK) red_kernel(Args a) {
 // thread t polls slots t, t + BLOCK, ... in order (volatile loads), folds
 // each as it appears, resets it to zero; block reduce; done.
 constexpr unsigned long long kMask = 0x7ff4000000000001ull;
-template <class T, int NL, int UNR>
+__device__ __forceinline__ DD warp_dd(DD v) {
+  for (int o = 16; o; o >>= 1) {
+    DD w; w.hi = __shfl_xor_sync(~0u, v.hi, o); w.lo = __shfl_xor_sync(~0u, v.lo, o);
+    v = dd_add(v, w);
+  }
+  return v;
+}
+// V2 = 1: one warp collects (lane l folds slots l, l + 32, ... in order),
+// polling up to 8 of its slots per round trip; the final fold is one warp
+// shuffle tree.  V2 = 0: all BLOCK threads, one slot per round trip.
+template <class T, int NL, int UNR, int V2>
 __global__ void __launch_bounds__(BLOCK) coll_kernel(Args a) {
   __shared__ DD sm[BLOCK / 32];
   unsigned long long* slots = (unsigned long long*)a.partials;
   const unsigned np = gridDim.x - 1;
+  if (blockIdx.x == 0 && V2) {
+    if (threadIdx.x >= 32) return;
+    DD v{0, 0};
+    unsigned q = threadIdx.x;  // next slot of this lane
+    while (q < np) {
+      unsigned long long h[8], l[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const unsigned s = q + 32u * i;
+        if (s < np) asm volatile("ld.volatile.global.v2.u64 {%0,%1}, [%2];" : "=l"(h[i]), "=l"(l[i]) : "l"(slots + 2 * s));
+        else { h[i] = 1; l[i] = 1; }
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const unsigned s = q;
+        if (s >= np || h[i] == 0ull || l[i] == 0ull) break;
+        DD p; p.hi = __longlong_as_double((long long)(h[i] ^ kMask)); p.lo = __longlong_as_double((long long)(l[i] ^ kMask));
+        v = dd_add(v, p);
+        asm volatile("st.global.v2.u64 [%0], {%1,%2};" :: "l"(slots + 2 * s), "l"(0ull), "l"(0ull) : "memory");
+        q += 32u;
+      }
+    }
+    v = warp_dd(v);
+    if (threadIdx.x == 0) *a.out = v;
+    return;
+  }
   if (blockIdx.x == 0) {
     DD v{0, 0};
     for (unsigned q = threadIdx.x; q < np; q += BLOCK) {
@@ -335,10 +371,16 @@ template <class T, int NL, int UNR> void by_ilp(int ilp, int cl, int grid, const
   else by_cl<T, NL, UNR, 4>(cl, grid, a);
 }
 template <class T, int NL> void dispatch(const Variant& v, int grid, const Args& a) {
-  if (v.combine == 3) {
-    if (v.unr == 4) coll_kernel<T, NL, 4><<<grid + 1, BLOCK>>>(a);
-    else if (v.unr == 8) coll_kernel<T, NL, 8><<<grid + 1, BLOCK>>>(a);
-    else coll_kernel<T, NL, 2><<<grid + 1, BLOCK>>>(a);
+  if (v.combine == 3 || v.combine == 4) {
+    if (v.combine == 4) {
+      if (v.unr == 4) coll_kernel<T, NL, 4, 1><<<grid + 1, BLOCK>>>(a);
+      else if (v.unr == 8) coll_kernel<T, NL, 8, 1><<<grid + 1, BLOCK>>>(a);
+      else coll_kernel<T, NL, 2, 1><<<grid + 1, BLOCK>>>(a);
+      return;
+    }
+    if (v.unr == 4) coll_kernel<T, NL, 4, 0><<<grid + 1, BLOCK>>>(a);
+    else if (v.unr == 8) coll_kernel<T, NL, 8, 0><<<grid + 1, BLOCK>>>(a);
+    else coll_kernel<T, NL, 2, 0><<<grid + 1, BLOCK>>>(a);
     return;
   }
   if (v.unr == 2) by_ilp<T, NL, 2>(v.ilp, v.cl, grid, a);
@@ -405,9 +447,11 @@ int main(int argc, char** argv) {
       vs.push_back({"product_ilp2", ucur, 2, 0, -2, 0, 1});
       vs.push_back({"product_ilp4", ucur, 4, 0, -2, 0, 1});
       vs.push_back({"coll_product", ucur, 1, 0, -2, 1 << 30, 3});
+      vs.push_back({"cwarp_product", ucur, 1, 0, -2, 1 << 30, 4});
       for (int u : {2, 4, 8})
         for (int K : {1, 2, 4}) {
           vs.push_back({"coll_U" + std::to_string(u) + "_K" + std::to_string(K), u, 1, 0, K, 1 << 30, 3});
+          vs.push_back({"cwarp_U" + std::to_string(u) + "_K" + std::to_string(K), u, 1, 0, K, 1 << 30, 4});
           vs.push_back({"nocomb_U" + std::to_string(u) + "_K" + std::to_string(K), u, 1, 0, K, 1 << 30, 0});
         }
       if (getenv("PROBE_ALL"))
@@ -436,7 +480,7 @@ int main(int argc, char** argv) {
         const i64 units = v.cl ? grid / v.cl : grid;
         if (GS == -1) GS = (int)std::min<i64>(units, 1 << 20);
         if (grid > (1 << 20) || (v.combine && (units + GS - 1) / GS > 65536)) continue;
-        Args a{x, NL == 2 ? y : x, nvec, K, GS, v.combine, v.combine == 3 ? cparts : parts, gpart, gt, tk, out};
+        Args a{x, NL == 2 ? y : x, nvec, K, GS, v.combine, v.combine >= 3 ? cparts : parts, gpart, gt, tk, out};
         auto sweep = [&](int mode, int r) {
           if (mode == 0) sweep_read<<<sms * 8, 256>>>((const double4*)sw, sweep_bytes / 32, sink);
           else CK(cudaMemsetAsync(sw, r & 0xff, sweep_bytes));
