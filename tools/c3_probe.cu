@@ -391,7 +391,7 @@ template <class T, int NL> void dispatch(const Variant& v, int grid, const Args&
 int main(int argc, char** argv) {
   int reps = argc > 1 ? atoi(argv[1]) : 15;
   setvbuf(stdout, nullptr, _IOLBF, 0);
-  const i64 maxn = i64(1) << 27;
+  const i64 maxn = i64(1) << 28;
   void *x, *y;
   CK(cudaMalloc(&x, maxn * 8));
   CK(cudaMalloc(&y, maxn * 8));
