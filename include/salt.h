@@ -287,9 +287,10 @@ int salt_assign_reduce_host(int dtype, const char* assign_sig, const char* reduc
                             void* const* streams3, void* out_host);
 
 /* Bytes of device scratch salt_reduce / salt_assign_reduce need.  Only the
- * first SALT_WORKSPACE_TICKET_BYTES (the arrival counters) must be zero
- * before the first use; the kernels reset them after every reduction. */
-#define SALT_WORKSPACE_TICKET_BYTES 16640
+ * first SALT_WORKSPACE_TICKET_BYTES (arrival counters and collector slots)
+ * must be zero before the first use; the kernels leave them zero again after
+ * every reduction. */
+#define SALT_WORKSPACE_TICKET_BYTES 1065216
 size_t salt_reduce_workspace_bytes(void);
 /* Two-step host result for callers that release a lock while waiting:
  * enqueue the device->host copy of a reduction result (out_dev, <= 64

@@ -24,7 +24,7 @@ __all__ = [
     "HEADER_SYMBOLS",
 ]
 
-SALT_WORKSPACE_TICKET_BYTES = 16640
+SALT_WORKSPACE_TICKET_BYTES = 1065216
 SALT_MAX_LEAVES = 16
 SALT_MAX_SCALARS = 32
 SALT_MAX_ROOTS = 4

@@ -136,6 +136,32 @@ int assign_tiles_per_cta() {
   return env > 0 ? env : 1;
 }
 
+// Collector combine (salt_expr.cuh collect_epilogue) for reductions whose
+// grid has between collect_min() and MAX_COLLECT streaming CTAs of
+// collect_tiles() tiles each; SALT_COMBINE=ticket disables it (tests,
+// tuning), SALT_COLLECT_TILES / SALT_COLLECT_MIN tune it (tools/c3_probe.cu).
+bool collect_enabled() {
+  static const bool env = [] {
+    const char* e = getenv("SALT_COMBINE");
+    return !(e && std::string(e) == "ticket");
+  }();
+  return env;
+}
+int collect_tiles() {
+  static const int env = [] {
+    const char* e = getenv("SALT_COLLECT_TILES");
+    return e ? atoi(e) : 0;
+  }();
+  return env > 0 ? env : 2;
+}
+int collect_min() {
+  static const int env = [] {
+    const char* e = getenv("SALT_COLLECT_MIN");
+    return e ? atoi(e) : -1;
+  }();
+  return env >= 0 ? env : 256;
+}
+
 int reduce_tiles_per_cta(int nl) {
   static const int env = [] {
     const char* e = getenv("SALT_REDUCE_TILES");
@@ -635,7 +661,7 @@ int run_fused(Plan& p, void* const* dsts, int ndst, const void* const* leaves, i
   const i64 per_tile = (i64)kBlock * k->unroll;
   const i64 ntiles = (a.nvec + per_tile - 1) / per_tile;
   i64 K = assign_tiles_per_cta(), cap = i64(0x7fffffff);
-  bool cluster = false, one_group = false;
+  bool cluster = false, one_group = false, collect = false;
   if (reduce && ntiles > 2 && ntiles <= (i64)max_cluster() * cluster_tiles()) {
     // Small n (3 .. 16 x 2 tiles; up to 2 tiles one CTA is quicker): one cluster
     // of <= 16 CTAs, partials combined in distributed shared memory — no
@@ -644,6 +670,18 @@ int run_fused(Plan& p, void* const* dsts, int ndst, const void* const* leaves, i
     // sdot 2^17 5.35 -> 4.28 us, fused axpy->dot 2^14 5.18 -> 4.07 us.
     K = (ntiles + max_cluster() - 1) / max_cluster();
     cluster = true;
+  } else if (reduce && ntiles > 2 && collect_enabled() &&
+             (ntiles + collect_tiles() - 1) / collect_tiles() >= collect_min()) {
+    // Mid and large n: streaming CTAs of collect_tiles() tiles that only
+    // store their partial, plus one collector CTA (tools/c3_probe.cu,
+    // profiles/r02_c3_probe*.txt: at 2^24 ddot 46.6 -> 42.6 us, sdot 25.7 ->
+    // 24.3 us, dnrm2 26.4 -> 25.5 us; the fence + ticket atomic each
+    // streaming CTA paid in the two-level combine held its SM slot).
+    // (beyond MAX_COLLECT CTAs of collect_tiles() tiles, more tiles per CTA:
+    // 2^27-2^28 measured equal for 2 and 4)
+    K = collect_tiles();
+    if ((ntiles + K - 1) / K > salt::MAX_COLLECT) K = (ntiles + salt::MAX_COLLECT - 1) / salt::MAX_COLLECT;
+    collect = true;
   } else if (reduce) {
     K = reduce_tiles_per_cta(p.nl);
     cap = salt::MAX_REDUCE_CTAS;
@@ -671,7 +709,9 @@ int run_fused(Plan& p, void* const* dsts, int ndst, const void* const* leaves, i
   if ((ntiles + K - 1) / K > cap) K = (ntiles + cap - 1) / cap;
   i64 g64 = (ntiles + K - 1) / K;
   if (g64 < 1) g64 = 1;
+  if (collect) g64 += 1;  // CTA 0: the collector
   const int grid = (int)g64;
+  a.first = collect ? 1 : 0;
   a.tiles_per_cta = K;
   // CTAs per combine group: the whole grid when it was sized as one group
   // (at most 2 x GROUP), else GROUP (a grid of <= GROUP CTAs is one group
@@ -683,6 +723,7 @@ int run_fused(Plan& p, void* const* dsts, int ndst, const void* const* leaves, i
     a.group_tickets = (unsigned int*)(w + salt::WsLayout::group_tickets);
     a.group_partials = (salt::DD*)(w + salt::WsLayout::group_partials);
     a.partials = (salt::DD*)(w + salt::WsLayout::partials);
+    a.slots = (unsigned long long*)(w + salt::WsLayout::slots);
     a.out = out_dev;
     if (x) {
       if (x->world < 1 || x->world > salt::XCHG_MAX_RANKS || x->rank < 0 || x->rank >= x->world ||

@@ -174,15 +174,22 @@ template <class T> struct Args {
   int cluster;                    // reduce modes: 1 = the grid is ONE thread-block cluster
   int group;                      // reduce modes: CTAs per group (GROUP, or the whole grid
                                   // when it is one group of <= MAX_ONE_GROUP CTAs)
+  int first;                      // 1: CTA 0 is the collector (see collect_epilogue), the
+                                  // streaming CTAs are 1..gridDim.x-1; 0: no collector
+  unsigned long long* slots;      // collector slots (2 words per streaming CTA, zero = empty)
   Xchg xchg;                      // sharded reductions over NVLink (world 0: off)
 };
 
-// Reduction workspace: [ticket | group tickets | group partials | CTA partials].
-enum { GROUP = 256, MAX_GROUPS = 4096, MAX_REDUCE_CTAS = GROUP * MAX_GROUPS, MAX_ONE_GROUP = 1024 };
+// Reduction workspace: [ticket | group tickets | collector slots | group
+// partials | CTA partials]; everything before group_partials must be zero
+// before the first use (the kernels leave it zero again).
+enum { GROUP = 256, MAX_GROUPS = 4096, MAX_REDUCE_CTAS = GROUP * MAX_GROUPS, MAX_ONE_GROUP = 1024,
+       MAX_COLLECT = 65536 };
 struct WsLayout {
   static constexpr i64 ticket = 0;
   static constexpr i64 group_tickets = 256;
-  static constexpr i64 group_partials = group_tickets + 4 * (i64)MAX_GROUPS;
+  static constexpr i64 slots = group_tickets + 4 * (i64)MAX_GROUPS;
+  static constexpr i64 group_partials = slots + 16 * (i64)MAX_COLLECT;
   static constexpr i64 partials = group_partials + 16 * (i64)MAX_GROUPS;
   static constexpr i64 bytes = partials + 16 * (i64)MAX_REDUCE_CTAS;
 };
@@ -430,6 +437,82 @@ template <int BLOCK> __device__ __forceinline__ DD block_reduce_dd(DD v, DD* sme
   return v;  // valid in thread 0
 }
 
+template <class T> __device__ __forceinline__ void finish_store(DD tot, int flags, void* out);
+
+// Warp shuffle tree over a double-double (valid in every lane).
+__device__ __forceinline__ DD warp_reduce_dd(DD v) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    DD o;
+    o.hi = __shfl_xor_sync(0xffffffffu, v.hi, off);
+    o.lo = __shfl_xor_sync(0xffffffffu, v.lo, off);
+    v = dd_add(v, o);
+  }
+  return v;
+}
+
+// Collector combine (mid and large reductions; tools/c3_probe.cu,
+// profiles/r02_c3_probe*.txt).  The grid is 1 + P CTAs: CTAs 1..P stream
+// their tiles, reduce them in the CTA and store the partial into their slot
+// with ONE plain 16-byte store — no fence, no atomic, so a streaming CTA
+// frees its SM slot as soon as its loads retire.  A slot holds the two
+// words of the partial XOR kSlotMask, so zero memory means "not written
+// yet": kSlotMask's words are signalling-NaN patterns, which no arithmetic
+// result (all partials are sums) can be.  Each 8-byte word is written once
+// and read whole, so a reader that sees both words non-zero has the value.
+// CTA 0's first warp is the collector: lane l folds slots l, l+32, l+64, ...
+// IN ORDER as they appear (polling up to 8 of its slots per round trip,
+// volatile loads), zeroes each slot it has consumed (the next launch is
+// stream-ordered after this one), then one warp shuffle tree gives the
+// total — fixed order, so the bits depend only on n.  Whatever order the
+// CTAs are scheduled in, nothing waits on the collector, so it cannot
+// deadlock; the collector only waits for stores that are certain to come.
+constexpr unsigned long long kSlotMask = 0x7ff4000000000001ull;
+
+template <class T, int BLOCK>
+__device__ __forceinline__ void collect_epilogue(DD mine, const Args<T>& a, DD* smem) {
+  const unsigned np = gridDim.x - 1;
+  if (blockIdx.x != 0) {
+    DD part = block_reduce_dd<BLOCK>(mine, smem);
+    if (threadIdx.x == 0) {
+      const unsigned long long h = (unsigned long long)__double_as_longlong(part.hi) ^ kSlotMask;
+      const unsigned long long l = (unsigned long long)__double_as_longlong(part.lo) ^ kSlotMask;
+      asm volatile("st.global.v2.u64 [%0], {%1,%2};" ::"l"(a.slots + 2 * (blockIdx.x - 1)), "l"(h), "l"(l)
+                   : "memory");
+    }
+    return;
+  }
+  if (threadIdx.x >= 32) return;
+  DD v; v.hi = 0.0; v.lo = 0.0;
+  unsigned q = threadIdx.x;  // this lane's next slot
+  while (q < np) {
+    unsigned long long h[8], l[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const unsigned s = q + 32u * i;
+      if (s < np)
+        asm volatile("ld.volatile.global.v2.u64 {%0,%1}, [%2];" : "=l"(h[i]), "=l"(l[i]) : "l"(a.slots + 2 * s));
+      else
+        h[i] = l[i] = 0ull;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if (q >= np || h[i] == 0ull || l[i] == 0ull) break;
+      DD p;
+      p.hi = __longlong_as_double((long long)(h[i] ^ kSlotMask));
+      p.lo = __longlong_as_double((long long)(l[i] ^ kSlotMask));
+      v = dd_add(v, p);
+      asm volatile("st.global.v2.u64 [%0], {%1,%2};" ::"l"(a.slots + 2 * q), "l"(0ull), "l"(0ull) : "memory");
+      q += 32u;
+    }
+  }
+  v = warp_reduce_dd(v);
+  if (threadIdx.x == 0) {
+    if (a.xchg.world > 0) v = exchange_dd(v, a.xchg);
+    finish_store<T>(v, a.flags, a.out);
+  }
+}
+
 // Round a double-double total to the element type, optional sqrt, store.
 template <class T> __device__ __forceinline__ void finish_store(DD tot, int flags, void* out) {
   if (flags & FLAG_PARTIAL) {
@@ -476,6 +559,10 @@ __device__ __forceinline__ void reduce_epilogue(DD mine, const Args<T>& a) {
   static_assert(MAX_ONE_GROUP % BLOCK == 0 && GROUP <= MAX_ONE_GROUP, "group fold layout");
   __shared__ DD smem[BLOCK / 32];
   __shared__ int stage;  // 0 done, 1 group finisher, 2 group + final finisher
+  if (a.first) {
+    collect_epilogue<T, BLOCK>(mine, a, smem);
+    return;
+  }
   DD part = block_reduce_dd<BLOCK>(mine, smem);
   if (gridDim.x == 1) {  // small n: no partials, no tickets, no fences
     if (threadIdx.x == 0) {
@@ -617,11 +704,13 @@ __global__ void SALT_BOUNDS(BLOCK) fused_kernel(Args<T> a) {
 
   Acc<T> acc;
   constexpr int ND = Roots<EA>::N;
-  const i64 nthreads = (i64)gridDim.x * BLOCK;
-  const i64 gtid = (i64)blockIdx.x * BLOCK + threadIdx.x;
+  // streaming CTA index (the collector CTA, if any, is blockIdx 0: cta < 0)
+  const i64 cta = (i64)blockIdx.x - a.first;
+  const i64 nthreads = ((i64)gridDim.x - a.first) * BLOCK;
+  const i64 gtid = cta * BLOCK + threadIdx.x;
 
   // ---- scalar head + tail (at most 2*(V-1) elements, or all of them if V == 1)
-  {
+  if (cta >= 0) {
     const i64 tail0 = a.head + a.nvec * V;
     const i64 nscalar = a.head + (a.n - tail0);
     for (i64 t = gtid; t < nscalar; t += nthreads) {
@@ -639,10 +728,10 @@ __global__ void SALT_BOUNDS(BLOCK) fused_kernel(Args<T> a) {
   }
 
   // ---- vector body: this CTA's run of consecutive tiles of BLOCK*UNR vectors
-  const i64 tile0 = (i64)blockIdx.x * a.tiles_per_cta;
+  const i64 tile0 = cta * a.tiles_per_cta;
   const i64 ntiles = (a.nvec + (i64)BLOCK * UNR - 1) / ((i64)BLOCK * UNR);
   const i64 tile1 = tile0 + a.tiles_per_cta < ntiles ? tile0 + a.tiles_per_cta : ntiles;
-  for (i64 t = tile0; t < tile1; ++t) {
+  for (i64 t = cta < 0 ? tile1 : tile0; t < tile1; ++t) {
     const i64 base = t * BLOCK * UNR + threadIdx.x;
     E1 e[UNR];
 #pragma unroll

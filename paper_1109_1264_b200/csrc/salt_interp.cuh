@@ -121,9 +121,10 @@ __global__ void __launch_bounds__(BLOCK) interp_kernel(InterpArgs<T> ia) {
   extern __shared__ __align__(16) unsigned char interp_smem[];
   T* sm = (T*)interp_smem;
   Acc<T> acc;
-  const i64 nthreads = (i64)gridDim.x * BLOCK;
-  const i64 gtid = (i64)blockIdx.x * BLOCK + threadIdx.x;
-  {  // scalar head + tail, as fused_kernel
+  const i64 cta = (i64)blockIdx.x - a.first;  // < 0: the collector CTA
+  const i64 nthreads = ((i64)gridDim.x - a.first) * BLOCK;
+  const i64 gtid = cta * BLOCK + threadIdx.x;
+  if (cta >= 0) {  // scalar head + tail, as fused_kernel
     const i64 tail0 = a.head + a.nvec * V;
     const i64 nscalar = a.head + (a.n - tail0);
     for (i64 t = gtid; t < nscalar; t += nthreads) {
@@ -132,9 +133,9 @@ __global__ void __launch_bounds__(BLOCK) interp_kernel(InterpArgs<T> ia) {
     }
   }
   const i64 ntiles = (a.nvec + (i64)BLOCK * UNR - 1) / ((i64)BLOCK * UNR);
-  const i64 tile0 = (i64)blockIdx.x * a.tiles_per_cta;
+  const i64 tile0 = cta * a.tiles_per_cta;
   const i64 tile1 = tile0 + a.tiles_per_cta < ntiles ? tile0 + a.tiles_per_cta : ntiles;
-  for (i64 t = tile0; t < tile1; ++t) {
+  for (i64 t = cta < 0 ? tile1 : tile0; t < tile1; ++t) {
     const i64 base = t * BLOCK * UNR + threadIdx.x;
     for (int u = 0; u < UNR; ++u) {
       const i64 j = base + (i64)u * BLOCK;
