@@ -8,6 +8,9 @@
 //
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -fmad=false \
 //        -o tools/c3_probe tools/c3_probe.cu && tools/c3_probe
+// PROBE_SET=final with -DWITH_SALT (link -Lpaper_1109_1264_b200 -lsalt):
+// the bare-read floors next to the PRODUCT (salt_reduce through the C ABI),
+// same process, same sweeps, same timing.
 //
 // Every variant computes the same compensated double-double sum as the
 // product (TwoSum per f64 term / exact f64 sum of f32 terms) and is checked
@@ -26,6 +29,9 @@
 //   cl8_* cl4_*  clusters of 8 / 4 CTAs fold in DSMEM; one ticket level over
 //                the clusters (the last cluster leader folds their partials)
 #include <cuda_runtime.h>
+#ifdef WITH_SALT
+#include "../include/salt.h"  // the product, for an apples-to-apples row ("salt")
+#endif
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -419,6 +425,11 @@ int main(int argc, char** argv) {
   CK(cudaMemset(gt, 0, 4 << 16));
   CK(cudaMemset(tk, 0, 256));
   CK(cudaMalloc(&out, 16));
+#ifdef WITH_SALT
+  void* salt_ws;
+  CK(cudaMalloc(&salt_ws, salt_reduce_workspace_bytes()));
+  CK(cudaMemset(salt_ws, 0, SALT_WORKSPACE_TICKET_BYTES));
+#endif
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
@@ -428,6 +439,7 @@ int main(int argc, char** argv) {
 
   const char* ops[4] = {"nrm2_f64", "dot_f64", "nrm2_f32", "dot_f32"};
   for (int op = 0; op < 4; ++op) {
+    if (getenv("PROBE_OP") && atoi(getenv("PROBE_OP")) != op) continue;  // 0 nrm2_f64 1 dot_f64 2 nrm2_f32 3 dot_f32
     const bool f64 = op < 2;
     const int NL = (op & 1) ? 2 : 1;
     const int es = f64 ? 8 : 4;
@@ -439,6 +451,14 @@ int main(int argc, char** argv) {
       const double bytes = (double)n * es * NL;
       std::vector<Variant> vs;
       const int ucur = (!f64 || NL == 1) ? 4 : 2;
+      const bool final_set = getenv("PROBE_SET") && !strcmp(getenv("PROBE_SET"), "final");
+      if (final_set) {
+        vs.push_back({"floor", ucur, 1, 0, 1, 1 << 30, 0});
+        vs.push_back({"nocomb_U2_K1", 2, 1, 0, 1, 1 << 30, 0});
+        vs.push_back({"nocomb_U2_K2", 2, 1, 0, 2, 1 << 30, 0});
+        vs.push_back({"nocomb_U4_K2", 4, 1, 0, 2, 1 << 30, 0});
+        vs.push_back({"salt", ucur, 1, 0, 1, 1 << 30, 9});
+      } else {
       // K: > 0 fixed; -2 the round-1 product rule (one group of <= 512 / 256
       // CTAs); GS: CTAs (or clusters) per combine group, -1 = the whole grid
       vs.push_back({"floor", ucur, 1, 0, 1, 1 << 30, 0});
@@ -454,7 +474,8 @@ int main(int argc, char** argv) {
           vs.push_back({"cwarp_U" + std::to_string(u) + "_K" + std::to_string(K), u, 1, 0, K, 1 << 30, 4});
           vs.push_back({"nocomb_U" + std::to_string(u) + "_K" + std::to_string(K), u, 1, 0, K, 1 << 30, 0});
         }
-      if (getenv("PROBE_ALL"))
+      }
+      if (getenv("PROBE_ALL") && !final_set)
       for (int u : {4, 8})
         for (int ilp : {1, 2})
           for (int K : {1, 2}) {
@@ -486,6 +507,15 @@ int main(int argc, char** argv) {
           else CK(cudaMemsetAsync(sw, r & 0xff, sweep_bytes));
         };
         auto kern = [&]() {
+#ifdef WITH_SALT
+          if (v.combine == 9) {  // the product: salt_reduce(sum of squares / products), device result
+            const void* lv[2] = {x, y};
+            int rc = salt_reduce(f64 ? SALT_F64 : SALT_F32, NL == 1 ? "L0 L0 *" : "L0 L1 *", lv, NL, nullptr, 0,
+                                 n, 0, salt_ws, salt_reduce_workspace_bytes(), out, nullptr, nullptr);
+            if (rc) { printf("salt_reduce: %s\n", salt_last_error()); exit(1); }
+            return;
+          }
+#endif
           if (f64) (NL == 1 ? dispatch<double, 1>(v, (int)grid, a) : dispatch<double, 2>(v, (int)grid, a));
           else (NL == 1 ? dispatch<float, 1>(v, (int)grid, a) : dispatch<float, 2>(v, (int)grid, a));
         };
@@ -509,7 +539,7 @@ int main(int argc, char** argv) {
             best = std::min(best, (double)(ms_pair - ms_sweep) * 1000.0 / reps);
           }
           CK(cudaGetLastError());
-          if (v.combine && mode == 0) {
+          if (v.combine && v.combine != 9 && mode == 0) {
             DD h;
             CK(cudaMemcpy(&h, out, 16, cudaMemcpyDeviceToHost));
             if (std::isnan(ref)) ref = h.hi;
