@@ -128,6 +128,23 @@ int salt_fused(int dtype, const char* assign_sigs, const char* reduce_sig,
                void* workspace, size_t workspace_bytes,
                void* out_dev, void* out_host, void* stream);
 
+/* salt_fused with a SCALAR PROGRAM: the tree's device scalars P<k> are
+ * computed once per thread in the kernel prologue from the raw device
+ * scalars (pscalars[i], token "p<i>") and host scalars (scalars[j], "S<j>")
+ * by a postfix program of "+ - * /" and "neg"; "=<k>" pops into P<k>.  E.g.
+ * a CG step length alpha = rr / pq feeding x += alpha*p, r -= alpha*q:
+ * scalar_prog "p0 p1 / =0" with pscalars {&rr, &pq} — one launch instead
+ * of a division kernel plus the update.  Each op is one IEEE op in dtype
+ * (the bits of the same arithmetic on 1-element device tensors).  At most
+ * 32 ops, stack depth 8, 8 raw and 8 derived scalars; every P<k> the tree
+ * reads must be written.  NULL / "" scalar_prog = salt_fused. */
+int salt_fused_prog(int dtype, const char* assign_sigs, const char* reduce_sig,
+                    void* const* dsts, int ndst, const void* const* leaves, int nleaves,
+                    const double* scalars, int nscalars, const void* const* pscalars,
+                    int npscalars, const char* scalar_prog, int64_t n, int flags,
+                    void* workspace, size_t workspace_bytes, void* out_dev, void* out_host,
+                    void* stream);
+
 /* Combine `count` {hi, lo} partials (e.g. all-gathered from the ranks, in
  * rank order) in fixed order, round to dtype, optional SALT_SQRT. */
 int salt_reduce_finish(int dtype, const void* partials_dev, int count, int flags,
@@ -180,6 +197,12 @@ int salt_fused_exchange(int dtype, const char* assign_sigs, const char* reduce_s
                         void* workspace, size_t workspace_bytes,
                         const salt_exchange* exchange,
                         void* out_dev, void* out_host, void* stream);
+int salt_fused_exchange_prog(int dtype, const char* assign_sigs, const char* reduce_sig,
+                             void* const* dsts, int ndst, const void* const* leaves, int nleaves,
+                             const double* scalars, int nscalars, const void* const* pscalars,
+                             int npscalars, const char* scalar_prog, int64_t n, int flags,
+                             void* workspace, size_t workspace_bytes, const salt_exchange* exchange,
+                             void* out_dev, void* out_host, void* stream);
 
 /* Test hook: `world` thread blocks of ONE cooperative launch play the ranks
  * of the exchange protocol for `rounds` consecutive epochs (epoch0 ...),

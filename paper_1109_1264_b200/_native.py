@@ -42,6 +42,7 @@ HEADER_SYMBOLS = (
     "salt_reduce",
     "salt_assign_reduce",
     "salt_fused",
+    "salt_fused_prog",
     "salt_assign_batch",
     "salt_reduce_batch",
     "salt_reduce_finish",
@@ -55,6 +56,7 @@ HEADER_SYMBOLS = (
     "salt_reduce_exchange",
     "salt_assign_reduce_exchange",
     "salt_fused_exchange",
+    "salt_fused_exchange_prog",
     "salt_exchange_emulate",
     "salt_allreduce_sum",
     "salt_allreduce_sum_flags",
@@ -102,6 +104,16 @@ _SIGNATURES = {
         _c_int,
         [_c_int, _c_str, _c_str, _c_vpp, _c_int, _c_vpp, _c_int, _c_dp, _c_int, _c_vpp, _c_int,
          _c_i64, _c_int, _c_vp, _c_size, _c_vp, _c_vp, _c_vp],
+    ),
+    "salt_fused_prog": (
+        _c_int,
+        [_c_int, _c_str, _c_str, _c_vpp, _c_int, _c_vpp, _c_int, _c_dp, _c_int, _c_vpp, _c_int, _c_str,
+         _c_i64, _c_int, _c_vp, _c_size, _c_vp, _c_vp, _c_vp],
+    ),
+    "salt_fused_exchange_prog": (
+        _c_int,
+        [_c_int, _c_str, _c_str, _c_vpp, _c_int, _c_vpp, _c_int, _c_dp, _c_int, _c_vpp, _c_int, _c_str,
+         _c_i64, _c_int, _c_vp, _c_size, _c_vp, _c_vp, _c_vp, _c_vp],
     ),
     "salt_reduce_finish": (_c_int, [_c_int, _c_vp, _c_int, _c_int, _c_vp, _c_vp, _c_vp]),
     "salt_assign_batch": (_c_int, [_c_int, _c_str, _c_int, _c_vpp, _c_vpp, _c_int, _c_dp, _c_int, _c_vp, _c_vp]),

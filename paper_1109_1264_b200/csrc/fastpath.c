@@ -126,11 +126,17 @@ static int leaf(Walk* w, PyObject* vec) {
   return emit(w, tok);
 }
 
-/* DeviceScalar -> w->ps[w->nps++]; must live on the kernel's device */
+/* DeviceScalar -> w->ps[w->nps++]; must live on the kernel's device.  A
+ * LAZY DeviceScalar (an unevaluated scalar operation, _tensor None) is
+ * declined: the Python path compiles it into the kernel's scalar program. */
 static int device_scalar(Walk* w, PyObject* ds) {
   if (w->nps == MAX_PSCALARS) return 0;
   PyObject* t = PyObject_GetAttr(ds, s_tensor);
   if (!t) return -1;
+  if (t == Py_None) {
+    Py_DECREF(t);
+    return 0;
+  }
   PyObject* d = PyObject_CallMethodNoArgs(t, s_get_device);
   PyObject* p = d ? PyObject_CallMethodNoArgs(t, s_data_ptr) : NULL;
   Py_DECREF(t);
@@ -867,7 +873,7 @@ PyMODINIT_FUNC PyInit__fastpath(void) {
   s_n = PyUnicode_InternFromString("_n");
   s_code = PyUnicode_InternFromString("_code");
   s_data_ptr = PyUnicode_InternFromString("data_ptr");
-  s_tensor = PyUnicode_InternFromString("tensor");
+  s_tensor = PyUnicode_InternFromString("_tensor");
   s_get_device = PyUnicode_InternFromString("get_device");
   return PyModule_Create(&module);
 }

@@ -581,11 +581,74 @@ int result_enqueue(const void* out_dev, size_t bytes, cudaStream_t st, void** ho
   return 0;
 }
 
+// Parse a scalar program (include/salt.h salt_fused_prog): tokens
+// "p<i>" (raw device scalar i), "S<j>" (host scalar j), "+ - * /", "neg",
+// "=<k>" (pop into the tree's P<k>).  Checks indices and the stack; `defined`
+// gets bit k for every P<k> the program writes.  Cached per thread by text.
+int parse_sprog(const char* text, int nraw, int nhost, salt::SProg& out, unsigned& defined) {
+  thread_local std::unordered_map<std::string, std::pair<salt::SProg, unsigned>> cache;
+  auto it = cache.find(text);
+  if (it == cache.end()) {
+    salt::SProg sp;
+    memset(&sp, 0, sizeof sp);
+    unsigned def = 0;
+    int depth = 0;
+    std::istringstream in(text);
+    std::string tok;
+    while (in >> tok) {
+      if (sp.len == salt::SPROG_MAX) return fail(SALT_EINVAL, "scalar program longer than 32 ops");
+      int op, arg = 0;
+      if ((tok[0] == 'p' || tok[0] == 'S' || tok[0] == '=') && tok.size() > 1) {
+        char* end = nullptr;
+        const long v = strtol(tok.c_str() + 1, &end, 10);
+        if (*end || v < 0 || v > 255) return fail(SALT_EINVAL, "bad scalar program token '" + tok + "'");
+        arg = (int)v;
+        op = tok[0] == 'p' ? salt::SP_RAW : tok[0] == 'S' ? salt::SP_HOST : salt::SP_OUT;
+      } else if (tok == "+") op = salt::SP_ADD;
+      else if (tok == "-") op = salt::SP_SUB;
+      else if (tok == "*") op = salt::SP_MUL;
+      else if (tok == "/") op = salt::SP_DIV;
+      else if (tok == "neg") op = salt::SP_NEG;
+      else return fail(SALT_EINVAL, "bad scalar program token '" + tok + "'");
+      if (op == salt::SP_RAW || op == salt::SP_HOST) {
+        if (++depth > salt::SPROG_STACK) return fail(SALT_EINVAL, "scalar program stack deeper than 8");
+      } else if (op == salt::SP_NEG) {
+        if (depth < 1) return fail(SALT_EINVAL, "scalar program stack underflow");
+      } else if (op == salt::SP_OUT) {
+        if (depth < 1) return fail(SALT_EINVAL, "scalar program stack underflow");
+        if (arg >= salt::MAX_PSCALARS) return fail(SALT_EINVAL, "scalar program output index >= 8");
+        --depth;
+        def |= 1u << arg;
+      } else {
+        if (depth < 2) return fail(SALT_EINVAL, "scalar program stack underflow");
+        --depth;
+      }
+      sp.op[sp.len] = (unsigned char)op;
+      sp.arg[sp.len] = (unsigned char)arg;
+      ++sp.len;
+    }
+    if (depth != 0) return fail(SALT_EINVAL, "scalar program leaves values on its stack");
+    it = cache.emplace(text, std::make_pair(sp, def)).first;
+  }
+  const salt::SProg& sp = it->second.first;
+  for (int i = 0; i < sp.len; ++i) {
+    if (sp.op[i] == salt::SP_RAW && sp.arg[i] >= nraw)
+      return fail(SALT_EINVAL, "scalar program reads device scalar " + std::to_string(sp.arg[i]) + " of " +
+                                   std::to_string(nraw));
+    if (sp.op[i] == salt::SP_HOST && sp.arg[i] >= nhost)
+      return fail(SALT_EINVAL, "scalar program reads host scalar " + std::to_string(sp.arg[i]) + " of " +
+                                   std::to_string(nhost));
+  }
+  out = sp;
+  defined = it->second.second;
+  return 0;
+}
+
 template <class T>
 int run_fused(Plan& p, void* const* dsts, int ndst, const void* const* leaves, int nleaves,
               const double* scalars, int nscalars, i64 n, int flags, void* ws, size_t ws_bytes,
               void* out_dev, void* out_host, cudaStream_t st, const salt_exchange* x,
-              const void* const* pscalars, int npscalars) {
+              const void* const* pscalars, int npscalars, const char* sprog = nullptr) {
   if (n < 0) return fail(SALT_EINVAL, "negative length");
   const bool reduce = p.mode != salt::MODE_ASSIGN;
   if (!reduce && n == 0) return 0;  // zero length assign is a no-op (test_engine.py:147-153)
@@ -609,14 +672,28 @@ int run_fused(Plan& p, void* const* dsts, int ndst, const void* const* leaves, i
   memset(&a, 0, sizeof(a));
   for (int r = 0; r < nroots; ++r) a.dst[r] = (T*)dsts[r];
   for (int l = 0; l < p.nl; ++l) a.leaf[l] = leaves ? (const T*)leaves[l] : nullptr;
-  for (int s = 0; s < p.ns; ++s) a.sc[s] = (T)scalars[s];
-  if (npscalars < p.np || npscalars > salt::MAX_PSCALARS)
+  if (nscalars < p.ns || nscalars > salt::MAX_SCALARS)
+    return fail(SALT_EINVAL, "signature reads " + std::to_string(p.ns) + " scalars but " +
+                                 std::to_string(nscalars) + " were passed (at most 32)");
+  for (int s = 0; s < nscalars; ++s) a.sc[s] = (T)scalars[s];
+  if (npscalars < 0 || npscalars > salt::MAX_PSCALARS)
+    return fail(SALT_EINVAL, "at most 8 device scalars, got " + std::to_string(npscalars));
+  if (sprog && *sprog) {
+    unsigned defined = 0;
+    int rc = parse_sprog(sprog, npscalars, nscalars, a.sp, defined);
+    if (rc) return rc;
+    for (int q = 0; q < p.np; ++q)
+      if (!(defined >> q & 1u))
+        return fail(SALT_EINVAL, "the scalar program does not define P" + std::to_string(q));
+  } else if (npscalars < p.np) {
     return fail(SALT_EINVAL, "signature reads " + std::to_string(p.np) + " device scalars but " +
                                  std::to_string(npscalars) + " were passed");
-  for (int q = 0; q < p.np; ++q) {
+  }
+  for (int q = 0; q < npscalars; ++q) {
     if (!pscalars || !pscalars[q]) return fail(SALT_EINVAL, "NULL device scalar");
     a.ps[q] = (const T*)pscalars[q];
   }
+  a.nps = npscalars;
   a.n = n;
   a.flags = flags;
   int vec;
@@ -677,10 +754,14 @@ int run_fused(Plan& p, void* const* dsts, int ndst, const void* const* leaves, i
     // profiles/r02_c3_probe*.txt: at 2^24 ddot 46.6 -> 42.6 us, sdot 25.7 ->
     // 24.3 us, dnrm2 26.4 -> 25.5 us; the fence + ticket atomic each
     // streaming CTA paid in the two-level combine held its SM slot).
-    // (beyond MAX_COLLECT CTAs of collect_tiles() tiles, more tiles per CTA:
-    // 2^27-2^28 measured equal for 2 and 4)
+    // Beyond kCollectCtas streaming CTAs, more tiles per CTA (2^27-2^28
+    // measured equal for 2 and 4 tiles): the collector warp then folds at
+    // most ~30 partials per microsecond, well within its 4-slots-per-lane
+    // round trips, so it never falls behind the streaming CTAs.
+    constexpr i64 kCollectCtas = 16384;
+    static_assert(kCollectCtas <= salt::MAX_COLLECT, "collector slots");
     K = collect_tiles();
-    if ((ntiles + K - 1) / K > salt::MAX_COLLECT) K = (ntiles + salt::MAX_COLLECT - 1) / salt::MAX_COLLECT;
+    if ((ntiles + K - 1) / K > kCollectCtas) K = (ntiles + kCollectCtas - 1) / kCollectCtas;
     collect = true;
   } else if (reduce) {
     K = reduce_tiles_per_cta(p.nl);
@@ -778,12 +859,12 @@ int dispatch(int dtype, Plan& p, void* const* dsts, int ndst, const void* const*
              int nleaves, const double* scalars, int nscalars, i64 n, int flags, void* ws,
              size_t ws_bytes, void* out_dev, void* out_host, cudaStream_t st,
              const salt_exchange* x = nullptr, const void* const* pscalars = nullptr,
-             int npscalars = 0) {
+             int npscalars = 0, const char* sprog = nullptr) {
   if (dtype == SALT_F32)
     return run_fused<float>(p, dsts, ndst, leaves, nleaves, scalars, nscalars, n, flags, ws,
-                            ws_bytes, out_dev, out_host, st, x, pscalars, npscalars);
+                            ws_bytes, out_dev, out_host, st, x, pscalars, npscalars, sprog);
   return run_fused<double>(p, dsts, ndst, leaves, nleaves, scalars, nscalars, n, flags, ws,
-                           ws_bytes, out_dev, out_host, st, x, pscalars, npscalars);
+                           ws_bytes, out_dev, out_host, st, x, pscalars, npscalars, sprog);
 }
 
 #include "salt_abi_batch.inc"
@@ -940,6 +1021,17 @@ int salt_fused_exchange(int dtype, const char* assign_sigs, const char* reduce_s
                         int npscalars, int64_t n, int flags, void* workspace,
                         size_t workspace_bytes, const salt_exchange* exchange, void* out_dev,
                         void* out_host, void* stream) {
+  return salt_fused_exchange_prog(dtype, assign_sigs, reduce_sig, dsts, ndst, leaves, nleaves, scalars,
+                                  nscalars, pscalars, npscalars, nullptr, n, flags, workspace,
+                                  workspace_bytes, exchange, out_dev, out_host, stream);
+}
+
+int salt_fused_exchange_prog(int dtype, const char* assign_sigs, const char* reduce_sig,
+                             void* const* dsts, int ndst, const void* const* leaves, int nleaves,
+                             const double* scalars, int nscalars, const void* const* pscalars,
+                             int npscalars, const char* scalar_prog, int64_t n, int flags,
+                             void* workspace, size_t workspace_bytes, const salt_exchange* exchange,
+                             void* out_dev, void* out_host, void* stream) {
   if (!exchange) return fail(SALT_EINVAL, "NULL exchange descriptor");
   if (!reduce_sig) return fail(SALT_EINVAL, "salt_fused_exchange needs a reduction");
   Plan* p;
@@ -948,7 +1040,7 @@ int salt_fused_exchange(int dtype, const char* assign_sigs, const char* reduce_s
   if (rc) return rc;
   return dispatch(dtype, *p, dsts, ndst, leaves, nleaves, scalars, nscalars, n, flags, workspace,
                   workspace_bytes, out_dev, out_host, (cudaStream_t)stream, exchange, pscalars,
-                  npscalars);
+                  npscalars, scalar_prog);
 }
 
 int salt_exchange_emulate(int world, int rounds, uint64_t epoch0, const void* totals_dev,
@@ -976,6 +1068,16 @@ int salt_fused(int dtype, const char* assign_sigs, const char* reduce_sig, void*
                int nscalars, const void* const* pscalars, int npscalars, int64_t n, int flags,
                void* workspace, size_t workspace_bytes, void* out_dev, void* out_host,
                void* stream) {
+  return salt_fused_prog(dtype, assign_sigs, reduce_sig, dsts, ndst, leaves, nleaves, scalars, nscalars,
+                         pscalars, npscalars, nullptr, n, flags, workspace, workspace_bytes, out_dev,
+                         out_host, stream);
+}
+
+int salt_fused_prog(int dtype, const char* assign_sigs, const char* reduce_sig, void* const* dsts,
+                    int ndst, const void* const* leaves, int nleaves, const double* scalars,
+                    int nscalars, const void* const* pscalars, int npscalars, const char* scalar_prog,
+                    int64_t n, int flags, void* workspace, size_t workspace_bytes, void* out_dev,
+                    void* out_host, void* stream) {
   Plan* p;
   if (!assign_sigs && !reduce_sig) return fail(SALT_EINVAL, "nothing to evaluate");
   const int mode = !assign_sigs ? salt::MODE_REDUCE
@@ -984,7 +1086,7 @@ int salt_fused(int dtype, const char* assign_sigs, const char* reduce_sig, void*
   if (rc) return rc;
   return dispatch(dtype, *p, dsts, ndst, leaves, nleaves, scalars, nscalars, n, flags, workspace,
                   workspace_bytes, out_dev, out_host, (cudaStream_t)stream, nullptr, pscalars,
-                  npscalars);
+                  npscalars, scalar_prog);
 }
 
 int salt_reduce_finish(int dtype, const void* partials_dev, int count, int flags, void* out_dev,

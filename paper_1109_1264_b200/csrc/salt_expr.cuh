@@ -36,12 +36,14 @@ template <> struct Arith<double> {
   static __device__ __forceinline__ double sub(double a, double b) { return __dsub_rn(a, b); }
   static __device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
   static __device__ __forceinline__ double sqrt_rn(double a) { return __dsqrt_rn(a); }
+  static __device__ __forceinline__ double div(double a, double b) { return __ddiv_rn(a, b); }
 };
 template <> struct Arith<float> {
   static __device__ __forceinline__ float add(float a, float b) { return __fadd_rn(a, b); }
   static __device__ __forceinline__ float sub(float a, float b) { return __fsub_rn(a, b); }
   static __device__ __forceinline__ float mul(float a, float b) { return __fmul_rn(a, b); }
   static __device__ __forceinline__ float sqrt_rn(float a) { return __fsqrt_rn(a); }
+  static __device__ __forceinline__ float div(float a, float b) { return __fdiv_rn(a, b); }
 };
 
 __host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
@@ -154,12 +156,28 @@ struct Xchg {
   unsigned int* error;                 // set to 1 on timeout (local memory)
 };
 
+// Scalar program: derived device scalars computed once per thread in the
+// kernel prologue from the raw device scalars (ps[i]) and host scalars
+// (sc[j]) — e.g. a CG step length rr / pq — instead of a separate launch
+// per scalar operation.  Postfix; SP_OUT k pops into the tree's P<k>.
+// Every op is one IEEE op in the element type (the bits of the same torch
+// op on 1-element tensors).
+enum { SPROG_MAX = 32, SPROG_STACK = 8 };
+enum { SP_RAW = 0, SP_HOST, SP_ADD, SP_SUB, SP_MUL, SP_DIV, SP_NEG, SP_OUT };
+struct SProg {
+  int len;  // 0: no program, P<k> = *ps[k]
+  unsigned char op[SPROG_MAX];
+  unsigned char arg[SPROG_MAX];
+};
+
 // One by-value parameter block shared by AOT and JIT kernels.
 template <class T> struct Args {
   T* dst[MAX_ROOTS];              // assign modes: one destination per root
   const T* leaf[MAX_LEAVES];
   T sc[MAX_SCALARS];
-  const T* ps[MAX_PSCALARS];      // device-resident scalars (P<k>)
+  const T* ps[MAX_PSCALARS];      // device-resident scalars (P<k>, or the program's inputs)
+  int nps;                        // pointers in ps
+  SProg sp;                       // scalar program (sp.len == 0: none)
   i64 n;                          // elements
   i64 head;                       // scalar elements before the first aligned vector
   i64 nvec;                       // aligned vectors of V elements after `head`
@@ -439,6 +457,41 @@ template <int BLOCK> __device__ __forceinline__ DD block_reduce_dd(DD v, DD* sme
 
 template <class T> __device__ __forceinline__ void finish_store(DD tot, int flags, void* out);
 
+// The tree's device scalars pv[0..NPV) for this thread: loaded from ps, or
+// computed by the scalar program (uniform across threads; a few ops).
+template <class T, int NPV>
+__device__ __forceinline__ void load_pscalars(const Args<T>& a, T (&pv)[NPV], int np) {
+  if (a.sp.len == 0) {
+#pragma unroll
+    for (int q = 0; q < NPV; ++q)
+      if (q < np) pv[q] = __ldg(a.ps[q]);
+    return;
+  }
+  T stk[SPROG_STACK];
+  int top = 0;
+  for (int i = 0; i < a.sp.len; ++i) {
+    const int op = a.sp.op[i], k = a.sp.arg[i];
+    if (op == SP_RAW) {
+      stk[top++] = __ldg(a.ps[k]);
+    } else if (op == SP_HOST) {
+      stk[top++] = a.sc[k];
+    } else if (op == SP_NEG) {
+      stk[top - 1] = -stk[top - 1];
+    } else if (op == SP_OUT) {
+      const T v = stk[--top];
+#pragma unroll
+      for (int q = 0; q < NPV; ++q)
+        if (q == k) pv[q] = v;
+    } else {
+      const T r = stk[--top];
+      const T l = stk[--top];
+      stk[top++] = op == SP_ADD ? Arith<T>::add(l, r)
+                   : op == SP_SUB ? Arith<T>::sub(l, r)
+                   : op == SP_MUL ? Arith<T>::mul(l, r) : Arith<T>::div(l, r);
+    }
+  }
+}
+
 // Warp shuffle tree over a double-double (valid in every lane).
 __device__ __forceinline__ DD warp_reduce_dd(DD v) {
 #pragma unroll
@@ -461,13 +514,16 @@ __device__ __forceinline__ DD warp_reduce_dd(DD v) {
 // result (all partials are sums) can be.  Each 8-byte word is written once
 // and read whole, so a reader that sees both words non-zero has the value.
 // CTA 0's first warp is the collector: lane l folds slots l, l+32, l+64, ...
-// IN ORDER as they appear (polling up to 8 of its slots per round trip,
+// IN ORDER as they appear (polling up to kCollectBatch of its slots per round trip,
 // volatile loads), zeroes each slot it has consumed (the next launch is
 // stream-ordered after this one), then one warp shuffle tree gives the
 // total — fixed order, so the bits depend only on n.  Whatever order the
 // CTAs are scheduled in, nothing waits on the collector, so it cannot
 // deadlock; the collector only waits for stores that are certain to come.
 constexpr unsigned long long kSlotMask = 0x7ff4000000000001ull;
+// slots a collector lane polls per round trip (8 cost the streaming path
+// registers: the collector shares the kernel's register allocation)
+constexpr int kCollectBatch = 4;
 
 template <class T, int BLOCK>
 __device__ __forceinline__ void collect_epilogue(DD mine, const Args<T>& a, DD* smem) {
@@ -486,9 +542,9 @@ __device__ __forceinline__ void collect_epilogue(DD mine, const Args<T>& a, DD* 
   DD v; v.hi = 0.0; v.lo = 0.0;
   unsigned q = threadIdx.x;  // this lane's next slot
   while (q < np) {
-    unsigned long long h[8], l[8];
+    unsigned long long h[kCollectBatch], l[kCollectBatch];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < kCollectBatch; ++i) {
       const unsigned s = q + 32u * i;
       if (s < np)
         asm volatile("ld.volatile.global.v2.u64 {%0,%1}, [%2];" : "=l"(h[i]), "=l"(l[i]) : "l"(a.slots + 2 * s));
@@ -496,7 +552,7 @@ __device__ __forceinline__ void collect_epilogue(DD mine, const Args<T>& a, DD* 
         h[i] = l[i] = 0ull;
     }
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < kCollectBatch; ++i) {
       if (q >= np || h[i] == 0ull || l[i] == 0ull) break;
       DD p;
       p.hi = __longlong_as_double((long long)(h[i] ^ kSlotMask));
@@ -698,9 +754,8 @@ __global__ void SALT_BOUNDS(BLOCK) fused_kernel(Args<T> a) {
   // (tools/pdl_probe.cu): 2^20 f64 4.74 -> 2.87 us per launch eager,
   // 2.97 -> 2.71 us in a CUDA graph.
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  T pv[NP > 0 ? NP : 1];  // device scalars, loaded once per thread
-#pragma unroll
-  for (int q = 0; q < NP; ++q) pv[q] = __ldg(a.ps[q]);
+  T pv[NP > 0 ? NP : 1];  // device scalars, loaded (or computed) once per thread
+  if (NP > 0) load_pscalars(a, pv, NP);
 
   Acc<T> acc;
   constexpr int ND = Roots<EA>::N;

@@ -48,8 +48,8 @@ __host__ __device__ inline int interp_smem_bytes(const Prog& pg, int V, int bloc
 }
 
 template <class T, int W, int BLOCK>
-__device__ __forceinline__ void interp_eval(const Prog& pg, const Args<T>& a, T* sm, i64 off,
-                                            Acc<T>& acc) {
+__device__ __forceinline__ void interp_eval(const Prog& pg, const Args<T>& a, const T* pv, T* sm,
+                                            i64 off, Acc<T>& acc) {
   const int tid = threadIdx.x;
   T* X = sm;                                   // [nl][W][BLOCK]
   T* STK = sm + pg.nl * W * BLOCK;             // [slots][W][BLOCK]
@@ -85,7 +85,7 @@ __device__ __forceinline__ void interp_eval(const Prog& pg, const Args<T>& a, T*
 #pragma unroll
         for (int w = 0; w < W; ++w) tos[w] = s;
       } else if (op == OP_PSCALAR) {
-        const T s = __ldg(a.ps[k]);
+        const T s = pv[k];
 #pragma unroll
         for (int w = 0; w < W; ++w) tos[w] = s;
       } else {
@@ -121,6 +121,8 @@ __global__ void __launch_bounds__(BLOCK) interp_kernel(InterpArgs<T> ia) {
   extern __shared__ __align__(16) unsigned char interp_smem[];
   T* sm = (T*)interp_smem;
   Acc<T> acc;
+  T pv[MAX_PSCALARS];  // device scalars (loaded or computed once per thread)
+  load_pscalars(a, pv, a.nps);
   const i64 cta = (i64)blockIdx.x - a.first;  // < 0: the collector CTA
   const i64 nthreads = ((i64)gridDim.x - a.first) * BLOCK;
   const i64 gtid = cta * BLOCK + threadIdx.x;
@@ -129,7 +131,7 @@ __global__ void __launch_bounds__(BLOCK) interp_kernel(InterpArgs<T> ia) {
     const i64 nscalar = a.head + (a.n - tail0);
     for (i64 t = gtid; t < nscalar; t += nthreads) {
       const i64 i = t < a.head ? t : tail0 + (t - a.head);
-      interp_eval<T, 1, BLOCK>(pg, a, sm, i, acc);
+      interp_eval<T, 1, BLOCK>(pg, a, pv, sm, i, acc);
     }
   }
   const i64 ntiles = (a.nvec + (i64)BLOCK * UNR - 1) / ((i64)BLOCK * UNR);
@@ -139,7 +141,7 @@ __global__ void __launch_bounds__(BLOCK) interp_kernel(InterpArgs<T> ia) {
     const i64 base = t * BLOCK * UNR + threadIdx.x;
     for (int u = 0; u < UNR; ++u) {
       const i64 j = base + (i64)u * BLOCK;
-      if (j < a.nvec) interp_eval<T, V, BLOCK>(pg, a, sm, a.head + j * V, acc);
+      if (j < a.nvec) interp_eval<T, V, BLOCK>(pg, a, pv, sm, a.head + j * V, acc);
     }
   }
   if (pg.reduce) reduce_epilogue<T, BLOCK>(acc.get(), a);

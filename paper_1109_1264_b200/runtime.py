@@ -582,37 +582,88 @@ def run_fused(asig, rsig, lw, dests, dtype, n, flags=0, lazy=False):
     else:
         dev, ptrs, _ = fast
     for ds in lw.pscalars:
-        if ds.tensor.get_device() != dev:
+        if ds.device.index != dev:
             raise ValueError("a device scalar must live on the vectors' device")
     nl = len(lw.vectors)
     leaves, keep_l = _native.ptr_array(ptrs[:nl])
     dsts, keep_d = _native.ptr_array(ptrs[nl:])
-    scal, keep_s = _native.double_array(lw.scalars)
-    pscal, keep_p = _native.ptr_array([ds.tensor.data_ptr() for ds in lw.pscalars])
+    raw, host, prog = _scalar_program(lw.pscalars, list(lw.scalars))
+    scal, keep_s = _native.double_array(host)
+    pscal, keep_p = _native.ptr_array([ds.tensor.data_ptr() for ds in raw])
     dt = as_dtype(dtype)
     code = _dtype_code(dt)
     lib = _native.lib()
     a = asig.encode() if asig is not None else None
     r = rsig.encode() if rsig is not None else None
-    np_ = len(lw.pscalars)
+    np_ = len(raw)
+    sp = prog.encode() if prog else None
     with _OnDevice(dev):
         if rsig is None:
-            _native.check(lib.salt_fused(code, a, None, dsts, len(dests), leaves, nl, scal,
-                                         len(lw.scalars), pscal, np_, n, 0, None, 0, None, None,
-                                         _raw_stream(dev)))
+            _native.check(lib.salt_fused_prog(code, a, None, dsts, len(dests), leaves, nl, scal,
+                                              len(host), pscal, np_, sp, n, 0, None, 0, None, None,
+                                              _raw_stream(dev)))
             return True, None
 
         def call(fl, ws, wsb, od, oh, st):
-            return lib.salt_fused(code, a, r, dsts, len(dests), leaves, nl, scal, len(lw.scalars),
-                                  pscal, np_, n, fl, ws, wsb, od, oh, st)
+            return lib.salt_fused_prog(code, a, r, dsts, len(dests), leaves, nl, scal, len(host),
+                                       pscal, np_, sp, n, fl, ws, wsb, od, oh, st)
 
         def xcall(fl, ws, wsb, x, od, oh, st):
-            return lib.salt_fused_exchange(code, a, r, dsts, len(dests), leaves, nl, scal,
-                                           len(lw.scalars), pscal, np_, n, fl, ws, wsb, x, od, oh,
-                                           st)
+            return lib.salt_fused_exchange_prog(code, a, r, dsts, len(dests), leaves, nl, scal,
+                                                len(host), pscal, np_, sp, n, fl, ws, wsb, x, od,
+                                                oh, st)
 
         return True, _device_reduce(dev, dt, call, flags, lazy, sharded,
                                     xcall if sharded is not None else None)
+
+
+def _scalar_program(pscalars, host):
+    """(raw device scalars, host scalars, program text or None) for the
+    tree's device-scalar operands P0..P(k-1).  Without a lazy operand the raw
+    list IS pscalars and there is no program.  Otherwise every P<k> gets a
+    postfix program over the raw (materialised) device scalars "p<i>" and
+    host scalars "S<j>" (appended to `host`), evaluated once per thread in
+    the kernel prologue (csrc/salt_expr.cuh load_pscalars)."""
+    budget = DeviceScalar.MAX_PROGRAM_OPS
+    if not any(ds.lazy for ds in pscalars):
+        return list(pscalars), host, None
+    raw, raw_ids, toks = [], {}, []
+
+    def emit(x):
+        if isinstance(x, DeviceScalar) and (not x.lazy or x.program_size() > budget):
+            i = raw_ids.get(id(x))
+            if i is None:
+                if len(raw) == _native.SALT_MAX_PSCALARS:
+                    raise _ProgramTooLarge
+                i = raw_ids[id(x)] = len(raw)
+                raw.append(x)
+            toks.append(f"p{i}")
+        elif isinstance(x, DeviceScalar):
+            op, *args = x._expr
+            for arg in args:
+                emit(arg)
+            toks.append(op)
+        else:
+            if len(host) == _native.SALT_MAX_SCALARS:
+                raise _ProgramTooLarge
+            toks.append(f"S{len(host)}")
+            host.append(float(x))
+
+    n0 = len(host)
+    try:
+        for k, ds in enumerate(pscalars):
+            emit(ds)
+            toks.append(f"={k}")
+        if len(toks) > 32:
+            raise _ProgramTooLarge
+    except _ProgramTooLarge:  # materialise everything: one raw pointer per operand
+        del host[n0:]
+        return list(pscalars), host, None
+    return raw, host, " ".join(toks)
+
+
+class _ProgramTooLarge(Exception):
+    pass
 
 
 def _sharded_operands(vectors):

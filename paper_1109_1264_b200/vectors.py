@@ -234,29 +234,77 @@ class DeviceScalar:
     synchronisation).  It can scale an expression like a Python number —
     `a * p` with `a` a DeviceScalar builds a ScaleNode whose alpha the fused
     kernel reads from device memory — and DeviceScalars combine with + - * /
-    on the device (one tiny torch op each, IEEE round-to-nearest in the
-    element type).  So a whole solver iteration (dot -> alpha = rr / pq ->
-    fused update) runs without a host round trip and can be captured in a
-    CUDA graph.  `.item()` / float() copy it to the host and return the
-    element-typed NumPy scalar the reference returns (test_ops.py:29-31).
+    and unary minus.  Those combinations are LAZY: `alpha = rr / pq` records
+    the operation instead of launching anything.  Used as an operand of a
+    fused tree it is compiled into the kernel's scalar program and computed
+    once per thread in that kernel's prologue (salt_fused_prog), so a whole
+    solver iteration (dots -> alpha = rr / pq -> fused update) is one launch
+    per reduction and one per update, with no host round trip, and can be
+    captured in a CUDA graph.  Anything that needs the value itself
+    (`.item()`, float(), `.tensor`, `.address`) materialises it once with
+    1-element torch ops.  Either way every operation is one IEEE
+    round-to-nearest op in the element type, so both give the same bits.
+    `.item()` / float() return the element-typed NumPy scalar the reference
+    returns (test_ops.py:29-31).
     """
 
-    __slots__ = ("tensor", "dtype", "guard")
+    __slots__ = ("_tensor", "dtype", "guard", "_expr")
 
     __array_ufunc__ = None
 
-    def __init__(self, tensor: torch.Tensor, dtype, guard=None):
-        self.tensor = tensor
+    # a lazy scalar with more operations than this is materialised instead
+    # of being compiled into a kernel's scalar program (32 ops, stack 8)
+    MAX_PROGRAM_OPS = 24
+
+    def __init__(self, tensor, dtype, guard=None, _expr=None):
+        self._tensor = tensor
         self.dtype = as_dtype(dtype)
         # guard(value): raises if the producing collective failed (a peer
         # exchange that timed out writes NaN; see sharding.PeerExchange.check)
         self.guard = guard
+        # (op, operand[, operand]) for a lazy result: op in + - * / neg,
+        # operands DeviceScalars or element-typed Python floats
+        self._expr = _expr
 
     @classmethod
     def full(cls, value, dtype="f64", device=None) -> "DeviceScalar":
         dt = as_dtype(dtype)
         return cls(torch.full((1,), float(dt.type(value)), dtype=_TORCH_DTYPES[dt],
                               device=_as_device(device)), dt)
+
+    # ---- value (materialised on demand) ----
+    @property
+    def lazy(self) -> bool:
+        """True while this scalar is an unevaluated operation."""
+        return self._tensor is None
+
+    @property
+    def tensor(self) -> torch.Tensor:
+        t = self._tensor
+        if t is None:
+            t = self._tensor = self._materialise()
+        return t
+
+    def _materialise(self) -> torch.Tensor:
+        op, *args = self._expr
+        ref = next(a for a in args if isinstance(a, DeviceScalar)).tensor
+        ts = [a.tensor if isinstance(a, DeviceScalar) else torch.full_like(ref, a) for a in args]
+        if op == "neg":
+            return torch.neg(ts[0])
+        fn = {"+": torch.add, "-": torch.sub, "*": torch.mul, "/": torch.div}[op]
+        return fn(ts[0], ts[1])
+
+    @property
+    def device(self) -> torch.device:
+        if self._tensor is not None:
+            return self._tensor.device
+        return next(a for a in self._expr[1:] if isinstance(a, DeviceScalar)).device
+
+    def program_size(self) -> int:
+        """Operations a scalar program needs to compute this scalar."""
+        if self._tensor is not None or self._expr is None:
+            return 1
+        return 1 + sum(a.program_size() if isinstance(a, DeviceScalar) else 1 for a in self._expr[1:])
 
     @property
     def address(self) -> int:
@@ -271,27 +319,26 @@ class DeviceScalar:
     def __float__(self):
         return float(self.item())
 
-    # ---- scalar arithmetic on the device (torch ops on one element) ----
-    def _other(self, other):
+    # ---- scalar arithmetic (lazy: recorded, evaluated in the consuming kernel) ----
+    def _operand(self, other):
         if isinstance(other, DeviceScalar):
             if other.dtype != self.dtype:
                 raise TypeError(f"mixed element types: {self.dtype} vs {other.dtype}")
-            return other.tensor
+            return other
         return float(self.dtype.type(other))
 
-    def _operand_tensor(self, other):
-        """`other` as a device tensor of this dtype.  Division needs it:
-        torch divides a CUDA tensor by a host number as a multiply by the
-        host-computed reciprocal, and number / tensor as reciprocal() *
-        number — two roundings each, up to 1 ulp off IEEE a / b."""
-        o = self._other(other)
-        return o if isinstance(o, torch.Tensor) else torch.full_like(self.tensor, o)
+    def _lazy(self, op, *args):
+        return DeviceScalar(None, self.dtype, _expr=(op,) + args)
 
     def __truediv__(self, other):
-        return DeviceScalar(torch.div(self.tensor, self._operand_tensor(other)), self.dtype)
+        if isinstance(other, (DeviceScalar, int, float, np.floating)):
+            return self._lazy("/", self, self._operand(other))
+        return NotImplemented
 
     def __rtruediv__(self, other):
-        return DeviceScalar(torch.div(self._operand_tensor(other), self.tensor), self.dtype)
+        if isinstance(other, (int, float, np.floating)):
+            return self._lazy("/", self._operand(other), self)
+        return NotImplemented
 
     def copy_(self, other) -> "DeviceScalar":
         """In-place assignment (keeps this scalar's device address, so a
@@ -302,32 +349,37 @@ class DeviceScalar:
 
     def __add__(self, other):
         if isinstance(other, (DeviceScalar, int, float, np.floating)):
-            return DeviceScalar(torch.add(self.tensor, self._other(other)), self.dtype)
+            return self._lazy("+", self, self._operand(other))
         return NotImplemented
 
-    __radd__ = __add__
+    def __radd__(self, other):
+        if isinstance(other, (int, float, np.floating)):
+            return self._lazy("+", self._operand(other), self)
+        return NotImplemented
 
     def __sub__(self, other):
         if isinstance(other, (DeviceScalar, int, float, np.floating)):
-            return DeviceScalar(torch.sub(self.tensor, self._other(other)), self.dtype)
+            return self._lazy("-", self, self._operand(other))
         return NotImplemented
 
     def __rsub__(self, other):
-        return DeviceScalar(torch.sub(self._other(other), self.tensor), self.dtype)
+        if isinstance(other, (int, float, np.floating)):
+            return self._lazy("-", self._operand(other), self)
+        return NotImplemented
 
     def __neg__(self):
-        return DeviceScalar(torch.neg(self.tensor), self.dtype)
+        return self._lazy("neg", self)
 
     def __mul__(self, other):
         if isinstance(other, (DeviceScalar, int, float, np.floating)):
-            return DeviceScalar(torch.mul(self.tensor, self._other(other)), self.dtype)
+            return self._lazy("*", self, self._operand(other))
         from .expressions import scale_node
 
         return scale_node(self, other)  # scalar * vector expression
 
     def __rmul__(self, other):
         if isinstance(other, (int, float, np.floating)):
-            return DeviceScalar(torch.mul(self._other(other), self.tensor), self.dtype)
+            return self._lazy("*", self._operand(other), self)
         return NotImplemented
 
     def __repr__(self):

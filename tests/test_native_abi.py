@@ -175,3 +175,29 @@ def test_c_fast_path_declines_what_it_cannot_take():
     assert fast.assign_reduce(y, as_node(y) + ScaleNode(0.5, as_node(x)), as_node(y) * as_node(x), 0) is None
     cv = lv.CountingVector.zeros(10, "f64", device="cpu")
     assert fast.assign(cv, as_node(x)) is False
+
+
+@pytest.mark.parametrize("prog,msg", [
+    (b"p0 p1 / =0 +", b"underflow"),
+    (b"p0 p1", b"leaves values"),
+    (b"p0 =1", b"does not define P0"),
+    (b"p5 =0", b"device scalar 5"),
+    (b"S9 =0", b"host scalar 9"),
+    (b"p0 % =0", b"bad scalar program token"),
+    (b"p0 =9", b"output index"),
+    (b" ".join([b"p0"] * 9) + b" " + b" ".join([b"+"] * 8) + b" =0", b"deeper than 8"),
+])
+def test_scalar_program_is_validated_before_any_launch(prog, msg):
+    """salt_fused_prog rejects malformed scalar programs with SALT_EINVAL and
+    a message, before touching the device (runs without a GPU)."""
+    lib = _native.lib()
+    dummy = ctypes.c_double(0.0)
+    ptr = ctypes.addressof(dummy)
+    leaves, k1 = _native.ptr_array([ptr])
+    dsts, k2 = _native.ptr_array([ptr])
+    ps, k3 = _native.ptr_array([ptr, ptr])
+    sc, k4 = _native.double_array([1.0])
+    rc = lib.salt_fused_prog(1, b"P0 L0 *", None, dsts, 1, leaves, 1, sc, 1, ps, 2, prog, 4, 0, None, 0,
+                             None, None, None)
+    assert rc == -1  # SALT_EINVAL
+    assert msg in lib.salt_last_error(), lib.salt_last_error()
