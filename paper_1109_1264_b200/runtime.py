@@ -627,6 +627,8 @@ def _scalar_program(pscalars, host):
     budget = DeviceScalar.MAX_PROGRAM_OPS
     if not any(ds.lazy for ds in pscalars):
         return list(pscalars), host, None
+    for ds in pscalars:
+        ds.check_operands()
     raw, raw_ids, toks = [], {}, []
 
     def emit(x):

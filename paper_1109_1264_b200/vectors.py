@@ -248,7 +248,7 @@ class DeviceScalar:
     returns (test_ops.py:29-31).
     """
 
-    __slots__ = ("_tensor", "dtype", "guard", "_expr")
+    __slots__ = ("_tensor", "dtype", "guard", "_expr", "_version", "_seen")
 
     __array_ufunc__ = None
 
@@ -265,6 +265,11 @@ class DeviceScalar:
         # (op, operand[, operand]) for a lazy result: op in + - * / neg,
         # operands DeviceScalars or element-typed Python floats
         self._expr = _expr
+        # copy_() bumps _version; a lazy result remembers its operands'
+        # versions (_seen) and refuses to run on an operand changed since
+        self._version = 0
+        self._seen = None if _expr is None else tuple(
+            a._version if isinstance(a, DeviceScalar) else None for a in _expr[1:])
 
     @classmethod
     def full(cls, value, dtype="f64", device=None) -> "DeviceScalar":
@@ -285,7 +290,22 @@ class DeviceScalar:
             t = self._tensor = self._materialise()
         return t
 
+    def check_operands(self) -> None:
+        """Raise if an operand of this lazy scalar was modified in place
+        (copy_) after the operation was recorded: the recorded operation
+        would no longer give what an eager evaluation would have given."""
+        if self._tensor is not None or self._expr is None:
+            return
+        for a, v in zip(self._expr[1:], self._seen):
+            if isinstance(a, DeviceScalar):
+                if a._version != v:
+                    raise RuntimeError("a DeviceScalar operand was modified in place (copy_) after this "
+                                       "lazy scalar operation was recorded; use it before modifying its "
+                                       "operands, or materialise it first (.tensor)")
+                a.check_operands()
+
     def _materialise(self) -> torch.Tensor:
+        self.check_operands()
         op, *args = self._expr
         ref = next(a for a in args if isinstance(a, DeviceScalar)).tensor
         ts = [a.tensor if isinstance(a, DeviceScalar) else torch.full_like(ref, a) for a in args]
@@ -345,6 +365,7 @@ class DeviceScalar:
         CUDA graph that reads it sees the new value on the next replay)."""
         self.tensor.copy_(other.tensor if isinstance(other, DeviceScalar) else
                           torch.tensor([float(self.dtype.type(other))], dtype=self.tensor.dtype))
+        self._version += 1
         return self
 
     def __add__(self, other):

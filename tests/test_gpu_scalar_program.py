@@ -164,3 +164,23 @@ def test_sharded_vectors_with_a_lazy_scalar():
     assert Y.local.to_array().tobytes() == y_new.tobytes()
     ex = restate.exact_sum(y_new * y_new)
     assert abs(float(r) - ex) <= 1e-12 * ex
+
+
+def test_lazy_scalar_refuses_an_operand_modified_in_place():
+    """copy_ into an operand after recording would silently change the
+    value a lazy scalar stands for: it raises instead."""
+    a, b, _ = scalars("f64", 11)
+    s = a / b
+    b.copy_(3.0)
+    with pytest.raises(RuntimeError, match="modified in place"):
+        s.item()
+    X = dev(np.ones(64), "f64")
+    t = a * 2.0
+    a.copy_(1.0)
+    with pytest.raises(RuntimeError, match="modified in place"):
+        X.assign(X + t * X)
+    # materialised before the copy_: keeps the old value (eager semantics)
+    u = a + 1.0
+    u.tensor
+    a.copy_(5.0)
+    assert u.item() == 2.0
