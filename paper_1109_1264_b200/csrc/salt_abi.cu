@@ -755,10 +755,9 @@ int run_fused(Plan& p, void* const* dsts, int ndst, const void* const* leaves, i
     // 24.3 us, dnrm2 26.4 -> 25.5 us; the fence + ticket atomic each
     // streaming CTA paid in the two-level combine held its SM slot).
     // Beyond kCollectCtas streaming CTAs, more tiles per CTA (2^27-2^28
-    // measured equal for 2 and 4 tiles): the collector warp then folds at
-    // most ~30 partials per microsecond, well within its 4-slots-per-lane
-    // round trips, so it never falls behind the streaming CTAs.
-    constexpr i64 kCollectCtas = 16384;
+    // measured equal for 2 and 4 tiles): fewer slots for the collector to
+    // fold, which keeps it far ahead of the streaming CTAs.
+    constexpr i64 kCollectCtas = 32768;
     static_assert(kCollectCtas <= salt::MAX_COLLECT, "collector slots");
     K = collect_tiles();
     if ((ntiles + K - 1) / K > kCollectCtas) K = (ntiles + kCollectCtas - 1) / kCollectCtas;

@@ -513,20 +513,27 @@ __device__ __forceinline__ DD warp_reduce_dd(DD v) {
 // yet": kSlotMask's words are signalling-NaN patterns, which no arithmetic
 // result (all partials are sums) can be.  Each 8-byte word is written once
 // and read whole, so a reader that sees both words non-zero has the value.
-// CTA 0's first warp is the collector: lane l folds slots l, l+32, l+64, ...
-// IN ORDER as they appear (polling up to kCollectBatch of its slots per round trip,
-// volatile loads), zeroes each slot it has consumed (the next launch is
-// stream-ordered after this one), then one warp shuffle tree gives the
-// total — fixed order, so the bits depend only on n.  Whatever order the
-// CTAs are scheduled in, nothing waits on the collector, so it cannot
-// deadlock; the collector only waits for stores that are certain to come.
+// CTA 0's first kCollectWarps warps are the collector: thread t folds slots
+// t, t + C, t + 2C, ... (C = 32 * kCollectWarps) IN ORDER as they appear,
+// polling up to kCollectBatch of its slots per round trip (volatile loads),
+// and zeroes each slot it has consumed (the next launch is stream-ordered
+// after this one); a shuffle tree per warp and the warps' totals in warp
+// order give the total — a fixed order, so the bits depend only on n.
+// C x kCollectBatch slots per round trip keep the collector ahead of the
+// streaming CTAs (they complete at most ~100 slots per microsecond; one
+// warp x 4 fell behind at 2^28, profiles/r02_c3_final_*.txt).  Whatever
+// order the CTAs are scheduled in, nothing waits on the collector, so it
+// cannot deadlock; the collector only waits for stores that are certain to
+// come.
 constexpr unsigned long long kSlotMask = 0x7ff4000000000001ull;
-// slots a collector lane polls per round trip (8 cost the streaming path
-// registers: the collector shares the kernel's register allocation)
+// (a bigger batch costs the streaming path registers: the collector shares
+// the kernel's register allocation — 8 took f32 nrm2 from 48 to 64)
 constexpr int kCollectBatch = 4;
+constexpr int kCollectWarps = 4;
 
 template <class T, int BLOCK>
 __device__ __forceinline__ void collect_epilogue(DD mine, const Args<T>& a, DD* smem) {
+  static_assert(BLOCK >= 32 * kCollectWarps, "collector warps");
   const unsigned np = gridDim.x - 1;
   if (blockIdx.x != 0) {
     DD part = block_reduce_dd<BLOCK>(mine, smem);
@@ -538,14 +545,15 @@ __device__ __forceinline__ void collect_epilogue(DD mine, const Args<T>& a, DD* 
     }
     return;
   }
-  if (threadIdx.x >= 32) return;
+  constexpr unsigned C = 32u * kCollectWarps;
+  if (threadIdx.x >= C) return;
   DD v; v.hi = 0.0; v.lo = 0.0;
-  unsigned q = threadIdx.x;  // this lane's next slot
+  unsigned q = threadIdx.x;  // this thread's next slot
   while (q < np) {
     unsigned long long h[kCollectBatch], l[kCollectBatch];
 #pragma unroll
     for (int i = 0; i < kCollectBatch; ++i) {
-      const unsigned s = q + 32u * i;
+      const unsigned s = q + C * i;
       if (s < np)
         asm volatile("ld.volatile.global.v2.u64 {%0,%1}, [%2];" : "=l"(h[i]), "=l"(l[i]) : "l"(a.slots + 2 * s));
       else
@@ -559,13 +567,19 @@ __device__ __forceinline__ void collect_epilogue(DD mine, const Args<T>& a, DD* 
       p.lo = __longlong_as_double((long long)(l[i] ^ kSlotMask));
       v = dd_add(v, p);
       asm volatile("st.global.v2.u64 [%0], {%1,%2};" ::"l"(a.slots + 2 * q), "l"(0ull), "l"(0ull) : "memory");
-      q += 32u;
+      q += C;
     }
   }
   v = warp_reduce_dd(v);
+  const unsigned warp = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) smem[warp] = v;
+  asm volatile("bar.sync 1, %0;" ::"n"(C) : "memory");  // the collector warps only
   if (threadIdx.x == 0) {
-    if (a.xchg.world > 0) v = exchange_dd(v, a.xchg);
-    finish_store<T>(v, a.flags, a.out);
+    DD tot = smem[0];
+#pragma unroll
+    for (int w = 1; w < kCollectWarps; ++w) tot = dd_add(tot, smem[w]);
+    if (a.xchg.world > 0) tot = exchange_dd(tot, a.xchg);
+    finish_store<T>(tot, a.flags, a.out);
   }
 }
 
