@@ -253,6 +253,7 @@ def fastpath():
                     runtime._workspace, np.float32, np.float64, runtime._lazy_out,
                     addr(h.salt_assign_batch), addr(h.salt_reduce_batch), runtime._batch_out,
                     addr(h.salt_result_enqueue), addr(h.salt_stream_synchronize),
+                    addr(h.salt_fused_prog),
                 )
                 _fast = _fastpath
             except (ImportError, AttributeError):

@@ -44,6 +44,9 @@ typedef int (*assign_batch_fn)(int, const char*, int, void* const*, const void* 
                                const double*, int, const int64_t*, void*);
 typedef int (*reduce_batch_fn)(int, const char*, int, const void* const*, int, const double*, int,
                                const int64_t*, int, void* const*, void*, size_t, void*);
+typedef int (*fused_prog_fn)(int, const char*, const char*, void* const*, int, const void* const*,
+                             int, const double*, int, const void* const*, int, const char*, int64_t,
+                             int, void*, size_t, void*, void*, void*);
 typedef const char* (*last_error_fn)(void);
 typedef int (*result_enqueue_fn)(const void*, size_t, void*, void**);
 typedef int (*stream_sync_fn)(void*);
@@ -56,6 +59,7 @@ static assign_batch_fn p_assign_batch;
 static reduce_batch_fn p_reduce_batch;
 static PyObject* batch_out; /* runtime._batch_out(device, count) -> (tensor, data_ptr) */
 static last_error_fn p_last_error;
+static fused_prog_fn p_fused_prog;
 static result_enqueue_fn p_result_enqueue;
 static stream_sync_fn p_stream_sync;
 static size_t ws_bytes;
@@ -63,7 +67,7 @@ static size_t ws_bytes;
 static PyObject *T_Leaf, *T_Add, *T_Sub, *T_Mul, *T_Scale, *T_Dense, *T_DevScalar;
 static PyObject *get_stream, *current_device, *workspace_fn, *np_f32, *np_f64, *lazy_out;
 static PyObject *s_vector, *s_left, *s_right, *s_child, *s_alpha, *s_ptr, *s_dev, *s_n, *s_code,
-    *s_data_ptr, *s_tensor, *s_get_device;
+    *s_data_ptr, *s_tensor, *s_get_device, *s_expr, *s_check_operands;
 
 typedef struct {
   char sig[MAX_SIG];
@@ -75,6 +79,15 @@ typedef struct {
   int nsc;
   const void* ps[MAX_PSCALARS]; /* DeviceScalar operands (P<k>) */
   int nps;
+  /* lazy DeviceScalars (unevaluated scalar operations): the tree's P<k>
+   * come from a scalar program over raw device scalars (salt_fused_prog) */
+  PyObject* pobj[MAX_PSCALARS];
+  int lazy;
+  char prog[512];
+  int plen;
+  const void* raw[MAX_PSCALARS];
+  PyObject* rawobj[MAX_PSCALARS];
+  int nraw;
   int dev, code;
   long long n;
   /* vectors assigned by earlier roots of the same kernel: a later tree reads
@@ -126,17 +139,36 @@ static int leaf(Walk* w, PyObject* vec) {
   return emit(w, tok);
 }
 
+/* Pointer of a materialised DeviceScalar on device `dev`: 1 ok, 0 other
+ * device, -1 error. */
+static int scalar_ptr(PyObject* t, int dev, void** ptr) {
+  PyObject* d = PyObject_CallMethodNoArgs(t, s_get_device);
+  PyObject* p = d ? PyObject_CallMethodNoArgs(t, s_data_ptr) : NULL;
+  if (!p) { Py_XDECREF(d); return -1; }
+  long dv = PyLong_AsLong(d);
+  *ptr = PyLong_AsVoidPtr(p);
+  Py_DECREF(d);
+  Py_DECREF(p);
+  if (PyErr_Occurred()) return -1;
+  return dv == dev ? 1 : 0;
+}
+
 /* DeviceScalar -> w->ps[w->nps++]; must live on the kernel's device.  A
- * LAZY DeviceScalar (an unevaluated scalar operation, _tensor None) is
- * declined: the Python path compiles it into the kernel's scalar program. */
+ * LAZY DeviceScalar (an unevaluated scalar operation, _tensor None) is kept
+ * as an object: build_program() turns the tree's device scalars into a
+ * scalar program over the raw device scalars underneath. */
 static int device_scalar(Walk* w, PyObject* ds) {
   if (w->nps == MAX_PSCALARS) return 0;
   PyObject* t = PyObject_GetAttr(ds, s_tensor);
   if (!t) return -1;
   if (t == Py_None) {
     Py_DECREF(t);
-    return 0;
+    w->pobj[w->nps] = ds;
+    w->ps[w->nps++] = NULL;
+    w->lazy = 1;
+    return 1;
   }
+  w->pobj[w->nps] = ds;
   PyObject* d = PyObject_CallMethodNoArgs(t, s_get_device);
   PyObject* p = d ? PyObject_CallMethodNoArgs(t, s_data_ptr) : NULL;
   Py_DECREF(t);
@@ -149,6 +181,103 @@ static int device_scalar(Walk* w, PyObject* ds) {
   if (dev != w->dev) return 0;
   w->ps[w->nps++] = ptr;
   return 1;
+}
+
+static int prog_tok(Walk* w, const char* tok) {
+  const int k = (int)strlen(tok);
+  if (w->plen + k + 2 >= (int)sizeof w->prog) return 0;
+  if (w->plen) w->prog[w->plen++] = ' ';
+  memcpy(w->prog + w->plen, tok, (size_t)k + 1);
+  w->plen += k;
+  return 1;
+}
+
+/* Postfix of one scalar operand (DeviceScalar, lazy or not, or a float)
+ * into w->prog; *depth tracks the program's stack.  0 = too large for one
+ * program (the Python path then materialises), -1 = Python error. */
+static int prog_operand(Walk* w, PyObject* x, int* depth, int* ops) {
+  char tok[16];
+  if (++*ops > 30) return 0;
+  if (PyFloat_Check(x)) {
+    if (w->nsc == MAX_SCALARS) return 0;
+    w->sc[w->nsc] = PyFloat_AS_DOUBLE(x);
+    snprintf(tok, sizeof tok, "S%d", w->nsc++);
+    if (++*depth > 8) return 0;
+    return prog_tok(w, tok);
+  }
+  if ((PyObject*)Py_TYPE(x) != T_DevScalar) return 0;
+  PyObject* t = PyObject_GetAttr(x, s_tensor);
+  if (!t) return -1;
+  if (t != Py_None) {  /* materialised: a raw device scalar */
+    int i = 0;
+    while (i < w->nraw && w->rawobj[i] != x) ++i;
+    if (i == w->nraw) {
+      if (w->nraw == MAX_PSCALARS) { Py_DECREF(t); return 0; }
+      void* ptr;
+      int rc = scalar_ptr(t, w->dev, &ptr);
+      Py_DECREF(t);
+      if (rc != 1) return rc;
+      w->rawobj[i] = x;
+      w->raw[i] = ptr;
+      ++w->nraw;
+    } else {
+      Py_DECREF(t);
+    }
+    snprintf(tok, sizeof tok, "p%d", i);
+    if (++*depth > 8) return 0;
+    return prog_tok(w, tok);
+  }
+  Py_DECREF(t);
+  PyObject* e = PyObject_GetAttr(x, s_expr);
+  if (!e) return -1;
+  int rc = 1;
+  if (!PyTuple_Check(e) || PyTuple_GET_SIZE(e) < 2) rc = 0;
+  for (Py_ssize_t i = 1; rc == 1 && i < PyTuple_GET_SIZE(e); ++i)
+    rc = prog_operand(w, PyTuple_GET_ITEM(e, i), depth, ops);
+  if (rc == 1) {
+    const char* op = PyUnicode_AsUTF8(PyTuple_GET_ITEM(e, 0));
+    if (!op) rc = -1;
+    else {
+      if (strcmp(op, "neg") != 0) --*depth;  /* binary: two in, one out */
+      rc = prog_tok(w, op);
+    }
+  }
+  Py_DECREF(e);
+  return rc;
+}
+
+/* With lazy device scalars: the scalar program that defines every P<k> of
+ * the tree, the raw device scalars it reads (w->raw) and its host constants
+ * (appended to w->sc).  1 ok (or nothing to do), 0 decline, -1 error. */
+static int build_program(Walk* w) {
+  if (!w->lazy) return 1;
+  for (int k = 0; k < w->nps; ++k) {
+    /* refuses operands modified in place since the operation was recorded */
+    PyObject* r = PyObject_CallMethodNoArgs(w->pobj[k], s_check_operands);
+    if (!r) return -1;
+    Py_DECREF(r);
+  }
+  int depth = 0, ops = 0;
+  char tok[16];
+  for (int k = 0; k < w->nps; ++k) {
+    int rc = prog_operand(w, w->pobj[k], &depth, &ops);
+    if (rc != 1) return rc;
+    snprintf(tok, sizeof tok, "=%d", k);
+    --depth;
+    if (!prog_tok(w, tok)) return 0;
+  }
+  return 1;
+}
+
+/* salt_fused, or salt_fused_prog when the tree has lazy device scalars */
+static int call_fused(Walk* w, const char* asig, const char* rsig, void* const* dsts, int ndst,
+                      int flags, void* ws, void* out, void* host, void* stream) {
+  const void* const* leaves = (const void* const*)w->ptrs;
+  if (w->lazy)
+    return p_fused_prog(w->code, asig, rsig, dsts, ndst, leaves, w->nvec, w->sc, w->nsc, w->raw,
+                        w->nraw, w->prog, w->n, flags, ws, ws ? ws_bytes : 0, out, host, stream);
+  return p_fused(w->code, asig, rsig, dsts, ndst, leaves, w->nvec, w->sc, w->nsc, w->ps, w->nps,
+                 w->n, flags, ws, ws ? ws_bytes : 0, out, host, stream);
 }
 
 static int walk(Walk* w, PyObject* node) {
@@ -283,11 +412,10 @@ static PyObject* fp_assign(PyObject* self, PyObject* args) {
   TRY(start(&w, dest, &dptr));
   TRY(walk(&w, src));
   if (w.nvec == 0) Py_RETURN_FALSE;
+  TRY(build_program(&w));
   TRY(stream_for(&w, &stream));
   if (w.n == 0) Py_RETURN_TRUE;
-  if (w.nps)
-    return check(p_fused(w.code, w.sig, NULL, &dptr, 1, (const void* const*)w.ptrs, w.nvec, w.sc,
-                         w.nsc, w.ps, w.nps, w.n, 0, NULL, 0, NULL, NULL, stream));
+  if (w.nps) return check(call_fused(&w, w.sig, NULL, &dptr, 1, 0, NULL, NULL, NULL, stream));
   return check(p_assign(w.code, w.sig, dptr, (const void* const*)w.ptrs, w.nvec, w.sc, w.nsc,
                         w.n, stream));
 }
@@ -322,8 +450,7 @@ static PyObject* launch_reduce(Walk* w, const char* asig, void* const* dptrs, in
   const void* const* leaves = (const void* const*)w->ptrs;
   int rc;
   if (w->nps || ndst > 1)
-    rc = p_fused(w->code, asig, w->sig, dptrs, ndst, leaves, w->nvec, w->sc, w->nsc, w->ps, w->nps,
-                 w->n, flags, ws, ws_bytes, out, NULL, stream);
+    rc = call_fused(w, asig, w->sig, dptrs, ndst, flags, ws, out, NULL, stream);
   else if (asig)
     rc = p_assign_reduce(w->code, asig, w->sig, dptrs[0], leaves, w->nvec, w->sc, w->nsc, w->n,
                          flags, ws, ws_bytes, out, NULL, stream);
@@ -372,6 +499,8 @@ static PyObject* fp_reduce(PyObject* self, PyObject* args) {
   if (rc == 0) Py_RETURN_NONE;
   rc = walk(&w, child);
   if (rc < 0) return NULL;
+  if (rc == 1) rc = build_program(&w);
+  if (rc < 0) return NULL;
   void* stream;
   if (rc == 0 || (rc = stream_for(&w, &stream)) == 0) Py_RETURN_NONE;
   if (rc < 0) return NULL;
@@ -399,6 +528,8 @@ static PyObject* fp_assign_reduce(PyObject* self, PyObject* args) {
   rc = walk(&w, child);
   if (rc <= 0) { if (rc < 0) return NULL; Py_RETURN_NONE; }
   if (w.nvec == 0) Py_RETURN_NONE;
+  rc = build_program(&w);
+  if (rc <= 0) { if (rc < 0) return NULL; Py_RETURN_NONE; }
   rc = stream_for(&w, &stream);
   if (rc <= 0) { if (rc < 0) return NULL; Py_RETURN_NONE; }
   void *ws, *slot;
@@ -451,14 +582,15 @@ static PyObject* fp_fused(PyObject* self, PyObject* args) {
     if (rc <= 0) { if (rc < 0) return NULL; Py_RETURN_NONE; }
   }
   if (w.nvec == 0) Py_RETURN_NONE;
+  rc = build_program(&w);
+  if (rc <= 0) { if (rc < 0) return NULL; Py_RETURN_NONE; }
   void* stream;
   rc = stream_for(&w, &stream);
   if (rc <= 0) { if (rc < 0) return NULL; Py_RETURN_NONE; }
   PyObject* result;
   if (total == Py_None) {
     if (w.n) {
-      rc = p_fused(w.code, asig, NULL, dptrs, (int)na, (const void* const*)w.ptrs, w.nvec, w.sc,
-                   w.nsc, w.ps, w.nps, w.n, 0, NULL, 0, NULL, NULL, stream);
+      rc = call_fused(&w, asig, NULL, dptrs, (int)na, 0, NULL, NULL, NULL, stream);
       if (rc != 0) return check(rc);
     }
     Py_INCREF(Py_None);
@@ -820,13 +952,14 @@ done:
 }
 
 static PyObject* fp_init(PyObject* self, PyObject* args) {
-  unsigned long long a, r, ar, fu, le, ab, rb, re, ss;
+  unsigned long long a, r, ar, fu, le, ab, rb, re, ss, fp;
   Py_ssize_t wsb;
-  if (!PyArg_ParseTuple(args, "KKKKKnOOOOOOOOOOOOOKKOKK", &a, &r, &ar, &fu, &le, &wsb, &T_Leaf, &T_Add,
+  if (!PyArg_ParseTuple(args, "KKKKKnOOOOOOOOOOOOOKKOKKK", &a, &r, &ar, &fu, &le, &wsb, &T_Leaf, &T_Add,
                         &T_Sub, &T_Mul, &T_Scale, &T_Dense, &T_DevScalar, &get_stream,
                         &current_device, &workspace_fn, &np_f32, &np_f64, &lazy_out, &ab, &rb,
-                        &batch_out, &re, &ss))
+                        &batch_out, &re, &ss, &fp))
     return NULL;
+  p_fused_prog = (fused_prog_fn)(uintptr_t)fp;
   p_result_enqueue = (result_enqueue_fn)(uintptr_t)re;
   p_stream_sync = (stream_sync_fn)(uintptr_t)ss;
   p_assign_batch = (assign_batch_fn)(uintptr_t)ab;
@@ -874,6 +1007,8 @@ PyMODINIT_FUNC PyInit__fastpath(void) {
   s_code = PyUnicode_InternFromString("_code");
   s_data_ptr = PyUnicode_InternFromString("data_ptr");
   s_tensor = PyUnicode_InternFromString("_tensor");
+  s_expr = PyUnicode_InternFromString("_expr");
+  s_check_operands = PyUnicode_InternFromString("check_operands");
   s_get_device = PyUnicode_InternFromString("get_device");
   return PyModule_Create(&module);
 }

@@ -184,3 +184,33 @@ def test_lazy_scalar_refuses_an_operand_modified_in_place():
     u.tensor
     a.copy_(5.0)
     assert u.item() == 2.0
+
+
+def test_c_fast_path_compiles_lazy_scalars(monkeypatch):
+    """The CPython fast path builds the scalar program itself (no Python
+    lowering, no torch launch): runtime.run_fused is never reached."""
+    from paper_1109_1264_b200 import runtime
+
+    def boom(*a, **k):
+        raise AssertionError("Python path taken")
+
+    n = 10_000
+    g = np.random.default_rng(12)
+    xv, yv = (g.standard_normal(n) for _ in range(2))
+    X, Y = dev(xv, "f64"), dev(yv, "f64")
+    a, b, c = scalars("f64", 13)
+    monkeypatch.setattr(runtime, "run_fused", boom)
+    s = (a - 0.5) / b + c
+    r = lv.fused((Y, Y + s * X), Y * X)                 # fused assign + reduce
+    Y.assign(Y - (a / c) * X)                           # plain assign with a lazy alpha
+    r2 = lv.dot(X, (b * 2.0) * Y)                       # reduce with a lazy alpha
+    assert s.lazy
+    monkeypatch.undo()
+    sv, acv, b2 = float(s.item()), float((a / c).item()), float((b * 2.0).item())
+    y1 = restate.eval_sig("L0 S0 L1 * +", [yv, xv], [sv], "f64")
+    y2 = restate.eval_sig("L0 S0 L1 * -", [y1, xv], [acv], "f64")
+    assert Y.to_array().tobytes() == y2.tobytes()
+    ex = restate.exact_sum(y1 * xv)
+    assert abs(float(r) - ex) <= 1e-12 * abs(ex)
+    ex2 = restate.exact_sum(xv * (b2 * y2))
+    assert abs(float(r2) - ex2) <= 1e-12 * abs(ex2)
