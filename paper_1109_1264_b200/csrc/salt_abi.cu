@@ -154,6 +154,13 @@ int collect_tiles() {
   }();
   return env > 0 ? env : 2;
 }
+int collect_warps() {
+  static const int env = [] {
+    const char* e = getenv("SALT_COLLECT_WARPS");
+    return e ? atoi(e) : 0;
+  }();
+  return env >= 1 && env <= 8 ? env : 4;
+}
 int collect_min() {
   static const int env = [] {
     const char* e = getenv("SALT_COLLECT_MIN");
@@ -792,6 +799,7 @@ int run_fused(Plan& p, void* const* dsts, int ndst, const void* const* leaves, i
   if (collect) g64 += 1;  // CTA 0: the collector
   const int grid = (int)g64;
   a.first = collect ? 1 : 0;
+  a.collect_warps = collect_warps();
   a.tiles_per_cta = K;
   // CTAs per combine group: the whole grid when it was sized as one group
   // (at most 2 x GROUP), else GROUP (a grid of <= GROUP CTAs is one group

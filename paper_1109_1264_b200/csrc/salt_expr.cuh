@@ -192,6 +192,7 @@ template <class T> struct Args {
   int cluster;                    // reduce modes: 1 = the grid is ONE thread-block cluster
   int group;                      // reduce modes: CTAs per group (GROUP, or the whole grid
                                   // when it is one group of <= MAX_ONE_GROUP CTAs)
+  int collect_warps;              // collector warps (1 .. 8)
   int first;                      // 1: CTA 0 is the collector (see collect_epilogue), the
                                   // streaming CTAs are 1..gridDim.x-1; 0: no collector
   unsigned long long* slots;      // collector slots (2 words per streaming CTA, zero = empty)
@@ -513,8 +514,8 @@ __device__ __forceinline__ DD warp_reduce_dd(DD v) {
 // yet": kSlotMask's words are signalling-NaN patterns, which no arithmetic
 // result (all partials are sums) can be.  Each 8-byte word is written once
 // and read whole, so a reader that sees both words non-zero has the value.
-// CTA 0's first kCollectWarps warps are the collector: thread t folds slots
-// t, t + C, t + 2C, ... (C = 32 * kCollectWarps) IN ORDER as they appear,
+// CTA 0's first a.collect_warps warps are the collector: thread t folds
+// slots t, t + C, t + 2C, ... (C = 32 * collect_warps) IN ORDER as they appear,
 // polling up to kCollectBatch of its slots per round trip (volatile loads),
 // and zeroes each slot it has consumed (the next launch is stream-ordered
 // after this one); a shuffle tree per warp and the warps' totals in warp
@@ -528,12 +529,15 @@ __device__ __forceinline__ DD warp_reduce_dd(DD v) {
 constexpr unsigned long long kSlotMask = 0x7ff4000000000001ull;
 // (a bigger batch costs the streaming path registers: the collector shares
 // the kernel's register allocation — 8 took f32 nrm2 from 48 to 64)
-constexpr int kCollectBatch = 4;
-constexpr int kCollectWarps = 4;
+#ifndef SALT_COLLECT_BATCH
+#define SALT_COLLECT_BATCH 4
+#endif
+constexpr int kCollectBatch = SALT_COLLECT_BATCH;
+constexpr int kCollectWarpsMax = 8;
 
 template <class T, int BLOCK>
 __device__ __forceinline__ void collect_epilogue(DD mine, const Args<T>& a, DD* smem) {
-  static_assert(BLOCK >= 32 * kCollectWarps, "collector warps");
+  static_assert(BLOCK >= 32 * kCollectWarpsMax, "collector warps");
   const unsigned np = gridDim.x - 1;
   if (blockIdx.x != 0) {
     DD part = block_reduce_dd<BLOCK>(mine, smem);
@@ -545,7 +549,8 @@ __device__ __forceinline__ void collect_epilogue(DD mine, const Args<T>& a, DD* 
     }
     return;
   }
-  constexpr unsigned C = 32u * kCollectWarps;
+  const int nw = a.collect_warps;  // 1 .. kCollectWarpsMax
+  const unsigned C = 32u * nw;
   if (threadIdx.x >= C) return;
   DD v; v.hi = 0.0; v.lo = 0.0;
   unsigned q = threadIdx.x;  // this thread's next slot
@@ -573,11 +578,10 @@ __device__ __forceinline__ void collect_epilogue(DD mine, const Args<T>& a, DD* 
   v = warp_reduce_dd(v);
   const unsigned warp = threadIdx.x >> 5;
   if ((threadIdx.x & 31) == 0) smem[warp] = v;
-  asm volatile("bar.sync 1, %0;" ::"n"(C) : "memory");  // the collector warps only
+  if (nw > 1) asm volatile("bar.sync 1, %0;" ::"r"(C) : "memory");  // the collector warps only
   if (threadIdx.x == 0) {
-    DD tot = smem[0];
-#pragma unroll
-    for (int w = 1; w < kCollectWarps; ++w) tot = dd_add(tot, smem[w]);
+    DD tot = v;
+    for (int w = 1; w < nw; ++w) tot = dd_add(tot, smem[w]);
     if (a.xchg.world > 0) tot = exchange_dd(tot, a.xchg);
     finish_store<T>(tot, a.flags, a.out);
   }
