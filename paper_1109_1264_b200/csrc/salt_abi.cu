@@ -159,7 +159,7 @@ int collect_warps() {
     const char* e = getenv("SALT_COLLECT_WARPS");
     return e ? atoi(e) : 0;
   }();
-  return env >= 1 && env <= 8 ? env : 4;
+  return env >= 1 && env <= 8 ? env : 2;
 }
 int collect_min() {
   static const int env = [] {

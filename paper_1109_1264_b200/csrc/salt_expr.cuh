@@ -521,8 +521,10 @@ __device__ __forceinline__ DD warp_reduce_dd(DD v) {
 // after this one); a shuffle tree per warp and the warps' totals in warp
 // order give the total — a fixed order, so the bits depend only on n.
 // C x kCollectBatch slots per round trip keep the collector ahead of the
-// streaming CTAs (they complete at most ~100 slots per microsecond; one
-// warp x 4 fell behind at 2^28, profiles/r02_c3_final_*.txt).  Whatever
+// streaming CTAs (they complete up to ~100 slots per microsecond): one
+// warp x 4 slots fell behind at 2^28; 2 warps x 4 (the default) matched
+// 1 x 8 and 2 x 8 and beat 4 warps over 2^22-2^28 on one box
+// (profiles/r02_collector_ab.txt) without the registers 8 slots cost.  Whatever
 // order the CTAs are scheduled in, nothing waits on the collector, so it
 // cannot deadlock; the collector only waits for stores that are certain to
 // come.
