@@ -321,6 +321,16 @@ size_t salt_reduce_workspace_bytes(void);
  * slot; after salt_stream_synchronize(stream) the slot holds the bytes. */
 int salt_result_enqueue(const void* out_dev, size_t bytes, void* stream, void** host_slot);
 int salt_stream_synchronize(void* stream);
+/* Device-observed trace (debug): while a buffer is set for this host thread,
+ * every salt_assign / salt_reduce / salt_fused call runs the NVRTC build of
+ * its tree compiled with -DSALT_TRACE, which records the events of ONE
+ * thread (thread 0 of the first streaming CTA) into trace_dev (int64):
+ * word 0 = event count, then (kind, element index, slot) triples — kind 0
+ * load (a slot's leaf vectors issued), 1 vector_op, 2 store, 3 single_op
+ * (a scalar head/tail element), 4 reduction (the CTA's partial is formed).
+ * The results are the same bits as the untraced kernel.  The buffer must be
+ * zeroed before the call.  trace_dev NULL turns tracing off. */
+int salt_set_trace(void* trace_dev, int64_t capacity);
 /* Identity of the CUDA graph capture in progress on `stream` (0: the stream
  * is not capturing).  A reduction captured into a graph needs a workspace
  * of its own (its tickets and partials are baked into the graph): hosts key

@@ -51,6 +51,7 @@ HEADER_SYMBOLS = (
     "salt_assign_reduce_host",
     "salt_reduce_workspace_bytes",
     "salt_capture_id",
+    "salt_set_trace",
     "salt_result_enqueue",
     "salt_stream_synchronize",
     "salt_reduce_exchange",
@@ -133,6 +134,7 @@ _SIGNATURES = {
     ),
     "salt_reduce_workspace_bytes": (_c_size, []),
     "salt_capture_id": (ctypes.c_uint64, [_c_vp]),
+    "salt_set_trace": (_c_int, [_c_vp, _c_i64]),
     "salt_result_enqueue": (_c_int, [_c_vp, _c_size, _c_vp, _c_vp]),
     "salt_stream_synchronize": (_c_int, [_c_vp]),
     "salt_reduce_exchange": (

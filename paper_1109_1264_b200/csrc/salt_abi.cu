@@ -179,6 +179,10 @@ int reduce_tiles_per_cta(int nl) {
 }
 constexpr int kMaxDevices = 64;
 
+// salt_set_trace: this host thread's device trace buffer (nullptr: off)
+thread_local long long* g_trace_buf = nullptr;
+thread_local long long g_trace_cap = 0;
+
 thread_local std::string g_err;
 std::atomic<uint64_t> g_launches{0};
 std::atomic<int> g_force_jit{0};
@@ -707,7 +711,14 @@ int run_fused(Plan& p, void* const* dsts, int ndst, const void* const* leaves, i
   geometry<T>(dsts, nroots, leaves, p.nl, n, vec, a.head, a.nvec);
   Kernel* k = nullptr;
   const bool force_interp = g_force_interp.load(std::memory_order_relaxed) != 0;
-  if (!force_interp) {
+  if (g_trace_buf) {
+    // device-observed trace (salt_set_trace): the NVRTC build of this tree
+    // with -DSALT_TRACE, recording one thread's events into the buffer
+    k = get_kernel(dtype_of<T>(), p.mode, vec, p.nl, p.sa.type, p.sr.type, false, nullptr, true);
+    if (!k) return fail(SALT_EJIT, "traced kernel: " + g_err);
+    a.trace = g_trace_buf;
+    a.trace_cap = g_trace_cap;
+  } else if (!force_interp) {
     Kernel*& slot = p.cached[g_force_jit.load(std::memory_order_relaxed)][vec == 1 ? 1 : 0];
     if (!slot) {
       // tiered: trees the interpreter can run do not wait for NVRTC (unless
@@ -928,6 +939,13 @@ int salt_result_enqueue(const void* out_dev, size_t bytes, void* stream, void** 
 
 int salt_stream_synchronize(void* stream) {
   SALT_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+  return 0;
+}
+
+int salt_set_trace(void* trace_dev, int64_t capacity) {
+  if (trace_dev && capacity < 4) return fail(SALT_EINVAL, "trace buffer needs at least 4 int64 words");
+  g_trace_buf = (long long*)trace_dev;
+  g_trace_cap = trace_dev ? capacity : 0;
   return 0;
 }
 

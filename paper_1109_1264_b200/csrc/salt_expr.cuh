@@ -193,6 +193,8 @@ template <class T> struct Args {
   int group;                      // reduce modes: CTAs per group (GROUP, or the whole grid
                                   // when it is one group of <= MAX_ONE_GROUP CTAs)
   int collect_warps;              // collector warps (1 .. 8)
+  long long* trace;               // -DSALT_TRACE builds: event buffer (salt_set_trace)
+  long long trace_cap;
   int first;                      // 1: CTA 0 is the collector (see collect_epilogue), the
                                   // streaming CTAs are 1..gridDim.x-1; 0: no collector
   unsigned long long* slots;      // collector slots (2 words per streaming CTA, zero = empty)
@@ -736,6 +738,24 @@ __device__ __forceinline__ void reduce_epilogue(DD mine, const Args<T>& a) {
   }
 }
 
+// Device-observed trace (-DSALT_TRACE, NVRTC builds only): thread 0 of the
+// first streaming CTA appends (kind, element index, slot) to a.trace.
+#ifdef SALT_TRACE
+template <class T>
+__device__ __forceinline__ void trace_event(const Args<T>& a, int kind, i64 idx, int slot) {
+  if (!a.trace || blockIdx.x != (unsigned)a.first || threadIdx.x != 0) return;
+  const long long k = a.trace[0];
+  if (1 + 3 * (k + 1) > a.trace_cap) return;
+  a.trace[1 + 3 * k] = kind;
+  a.trace[2 + 3 * k] = idx;
+  a.trace[3 + 3 * k] = slot;
+  a.trace[0] = k + 1;
+}
+#define SALT_TRACE_EVENT(kind, idx, slot) trace_event(a, kind, idx, slot)
+#else
+#define SALT_TRACE_EVENT(kind, idx, slot) ((void)0)
+#endif
+
 // ---------------------------------------------------------------- the kernel
 // MODE_ASSIGN:        dst[i] = EA(i)
 // MODE_REDUCE:        out    = sum_i ER(i)
@@ -799,6 +819,7 @@ __global__ void SALT_BOUNDS(BLOCK) fused_kernel(Args<T> a) {
       for (int q = 0; q < NP; ++q) e.p[q] = pv[q];
       if (ASSIGN) AssignRoots<EA, 0, ND>::template one<T>(e, a.dst, i);
       if (REDUCE) acc.add(ER::ev(e, 0));
+      SALT_TRACE_EVENT(3, i, -1);
     }
   }
 
@@ -816,6 +837,7 @@ __global__ void SALT_BOUNDS(BLOCK) fused_kernel(Args<T> a) {
         const i64 off = a.head + j * V;
 #pragma unroll
         for (int l = 0; l < NL; ++l) VecIO<T, V>::load(e[u].x[l], a.leaf[l] + off);
+        SALT_TRACE_EVENT(0, off, u);
       }
     }
 #pragma unroll
@@ -826,7 +848,9 @@ __global__ void SALT_BOUNDS(BLOCK) fused_kernel(Args<T> a) {
         for (int s = 0; s < NS; ++s) e[u].s[s] = a.sc[s];
 #pragma unroll
         for (int q = 0; q < NP; ++q) e[u].p[q] = pv[q];
+        SALT_TRACE_EVENT(1, a.head + j * V, u);
         if (ASSIGN) AssignRoots<EA, 0, ND>::template vec<T>(e[u], a.dst, a.head + j * V);
+        if (ASSIGN) SALT_TRACE_EVENT(2, a.head + j * V, u);
         if (REDUCE) {
 #pragma unroll
           for (int k = 0; k < V; ++k) acc.add(ER::ev(e[u], k));
@@ -835,7 +859,10 @@ __global__ void SALT_BOUNDS(BLOCK) fused_kernel(Args<T> a) {
     }
   }
 
-  if (REDUCE) reduce_epilogue<T, BLOCK>(acc.get(), a);
+  if (REDUCE) {
+    SALT_TRACE_EVENT(4, -1, -1);
+    reduce_epilogue<T, BLOCK>(acc.get(), a);
+  }
 }
 
 // ---------------------------------------------------------------- batches

@@ -201,3 +201,24 @@ def test_scalar_program_is_validated_before_any_launch(prog, msg):
                              None, None, None)
     assert rc == -1  # SALT_EINVAL
     assert msg in lib.salt_last_error(), lib.salt_last_error()
+
+
+def test_traced_kernel_source_compiles_with_nvrtc():
+    """salt_set_trace switches a call to the NVRTC build of its tree with
+    -DSALT_TRACE.  Without a GPU the call must get past the JIT (the traced
+    source compiles) and fail only at the first CUDA runtime call."""
+    lib = _native.lib()
+    dummy = ctypes.c_double(0.0)
+    ptr = ctypes.addressof(dummy)
+    leaves, k1 = _native.ptr_array([ptr, ptr])
+    sc, k2 = _native.double_array([0.5])
+    buf = (ctypes.c_int64 * 64)()
+    assert lib.salt_set_trace(ctypes.addressof(buf), 64) == 0
+    try:
+        rc = lib.salt_assign(1, b"L0 S0 L1 * -", ctypes.c_void_p(ptr), leaves, 2, sc, 1, 4096, None)
+        msg = lib.salt_last_error().decode()
+    finally:
+        assert lib.salt_set_trace(None, 0) == 0
+    assert rc != 0
+    assert "traced kernel" not in msg and "NVRTC" not in msg, msg
+    assert lib.salt_set_trace(ctypes.addressof(buf), 2) != 0  # too small a buffer
