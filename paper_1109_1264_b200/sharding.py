@@ -233,9 +233,14 @@ class ShardedVector(VectorOps):
         16-byte NCCL all-gather per rank over NVLink; gloo on CPU)."""
         if not (dist.is_available() and dist.is_initialized()):
             return part.reshape(-1)
-        out = [torch.empty_like(part) for _ in range(self.world)]
-        dist.all_gather(out, part, group=self.group)
-        return torch.cat(out)
+        out = torch.empty(self.world * part.numel(), dtype=part.dtype, device=part.device)
+        if hasattr(dist, "all_gather_into_tensor") and dist.get_backend(self.group) == "nccl":
+            # one collective straight into the rank-ordered buffer (no torch.cat launch)
+            dist.all_gather_into_tensor(out, part.reshape(-1), group=self.group)
+            return out
+        parts = list(out.view(self.world, -1).unbind(0))
+        dist.all_gather(parts, part.reshape(-1), group=self.group)
+        return out
 
     # ---- inspection (collective: every rank must call) ----
     def to_array(self) -> np.ndarray:
