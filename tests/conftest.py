@@ -20,6 +20,36 @@ if str(ROOT) not in sys.path:
 GOLDEN = ROOT / "tests" / "golden"
 NP = {"f32": np.float32, "f64": np.float64}
 
+# The reference's own unit tests (tests/reference_suite/): __graft_entry__.build()
+# packs them into a git-ignored archive; they are extracted here for the
+# length of the session (collected from tests/reference_suite/_vendored/)
+# and removed again in pytest_sessionfinish.
+REF_SUITE = ROOT / "tests" / "reference_suite"
+REF_ARCHIVE = REF_SUITE / "reference_tests.tar.gz"
+REF_DIR = REF_SUITE / "_vendored"
+
+
+def _extract_reference_suite():
+    import tarfile
+
+    if not REF_ARCHIVE.exists():
+        return
+    REF_DIR.mkdir(exist_ok=True)
+    with tarfile.open(REF_ARCHIVE) as tar:
+        for m in tar.getmembers():
+            if m.isfile() and m.name.startswith("test_") and m.name.endswith(".py") and "/" not in m.name:
+                tar.extract(m, REF_DIR, filter="data")
+
+
+_extract_reference_suite()
+
+
+def pytest_sessionfinish(session, exitstatus):
+    import shutil
+
+    if REF_ARCHIVE.exists():
+        shutil.rmtree(REF_DIR, ignore_errors=True)
+
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200)")

@@ -1,9 +1,10 @@
 """Run the reference's OWN unit tests (pkg/tests/*.py) against this package.
 
-build() copies /root/reference/pkg/tests/test_*.py, unmodified, into
-tests/reference_suite/_vendored/ (git-ignored: reference sources stay out of
-this repository's history; the copy travels to the GPU box with the
-snapshot like the built .so files).  This conftest makes `import lanevec`
+build() packs /root/reference/pkg/tests/test_*.py, unmodified, into the
+git-ignored archive reference_tests.tar.gz (reference sources stay out of
+this repository's history; the archive travels to the GPU box with the
+snapshot like the built .so files).  tests/conftest.py extracts them into
+_vendored/ for the length of a pytest session only.  This conftest makes `import lanevec`
 resolve to paper_1109_1264_b200 — the drop-in claim of SURVEY.md §8(b) —
 before those modules are imported:
 
