@@ -80,8 +80,9 @@ def main():
                        [bool(v) for v in flags.tolist()]))
         res["world"] = world
         res["values"] = [float(r).hex(), float(nr).hex(), float(rr).hex(), float(cg.item()).hex()]
-        res["exchange"] = os.environ.get("SALT_EXCHANGE", "peer")
         from paper_1109_1264_b200 import sharding
+
+        res["exchange"] = sharding.exchange_route()
 
         ex = [e for e in sharding._exchanges.values() if e is not None]
         res["peer_exchange_active"] = bool(ex)
