@@ -261,11 +261,36 @@ def lanevec_1core(n=1 << 20):
                       "(unmodified reference engine from baseline/_ref, default plan, one core)"}
 
 
+def workload_config(n, world):
+    """The `config` object of both arms (one workload, one description)."""
+    return {
+        "workload": WORKLOAD,
+        "n_per_gpu": n,
+        "bytes_per_step_per_gpu": int(32 * n),
+        "l2": "inputs (8 GiB/GPU) >> 126 MB L2; no flush needed",
+        "parallelism": f"block-sharded x{world} (weak), no data-path collective",
+    }
+
+
+def _mem_available():
+    try:
+        for ln in open("/proc/meminfo"):
+            if ln.startswith("MemAvailable:"):
+                return int(ln.split()[1]) * 1024
+    except OSError:
+        pass
+    return 0
+
+
 def run_reference(args, world, rank):
     if rank != 0:
         return
     threads = _host_threads()
     n_sample = args.n_sample
+    if n_sample is None:
+        # the full 2^28-element workload (4 x 2 GiB of host arrays, ~70 ms a
+        # step on 16 threads) when the host has the memory, else a 2^25 sample
+        n_sample = args.n if _mem_available() >= 24 << 30 else 1 << 25
     gbs, per, done = cpu_reference_gbs(n_sample, args.steps, args.warmup, threads, seconds_cap=120)
     line = {
         "impl": "reference",
@@ -281,11 +306,13 @@ def run_reference(args, world, rank):
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (seeded, chunk-keyed numpy streams)",
-        "config": {"workload": WORKLOAD, "sample_n": n_sample},
+        "config": workload_config(args.n, args.gpus) if n_sample == args.n else
+                  dict(workload_config(args.n, args.gpus), sample_n=n_sample),
         "cpu_baseline": {
             "value": round(gbs, 3), "unit": "GB/s", "cores": threads, "kind": "port",
-            "sample": f"{n_sample} f64 elements per step (bounded sample of the 2^28 workload), "
-                      "oracle/salt_oracle.c tile evaluation, host threads",
+            "sample": (f"the full workload ({n_sample} f64 elements per step)" if n_sample == args.n else
+                       f"{n_sample} f64 elements per step (bounded sample of the 2^28 workload)")
+                      + ", oracle/salt_oracle.c tile evaluation, all host threads",
         },
         "e2e": {"value": round(gbs, 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
@@ -435,13 +462,7 @@ def run_gpu(args, world, rank, local):
             "vs_baseline": None,
             "dtype": "f64",
             "data": "synthetic (seeded, chunk-keyed numpy streams; BASELINE config 2 shapes)",
-            "config": {
-                "workload": WORKLOAD,
-                "n_per_gpu": n,
-                "bytes_per_step_per_gpu": int(bytes_step),
-                "l2": "inputs (8 GiB/GPU) >> 126 MB L2; no flush needed",
-                "parallelism": f"block-sharded x{world} (weak), no data-path collective",
-            },
+            "config": workload_config(n, world),
             "pct_hbm": round(value / (world * peak), 4),
             "roofline": {
                 "bound": "hbm",
@@ -627,8 +648,9 @@ def main(argv=None):
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-multi", action="store_true",
                     help="skip the config-4 / config-5 multi-GPU block")
-    ap.add_argument("--n-sample", type=int, default=1 << 25,
-                    help="elements per step of the --impl reference CPU sample")
+    ap.add_argument("--n-sample", type=int, default=None,
+                    help="elements per step of the --impl reference CPU run (default: the full "
+                         "workload if the host has 24 GiB available, else 2^25)")
     raw_argv = list(sys.argv[1:] if argv is None else argv)
     args = ap.parse_args(raw_argv)
     if args.warmup < 3:
