@@ -28,7 +28,10 @@ north_star's multi-GPU claims, measured at the run's N:
             block-sharded, 100 fused axpy->dot steps on ShardedVectors with
             the cross-rank reduction of every step inside the timed region;
             ms/step, the exchange route that ran, and whether r_100 is
-            bit-identical on every rank.
+            bit-identical on every rank;
+  config5_peer  the same over the opt-in in-kernel NVLink exchange (one
+            launch per step), probed first and reported — never raised — if
+            it fails (--no-peer skips it).
 
 --gpus is authoritative: under torchrun WORLD_SIZE must equal it (else exit
 2); without torchrun, --gpus N > 1 re-executes this script under
@@ -434,6 +437,12 @@ def run_gpu(args, world, rank, local):
         sampler.mark()
         multi = {"config4": run_config4(world, rank, dev, peak),
                  "config5": run_config5(world, rank, dev)}
+        if not args.no_peer:
+            if dist.is_initialized():
+                multi["config5_peer"] = run_config5(world, rank, dev, route="peer")
+            else:
+                multi["config5_peer"] = {"route": "peer", "status": "skipped: no process group "
+                                         "(single process without torchrun)"}
         sampler.mark()
         multi["clocks"] = sampler.summary(1)
     sampler.stop()
@@ -559,9 +568,17 @@ def run_config4(world, rank, dev, peak, steps=20, warmup=3):
     }
 
 
-def run_config5(world, rank, dev, iters=100, warmup=3):
+def run_config5(world, rank, dev, iters=100, warmup=3, route="nccl"):
     """BASELINE config 5: 100 fused axpy->dot steps on a global 2^31 f64
-    vector triple, block-sharded, with a cross-rank reduction per step."""
+    vector triple, block-sharded, with a cross-rank reduction per step.
+
+    route "nccl": the default route (16-byte NCCL all-gather + finish kernel).
+    route "peer": the opt-in in-kernel NVLink exchange (SALT_EXCHANGE=peer):
+    the reduction kernel itself trades the per-rank totals over peer memory,
+    ONE launch per step.  It is preceded by a 2-step probe with host results
+    (a timeout raises there) and an all-rank agreement, runs with a 5 s peer
+    timeout, and reports a failure instead of raising, so it can never cost
+    the headline."""
     import torch
     import torch.distributed as dist
 
@@ -569,44 +586,79 @@ def run_config5(world, rank, dev, iters=100, warmup=3):
     from paper_1109_1264_b200 import sharding, synth
     from paper_1109_1264_b200.sharding import shard_bounds
 
+    saved = {k: os.environ.get(k) for k in ("SALT_EXCHANGE", "SALT_PEER_TIMEOUT_MS")}
+    if route == "peer":
+        os.environ["SALT_EXCHANGE"] = "peer"
+        os.environ.setdefault("SALT_PEER_TIMEOUT_MS", "5000")
+
+    def agree(ok):
+        flag = torch.tensor([1 if ok else 0], dtype=torch.int32, device=dev)
+        if world > 1:
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        return int(flag.item()) == 1
+
     n = 1 << 31
     lo, hi = shard_bounds(n, world, rank)
     alpha = synth.scalars(5, 1)[0]
     vecs = []
-    for k in range(3):
-        v = lv.DenseVector.empty(hi - lo, "f64", device=dev)
-        synth.fill_device_philox(v.tensor, 5, k, lo)
-        vecs.append(lv.ShardedVector(v, n))
-    X, Y, Z = vecs
-    torch.cuda.synchronize(dev)
-    out = {}
+    try:
+        for k in range(3):
+            v = lv.DenseVector.empty(hi - lo, "f64", device=dev)
+            synth.fill_device_philox(v.tensor, 5, k, lo)
+            vecs.append(lv.ShardedVector(v, n))
+        X, Y, Z = vecs
+        torch.cuda.synchronize(dev)
+        if route == "peer":
+            err = None
+            try:  # probe: host results check the exchange's error word every step
+                for _ in range(2):
+                    lv.axpy_dot(0.0, X, Y, Z)
+            except RuntimeError as exc:
+                err = str(exc)[:300]
+            if not agree(err is None):
+                return {"route": "peer", "status": "failed in the probe", "error": err}
+        out = {}
 
-    def step(warm):
-        # warm-up steps use alpha = 0: y + 0*x == y bit for bit, so the timed
-        # 100 iterations start from the generated y
-        out["r"] = lv.axpy_dot(0.0 if warm else alpha, X, Y, Z, lazy=True)
+        def step(warm):
+            # warm-up steps use alpha = 0: y + 0*x == y bit for bit, so the
+            # timed 100 iterations start from the generated y
+            out["r"] = lv.axpy_dot(0.0 if warm else alpha, X, Y, Z, lazy=True)
 
-    ms, launches = _timed_region(world, dev, step, iters, warmup)
-    r100 = float(out["r"].item())
-    bits = torch.tensor([np.float64(r100).view(np.int64)], dtype=torch.int64, device=dev)
-    same = True
-    if world > 1:
-        allb = [torch.empty_like(bits) for _ in range(world)]
-        dist.all_gather(allb, bits)
-        same = all(int(b.item()) == int(bits.item()) for b in allb)
-    route = sharding.exchange_route()
-    peer = any(x is not None for x in sharding._exchanges.values())
+        ms, launches = _timed_region(world, dev, step, iters, warmup)
+        err = None
+        try:
+            r100 = float(out["r"].item())  # a peer timeout raises here (DeviceScalar guard)
+        except RuntimeError as exc:
+            err, r100 = str(exc)[:300], float("nan")
+        if not agree(err is None):
+            return {"route": route, "status": "failed", "error": err}
+        bits = torch.tensor([np.float64(r100).view(np.int64)], dtype=torch.int64, device=dev)
+        same = True
+        if world > 1:
+            allb = [torch.empty_like(bits) for _ in range(world)]
+            dist.all_gather(allb, bits)
+            same = all(int(b.item()) == int(bits.item()) for b in allb)
+        peer = route == "peer" and any(x is not None for x in sharding._exchanges.values())
+    finally:
+        X = Y = Z = None  # noqa: F841 (drop the 48 GiB before the next block)
+        vecs.clear()
+        torch.cuda.empty_cache()
+        for k, v in saved.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
     nbytes = 32.0 * n  # x, y, z read + y written, f64, global
-    del vecs, X, Y, Z
-    torch.cuda.empty_cache()
     return {
         "workload": "config5: y = alpha*x + y; r = dot(y, z), f64, n = 2^31 GLOBAL, block-sharded, "
                     "100 fused axpy->dot steps (lv.axpy_dot on ShardedVectors, lazy results)",
         "scaling": "strong",
-        "collective": ("in-kernel NVLink peer exchange" if peer else
+        "collective": ("in-kernel NVLink peer exchange (one launch per step)" if peer else
                        "NCCL all-gather of per-rank double-double partials + salt_reduce_finish")
                       + " per step, inside the timed region",
-        "exchange_route": "peer" if peer else route,
+        "exchange_route": "peer" if peer else "nccl",
+        "status": "ok" if route != "peer" or peer else "peer unavailable (no process group or "
+                                                        "symmetric memory): ran the NCCL route",
         "n_global": n, "iterations": iters, "warmup": warmup,
         "ms_per_step": round(ms / iters, 5),
         "value": round(nbytes * iters / (ms / 1e3) / 1e9, 3), "unit": "GB/s",
@@ -648,6 +700,8 @@ def main(argv=None):
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-multi", action="store_true",
                     help="skip the config-4 / config-5 multi-GPU block")
+    ap.add_argument("--no-peer", action="store_true",
+                    help="skip config 5 over the opt-in in-kernel NVLink exchange")
     ap.add_argument("--n-sample", type=int, default=None,
                     help="elements per step of the --impl reference CPU run (default: the full "
                          "workload if the host has 24 GiB available, else 2^25)")
