@@ -402,11 +402,22 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
 // rank can only reach epoch e+2 after every rank has published e+1, which
 // each does only after finishing its epoch-e reads, so a slot is never
 // overwritten while it is still being read.
-__device__ DD exchange_dd(DD mine, const Xchg& x) {
+// A rank that gives up (timeout, or poisoned by an earlier one) raises the
+// ABORT flag at every peer, so the others stop waiting for it at once —
+// they return NaN and poison themselves too — instead of each timing out.
+constexpr unsigned long long kXchgAbort = ~0ull;
+
+__device__ DD exchange_abort(const Xchg& x) {
   DD nan; nan.hi = __longlong_as_double(0x7ff8000000000000ll); nan.lo = 0.0;
-  // A previous exchange of this rank timed out: the protocol's epochs are
-  // out of step, so touch no slot (a late peer may have reused it) — NaN.
-  if (x.error && *(volatile unsigned int*)x.error) return nan;
+  if (x.error) *(volatile unsigned int*)x.error = 1u;
+  for (int p = 0; p < x.world; ++p) st_release_sys(x.flags[p] + x.rank, kXchgAbort);
+  return nan;
+}
+
+__device__ DD exchange_dd(DD mine, const Xchg& x) {
+  // A previous exchange of this rank failed: the protocol's epochs are out
+  // of step, so touch no slot (a late peer may have reused it) — NaN.
+  if (x.error && *(volatile unsigned int*)x.error) return exchange_abort(x);
   const int par = (int)(x.epoch & 1ull);
   for (int p = 0; p < x.world; ++p) {
     volatile DD* dst = (volatile DD*)(x.slots[p] + par * XCHG_MAX_RANKS + x.rank);
@@ -418,11 +429,11 @@ __device__ DD exchange_dd(DD mine, const Xchg& x) {
   DD acc; acc.hi = 0.0; acc.lo = 0.0;
   const unsigned long long t0 = x.timeout_ns ? globaltimer_ns() : 0ull;
   for (int q = 0; q < x.world; ++q) {
-    while (ld_acquire_sys(x.flags[x.rank] + q) < x.epoch) {
-      if (x.timeout_ns && globaltimer_ns() - t0 > x.timeout_ns) {
-        if (x.error) *x.error = 1u;
-        return nan;  // the peer never arrived
-      }
+    for (;;) {
+      const unsigned long long f = ld_acquire_sys(x.flags[x.rank] + q);
+      if (f == kXchgAbort) return exchange_abort(x);  // a peer gave up
+      if (f >= x.epoch) break;
+      if (x.timeout_ns && globaltimer_ns() - t0 > x.timeout_ns) return exchange_abort(x);
     }
     volatile DD* src = (volatile DD*)(x.slots[x.rank] + par * XCHG_MAX_RANKS + q);
     DD v;

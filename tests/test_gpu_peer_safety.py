@@ -106,8 +106,28 @@ def test_device_poison_returns_at_once(monkeypatch, sharded_pair):
     with pytest.raises(RuntimeError):
         lv.dot(X, Y)
     assert time.perf_counter() - t0 < 5.0
-    # slots untouched (rank 0 publishes nothing once poisoned)
-    assert int(fake.buffer.abs().sum().item()) == 0
+    # no slot touched (rank 0 publishes no total once poisoned); its flag at
+    # every peer carries ABORT instead, so the peers stop waiting for it
+    words = fake.buffer.view(2, -1)  # [rank buffer][int64 words]
+    nslot = 2 * _native.XCHG_MAX_RANKS * 2
+    assert int(words[:, :nslot].abs().sum().item()) == 0
+    assert int(words[0, nslot + 0].item()) == -1 and int(words[1, nslot + 0].item()) == -1
+
+
+def test_a_peer_abort_ends_the_wait_at_once(monkeypatch, sharded_pair):
+    """Rank 1 gave up (its ABORT flag is set in rank 0's buffer): rank 0
+    returns NaN and raises at once instead of waiting out a 60 s timeout."""
+    X, Y, _, _ = sharded_pair
+    fake = LocalPeerExchange(timeout_ns=60_000_000_000)
+    flags = fake.buffer[2 * _native.XCHG_MAX_RANKS * 2:]
+    flags[1] = -1  # ~0: ABORT from rank 1
+    torch.cuda.synchronize()
+    monkeypatch.setattr(sharding, "peer_exchange", lambda group, device: fake)
+    t0 = time.perf_counter()
+    with pytest.raises(RuntimeError, match="peer exchange"):
+        lv.dot(X, Y)
+    assert time.perf_counter() - t0 < 5.0
+    assert int(fake.error.item()) == 1
 
 
 def test_peer_route_bits_match_the_allgather_route(monkeypatch, sharded_pair):
