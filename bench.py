@@ -183,7 +183,9 @@ def _dist_setup():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1 and not dist.is_initialized():
+    if "WORLD_SIZE" in os.environ and not dist.is_initialized():
+        # under torchrun (even at N = 1): a process group, so the sharded
+        # paths run their real collectives (config5 / config5_peer)
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     elif torch.cuda.is_available():
