@@ -158,7 +158,11 @@ int salt_reduce_finish(int dtype, const void* partials_dev, int count, int flags
  * one per exchange, identically on every rank.  The reduction kernel's last
  * CTA publishes this rank's total to every peer, waits for all of them and
  * folds them in rank order — the collective runs inside the reduction
- * kernel, with no NCCL call.  On timeout the result is NaN and *error = 1. */
+ * kernel, with no NCCL call.  On timeout the result is NaN, *error = 1 and
+ * the rank stores ABORT (~0) into its flag at every peer, which makes the
+ * peers give up at once too; a rank whose *error is already set touches no
+ * slot and aborts immediately (the error word is sticky: recreate the
+ * buffers to recover).  Callers must check *error when a result is NaN. */
 #define SALT_XCHG_MAX_RANKS 8
 #define SALT_XCHG_BUFFER_BYTES 512
 typedef struct salt_exchange {
