@@ -264,6 +264,20 @@ int salt_group_fused(void* group, int dtype, const char* assign_sigs, const char
                      const int64_t* ns, int flags, void* const* ws, size_t ws_bytes,
                      void* const* out_dev, void* const* streams);
 int salt_group_issue_times(void* group, int64_t* start_ns, int64_t* end_ns);
+/* salt_group_fused with the reduction's total exchanged IN-KERNEL between the
+ * members over peer memory (salt_fused_exchange per member): exchanges[i] is
+ * member i's descriptor (rank i of world G; its slots / flags point at every
+ * member's buffer, reachable after salt_enable_peer_access).  Every member
+ * ends with the same total in out_dev[i] — one launch per device, no NCCL. */
+int salt_group_fused_exchange(void* group, int dtype, const char* assign_sigs, const char* reduce_sig,
+                              void* const* dsts, int ndst, const void* const* leaves, int nleaves,
+                              const double* scalars, int nscalars, const void* const* pscalars,
+                              int npscalars, const int64_t* ns, int flags, void* const* ws,
+                              size_t ws_bytes, const salt_exchange* exchanges, void* const* out_dev,
+                              void* const* streams);
+/* cudaDeviceEnablePeerAccess between every pair of the G devices (already
+ * enabled pairs are fine); SALT_ECUDA if a pair cannot reach each other. */
+int salt_enable_peer_access(int G, const int* devices);
 
 /* Batched assignments: `count` independent evaluations of ONE tree shape
  * `sig` (single root, no device scalars) over different vectors, scalars

@@ -68,6 +68,8 @@ HEADER_SYMBOLS = (
     "salt_group_size",
     "salt_group_fused",
     "salt_group_issue_times",
+    "salt_group_fused_exchange",
+    "salt_enable_peer_access",
     "salt_signature_kind",
     "salt_prepare",
     "salt_set_force_jit",
@@ -166,6 +168,12 @@ _SIGNATURES = {
          _c_vp, _c_int, _c_vpp, _c_size, _c_vpp, _c_vpp],
     ),
     "salt_group_issue_times": (_c_int, [_c_vp, _c_vp, _c_vp]),
+    "salt_group_fused_exchange": (
+        _c_int,
+        [_c_vp, _c_int, _c_str, _c_str, _c_vpp, _c_int, _c_vpp, _c_int, _c_dp, _c_int, _c_vpp, _c_int,
+         _c_vp, _c_int, _c_vpp, _c_size, _c_vp, _c_vpp, _c_vpp],
+    ),
+    "salt_enable_peer_access": (_c_int, [_c_int, _c_vp]),
     "salt_signature_kind": (_c_int, [_c_int, _c_str, _c_str, _c_int]),
     "salt_prepare": (_c_int, [_c_int, _c_str, _c_str, _c_int]),
     "salt_set_force_jit": (None, [_c_int]),

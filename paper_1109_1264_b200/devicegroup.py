@@ -47,10 +47,23 @@ __all__ = ["DeviceGroup"]
 
 
 class DeviceGroup:
-    """G CUDA devices of this process and their NCCL communicators."""
+    """G CUDA devices of this process and their NCCL communicators.
 
-    def __init__(self, devices=None):
+    exchange="nccl" (default): a reduction's per-device partials are
+    combined by salt_allreduce_sum (NCCL all-gathers + a finish kernel).
+    exchange="peer": peer access is enabled between the devices and the
+    reduction kernel of every device trades its total with the others over
+    peer memory INSIDE the kernel (salt_group_fused_exchange) — one launch
+    per device and no NCCL call; same bits (the same rank-order fold).  A
+    device that does not arrive within `peer_timeout_ms` makes the results
+    NaN, and the call (or DeviceScalar.item()) raises."""
+
+    def __init__(self, devices=None, exchange: str = "nccl", peer_timeout_ms: float = 60_000):
         _require_cuda()
+        if exchange not in ("nccl", "peer"):
+            raise ValueError(f"exchange must be 'nccl' or 'peer', got {exchange!r}")
+        self.exchange = exchange
+        self._peer = None
         if devices is None:
             devices = list(range(torch.cuda.device_count()))
         devices = [int(d) for d in devices]
@@ -68,6 +81,9 @@ class DeviceGroup:
         self._comms = (ctypes.c_void_p * self.size)()
         _native.check(_native.lib().salt_nccl_comm_init_all(self.size, ctypes.addressof(devs),
                                                             ctypes.addressof(self._comms)))
+        if exchange == "peer":
+            _native.check(_native.lib().salt_enable_peer_access(self.size, ctypes.addressof(devs)))
+            self._peer = _PeerBuffers(self.devices, peer_timeout_ms)
 
     def close(self) -> None:
         if self._comms is not None:
@@ -86,11 +102,13 @@ class DeviceGroup:
                                                            ctypes.addressof(en)))
         return list(zip(st, en))
 
-    def _issue(self, code, asig, rsig, members, flags):
+    def _issue(self, code, asig, rsig, members, flags, exchange=False):
         """members[g] = (dst ptrs, leaf ptrs, scalars, pscalar ptrs, n, ws, out ptr, stream):
         one salt_fused per device, all issued at once when the scalars agree
-        (the signature is the caller's, shared by construction)."""
+        (the signature is the caller's, shared by construction).  exchange:
+        the totals are traded in-kernel over peer memory (next epoch)."""
         lib = _native.lib()
+        descs = self._peer.next() if exchange else None
         scal0 = members[0][2]
         if all(m[2] == scal0 for m in members):
             nd, nl, npq = len(members[0][0]), len(members[0][1]), len(members[0][3])
@@ -106,20 +124,28 @@ class DeviceGroup:
             wss = arr([m[5] for m in members])
             outs = arr([m[6] for m in members])
             strs = arr([m[7] for m in members])
-            _native.check(lib.salt_group_fused(
+            _native.check(lib.salt_group_fused_exchange(
                 self._group, code, asig.encode() if asig else None, rsig.encode() if rsig else None,
                 dsts, nd, leaves, nl, scal, len(scal0), psc, npq, ns, flags, wss,
-                lib.salt_reduce_workspace_bytes() if rsig else 0, outs, strs))
+                lib.salt_reduce_workspace_bytes() if rsig else 0,
+                ctypes.addressof(descs) if descs is not None else None, outs, strs))
             return
         for g, (dst, lv_, sc, pq, n, ws, out, stream) in enumerate(members):
             keep = [_native.ptr_array(dst), _native.ptr_array(lv_), _native.double_array(sc),
                     _native.ptr_array(pq)]
+            wsb = lib.salt_reduce_workspace_bytes() if rsig else 0
+            a = asig.encode() if asig else None
+            r = rsig.encode() if rsig else None
             with _OnDevice(self.devices[g]):
-                _native.check(lib.salt_fused(code, asig.encode() if asig else None,
-                                             rsig.encode() if rsig else None, keep[0][0], len(dst),
-                                             keep[1][0], len(lv_), keep[2][0], len(sc), keep[3][0],
-                                             len(pq), n, flags, ws, lib.salt_reduce_workspace_bytes()
-                                             if rsig else 0, out, None, stream))
+                if descs is not None:  # launches are asynchronous: issuing in turn cannot deadlock
+                    _native.check(lib.salt_fused_exchange_prog(
+                        code, a, r, keep[0][0], len(dst), keep[1][0], len(lv_), keep[2][0], len(sc),
+                        keep[3][0], len(pq), None, n, flags, ws, wsb, ctypes.addressof(descs[g]), out,
+                        None, stream))
+                else:
+                    _native.check(lib.salt_fused(code, a, r, keep[0][0], len(dst), keep[1][0], len(lv_),
+                                                 keep[2][0], len(sc), keep[3][0], len(pq), n, flags, ws,
+                                                 wsb, out, None, stream))
 
     def __enter__(self):
         return self
@@ -231,6 +257,9 @@ class DeviceGroup:
             streams.append(stream)
         if len(sigs) != 1:
             raise ValueError(f"every device's summand must have the same tree shape, got {sorted(sigs)}")
+        if self._peer is not None:
+            self._issue(code, None, sigs.pop(), members, _native.SALT_SQRT if sqrt else 0, exchange=True)
+            return self._peer_results(parts, dt, lazy)
         self._issue(code, None, sigs.pop(), members, _native.SALT_PARTIAL)
         return self._allreduce(parts, streams, dt, _native.SALT_SQRT if sqrt else 0, lazy)
 
@@ -282,6 +311,9 @@ class DeviceGroup:
             raise TypeError("all devices' statements must have one element type")
         if len(sigs) != 1:
             raise ValueError(f"every device's statements must have the same tree shape, got {sorted(sigs)}")
+        if self._peer is not None:
+            self._issue(_dtype_code(next(iter(dts))), *sigs.pop(), members, 0, exchange=True)
+            return self._peer_results(parts, dts.pop(), lazy)
         self._issue(_dtype_code(next(iter(dts))), *sigs.pop(), members, _native.SALT_PARTIAL)
         return self._allreduce(parts, streams, dts.pop(), 0, lazy)
 
@@ -300,8 +332,59 @@ class DeviceGroup:
         scalars = [DeviceScalar(p.view(torch.float32)[:1] if dt.itemsize == 4 else p[:1], dt) for p in parts]
         return scalars if lazy else scalars[0].item()
 
+    def _peer_results(self, outs, dt, lazy):
+        """Per-device totals written by the exchanging kernels (the same bits
+        on every device); NaN + a set error word on any device raises."""
+        scalars = [DeviceScalar(p.view(torch.float32)[:1] if dt.itemsize == 4 else p[:1], dt,
+                                guard=self._peer.check) for p in outs]
+        return scalars if lazy else scalars[0].item()
+
     def dot(self, xs, ys, **kw):
         return self.reduce([x * y for x, y in zip(xs, ys)], **kw)
 
     def norm2(self, xs, **kw):
         return self.reduce([x * x for x in xs], sqrt=True, **kw)
+
+
+class _PeerBuffers:
+    """One 512-byte exchange buffer + error word per device (plain device
+    memory: in one process, a device reaches the others' buffers over peer
+    access), and the G descriptors of the in-kernel exchange."""
+
+    def __init__(self, devices, timeout_ms):
+        G = len(devices)
+        self.buffers = [torch.zeros(_native.XCHG_BUFFER_BYTES // 8, dtype=torch.int64,
+                                    device=torch.device("cuda", d)) for d in devices]
+        self.errors = [torch.zeros(1, dtype=torch.int32, device=torch.device("cuda", d)) for d in devices]
+        for d in devices:
+            torch.cuda.synchronize(d)
+        self.descs = (_native.Exchange * G)()
+        for g in range(G):
+            x = self.descs[g]
+            x.rank, x.world = g, G
+            x.timeout_ns = int(timeout_ms * 1e6)
+            x.error = self.errors[g].data_ptr()
+            for p in range(G):
+                base = self.buffers[p].data_ptr()
+                x.slots[p] = base
+                x.flags[p] = base + 2 * _native.XCHG_MAX_RANKS * 16
+        self.epoch = 0
+        self.failed = False
+
+    def next(self):
+        if self.failed:
+            raise RuntimeError("the in-kernel peer exchange of this DeviceGroup failed earlier; "
+                               "recreate the group (or use exchange='nccl')")
+        self.epoch += 1
+        for x in self.descs:
+            x.epoch = self.epoch
+        return self.descs
+
+    def check(self, value=None):
+        if value is not None and value == value:
+            return
+        if self.failed or any(int(e.item()) != 0 for e in self.errors):
+            self.failed = True
+            raise RuntimeError("in-kernel peer exchange of a DeviceGroup timed out: a device did not "
+                               "arrive (results are NaN)")
+

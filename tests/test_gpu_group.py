@@ -143,3 +143,75 @@ def test_devicegroup_assign_and_fused_use_the_group():
         assert dg.gather(E).tobytes() == want.tobytes()
         st = dg.issue_times()
         assert len(st) == 1 and st[0][0] <= st[0][1]
+
+
+def _exchange_descs(G, timeout_ns=10_000_000_000):
+    """G in-kernel exchange descriptors whose buffers all live on device 0
+    (members on one GPU: no peer access needed)."""
+    nb = _native.XCHG_BUFFER_BYTES
+    bufs = [torch.zeros(nb // 8, dtype=torch.int64, device="cuda") for _ in range(G)]
+    errs = [torch.zeros(1, dtype=torch.int32, device="cuda") for _ in range(G)]
+    descs = (_native.Exchange * G)()
+    for g in range(G):
+        d = descs[g]
+        d.rank, d.world, d.epoch, d.timeout_ns, d.error = g, G, 1, timeout_ns, errs[g].data_ptr()
+        for p in range(G):
+            d.slots[p] = bufs[p].data_ptr()
+            d.flags[p] = bufs[p].data_ptr() + 2 * _native.XCHG_MAX_RANKS * 16
+    return descs, bufs, errs
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("G", [2, 4])
+def test_group_in_kernel_exchange_between_concurrent_kernels(G):
+    """G members on ONE GPU, each a dot over its own block, trading their
+    totals inside the reduction kernels (two concurrently running kernels
+    waiting on each other's flags): every member ends with the same bits,
+    the rank-order fold of the members' partials, for 3 consecutive epochs."""
+    lib = _native.lib()
+    n = (1 << 22) + 5
+    rng = np.random.default_rng([21, G])
+    xs = [rng.standard_normal(n) for _ in range(G)]
+    ys = [rng.standard_normal(n) for _ in range(G)]
+    X = [torch.from_numpy(v).cuda() for v in xs]
+    Y = [torch.from_numpy(v).cuda() for v in ys]
+    streams = [torch.cuda.Stream() for _ in range(G)]
+    wsb = lib.salt_reduce_workspace_bytes()
+    ws = [torch.zeros(wsb + 256, dtype=torch.uint8, device="cuda") for _ in range(G)]
+    outs = [torch.zeros(2, dtype=torch.float64, device="cuda") for _ in range(G)]
+    descs, bufs, errs = _exchange_descs(G)
+    grp = _group(G)
+    try:
+        leaves, k1 = _native.ptr_array([t.data_ptr() for g in range(G) for t in (X[g], Y[g])])
+        sc, k2 = _native.double_array([])
+        nn, k3 = _native.i64_array([n] * G)
+        wss, k4 = _native.ptr_array([w.data_ptr() for w in ws])
+        ops, k5 = _native.ptr_array([o.data_ptr() for o in outs])
+        strs, k6 = _native.ptr_array([s.cuda_stream for s in streams])
+        for epoch in (1, 2, 3):
+            for d in descs:
+                d.epoch = epoch
+            _native.check(lib.salt_group_fused_exchange(grp, _native.SALT_F64, None, b"L0 L1 *", None, 0, leaves,
+                                                        2, sc, 0, None, 0, nn, 0, wss, wsb,
+                                                        ctypes.addressof(descs), ops, strs))
+            torch.cuda.synchronize()
+            vals = [o[0].item() for o in outs]
+            assert all(np.float64(v).tobytes() == np.float64(vals[0]).tobytes() for v in vals)
+            ex = restate.exact_sum(np.concatenate([x * y for x, y in zip(xs, ys)]))
+            assert abs(vals[0] - ex) <= 1e-12 * abs(ex)
+        assert all(int(e.item()) == 0 for e in errs)
+    finally:
+        _native.check(lib.salt_group_destroy(grp))
+
+
+def test_devicegroup_peer_exchange_matches_the_nccl_route():
+    n = 300_001
+    rng = np.random.default_rng(31)
+    x, y, z = (rng.standard_normal(n) for _ in range(3))
+    res = {}
+    for ex in ("nccl", "peer"):
+        with lv.DeviceGroup([0], exchange=ex) as dg:
+            X, Y, Z = dg.scatter(x, "f64"), dg.scatter(y, "f64"), dg.scatter(z, "f64")
+            res[ex] = (dg.dot(X, Y), dg.norm2(Z), dg.axpy_dot(0.5, X, Y, Z),
+                       dg.dot(X, Z, lazy=True)[0].item())
+    assert [np.float64(v).tobytes() for v in res["nccl"]] == [np.float64(v).tobytes() for v in res["peer"]]
