@@ -156,6 +156,14 @@ def peer_exchange(group, device):
     key = (id(group), device.index)
     with _exchange_lock:
         if key not in _exchanges:
+            # Agree BEFORE the collective construction (symmetric-memory
+            # rendezvous): every rank must be able to reach every other
+            # rank's device over peer memory and import symmetric memory;
+            # otherwise no rank enters the rendezvous (a rank failing alone
+            # inside it would leave the others waiting).
+            if not _agree(group, device, _peer_capable(group, device)):
+                _exchanges[key] = None
+                return None
             try:
                 xchg = PeerExchange(group, device)
             except Exception:
@@ -165,6 +173,30 @@ def peer_exchange(group, device):
             dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)
             _exchanges[key] = xchg if int(ok.item()) == 1 else None
         return _exchanges[key]
+
+
+def _agree(group, device, ok: bool) -> bool:
+    flag = torch.tensor([1 if ok else 0], dtype=torch.int32, device=device)
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
+    return int(flag.item()) == 1
+
+
+def _peer_capable(group, device) -> bool:
+    """This rank can map every rank's device (all-gathers the device
+    ordinals; same-node ranks) and has torch symmetric memory."""
+    try:
+        import torch.distributed._symmetric_memory  # noqa: F401
+    except Exception:
+        return False
+    world = dist.get_world_size(group)
+    mine = torch.tensor([device.index], dtype=torch.int64, device=device)
+    allv = torch.empty(world, dtype=torch.int64, device=device)
+    dist.all_gather_into_tensor(allv, mine, group=group)
+    try:
+        return all(d == device.index or torch.cuda.can_device_access_peer(device.index, d)
+                   for d in (int(v) for v in allv.tolist()))
+    except Exception:
+        return False
 
 
 def _world(group):
