@@ -2,7 +2,8 @@
 # Refresh the measurement records under profiles/ on the B200 box.
 #   bash tools/refresh_profiles.sh measure   # bench (both arms), config sweep, API overhead, CG example
 #   bash tools/refresh_profiles.sh ncu       # bench launch list + ncu --set full summaries of the hot kernels
-#   bash tools/refresh_profiles.sh all       # both
+#   bash tools/refresh_profiles.sh reduce    # round 2: config-3 floors vs product, sweeps, launch floor, group skew
+#   bash tools/refresh_profiles.sh all       # everything
 # Outputs in gpurun_out/refresh/ (small files only: .ncu-rep files stay in /tmp
 # on the box and are summarised there by tools/ncu_summary.py).
 set -u
@@ -37,3 +38,13 @@ if [ $MODE = ncu ] || [ $MODE = all ]; then
       --note "ncu --set full of tools/profile_target.py --case $c (one launch after 3 warm-ups)" > /dev/null 2>> $O/status
   done
 fi
+if [ $MODE = reduce ] || [ $MODE = all ]; then
+  # round 2: config 3 product vs bare-read floors in one process (PROBE_SET=final), product sweeps
+  nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -fmad=false -lineinfo -DWITH_SALT -o tools/c3_probe_bin \
+    tools/c3_probe.cu -Lpaper_1109_1264_b200 -lsalt -Xlinker -rpath -Xlinker '$ORIGIN/../paper_1109_1264_b200' > $O/c3_nvcc.log 2>&1
+  PROBE_SET=final PROBE_LG_LO=20 PROBE_LG_HI=28 T 900 tools/c3_probe_bin 15 > $O/c3_final.txt 2>&1; echo "c3 rc=$?" >> $O/status
+  T 600 python tools/reduce_sweep.py > $O/reduce_sweep.jsonl 2> $O/reduce_sweep.err; echo "rsweep rc=$?" >> $O/status
+  T 300 python tools/launch_floor_probe.py > $O/launch_floor.json 2> $O/launch_floor.err; echo "floor rc=$?" >> $O/status
+  T 300 python tools/group_issue_probe.py > $O/group_issue.json 2> $O/group_issue.err; echo "group rc=$?" >> $O/status
+fi
+
