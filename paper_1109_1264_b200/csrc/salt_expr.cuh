@@ -526,7 +526,10 @@ __device__ __forceinline__ DD warp_reduce_dd(DD v) {
 // words of the partial XOR kSlotMask, so zero memory means "not written
 // yet": kSlotMask's words are signalling-NaN patterns, which no arithmetic
 // result (all partials are sums) can be.  Each 8-byte word is written once
-// and read whole, so a reader that sees both words non-zero has the value.
+// and read whole (aligned 64-bit accesses are single-copy atomic; stores and
+// loads of the slots are volatile, i.e. relaxed at system scope, so the
+// slots are never the target of a weak racing access), so a reader that
+// sees both words non-zero has the value.
 // CTA 0's first a.collect_warps warps are the collector: thread t folds
 // slots t, t + C, t + 2C, ... (C = 32 * collect_warps) IN ORDER as they appear,
 // polling up to kCollectBatch of its slots per round trip (volatile loads),
@@ -559,7 +562,7 @@ __device__ __forceinline__ void collect_epilogue(DD mine, const Args<T>& a, DD* 
     if (threadIdx.x == 0) {
       const unsigned long long h = (unsigned long long)__double_as_longlong(part.hi) ^ kSlotMask;
       const unsigned long long l = (unsigned long long)__double_as_longlong(part.lo) ^ kSlotMask;
-      asm volatile("st.global.v2.u64 [%0], {%1,%2};" ::"l"(a.slots + 2 * (blockIdx.x - 1)), "l"(h), "l"(l)
+      asm volatile("st.volatile.global.v2.u64 [%0], {%1,%2};" ::"l"(a.slots + 2 * (blockIdx.x - 1)), "l"(h), "l"(l)
                    : "memory");
     }
     return;
@@ -586,7 +589,7 @@ __device__ __forceinline__ void collect_epilogue(DD mine, const Args<T>& a, DD* 
       p.hi = __longlong_as_double((long long)(h[i] ^ kSlotMask));
       p.lo = __longlong_as_double((long long)(l[i] ^ kSlotMask));
       v = dd_add(v, p);
-      asm volatile("st.global.v2.u64 [%0], {%1,%2};" ::"l"(a.slots + 2 * q), "l"(0ull), "l"(0ull) : "memory");
+      asm volatile("st.volatile.global.v2.u64 [%0], {%1,%2};" ::"l"(a.slots + 2 * q), "l"(0ull), "l"(0ull) : "memory");
       q += C;
     }
   }
