@@ -193,6 +193,16 @@ def _dist_setup():
     return world, rank, local
 
 
+def _cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def _host_threads():
     try:
         return len(os.sched_getaffinity(0))
@@ -323,6 +333,7 @@ def run_reference(args, world, rank):
                 "d2h_bytes_per_step": 0},
     }
     line["cpu_baseline"]["lanevec_1core"] = lanevec_1core()
+    line["cpu_baseline"].update(cpu_model=_cpu_model(), nproc=os.cpu_count())
     print(json.dumps(line), flush=True)
 
 
@@ -457,7 +468,7 @@ def run_gpu(args, world, rank, local):
         cpu = {"value": round(gbs, 3), "unit": "GB/s", "cores": threads, "kind": "port",
                "sample": f"{done} evaluations of the tree on {n_sample} f64 elements "
                          "(oracle/salt_oracle.c, reference per-node tile evaluation)",
-               "lanevec_1core": lanevec_1core()}
+               "lanevec_1core": lanevec_1core(), "cpu_model": _cpu_model(), "nproc": os.cpu_count()}
 
     if rank == 0:
         line = {
