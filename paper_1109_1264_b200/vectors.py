@@ -348,7 +348,10 @@ class DeviceScalar:
         return float(self.dtype.type(other))
 
     def _lazy(self, op, *args):
-        return DeviceScalar(None, self.dtype, _expr=(op,) + args)
+        # a result inherits its operands' guard (a failed collective behind
+        # an operand still raises at .item() of anything computed from it)
+        guard = next((a.guard for a in args if isinstance(a, DeviceScalar) and a.guard is not None), None)
+        return DeviceScalar(None, self.dtype, guard=guard, _expr=(op,) + args)
 
     def __truediv__(self, other):
         if isinstance(other, (DeviceScalar, int, float, np.floating)):

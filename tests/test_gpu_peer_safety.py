@@ -89,6 +89,9 @@ def test_lazy_result_raises_at_item(monkeypatch, sharded_pair):
     fake = LocalPeerExchange(timeout_ns=1_000_000)
     monkeypatch.setattr(sharding, "peer_exchange", lambda group, device: fake)
     r = lv.dot(X, Y, lazy=True)  # no host synchronisation yet
+    derived = (r + 1.0) / 2.0    # lazy scalar arithmetic inherits the guard
+    with pytest.raises(RuntimeError, match="peer exchange"):
+        derived.item()
     with pytest.raises(RuntimeError, match="peer exchange"):
         r.item()
     with pytest.raises(RuntimeError):
