@@ -625,8 +625,8 @@ def _scalar_program(pscalars, host):
     host scalars "S<j>" (appended to `host`), evaluated once per thread in
     the kernel prologue (csrc/salt_expr.cuh load_pscalars)."""
     budget = DeviceScalar.MAX_PROGRAM_OPS
-    if not any(ds.lazy for ds in pscalars):
-        return list(pscalars), host, None
+    if not any(ds.lazy and ds.program_size() <= budget for ds in pscalars):
+        return list(pscalars), host, None  # (an oversized lazy scalar materialises when read)
     for ds in pscalars:
         ds.check_operands()
     raw, raw_ids, toks = [], {}, []
