@@ -152,7 +152,11 @@ int collect_tiles() {
     const char* e = getenv("SALT_COLLECT_TILES");
     return e ? atoi(e) : 0;
   }();
-  return env > 0 ? env : 2;
+  // 1 tile per streaming CTA: the block scheduler refills an SM the moment
+  // a CTA retires, as for assignments (same-box A/B over 1-4 tiles,
+  // profiles/r02_collect_tiles_ab.txt: 1 equal or better for dot / nrm2,
+  // f32 / f64, 2^22-2^27)
+  return env > 0 ? env : 1;
 }
 int collect_warps() {
   static const int env = [] {
