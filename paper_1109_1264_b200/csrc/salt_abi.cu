@@ -776,10 +776,13 @@ int run_fused(Plan& p, void* const* dsts, int ndst, const void* const* leaves, i
     // profiles/r02_c3_probe*.txt: at 2^24 ddot 46.6 -> 42.6 us, sdot 25.7 ->
     // 24.3 us, dnrm2 26.4 -> 25.5 us; the fence + ticket atomic each
     // streaming CTA paid in the two-level combine held its SM slot).
-    // Beyond kCollectCtas streaming CTAs, more tiles per CTA (2^27-2^28
-    // measured equal for 2 and 4 tiles): fewer slots for the collector to
-    // fold, which keeps it far ahead of the streaming CTAs.
-    constexpr i64 kCollectCtas = 32768;
+    // Beyond kCollectCtas streaming CTAs (the slots the workspace holds),
+    // more tiles per CTA: 2 for the f64 2^28 fused multi-leaf trees, the
+    // K round 1 measured best for them (7.26 TB/s, r01_reduce_variants.txt);
+    // a cap of 32,768 (K = 4 there) cost the CG update 2.3 %
+    // (profiles/r02_ncu_cgupdate.txt).  The collector keeps up easily: at
+    // most ~60 slots per microsecond at these sizes.
+    constexpr i64 kCollectCtas = salt::MAX_COLLECT;
     static_assert(kCollectCtas <= salt::MAX_COLLECT, "collector slots");
     K = collect_tiles();
     if ((ntiles + K - 1) / K > kCollectCtas) K = (ntiles + kCollectCtas - 1) / kCollectCtas;
