@@ -10,7 +10,8 @@
 //        -o tools/c3_probe tools/c3_probe.cu && tools/c3_probe
 // PROBE_SET=final with -DWITH_SALT (link -Lpaper_1109_1264_b200 -lsalt):
 // the bare-read floors next to the PRODUCT (salt_reduce through the C ABI),
-// same process, same sweeps, same timing.
+// same process, same sweeps, same timing.  PROBE_PDL=1 launches the floor
+// kernels with programmatic dependent launch, like the product's.
 //
 // Every variant computes the same compensated double-double sum as the
 // product (TwoSum per f64 term / exact f64 sum of f32 terms) and is checked
@@ -145,6 +146,7 @@ __device__ __forceinline__ unsigned nclusters_x() {
 
 template <class T, int NL, int UNR, int ILP, int CL>
 __global__ void __launch_bounds__(BLOCK) red_kernel(Args a) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // a no-op unless launched with PDL (PROBE_PDL=1)
   const T* x = (const T*)a.x;
   const T* y = (const T*)a.y;
   Acc<T> acc[ILP];
@@ -353,6 +355,19 @@ struct Variant { std::string name; int unr; int ilp; int cl; i64 K; int GS; int 
 
 template <class T, int NL, int UNR, int ILP, int CL> void launch(int grid, const Args& a) {
   auto fn = red_kernel<T, NL, UNR, ILP, CL>;
+  static const bool pdl = getenv("PROBE_PDL") && atoi(getenv("PROBE_PDL")) != 0;
+  if (CL == 0 && pdl) {  // programmatic dependent launch, as the product's kernels are launched
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(BLOCK);
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&cfg, fn, a));
+    return;
+  }
   if (CL == 0) { fn<<<grid, BLOCK>>>(a); return; }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
