@@ -30,8 +30,10 @@ north_star's multi-GPU claims, measured at the run's N:
             ms/step, the exchange route that ran, and whether r_100 is
             bit-identical on every rank;
   config5_peer  the same over the opt-in in-kernel NVLink exchange (one
-            launch per step), probed first and reported — never raised — if
-            it fails (--no-peer skips it).
+            launch per step), in a child process per rank with its own
+            process group and a time limit, so a fault or hang there cannot
+            cost the line; probed first and reported — never raised — if it
+            fails (--no-peer skips it).
 
 --gpus is authoritative: under torchrun WORLD_SIZE must equal it (else exit
 2); without torchrun, --gpus N > 1 re-executes this script under
@@ -452,7 +454,7 @@ def run_gpu(args, world, rank, local):
                  "config5": run_config5(world, rank, dev)}
         if not args.no_peer:
             if dist.is_initialized():
-                multi["config5_peer"] = run_config5(world, rank, dev, route="peer")
+                multi["config5_peer"] = run_config5_peer_isolated(world, rank, local, dev)
             else:
                 multi["config5_peer"] = {"route": "peer", "status": "skipped: no process group "
                                          "(single process without torchrun)"}
@@ -683,20 +685,115 @@ def run_config5(world, rank, dev, iters=100, warmup=3, route="nccl"):
     }
 
 
-def _launch_ranks(args, argv):
-    """--gpus N > 1 without torchrun: re-run this script as N ranks."""
+PEER_CHILD_TIMEOUT_S = 300
+
+
+def _child_env(world, rank, local, port):
+    """Environment of a peer-block child: its own env:// rendezvous on
+    `port`.  TORCHELASTIC_* is dropped so the child hosts / joins its own
+    TCP store instead of the torchrun agent's."""
+    env = {k: v for k, v in os.environ.items() if not k.startswith("TORCHELASTIC")}
+    env.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+               WORLD_SIZE=str(world), LOCAL_RANK=str(local), LOCAL_WORLD_SIZE=str(world))
+    return env
+
+
+def run_config5_peer_isolated(world, rank, local, dev, timeout=PEER_CHILD_TIMEOUT_S,
+                              child_flag="--peer-child"):
+    """config5_peer in a child process per rank with its own process group.
+
+    The in-kernel NVLink exchange is opt-in and has not had a multi-GPU run
+    on real hardware, so it must not be able to take the headline down: a
+    device fault there kills the child's CUDA context, not this one, and a
+    hang is bounded by `timeout` (the child's process group is killed).
+    Every rank reports whether its child finished; the block is "ok" only if
+    all did, with rank 0's child line as the numbers.  (`child_flag`
+    --peer-child-selftest runs the same plumbing with a gloo child on CPU,
+    for tests/test_bench_launch.py.)"""
+    import signal
+
+    import torch
+    import torch.distributed as dist
+
+    port = torch.tensor([_free_port() if rank == 0 else 0], dtype=torch.int64, device=dev)
+    if world > 1:
+        dist.broadcast(port, 0)
+    cmd = [sys.executable, str(Path(__file__).resolve()), child_flag, "--gpus", str(world)]
+    t0 = time.perf_counter()
+    proc = subprocess.Popen(cmd, env=_child_env(world, rank, local, int(port.item())),
+                            stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True,
+                            start_new_session=True, cwd=str(ROOT))
+    err = None
+    try:
+        out, errout = proc.communicate(timeout=timeout)
+    except subprocess.TimeoutExpired:
+        os.killpg(proc.pid, signal.SIGKILL)
+        out, errout = proc.communicate()
+        err = f"child timed out after {timeout} s (killed)"
+    res = None
+    if err is None:
+        lines = [ln for ln in out.splitlines() if ln.startswith("{")]
+        if proc.returncode == 0 and lines:
+            res = json.loads(lines[-1])
+        else:
+            err = f"child exited {proc.returncode}: {(errout or '').strip()[-300:]}"
+    ok = torch.tensor([1 if res is not None else 0], dtype=torch.int32, device=dev)
+    if world > 1:
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+    wall = round(time.perf_counter() - t0, 2)
+    if res is None:
+        return {"route": "peer", "status": "failed", "error": err,
+                "isolation": "child process per rank, own process group", "child_wall_s": wall}
+    if int(ok.item()) != 1:
+        res = {"route": "peer", "status": "failed on another rank", "rank0_child": res}
+    res["isolation"] = "child process per rank, own process group"
+    res["child_wall_s"] = wall
+    return res
+
+
+def _run_peer_child(selftest=False):
+    """Entry of the child: config 5 over the peer route, one JSON line from
+    every rank (the parent reads its own child's).  selftest: a gloo process
+    group and one all_reduce, no GPU (the plumbing test)."""
+    import torch
+    import torch.distributed as dist
+
+    if selftest:
+        dist.init_process_group("gloo")
+        t = torch.ones(1)
+        dist.all_reduce(t)
+        if os.environ.get("SALT_BENCH_SELFTEST_HANG") == os.environ["RANK"]:
+            time.sleep(3600)
+        res = {"route": "selftest", "status": "ok", "rank": dist.get_rank(),
+               "world": dist.get_world_size(), "sum": float(t.item()),
+               "torchelastic_env": sorted(k for k in os.environ if k.startswith("TORCHELASTIC"))}
+    else:
+        world, rank, local = _dist_setup()
+        res = run_config5(world, rank, torch.device("cuda", local), route="peer")
+    print(json.dumps(res), flush=True)
+    if dist.is_initialized():
+        dist.destroy_process_group()
+
+
+def _free_port():
     import socket
 
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _launch_ranks(args, argv):
+    """--gpus N > 1 without torchrun: re-run this script as N ranks."""
     import torch
 
     have = torch.cuda.device_count()
     if have < args.gpus:
         print(f"bench.py: --gpus {args.gpus} but this host has {have} GPU(s)", file=sys.stderr)
         sys.exit(2)
-    s = socket.socket()
-    s.bind(("127.0.0.1", 0))
-    port = s.getsockname()[1]
-    s.close()
+    port = _free_port()
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
            "--master-addr=127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve())] + list(argv)
     sys.exit(subprocess.run(cmd).returncode)
@@ -715,6 +812,8 @@ def main(argv=None):
                     help="skip the config-4 / config-5 multi-GPU block")
     ap.add_argument("--no-peer", action="store_true",
                     help="skip config 5 over the opt-in in-kernel NVLink exchange")
+    ap.add_argument("--peer-child", action="store_true", help=argparse.SUPPRESS)
+    ap.add_argument("--peer-child-selftest", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--n-sample", type=int, default=None,
                     help="elements per step of the --impl reference CPU run (default: the full "
                          "workload if the host has 24 GiB available, else 2^25)")
@@ -730,6 +829,9 @@ def main(argv=None):
               f"{os.environ['WORLD_SIZE']} ranks", file=sys.stderr)
         sys.exit(2)
     _ensure_built()
+    if args.peer_child or args.peer_child_selftest:
+        _run_peer_child(selftest=args.peer_child_selftest)
+        return
     if args.impl == "salt" and not under_torchrun and args.gpus > 1:
         _launch_ranks(args, raw_argv)
     if args.impl == "reference":

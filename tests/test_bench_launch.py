@@ -83,3 +83,51 @@ def test_reference_arm_two_ranks_one_line():
     assert len(lines) == 1
     d = json.loads(lines[0])
     assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
+
+
+ISOLATED_DRIVER = r"""
+import json, os, sys
+sys.path.insert(0, sys.argv[1])
+import torch, torch.distributed as dist
+import bench
+dist.init_process_group("gloo")
+r = bench.run_config5_peer_isolated(dist.get_world_size(), dist.get_rank(), int(os.environ["LOCAL_RANK"]),
+                                    torch.device("cpu"), timeout=float(sys.argv[2]),
+                                    child_flag="--peer-child-selftest")
+if dist.get_rank() == 0:
+    print(json.dumps(r), flush=True)
+dist.destroy_process_group()
+"""
+
+
+def _isolated(tmp_path, timeout, hang_rank=None):
+    drv = tmp_path / "drv.py"
+    drv.write_text(ISOLATED_DRIVER)
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    if hang_rank is not None:
+        env["SALT_BENCH_SELFTEST_HANG"] = str(hang_rank)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", str(drv), str(ROOT), str(timeout)]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.strip().startswith("{")]
+    assert len(lines) == 1, r.stdout
+    return json.loads(lines[0])
+
+
+def test_peer_block_child_has_its_own_process_group(tmp_path):
+    """config5_peer runs in a child per rank with its own rendezvous (a port
+    broadcast from rank 0, no torchrun agent store): the 2 children form a
+    world-2 group of their own."""
+    d = _isolated(tmp_path, 240)
+    assert d["status"] == "ok" and d["world"] == 2 and d["rank"] == 0 and d["sum"] == 2.0
+    assert d["torchelastic_env"] == [] and d["isolation"].startswith("child process")
+
+
+def test_peer_block_child_hang_is_bounded(tmp_path):
+    """A child that never returns is killed after the time limit and the
+    block reports the failure on every rank; the parent job still exits 0
+    and prints its line."""
+    d = _isolated(tmp_path, 20, hang_rank=1)
+    assert d["status"] == "failed on another rank"
+    assert d["rank0_child"]["status"] == "ok"
