@@ -64,8 +64,11 @@ def test_assign_trace_is_a_load_burst_then_ops_in_slot_order():
     assert [e.slot for e in ref_body[:unr]] == [e.slot for e in body[:unr]]
 
 
-def test_reduction_trace_walks_its_tiles_then_joins_the_combine():
-    n = 1 << 20                           # collector combine: 2 tiles per streaming CTA
+@pytest.mark.parametrize("n,ntiles", [
+    (1 << 20, 1),                 # collector combine: one tile per streaming CTA
+    ((1 << 27) + 4 * BLOCK * V64, 2),  # > 65,536 streaming CTAs (MAX_COLLECT): 2 tiles each
+])
+def test_reduction_trace_walks_its_tiles_then_joins_the_combine(n, ntiles):
     g = np.random.default_rng(2)
     x, y = g.standard_normal(n), g.standard_normal(n)
     X, Y = dev(x), dev(y)
@@ -73,7 +76,7 @@ def test_reduction_trace_walks_its_tiles_then_joins_the_combine():
     ev = tr.events
     assert ev[-1].kind == "reduction"
     ts = tiles(ev)
-    assert len(ts) == 2
+    assert len(ts) == ntiles
     unr = sum(1 for e in ts[0] if e.kind == "load")
     per_tile = BLOCK * unr * V64
     for t, tile in enumerate(ts):
