@@ -53,6 +53,7 @@ namespace {
 using salt::i64;
 
 constexpr int kBlock = 256;
+constexpr int kInterpSmemCap = 216 * 1024;  // dynamic shared memory of the interpreter kernel (27 slots)
 static_assert(SALT_WORKSPACE_TICKET_BYTES == salt::WsLayout::group_partials,
               "salt.h ticket prefix must match the kernel workspace layout");
 // 256-bit vectors in flight per leaf per thread.  2 for assignments; 4 for
@@ -158,12 +159,22 @@ int collect_tiles() {
   // f32 / f64, 2^22-2^27)
   return env > 0 ? env : 1;
 }
-int collect_warps() {
+// Collector warps for a grid of `nstream` streaming CTAs (a function of n
+// only, so the fold order — and the bits — still depend only on n).  The
+// collector must retire slots as fast as the streaming CTAs fill them: f32
+// nrm2 at 2^28 completes ~220 slots per microsecond, and two warps x 4 slots
+// per L2 round trip fell behind there once the cheap epilogue shortened the
+// streaming CTAs (168 us against a 147 us floor; four warps: 148 us,
+// profiles/r02_cheap_epilogue.txt).  Below 8,192 streaming CTAs two warps
+// are equal or a little better (fewer warps polling beside the streaming
+// CTAs of that SM).
+int collect_warps(i64 nstream) {
   static const int env = [] {
     const char* e = getenv("SALT_COLLECT_WARPS");
     return e ? atoi(e) : 0;
   }();
-  return env >= 1 && env <= 8 ? env : 2;
+  if (env >= 1 && env <= 8) return env;
+  return nstream >= 8192 ? 4 : 2;
 }
 int collect_min() {
   static const int env = [] {
@@ -493,10 +504,12 @@ std::string encode_prog(const Plan& p, salt::Prog& g) {
     g.reduce = 1;
   }
   g.nl = p.nl;
-  // 8 KiB per slot (32-byte vectors x 256 threads); stay below 224 KiB
-  if (salt::interp_smem_bytes(g, 4, kBlock, 8) > 224 * 1024)
+  // 8 KiB per slot (32-byte vectors x 256 threads); 27 slots + the 4 KiB of
+  // static shared memory the reduction epilogue's CTA fold uses stay below
+  // the 227 KiB a CTA may have
+  if (salt::interp_smem_bytes(g, 4, kBlock, 8) > kInterpSmemCap)
     return "tree needs " + std::to_string(g.nl + g.slots + g.nroots) +
-           " interpreter slots (leaves + stack depth + roots > 28)";
+           " interpreter slots (leaves + stack depth + roots > 27)";
   return "";
 }
 
@@ -817,7 +830,7 @@ int run_fused(Plan& p, void* const* dsts, int ndst, const void* const* leaves, i
   if (collect) g64 += 1;  // CTA 0: the collector
   const int grid = (int)g64;
   a.first = collect ? 1 : 0;
-  a.collect_warps = collect_warps();
+  a.collect_warps = collect_warps(g64 - 1);
   a.tiles_per_cta = K;
   // CTAs per combine group: the whole grid when it was sized as one group
   // (at most 2 x GROUP), else GROUP (a grid of <= GROUP CTAs is one group
@@ -865,7 +878,7 @@ int run_fused(Plan& p, void* const* dsts, int ndst, const void* const* leaves, i
     ia.pg = p.prog;
     const int smem = salt::interp_smem_bytes(p.prog, vec, kBlock, (int)sizeof(T));
     if (!k->smem_limit[dev].load(std::memory_order_acquire)) {  // once per device: the cap
-      SALT_CUDA(cudaFuncSetAttribute(k->aot, cudaFuncAttributeMaxDynamicSharedMemorySize, 224 * 1024));
+      SALT_CUDA(cudaFuncSetAttribute(k->aot, cudaFuncAttributeMaxDynamicSharedMemorySize, kInterpSmemCap));
       k->smem_limit[dev].store(1, std::memory_order_release);
     }
     rc = launch_raw(k, dev, grid, &ia, (size_t)smem, st);

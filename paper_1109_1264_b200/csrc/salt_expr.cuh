@@ -306,21 +306,38 @@ __device__ __forceinline__ void two_sum(double a, double b, double& s, double& e
 // x - x == 0 exactly for finite x; NaN for +-inf and NaN.
 __device__ __forceinline__ bool finite(double x) { return __dsub_rn(x, x) == 0.0; }
 
-// Double-double addition.  Once a sum is not finite (an inf or NaN term, or
-// overflow) the compensation is meaningless (inf - inf = NaN); the plain
-// IEEE sum carries on alone, which is what the reference's element-typed
-// accumulation produces in that case (inf, or NaN for inf + -inf).
+// Double-double accumulation (round 2: the cheap form).  The high words are
+// added exactly (TwoSum: s + e == a.hi + b.hi); the low words and e are
+// summed in plain f64; the pair is NOT renormalised between additions
+// (|lo| stays within a few hundred ulps of hi over any fold in this file, so
+// the low word's own rounding errors are ~2^-96 of the sum).  8 FP64
+// operations with a ONE-add dependency chain through hi, instead of 18 with
+// a 13-deep chain for a renormalising add: at one tile per CTA the CTA
+// epilogue was 40 % of an f64 nrm2's FP64 instructions, and the FP64 pipe
+// (64 lanes / clk / SM) sat at ~70 % beside the loads
+// (profiles/r02_cheap_epilogue.txt).
+// Once a sum is not finite (an inf or NaN term, or overflow) e and lo turn
+// NaN while hi carries the plain IEEE sum on — inf, or NaN for inf + -inf,
+// which is what the reference's element-typed accumulation produces;
+// dd_norm / finish_store drop the meaningless low word at the end.
 __device__ __forceinline__ DD dd_add(DD a, DD b) {
-  double s, e;
-  two_sum(a.hi, b.hi, s, e);
   DD r;
-  if (!finite(s)) {
-    r.hi = s;
+  double e;
+  two_sum(a.hi, b.hi, r.hi, e);
+  r.lo = __dadd_rn(a.lo, __dadd_rn(b.lo, e));
+  return r;
+}
+// Canonical form of a pair: |lo| <= ulp(hi) / 2, or (hi, 0) when hi is not
+// finite.  Applied where a pair leaves the kernel (partial outputs, the
+// cross-rank exchange), so every route folds the same values.
+__device__ __forceinline__ DD dd_norm(DD v) {
+  DD r;
+  if (!finite(v.hi)) {
+    r.hi = v.hi;
     r.lo = 0.0;
     return r;
   }
-  e = __dadd_rn(e, __dadd_rn(a.lo, b.lo));
-  two_sum(s, e, r.hi, r.lo);
+  two_sum(v.hi, v.lo, r.hi, r.lo);
   return r;
 }
 
@@ -337,16 +354,8 @@ template <> struct Acc<double> {
     hi = s;
     lo = __dadd_rn(lo, e);
   }
-  __device__ __forceinline__ DD get() const {
-    DD r;
-    if (!finite(hi)) {  // lo is NaN once hi saw an inf; keep the plain sum
-      r.hi = hi;
-      r.lo = 0.0;
-      return r;
-    }
-    two_sum(hi, lo, r.hi, r.lo);
-    return r;
-  }
+  // not renormalised (dd_add does not need it)
+  __device__ __forceinline__ DD get() const { DD r; r.hi = hi; r.lo = lo; return r; }
 };
 template <> struct Acc<float> {
   double hi = 0.0;
@@ -418,6 +427,7 @@ __device__ DD exchange_dd(DD mine, const Xchg& x) {
   // A previous exchange of this rank failed: the protocol's epochs are out
   // of step, so touch no slot (a late peer may have reused it) — NaN.
   if (x.error && *(volatile unsigned int*)x.error) return exchange_abort(x);
+  mine = dd_norm(mine);  // what finish_store hands the all-gather route
   const int par = (int)(x.epoch & 1ull);
   for (int p = 0; p < x.world; ++p) {
     volatile DD* dst = (volatile DD*)(x.slots[p] + par * XCHG_MAX_RANKS + x.rank);
@@ -444,20 +454,25 @@ __device__ DD exchange_dd(DD mine, const Xchg& x) {
   return acc;
 }
 
+// CTA fold of one pair per thread; `smem` holds BLOCK pairs.  Every thread
+// leaves its pair in shared memory; the first warp's lane l then folds
+// threads l, l + 32, ... in that order and a shuffle tree folds the lanes —
+// a fixed order.  Only ONE warp runs FP64 here: 12 dd_adds per CTA instead
+// of the 8 x 5 + 5 a shuffle tree in every warp costs (the FP64 pipe charges
+// per warp instruction, not per useful lane).
 template <int BLOCK> __device__ __forceinline__ DD block_reduce_dd(DD v, DD* smem) {
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
-    DD o;
-    o.hi = __shfl_xor_sync(0xffffffffu, v.hi, off);
-    o.lo = __shfl_xor_sync(0xffffffffu, v.lo, off);
-    v = dd_add(v, o);
-  }
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (lane == 0) smem[warp] = v;
+  double* const sh = (double*)smem;  // hi[BLOCK], then lo[BLOCK]: conflict-free
+  sh[threadIdx.x] = v.hi;
+  sh[BLOCK + threadIdx.x] = v.lo;
   __syncthreads();
-  if (warp == 0) {
-    DD z; z.hi = 0.0; z.lo = 0.0;
-    v = lane < BLOCK / 32 ? smem[lane] : z;
+  if (threadIdx.x < 32) {
+#pragma unroll
+    for (int w = 1; w < BLOCK / 32; ++w) {
+      DD o;
+      o.hi = sh[threadIdx.x + 32 * w];
+      o.lo = sh[BLOCK + threadIdx.x + 32 * w];
+      v = dd_add(v, o);
+    }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
       DD o;
@@ -608,7 +623,7 @@ __device__ __forceinline__ void collect_epilogue(DD mine, const Args<T>& a, DD* 
 // Round a double-double total to the element type, optional sqrt, store.
 template <class T> __device__ __forceinline__ void finish_store(DD tot, int flags, void* out) {
   if (flags & FLAG_PARTIAL) {
-    *(DD*)out = tot;
+    *(DD*)out = dd_norm(tot);
     return;
   }
   T r = (T)(finite(tot.hi) ? __dadd_rn(tot.hi, tot.lo) : tot.hi);
@@ -649,7 +664,7 @@ __device__ __forceinline__ void reduce_epilogue(DD mine, const Args<T>& a) {
   // the order, so the result depends only on n — not on scheduling, SM
   // count or occupancy.
   static_assert(MAX_ONE_GROUP % BLOCK == 0 && GROUP <= MAX_ONE_GROUP, "group fold layout");
-  __shared__ DD smem[BLOCK / 32];
+  __shared__ DD smem[BLOCK];
   __shared__ int stage;  // 0 done, 1 group finisher, 2 group + final finisher
   if (a.first) {
     collect_epilogue<T, BLOCK>(mine, a, smem);
@@ -1005,7 +1020,7 @@ __global__ void SALT_BOUNDS(BLOCK) batch_reduce_kernel(BatchArgs<T> a, int flags
       }
     }
   }
-  __shared__ DD smem[BLOCK / 32];
+  __shared__ DD smem[BLOCK];
   DD part = block_reduce_dd<BLOCK>(acc.get(), smem);
   if (threadIdx.x == 0) finish_store<T>(part, flags, P.dst);
 }
@@ -1016,7 +1031,7 @@ __global__ void SALT_BOUNDS(BLOCK) batch_reduce_kernel(BatchArgs<T> a, int flags
 // exchange path give identical bits.
 template <class T, int BLOCK>
 __global__ void __launch_bounds__(BLOCK) finish_kernel(const DD* parts, int count, int flags, void* out) {
-  __shared__ DD smem[BLOCK / 32];
+  __shared__ DD smem[BLOCK];
   if (count <= XCHG_MAX_RANKS) {
     if (threadIdx.x == 0) {
       DD v; v.hi = 0.0; v.lo = 0.0;

@@ -248,6 +248,60 @@ __global__ void __launch_bounds__(BLOCK) red_kernel(Args a) {
   if (threadIdx.x == 0) { *a.ticket = 0; *a.out = tot; }
 }
 
+// The product's round-2 "cheap" epilogue on the floor geometry (partials
+// only): pairs are accumulated without renormalising (8 FP64 ops, hi chain
+// of one add) and ONE warp folds the CTA from shared memory, instead of a
+// renormalising shuffle tree in all 8 warps.  Same sum to ~2^-96.
+__device__ __forceinline__ DD dd_acc(DD a, DD b) {
+  DD r; double e;
+  two_sum(a.hi, b.hi, r.hi, e);
+  r.lo = __dadd_rn(a.lo, __dadd_rn(b.lo, e));
+  return r;
+}
+template <class T, int NL, int UNR>
+__global__ void __launch_bounds__(BLOCK) red_cheap(Args a) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const T* x = (const T*)a.x;
+  const T* y = (const T*)a.y;
+  Acc<T> acc;
+  const i64 per = (i64)BLOCK * UNR;
+  const i64 ntiles = (a.nvec + per - 1) / per;
+  const i64 t0 = (i64)blockIdx.x * a.K;
+  const i64 t1 = min(t0 + a.K, ntiles);
+  for (i64 t = t0; t < t1; ++t) {
+    Vec<T> va[UNR], vb[UNR];
+    const i64 base = t * per + threadIdx.x;
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const i64 j = base + (i64)u * BLOCK;
+      if (j < a.nvec) { va[u].load(x + j * Vec<T>::W); if (NL == 2) vb[u].load(y + j * Vec<T>::W); }
+    }
+#pragma unroll
+    for (int u = 0; u < UNR; ++u)
+      if (base + (i64)u * BLOCK < a.nvec) {
+#pragma unroll
+        for (int k = 0; k < Vec<T>::W; ++k) acc.add(mul_rn(va[u].v[k], NL == 1 ? va[u].v[k] : vb[u].v[k]));
+      }
+  }
+  __shared__ double sh[2 * BLOCK];
+  DD v; v.hi = acc.hi; v.lo = 0.0;
+  if constexpr (sizeof(T) == 8) v.lo = acc.lo;
+  sh[threadIdx.x] = v.hi;
+  sh[BLOCK + threadIdx.x] = v.lo;
+  __syncthreads();
+  if (threadIdx.x >= 32) return;
+#pragma unroll
+  for (int w = 1; w < BLOCK / 32; ++w) {
+    DD o; o.hi = sh[threadIdx.x + 32 * w]; o.lo = sh[BLOCK + threadIdx.x + 32 * w];
+    v = dd_acc(v, o);
+  }
+  for (int o = 16; o; o >>= 1) {
+    DD w; w.hi = __shfl_xor_sync(~0u, v.hi, o); w.lo = __shfl_xor_sync(~0u, v.lo, o);
+    v = dd_acc(v, w);
+  }
+  if (threadIdx.x == 0) a.partials[blockIdx.x] = v;
+}
+
 // Collector combine (no fences, no atomics on the streaming CTAs): CTA 0
 // folds; CTAs 1.. stream K tiles each and store their partial XOR-encoded
 // (zero memory = "not written": MASK is a signalling-NaN pattern no
@@ -392,6 +446,12 @@ template <class T, int NL, int UNR> void by_ilp(int ilp, int cl, int grid, const
   else by_cl<T, NL, UNR, 4>(cl, grid, a);
 }
 template <class T, int NL> void dispatch(const Variant& v, int grid, const Args& a) {
+  if (v.combine == 5) {  // floor_cheap: the cheap epilogue, partials only
+    if (v.unr == 4) red_cheap<T, NL, 4><<<grid, BLOCK>>>(a);
+    else if (v.unr == 8) red_cheap<T, NL, 8><<<grid, BLOCK>>>(a);
+    else red_cheap<T, NL, 2><<<grid, BLOCK>>>(a);
+    return;
+  }
   if (v.combine == 3 || v.combine == 4) {
     if (v.combine == 4) {
       if (v.unr == 4) coll_kernel<T, NL, 4, 1><<<grid + 1, BLOCK>>>(a);
@@ -472,6 +532,7 @@ int main(int argc, char** argv) {
         vs.push_back({"nocomb_U2_K1", 2, 1, 0, 1, 1 << 30, 0});
         vs.push_back({"nocomb_U2_K2", 2, 1, 0, 2, 1 << 30, 0});
         vs.push_back({"nocomb_U4_K2", 4, 1, 0, 2, 1 << 30, 0});
+        vs.push_back({"floor_cheap", ucur, 1, 0, 1, 1 << 30, 5});
         vs.push_back({"salt", ucur, 1, 0, 1, 1 << 30, 9});
       } else {
       // K: > 0 fixed; -2 the round-1 product rule (one group of <= 512 / 256
@@ -516,7 +577,7 @@ int main(int argc, char** argv) {
         const i64 units = v.cl ? grid / v.cl : grid;
         if (GS == -1) GS = (int)std::min<i64>(units, 1 << 20);
         if (grid > (1 << 20) || (v.combine && (units + GS - 1) / GS > 65536)) continue;
-        Args a{x, NL == 2 ? y : x, nvec, K, GS, v.combine, v.combine >= 3 ? cparts : parts, gpart, gt, tk, out};
+        Args a{x, NL == 2 ? y : x, nvec, K, GS, v.combine, (v.combine >= 3 && v.combine != 5) ? cparts : parts, gpart, gt, tk, out};
         auto sweep = [&](int mode, int r) {
           if (mode == 0) sweep_read<<<sms * 8, 256>>>((const double4*)sw, sweep_bytes / 32, sink);
           else CK(cudaMemsetAsync(sw, r & 0xff, sweep_bytes));
@@ -554,7 +615,7 @@ int main(int argc, char** argv) {
             best = std::min(best, (double)(ms_pair - ms_sweep) * 1000.0 / reps);
           }
           CK(cudaGetLastError());
-          if (v.combine && v.combine != 9 && mode == 0) {
+          if (v.combine && v.combine != 9 && v.combine != 5 && mode == 0) {
             DD h;
             CK(cudaMemcpy(&h, out, 16, cudaMemcpyDeviceToHost));
             if (std::isnan(ref)) ref = h.hi;
