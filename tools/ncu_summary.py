@@ -27,6 +27,8 @@ KEYS = {
     "launch__occupancy_limit_registers": "occupancy_limit_registers",
     "sm__warps_active.avg.pct_of_peak_sustained_active": "achieved_occupancy_pct",
     "sm__throughput.avg.pct_of_peak_sustained_elapsed": "sm_throughput_pct",
+    "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active": "fp64_pipe_pct",
+    "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active": "fp64_pipe_cycles_pct",
     "lts__t_sector_hit_rate.pct": "l2_hit_pct",
     "smsp__inst_executed.sum": "instructions",
     "sm__cycles_elapsed.avg.per_second": "sm_clock_ghz",
@@ -102,7 +104,7 @@ def main(argv=None):
             for key in ("duration", "dram_read", "dram_write", "dram_bytes", "dram_gbs",
                         "algorithmic_gbs", "traffic_over_algorithmic", "dram_pct_of_ncu_peak",
                         "registers_per_thread", "grid", "achieved_occupancy_pct",
-                        "sm_throughput_pct", "l2_hit_pct", "sm_clock_ghz"):
+                        "sm_throughput_pct", "fp64_pipe_pct", "fp64_pipe_cycles_pct", "l2_hit_pct", "sm_clock_ghz"):
                 if key in k:
                     lines.append(f"  {key:28s} {k[key]:.6g}")
         if ks:
