@@ -167,21 +167,22 @@ int collect_tiles() {
 // streaming CTAs (168 us against a 147 us floor; four warps: 148 us,
 // profiles/r02_cheap_epilogue.txt).  Below 8,192 streaming CTAs two warps
 // are equal or a little better (fewer warps polling beside the streaming
-// CTAs of that SM).
+// CTAs of that SM), and below 128 one warp is (~0.1 us,
+// profiles/r02_collector_small_grids.txt).
 int collect_warps(i64 nstream) {
   static const int env = [] {
     const char* e = getenv("SALT_COLLECT_WARPS");
     return e ? atoi(e) : 0;
   }();
   if (env >= 1 && env <= 8) return env;
-  return nstream >= 8192 ? 4 : 2;
+  return nstream >= 8192 ? 4 : nstream >= 128 ? 2 : 1;
 }
 int collect_min() {
   static const int env = [] {
     const char* e = getenv("SALT_COLLECT_MIN");
     return e ? atoi(e) : -1;
   }();
-  return env >= 0 ? env : 256;
+  return env >= 0 ? env : 3;
 }
 
 int reduce_tiles_per_cta(int nl) {
@@ -774,32 +775,37 @@ int run_fused(Plan& p, void* const* dsts, int ndst, const void* const* leaves, i
   const i64 ntiles = (a.nvec + per_tile - 1) / per_tile;
   i64 K = assign_tiles_per_cta(), cap = i64(0x7fffffff);
   bool cluster = false, one_group = false, collect = false;
-  if (reduce && ntiles > 2 && ntiles <= (i64)max_cluster() * cluster_tiles()) {
-    // Small n (3 .. 16 x 2 tiles; up to 2 tiles one CTA is quicker): one cluster
+  if (reduce && ntiles > 2 && collect_enabled() &&
+      (ntiles + collect_tiles() - 1) / collect_tiles() >= collect_min()) {
+    // From 3 tiles up: streaming CTAs of collect_tiles() tiles that only
+    // store their partial, plus one collector CTA (tools/c3_probe.cu,
+    // profiles/r02_c3_probe*.txt: at 2^24 ddot 46.6 -> 42.6 us, sdot 25.7 ->
+    // 24.3 us, dnrm2 26.4 -> 25.5 us; the fence + ticket atomic each
+    // streaming CTA paid in the two-level combine held its SM slot).  With
+    // the warp-uniform collector loop it is also the quickest combine for
+    // small grids (profiles/r02_collector_small_grids.txt, back-to-back
+    // launches: 2.5-3.0 us for 3-32 tiles against 2.8-4.0 us as one
+    // cluster, 2.9-3.3 us for 33-192 tiles against 3.6-4.6 us through the
+    // tickets), so the cluster and ticket combines below only run when
+    // SALT_COLLECT_MIN / SALT_COMBINE ask for them.
+    // Beyond kCollectCtas streaming CTAs (the slots the workspace holds),
+    // more tiles per CTA: 2 for the f64 2^28 fused multi-leaf trees, the
+    // K round 1 measured best for them (7.26 TB/s, r01_reduce_variants.txt);
+    // a cap of 32,768 (K = 4 there) cost the CG update 2.3 %
+    // (profiles/r02_ncu_cgupdate.txt).
+    constexpr i64 kCollectCtas = salt::MAX_COLLECT;
+    static_assert(kCollectCtas <= salt::MAX_COLLECT, "collector slots");
+    K = collect_tiles();
+    if ((ntiles + K - 1) / K > kCollectCtas) K = (ntiles + kCollectCtas - 1) / kCollectCtas;
+    collect = true;
+  } else if (reduce && ntiles > 2 && ntiles <= (i64)max_cluster() * cluster_tiles()) {
+    // (round 1; SALT_COLLECT_MIN=33 restores it) 3 .. 16 x 2 tiles: one cluster
     // of <= 16 CTAs, partials combined in distributed shared memory — no
     // workspace round trip, no ticket atomics.  B200, back-to-back launches
     // (profiles/r01_cluster_reduce.txt): nrm2 f64 2^16 6.33 -> 4.13 us,
     // sdot 2^17 5.35 -> 4.28 us, fused axpy->dot 2^14 5.18 -> 4.07 us.
     K = (ntiles + max_cluster() - 1) / max_cluster();
     cluster = true;
-  } else if (reduce && ntiles > 2 && collect_enabled() &&
-             (ntiles + collect_tiles() - 1) / collect_tiles() >= collect_min()) {
-    // Mid and large n: streaming CTAs of collect_tiles() tiles that only
-    // store their partial, plus one collector CTA (tools/c3_probe.cu,
-    // profiles/r02_c3_probe*.txt: at 2^24 ddot 46.6 -> 42.6 us, sdot 25.7 ->
-    // 24.3 us, dnrm2 26.4 -> 25.5 us; the fence + ticket atomic each
-    // streaming CTA paid in the two-level combine held its SM slot).
-    // Beyond kCollectCtas streaming CTAs (the slots the workspace holds),
-    // more tiles per CTA: 2 for the f64 2^28 fused multi-leaf trees, the
-    // K round 1 measured best for them (7.26 TB/s, r01_reduce_variants.txt);
-    // a cap of 32,768 (K = 4 there) cost the CG update 2.3 %
-    // (profiles/r02_ncu_cgupdate.txt).  The collector keeps up easily: at
-    // most ~60 slots per microsecond at these sizes.
-    constexpr i64 kCollectCtas = salt::MAX_COLLECT;
-    static_assert(kCollectCtas <= salt::MAX_COLLECT, "collector slots");
-    K = collect_tiles();
-    if ((ntiles + K - 1) / K > kCollectCtas) K = (ntiles + kCollectCtas - 1) / kCollectCtas;
-    collect = true;
   } else if (reduce) {
     K = reduce_tiles_per_cta(p.nl);
     cap = salt::MAX_REDUCE_CTAS;
