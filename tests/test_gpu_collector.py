@@ -19,9 +19,13 @@ from oracle import restate
 pytestmark = pytest.mark.gpu
 
 # f64 dot: 512-element vectors x UNR 2 per tile -> tiles = ceil(n / 2048);
-# >= 511 tiles (256 streaming CTAs of 2) take the collector, > 32768 CTAs of
-# 2 tiles grow the tiles per CTA
-SIZES = [2048 * 32 + 1, 2048 * 510, 2048 * 511 + 7, (1 << 22) + 3, (1 << 24) - 5, 2048 * 65536 + 2048 * 3 + 1]
+# 3+ tiles take the collector (one streaming CTA per tile; 1 collector warp
+# below 128 streaming CTAs, 2 below 8,192, 4 beyond); > 65,536 tiles grow the
+# tiles per CTA.  Streaming-CTA counts on both sides of every boundary, and
+# counts that leave the collector's warps partly filled.
+SIZES = [2048 * 2 + 1, 2048 * 3, 2048 * 5 - 7, 2048 * 31 + 3, 2048 * 32, 2048 * 32 + 1, 2048 * 33 + 5,
+         2048 * 127, 2048 * 127 + 1, 2048 * 128 + 9, 2048 * 510, 2048 * 511 + 7, (1 << 22) + 3,
+         2048 * 8191, 2048 * 8191 + 5, 2048 * 8192 + 1, (1 << 24) - 5, 2048 * 65536 + 2048 * 3 + 1]
 
 
 def _vals(n, seed):
@@ -42,8 +46,8 @@ def test_collector_sizes_are_exact_to_a_rounding_and_deterministic(n):
 
 
 @pytest.mark.parametrize("special", ["inf", "-inf", "nan", "inf-inf"])
-def test_collector_special_values(special):
-    n = 1 << 21  # collector geometry
+@pytest.mark.parametrize("n", [2048 * 5 + 3, 1 << 21])  # 6 and 1,024 streaming CTAs
+def test_collector_special_values(special, n):
     x = _vals(n, 3)
     where = [17, n // 3, n - 2]  # in the first, a middle and the last streaming CTA
     if special == "inf":
@@ -76,7 +80,7 @@ print(json.dumps(out))
 
 
 def test_collector_and_ticket_combines_agree_to_a_rounding():
-    sizes = [2048 * 600, (1 << 23) + 11]
+    sizes = [2048 * 7 + 1, 2048 * 40, 2048 * 600, (1 << 23) + 11]
     res = {}
     for combine in ("collector", "ticket"):
         env = dict(os.environ)
