@@ -64,7 +64,15 @@ static_assert(SALT_WORKSPACE_TICKET_BYTES == salt::WsLayout::group_partials,
 constexpr int unroll_for(int mode, int nl, int elem_bytes) {
   return mode == salt::MODE_REDUCE && (elem_bytes == 4 || nl <= 1) ? 4 : 2;
 }
-constexpr int kUnrollScalar = 4;  // V == 1 fallback (misaligned operands)
+// V == 1 fallback (operands that do not share one 32-byte misalignment):
+// elements in flight per leaf per thread.  64 bytes per leaf, like the vector
+// kernels' two 256-bit loads (32 with five or more leaves, for the
+// registers): with 4 elements (16-32 bytes) a misaligned f64 dot ran at
+// 4.6 TB/s and an f32 one at 5.3 against 7.2-7.3 aligned
+// (profiles/r02_misaligned.json).
+constexpr int unroll_scalar(int elem_bytes, int nl) {
+  return (elem_bytes == 8 ? 8 : 16) / (nl > 4 ? 2 : 1);
+}
 // Reductions: tiles (of BLOCK*UNR vectors) per CTA, so that every CTA
 // streams ~64 KiB before paying its partial/ticket epilogue: 4 tiles for
 // one-leaf trees (nrm2, sum), 2 for two or more leaves (dot, fused axpy->dot).
@@ -227,21 +235,25 @@ std::mutex g_dev_mu;
 // The interpreter kernels: per element type, the vector width and unroll of
 // every compiled kernel (so the interpreter walks the same tiles and its
 // reductions add in the same order).
-template <class T> Kernel* interp_kernel_for(int vec, int unroll) {
-  static Kernel k2, k4, k1;
+template <class T> Kernel* interp_kernel_for(int vec, int unroll, int nl) {
+  static Kernel k2, k4, k1, k1h;
   static std::once_flag once;
+  constexpr int U1 = unroll_scalar((int)sizeof(T), 1), U1H = unroll_scalar((int)sizeof(T), 8);
   std::call_once(once, [] {
     k2.aot = (const void*)&salt::interp_kernel<T, vec_of<T>(), 2, kBlock>;
     k4.aot = (const void*)&salt::interp_kernel<T, vec_of<T>(), 4, kBlock>;
-    k1.aot = (const void*)&salt::interp_kernel<T, 1, kUnrollScalar, kBlock>;
+    k1.aot = (const void*)&salt::interp_kernel<T, 1, U1, kBlock>;
+    k1h.aot = (const void*)&salt::interp_kernel<T, 1, U1H, kBlock>;
     k2.vec = k4.vec = vec_of<T>();
-    k1.vec = 1;
+    k1.vec = k1h.vec = 1;
     k2.unroll = 2;
     k4.unroll = 4;
-    k1.unroll = kUnrollScalar;
-    k2.interp = k4.interp = k1.interp = true;
+    k1.unroll = U1;
+    k1h.unroll = U1H;
+    k2.interp = k4.interp = k1.interp = k1h.interp = true;
   });
-  return vec == 1 ? &k1 : unroll == 4 ? &k4 : &k2;
+  if (vec == 1) return unroll_scalar((int)sizeof(T), nl) == U1 ? &k1 : &k1h;
+  return unroll == 4 ? &k4 : &k2;
 }
 
 int current_device(int& dev) {
@@ -757,8 +769,11 @@ int run_fused(Plan& p, void* const* dsts, int ndst, const void* const* leaves, i
     // the postfix interpreter evaluates the same trees (salt_interp.cuh).
     if (!p.prog_ok)
       return fail(SALT_EJIT, (force_interp ? std::string() : g_err + "; ") + "interpreter: " + p.prog_err);
-    k = interp_kernel_for<T>(vec, unroll_for(p.mode, p.nl, (int)sizeof(T)));
+    k = interp_kernel_for<T>(vec, unroll_for(p.mode, p.nl, (int)sizeof(T)), p.nl);
   }
+  // V == 1 kernels run whole tiles without bounds predicates (salt_expr.cuh):
+  // the ragged end joins the scalar tail, which every CTA shares.
+  if (vec == 1) a.nvec -= a.nvec % ((i64)kBlock * k->unroll);
   int dev;
   int rc = current_device(dev);
   if (rc) return rc;

@@ -268,9 +268,30 @@ template <> struct VecIO<float, 8> {
   }
 };
 #endif
-template <class T> struct VecIO<T, 1> {
-  static __device__ __forceinline__ void load(T (&r)[1], const T* p) { r[0] = *p; }
-  static __device__ __forceinline__ void store(T* p, const T (&r)[1]) { *p = r[0]; }
+// One element (operands that do not share one 32-byte misalignment).  The
+// loads are volatile asm like the vector ones, so a tile's whole load burst
+// is issued before the first use: with plain C++ loads the compiler merged
+// the load loop into the TwoSum chain of a reduction, one pair of loads
+// ahead of the arithmetic (a misaligned f64 dot: 3.5-4.6 TB/s; now 7.3,
+// profiles/r02_misaligned.json).  They allocate in L1, unlike the vector
+// loads: a warp's run of elements straddles two 128-byte lines here, and the
+// neighbouring warp's load of the shared line then hits L1 instead of L2
+// (f32 axpy at mixed offsets 6.56 -> 6.75 TB/s).
+template <> struct VecIO<double, 1> {
+  static __device__ __forceinline__ void load(double (&r)[1], const double* p) {
+    asm volatile("ld.global.f64 %0, [%1];" : "=d"(r[0]) : "l"(p));
+  }
+  static __device__ __forceinline__ void store(double* p, const double (&r)[1]) {
+    asm volatile("st.global.f64 [%0], %1;" :: "l"(p), "d"(r[0]) : "memory");
+  }
+};
+template <> struct VecIO<float, 1> {
+  static __device__ __forceinline__ void load(float (&r)[1], const float* p) {
+    asm volatile("ld.global.f32 %0, [%1];" : "=f"(r[0]) : "l"(p));
+  }
+  static __device__ __forceinline__ void store(float* p, const float (&r)[1]) {
+    asm volatile("st.global.f32 [%0], %1;" :: "l"(p), "f"(r[0]) : "memory");
+  }
 };
 
 // Registers of one unroll slot: V lanes of every leaf, the scalars, and the
@@ -863,13 +884,18 @@ __global__ void SALT_BOUNDS(BLOCK) fused_kernel(Args<T> a) {
   const i64 tile0 = cta * a.tiles_per_cta;
   const i64 ntiles = (a.nvec + (i64)BLOCK * UNR - 1) / ((i64)BLOCK * UNR);
   const i64 tile1 = tile0 + a.tiles_per_cta < ntiles ? tile0 + a.tiles_per_cta : ntiles;
+  // V == 1 (operands that do not share one misalignment): the host cuts nvec
+  // to whole tiles (the ragged end joins the scalar tail above), so no slot
+  // needs a bounds predicate — a V == 1 tile has 8-16 slots and only 7
+  // predicate registers, and the predicated form issued its last loads only
+  // after the first had returned.
   for (i64 t = cta < 0 ? tile1 : tile0; t < tile1; ++t) {
     const i64 base = t * BLOCK * UNR + threadIdx.x;
     E1 e[UNR];
 #pragma unroll
     for (int u = 0; u < UNR; ++u) {
       const i64 j = base + (i64)u * BLOCK;
-      if (j < a.nvec) {
+      if (V == 1 || j < a.nvec) {
         const i64 off = a.head + j * V;
 #pragma unroll
         for (int l = 0; l < NL; ++l) VecIO<T, V>::load(e[u].x[l], a.leaf[l] + off);
@@ -879,7 +905,7 @@ __global__ void SALT_BOUNDS(BLOCK) fused_kernel(Args<T> a) {
 #pragma unroll
     for (int u = 0; u < UNR; ++u) {
       const i64 j = base + (i64)u * BLOCK;
-      if (j < a.nvec) {
+      if (V == 1 || j < a.nvec) {
 #pragma unroll
         for (int s = 0; s < NS; ++s) e[u].s[s] = a.sc[s];
 #pragma unroll

@@ -238,7 +238,9 @@ def test_misaligned_views_and_ragged_lengths(dt):
     td = torch.zeros(base_n, dtype=ta.dtype, device="cuda")
     vec = 32 // np.dtype(NP[dt]).itemsize
     for oa, ob, oc, od in [(0, 0, 0, 0), (1, 1, 1, 1), (vec - 1,) * 4, (1, 2, 3, 0), (0, 1, 0, 1)]:
-        for n in (0, 1, vec - 1, vec, vec + 1, 2047, 2048, 2049, 65_537):
+        # 2,048 (f64) / 4,096 (f32) elements: one tile of the V = 1 kernels, which run
+        # whole tiles only (the ragged end joins the scalar tail)
+        for n in (0, 1, vec - 1, vec, vec + 1, 2047, 2048, 2049, 4095, 4096, 4097, 8192, 65_537):
             A = lv.DenseVector.from_tensor(ta[oa : oa + n])
             B = lv.DenseVector.from_tensor(tb[ob : ob + n])
             C = lv.DenseVector.from_tensor(tc[oc : oc + n])
