@@ -454,7 +454,7 @@ struct Plan {
   Sig sa, sr;
   int mode = 0;
   int nl = 0, ns = 0, np = 0;
-  Kernel* cached[2][2] = {};  // [force_jit][vec == 1]: table / JIT lookups done once
+  Kernel* cached[2][3] = {};  // [force_jit][vector / V == 1 / small assignment]: lookups done once
   salt::Prog prog;            // the same trees as an interpreter program
   bool prog_ok = false;
   std::string prog_err;
@@ -749,7 +749,11 @@ int run_fused(Plan& p, void* const* dsts, int ndst, const void* const* leaves, i
     a.trace = g_trace_buf;
     a.trace_cap = g_trace_cap;
   } else if (!force_interp) {
-    Kernel*& slot = p.cached[g_force_jit.load(std::memory_order_relaxed)][vec == 1 ? 1 : 0];
+    // small assignments: the UNR 1 kernel of the same tree (kAssignSmallKind)
+    const bool small = p.mode == salt::MODE_ASSIGN && vec != 1 && a.nvec <= kAssignSmallVectors &&
+                       tuning_unroll() <= 0;
+    const int kind = small ? kAssignSmallKind : p.mode;
+    Kernel*& slot = p.cached[g_force_jit.load(std::memory_order_relaxed)][vec == 1 ? 1 : small ? 2 : 0];
     if (!slot) {
       // tiered: trees the interpreter can run do not wait for NVRTC (unless
       // the JIT itself is being tested: salt_set_force_jit)
@@ -760,7 +764,7 @@ int run_fused(Plan& p, void* const* dsts, int ndst, const void* const* leaves, i
       const bool async = p.prog_ok && jit_async() && !g_force_jit.load(std::memory_order_relaxed) &&
                          cap == cudaStreamCaptureStatusNone;
       bool queued = false;
-      slot = get_kernel(dtype_of<T>(), p.mode, vec, p.nl, p.sa.type, p.sr.type, async, &queued);
+      slot = get_kernel(dtype_of<T>(), kind, vec, p.nl, p.sa.type, p.sr.type, async, &queued);
     }
     k = slot;
   }
