@@ -791,7 +791,13 @@ int run_fused(Plan& p, void* const* dsts, int ndst, const void* const* leaves, i
   // deterministic ticket levels (7.25 vs 6.88 TB/s persistent, fused
   // axpy->dot f64 2^28).  Both grids depend only on n.
   const i64 per_tile = (i64)kBlock * k->unroll;
-  const i64 ntiles = (a.nvec + per_tile - 1) / per_tile;
+  i64 ntiles = (a.nvec + per_tile - 1) / per_tile;
+  // V == 1: the ragged end (up to one tile: 2,047 / 4,095 elements) runs in
+  // the scalar loop, which strides over every streaming CTA — size the grid
+  // for it too (one element per thread), or a short misaligned vector would
+  // loop through it in a single CTA.  (The kernel derives its own tile count
+  // from nvec; CTAs beyond it only take scalar elements.)
+  if (vec == 1) ntiles = std::max(ntiles, (n - a.nvec + kBlock - 1) / kBlock);
   i64 K = assign_tiles_per_cta(), cap = i64(0x7fffffff);
   bool cluster = false, one_group = false, collect = false;
   if (reduce && ntiles > 2 && collect_enabled() &&
