@@ -338,6 +338,15 @@ size_t salt_reduce_workspace_bytes(void);
  * bytes) into this host thread's pinned slot on `stream` and return the
  * slot; after salt_stream_synchronize(stream) the slot holds the bytes. */
 int salt_result_enqueue(const void* out_dev, size_t bytes, void* stream, void** host_slot);
+/* One step less: this host thread's 64-byte pinned result slot, mapped into
+ * every device's address space at the same address.  Pass it as out_dev of
+ * a reduction and the kernel stores the result straight into host memory:
+ * after salt_stream_synchronize(stream) the slot holds it — no copy is
+ * enqueued (lv.dot at n = 1024: 18.1 -> 13 us per synchronising call).
+ * Fails (SALT_EINVAL) when the pool is exhausted (more than 256 host
+ * threads) or the platform does not map it at the host address; callers
+ * then use salt_result_enqueue. */
+int salt_result_slot(void** host_slot);
 int salt_stream_synchronize(void* stream);
 /* Device-observed trace (debug): while a buffer is set for this host thread,
  * every salt_assign / salt_reduce / salt_fused call runs the NVRTC build of

@@ -53,6 +53,7 @@ HEADER_SYMBOLS = (
     "salt_capture_id",
     "salt_set_trace",
     "salt_result_enqueue",
+    "salt_result_slot",
     "salt_stream_synchronize",
     "salt_reduce_exchange",
     "salt_assign_reduce_exchange",
@@ -138,6 +139,7 @@ _SIGNATURES = {
     "salt_capture_id": (ctypes.c_uint64, [_c_vp]),
     "salt_set_trace": (_c_int, [_c_vp, _c_i64]),
     "salt_result_enqueue": (_c_int, [_c_vp, _c_size, _c_vp, _c_vp]),
+    "salt_result_slot": (_c_int, [_c_vp]),
     "salt_stream_synchronize": (_c_int, [_c_vp]),
     "salt_reduce_exchange": (
         _c_int,
@@ -263,7 +265,7 @@ def fastpath():
                     runtime._workspace, np.float32, np.float64, runtime._lazy_out,
                     addr(h.salt_assign_batch), addr(h.salt_reduce_batch), runtime._batch_out,
                     addr(h.salt_result_enqueue), addr(h.salt_stream_synchronize),
-                    addr(h.salt_fused_prog),
+                    addr(h.salt_fused_prog), addr(h.salt_result_slot),
                 )
                 _fast = _fastpath
             except (ImportError, AttributeError):

@@ -49,6 +49,7 @@ typedef int (*fused_prog_fn)(int, const char*, const char*, void* const*, int, c
                              int, void*, size_t, void*, void*, void*);
 typedef const char* (*last_error_fn)(void);
 typedef int (*result_enqueue_fn)(const void*, size_t, void*, void**);
+typedef int (*result_slot_fn)(void**);
 typedef int (*stream_sync_fn)(void*);
 
 static assign_fn p_assign;
@@ -61,6 +62,7 @@ static PyObject* batch_out; /* runtime._batch_out(device, count) -> (tensor, dat
 static last_error_fn p_last_error;
 static fused_prog_fn p_fused_prog;
 static result_enqueue_fn p_result_enqueue;
+static result_slot_fn p_result_slot;
 static stream_sync_fn p_stream_sync;
 static size_t ws_bytes;
 
@@ -440,8 +442,14 @@ static PyObject* launch_reduce(Walk* w, const char* asig, void* const* dptrs, in
                                int lazy, void* ws, void* slot, void* stream) {
   PyObject* ds = NULL;
   void* out = slot;
+  void* direct = NULL; /* this thread's device-mapped pinned slot, if any */
   double host[2] = {0.0, 0.0};
   if (lazy && !(ds = lazy_slot(w, &out))) return NULL;
+  /* Non-lazy, preferred: the kernel stores the result straight into this
+   * thread's pinned host slot (mapped at the same address on the device),
+   * so nothing is copied afterwards. */
+  if (!lazy && p_result_slot && p_result_slot(&direct) == 0) out = direct;
+  else direct = NULL;
   /* Non-lazy: the kernel writes the workspace's result slot and the copy to
    * this thread's pinned slot is enqueued behind it with the GIL held (a
    * later reduction on the same stream — same workspace — is ordered after
@@ -463,9 +471,11 @@ static PyObject* launch_reduce(Walk* w, const char* asig, void* const* dptrs, in
   }
   if (lazy) return ds;
   const size_t bytes = (flags & 2) ? 16 : (w->code == 0 ? 4 : 8);
-  void* hslot = NULL;
-  rc = p_result_enqueue(out, bytes, stream, &hslot);
-  if (rc != 0) return check(rc);
+  void* hslot = direct;
+  if (!direct) {
+    rc = p_result_enqueue(out, bytes, stream, &hslot);
+    if (rc != 0) return check(rc);
+  }
   Py_BEGIN_ALLOW_THREADS
   rc = p_stream_sync(stream);
   Py_END_ALLOW_THREADS
@@ -952,14 +962,15 @@ done:
 }
 
 static PyObject* fp_init(PyObject* self, PyObject* args) {
-  unsigned long long a, r, ar, fu, le, ab, rb, re, ss, fp;
+  unsigned long long a, r, ar, fu, le, ab, rb, re, ss, fp, rs;
   Py_ssize_t wsb;
-  if (!PyArg_ParseTuple(args, "KKKKKnOOOOOOOOOOOOOKKOKKK", &a, &r, &ar, &fu, &le, &wsb, &T_Leaf, &T_Add,
+  if (!PyArg_ParseTuple(args, "KKKKKnOOOOOOOOOOOOOKKOKKKK", &a, &r, &ar, &fu, &le, &wsb, &T_Leaf, &T_Add,
                         &T_Sub, &T_Mul, &T_Scale, &T_Dense, &T_DevScalar, &get_stream,
                         &current_device, &workspace_fn, &np_f32, &np_f64, &lazy_out, &ab, &rb,
-                        &batch_out, &re, &ss, &fp))
+                        &batch_out, &re, &ss, &fp, &rs))
     return NULL;
   p_fused_prog = (fused_prog_fn)(uintptr_t)fp;
+  p_result_slot = (result_slot_fn)(uintptr_t)rs;
   p_result_enqueue = (result_enqueue_fn)(uintptr_t)re;
   p_stream_sync = (stream_sync_fn)(uintptr_t)ss;
   p_assign_batch = (assign_batch_fn)(uintptr_t)ab;

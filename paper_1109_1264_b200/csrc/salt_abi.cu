@@ -580,15 +580,24 @@ int make_plan(int dtype, const char* asig, const char* rsig, int mode, int nleav
 // small pinned pool, claimed once; beyond the pool, threads copy directly.
 constexpr int kResultSlots = 256;
 std::atomic<int> g_result_slot_next{0};
+std::atomic<bool> g_result_pool_mapped{false};
 // This host thread's 64-byte pinned result slot (nullptr beyond the pool).
 char* thread_result_slot() {
   static char* pool = nullptr;
   static std::once_flag once;
   std::call_once(once, [] {
-    if (cudaHostAlloc((void**)&pool, kResultSlots * 64, cudaHostAllocPortable) != cudaSuccess) {
+    if (cudaHostAlloc((void**)&pool, kResultSlots * 64, cudaHostAllocPortable | cudaHostAllocMapped) !=
+        cudaSuccess) {
       cudaGetLastError();
       pool = nullptr;
     }
+    // Under unified addressing a kernel can store through the host pointer
+    // itself (salt_result_slot); anything else keeps the copy route.
+    void* dev = nullptr;
+    if (pool && cudaHostGetDevicePointer(&dev, pool, 0) == cudaSuccess && dev == (void*)pool)
+      g_result_pool_mapped.store(true, std::memory_order_release);
+    else
+      cudaGetLastError();
   });
   thread_local int slot = -2;  // -2: not claimed yet, -1: none (direct copy)
   if (slot == -2) {
@@ -989,6 +998,15 @@ size_t salt_reduce_workspace_bytes(void) { return (size_t)salt::WsLayout::bytes;
 int salt_result_enqueue(const void* out_dev, size_t bytes, void* stream, void** host_slot) {
   if (!out_dev || !host_slot || bytes == 0 || bytes > 64) return fail(SALT_EINVAL, "bad result fetch");
   return result_enqueue(out_dev, bytes, (cudaStream_t)stream, host_slot);
+}
+
+int salt_result_slot(void** host_slot) {
+  if (!host_slot) return fail(SALT_EINVAL, "null result slot pointer");
+  char* slot = thread_result_slot();
+  if (!slot || !g_result_pool_mapped.load(std::memory_order_acquire))
+    return fail(SALT_EINVAL, "no device-mapped result slot for this thread");
+  *host_slot = slot;
+  return 0;
 }
 
 int salt_stream_synchronize(void* stream) {
