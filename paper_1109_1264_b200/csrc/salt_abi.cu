@@ -750,18 +750,18 @@ int run_fused(Plan& p, void* const* dsts, int ndst, const void* const* leaves, i
   geometry<T>(dsts, nroots, leaves, p.nl, n, vec, a.head, a.nvec);
   Kernel* k = nullptr;
   const bool force_interp = g_force_interp.load(std::memory_order_relaxed) != 0;
+  // small assignments: the UNR 1 kernel of the same tree (kAssignSmallKind)
+  const bool small = p.mode == salt::MODE_ASSIGN && vec != 1 && a.nvec <= kAssignSmallVectors &&
+                     tuning_unroll() <= 0;
+  const int kind = small ? kAssignSmallKind : p.mode;
   if (g_trace_buf) {
     // device-observed trace (salt_set_trace): the NVRTC build of this tree
     // with -DSALT_TRACE, recording one thread's events into the buffer
-    k = get_kernel(dtype_of<T>(), p.mode, vec, p.nl, p.sa.type, p.sr.type, false, nullptr, true);
+    k = get_kernel(dtype_of<T>(), kind, vec, p.nl, p.sa.type, p.sr.type, false, nullptr, true);
     if (!k) return fail(SALT_EJIT, "traced kernel: " + g_err);
     a.trace = g_trace_buf;
     a.trace_cap = g_trace_cap;
   } else if (!force_interp) {
-    // small assignments: the UNR 1 kernel of the same tree (kAssignSmallKind)
-    const bool small = p.mode == salt::MODE_ASSIGN && vec != 1 && a.nvec <= kAssignSmallVectors &&
-                       tuning_unroll() <= 0;
-    const int kind = small ? kAssignSmallKind : p.mode;
     Kernel*& slot = p.cached[g_force_jit.load(std::memory_order_relaxed)][vec == 1 ? 1 : small ? 2 : 0];
     if (!slot) {
       // tiered: trees the interpreter can run do not wait for NVRTC (unless

@@ -35,8 +35,12 @@ def tiles(events):
     return out
 
 
-def test_assign_trace_is_a_load_burst_then_ops_in_slot_order():
-    n = 4 * BLOCK * V64 * 2 + 3           # 4 tiles of UNR=2 slots, plus a 3-element tail
+@pytest.mark.parametrize("n,want_unr", [
+    (4 * BLOCK * V64 * 2 + 3, 1),         # small (<= 2^20 vectors): one vector per leaf per thread
+    ((1 << 22) + 4 * BLOCK * V64 * 2 + 3, 2),  # beyond: two
+])
+def test_assign_trace_is_a_load_burst_then_ops_in_slot_order(n, want_unr):
+    # whole tiles plus a 3-element tail
     g = np.random.default_rng(1)
     a, b, c = (g.standard_normal(n) for _ in range(3))
     A, B, C = dev(a), dev(b), dev(c)
@@ -50,7 +54,7 @@ def test_assign_trace_is_a_load_burst_then_ops_in_slot_order():
     assert ev[0].kind == "single_op" and ev[0].index == n - 3
     body = [e for e in ev if e.kind != "single_op"]
     unr = sum(1 for e in body if e.kind == "load")
-    assert unr == 2
+    assert unr == want_unr
     assert [e.kind for e in body] == ["load"] * unr + ["vector_op", "store"] * unr
     assert [e.slot for e in body[:unr]] == list(range(unr))
     assert [e.index for e in body[:unr]] == [u * BLOCK * V64 for u in range(unr)]
