@@ -795,10 +795,12 @@ int run_fused(Plan& p, void* const* dsts, int ndst, const void* const* leaves, i
   // Work split (tools/stream_variants.cu, tools/reduce_variants.cu on B200):
   // assignments take one BLOCK*UNR tile per CTA — the block scheduler
   // refills an SM the moment a CTA retires, which keeps loads in flight
-  // (7.29 TB/s vs 7.06 for a persistent grid-stride loop); reductions take
-  // reduce_tiles_per_cta() tiles per CTA and combine per-CTA partials in two
-  // deterministic ticket levels (7.25 vs 6.88 TB/s persistent, fused
-  // axpy->dot f64 2^28).  Both grids depend only on n.
+  // (7.29 TB/s vs 7.06 for a persistent grid-stride loop); reductions of
+  // three or more tiles do the same and hand their per-CTA partials to one
+  // collector CTA (below); the round-1 geometry — reduce_tiles_per_cta()
+  // tiles per CTA, partials combined in two deterministic ticket levels,
+  // 7.25 vs 6.88 TB/s persistent for the fused axpy->dot f64 2^28 — remains
+  // behind SALT_COMBINE=ticket.  Every grid depends only on n.
   const i64 per_tile = (i64)kBlock * k->unroll;
   i64 ntiles = (a.nvec + per_tile - 1) / per_tile;
   // V == 1: the ragged end (up to one tile: 2,047 / 4,095 elements) runs in

@@ -820,10 +820,12 @@ __device__ __forceinline__ void trace_event(const Args<T>& a, int kind, i64 idx,
 //
 // Layout of the index space: [0, head) scalar, then nvec aligned vectors of
 // V lanes, then the scalar tail.  The vectors are cut into tiles of
-// BLOCK*UNR; CTA b owns tiles [b*K, b*K + K) (K = tiles_per_cta: 1 for
-// assignments, 2 for reductions).  Per tile a thread issues all UNR x NL
-// 256-bit loads before any arithmetic: the GPU form of the reference's load
-// burst / vector_op burst / store burst (engine.py:209-225).
+// BLOCK*UNR; CTA b owns tiles [b*K, b*K + K) (K = tiles_per_cta: 1, or more
+// once a reduction would need more than 65,536 streaming CTAs).  Per tile a
+// thread issues all UNR x NL 256-bit loads before any arithmetic: the GPU
+// form of the reference's load burst / vector_op burst / store burst
+// (engine.py:209-225).  UNR: 2 for assignments (1 up to 2^20 vectors), 4 / 2
+// for reductions (salt_abi.cu unroll_for), 8 / 16 elements when V == 1.
 template <class T, class EA, class ER, int MODE, int V, int UNR, int BLOCK>
 // SALT_MIN_BLOCKS (tuning: SALT_JIT_MINB JIT-builds with it) caps registers
 // for that many CTAs per SM.  Left undefined on purpose: an explicit
