@@ -345,7 +345,9 @@ int salt_result_enqueue(const void* out_dev, size_t bytes, void* stream, void** 
  * enqueued (lv.dot at n = 1024: 18.1 -> 13 us per synchronising call).
  * Fails (SALT_EINVAL) when the pool is exhausted (more than 256 host
  * threads) or the platform does not map it at the host address; callers
- * then use salt_result_enqueue. */
+ * then use salt_result_enqueue.  (salt_reduce and the other reducing calls
+ * do the same on their own when given out_host: the kernel stores a second
+ * copy of the result into the slot, and the call only waits for the stream.) */
 int salt_result_slot(void** host_slot);
 int salt_stream_synchronize(void* stream);
 /* Device-observed trace (debug): while a buffer is set for this host thread,

@@ -889,6 +889,13 @@ int run_fused(Plan& p, void* const* dsts, int ndst, const void* const* leaves, i
     a.partials = (salt::DD*)(w + salt::WsLayout::partials);
     a.slots = (unsigned long long*)(w + salt::WsLayout::slots);
     a.out = out_dev;
+    // a host result too: the kernel also stores it into this thread's pinned
+    // slot (mapped on the device at the host address), so no copy follows
+    if (out_host && out_host != out_dev) {
+      char* slot = thread_result_slot();
+      if (slot && g_result_pool_mapped.load(std::memory_order_acquire) && slot != (char*)out_dev)
+        a.out2 = slot;
+    }
     if (x) {
       if (x->world < 1 || x->world > salt::XCHG_MAX_RANKS || x->rank < 0 || x->rank >= x->world ||
           x->epoch == 0)
@@ -933,8 +940,15 @@ int run_fused(Plan& p, void* const* dsts, int ndst, const void* const* leaves, i
     rc = launch<T>(k, dev, grid, a, st);
     if (rc) return rc;
   }
-  if (reduce && out_host)
-    return result_to_host(out_host, out_dev, (flags & SALT_PARTIAL) ? sizeof(salt::DD) : sizeof(T), st);
+  if (reduce && out_host) {
+    const size_t bytes = (flags & SALT_PARTIAL) ? sizeof(salt::DD) : sizeof(T);
+    if (a.out2) {  // the kernel stored it into this thread's mapped slot itself
+      SALT_CUDA(cudaStreamSynchronize(st));
+      memcpy(out_host, a.out2, bytes);
+      return 0;
+    }
+    return result_to_host(out_host, out_dev, bytes, st);
+  }
   return 0;
 }
 

@@ -188,6 +188,8 @@ template <class T> struct Args {
   unsigned int* group_tickets;    // arrival counters per group (zeroed, self-resetting)
   unsigned int* ticket;           // arrival counter of the groups (zeroed, self-resetting)
   void* out;                      // T result or DD partial
+  void* out2;                     // optional second copy of the result (the caller's
+                                  // device-mapped pinned host slot), or nullptr
   int flags;
   int cluster;                    // reduce modes: 1 = the grid is ONE thread-block cluster
   int group;                      // reduce modes: CTAs per group (GROUP, or the whole grid
@@ -506,6 +508,12 @@ template <int BLOCK> __device__ __forceinline__ DD block_reduce_dd(DD v, DD* sme
 }
 
 template <class T> __device__ __forceinline__ void finish_store(DD tot, int flags, void* out);
+// The kernel's result: to a.out and, when the caller also wants it in host
+// memory, to its device-mapped pinned slot (a.out2) — no copy afterwards.
+template <class T> __device__ __forceinline__ void finish_result(DD tot, const Args<T>& a) {
+  finish_store<T>(tot, a.flags, a.out);
+  if (a.out2) finish_store<T>(tot, a.flags, a.out2);
+}
 
 // The tree's device scalars pv[0..NPV) for this thread: loaded from ps, or
 // computed by the scalar program (uniform across threads; a few ops).
@@ -644,7 +652,7 @@ __device__ __forceinline__ void collect_epilogue(DD mine, const Args<T>& a, DD* 
     DD tot = v;
     for (int w = 1; w < nw; ++w) tot = dd_add(tot, smem[w]);
     if (a.xchg.world > 0) tot = exchange_dd(tot, a.xchg);
-    finish_store<T>(tot, a.flags, a.out);
+    finish_result<T>(tot, a);
   }
 }
 
@@ -702,7 +710,7 @@ __device__ __forceinline__ void reduce_epilogue(DD mine, const Args<T>& a) {
   if (gridDim.x == 1) {  // small n: no partials, no tickets, no fences
     if (threadIdx.x == 0) {
       if (a.xchg.world > 0) part = exchange_dd(part, a.xchg);
-      finish_store<T>(part, a.flags, a.out);
+      finish_result<T>(part, a);
     }
     return;
   }
@@ -727,7 +735,7 @@ __device__ __forceinline__ void reduce_epilogue(DD mine, const Args<T>& a) {
     DD q = block_reduce_dd<BLOCK>(v, smem);
     if (threadIdx.x == 0) {
       if (a.xchg.world > 0) q = exchange_dd(q, a.xchg);
-      finish_store<T>(q, a.flags, a.out);
+      finish_result<T>(q, a);
     }
     return;
   }
@@ -766,7 +774,7 @@ __device__ __forceinline__ void reduce_epilogue(DD mine, const Args<T>& a) {
     if (threadIdx.x == 0) {
       a.group_tickets[g] = 0u;
       if (a.xchg.world > 0) q = exchange_dd(q, a.xchg);
-      finish_store<T>(q, a.flags, a.out);
+      finish_result<T>(q, a);
     }
     return;
   }
@@ -791,7 +799,7 @@ __device__ __forceinline__ void reduce_epilogue(DD mine, const Args<T>& a) {
     // Sharded reduction: trade this rank's total with the other ranks over
     // NVLink peer memory inside this same kernel — no separate collective.
     if (a.xchg.world > 0) tot = exchange_dd(tot, a.xchg);
-    finish_store<T>(tot, a.flags, a.out);
+    finish_result<T>(tot, a);
   }
 }
 
