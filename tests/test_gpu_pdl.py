@@ -107,3 +107,33 @@ def test_cluster_reduction_chain(n):
 
     a, b = run(False), run(True)
     assert a[0].tobytes() == b[0].tobytes() and a[1] == b[1]
+
+
+@pytest.mark.parametrize("dt", ["f64", "f32"])
+def test_chain_over_misaligned_views_is_sequential(dt):
+    """The V = 1 kernels (operands at different misalignments) load through
+    L1; a chain in which every launch reads what the previous launch wrote —
+    to shifted positions, i.e. from other threads, CTAs and SMs — must still
+    see each write (no stale L1 line survives a launch boundary under
+    programmatic dependent launch)."""
+    npdt = np.float64 if dt == "f64" else np.float32
+    n = (1 << 18) + 37
+    g = np.random.default_rng(21)
+    base = [g.uniform(-1, 1, n + 4100).astype(npdt) for _ in range(2)]
+    t = [torch.from_numpy(b).cuda() for b in base]
+    # X at element offset 1, Y at offset 2: mixed misalignment -> V = 1
+    X = lv.DenseVector.from_tensor(t[0][1:1 + n])
+    Y = lv.DenseVector.from_tensor(t[1][2:2 + n])
+    # the same storage seen 4,099 elements later (another CTA's elements)
+    Xs = lv.DenseVector.from_tensor(t[0][1 + 4099:1 + 4099 + n - 4099])
+    Ys = lv.DenseVector.from_tensor(t[1][2:2 + n - 4099])
+    hx, hy = base[0].copy(), base[1].copy()
+    for k in range(200):
+        al = 0.5 if k % 2 else -0.25
+        lv.axpy(al, X, Y)                 # Y += al X
+        hy[2:2 + n] = restate.eval_sig("L0 S0 L1 * +", [hy[2:2 + n], hx[1:1 + n]], [al], dt)
+        Xs.assign(Xs + 0.125 * Ys)        # X[4099:] += Y[:n-4099] / 8 (reads the previous launch's Y)
+        hx[1 + 4099:1 + n] = restate.eval_sig("L0 S0 L1 * +", [hx[1 + 4099:1 + n], hy[2:2 + n - 4099]],
+                                              [0.125], dt)
+    assert t[0].cpu().numpy().tobytes() == hx.tobytes()
+    assert t[1].cpu().numpy().tobytes() == hy.tobytes()
