@@ -38,7 +38,12 @@ def main():
     ap.add_argument("--max-logn", type=int, default=26)
     ap.add_argument("--seed", type=int, default=1109)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--misalign", action="store_true",
+                    help="every operand and the destination is a view at a random element offset (0-8) "
+                         "of its own buffer: mostly mixed misalignments (the V = 1 kernels), sometimes "
+                         "a shared one (scalar head + 256-bit body)")
     a = ap.parse_args()
+    import torch
     lib = _native.lib()
     rng = np.random.default_rng(a.seed)
     rows, fails = [], 0
@@ -49,14 +54,27 @@ def main():
         n = (1 << logn) + int(rng.integers(0, 64))
         nv = int(rng.integers(1, 9))
         host = [rng.uniform(-2, 2, n).astype(NP[dt]) for _ in range(nv)]
-        vecs = [lv.DenseVector.from_values(h, dt) for h in host]
+        if a.misalign:
+            share = int(rng.integers(0, 4)) == 0  # a quarter of the cases: one common offset
+            offs = [int(rng.integers(0, 9))] * (nv + 1) if share else [int(rng.integers(0, 9)) for _ in range(nv + 1)]
+            bufs = [torch.zeros(n + 16, dtype=torch.float32 if dt == "f32" else torch.float64, device="cuda")
+                    for _ in range(nv + 1)]
+            vecs = []
+            for h, b, o in zip(host, bufs, offs):
+                b[o:o + n].copy_(torch.from_numpy(h))
+                vecs.append(lv.DenseVector.from_tensor(b[o:o + n]))
+        else:
+            vecs = [lv.DenseVector.from_values(h, dt) for h in host]
         expr = as_node(random_tree(rng, vecs, int(rng.integers(1, 7))))
         lw = lower(expr)
         sig = " ".join(lw.tokens)
         idx = [next(i for i, v in enumerate(vecs) if v is u) for u in lw.vectors]
         leaves = [host[i] for i in idx]
         want = restate.eval_sig(sig, leaves, lw.scalars, dt)
-        out = lv.DenseVector.zeros(n, dt)
+        if a.misalign:
+            out = lv.DenseVector.from_tensor(bufs[nv][offs[nv]:offs[nv] + n])
+        else:
+            out = lv.DenseVector.zeros(n, dt)
         res = {}
         for mode in ("compiled", "interp"):
             lib.salt_set_force_interp(1 if mode == "interp" else 0)
@@ -79,6 +97,7 @@ def main():
                      "sum_within_tol": bool(ok_sum), "interp_sum_same_bits": bool(same)})
         print(json.dumps(rows[-1]), flush=True)
     summary = {"trees": a.trees, "failures": fails, "max_logn": a.max_logn, "seed": a.seed,
+               "misalign": bool(a.misalign),
                "seconds": round(time.time() - t0, 1), "gpu": __import__("torch").cuda.get_device_name()}
     print(json.dumps(summary))
     if a.out:
