@@ -831,7 +831,9 @@ int run_fused(Plan& p, void* const* dsts, int ndst, const void* const* leaves, i
     // more tiles per CTA: 2 for the f64 2^28 fused multi-leaf trees, the
     // K round 1 measured best for them (7.26 TB/s, r01_reduce_variants.txt);
     // a cap of 32,768 (K = 4 there) cost the CG update 2.3 %
-    // (profiles/r02_ncu_cgupdate.txt).
+    // (profiles/r02_ncu_cgupdate.txt); 131,072 slots (K = 1 for them) was a
+    // wash on one box: ddot f64 2^28 +0.7 %, the CG update -0.8 %, axpy->dot
+    // equal.
     constexpr i64 kCollectCtas = salt::MAX_COLLECT;
     static_assert(kCollectCtas <= salt::MAX_COLLECT, "collector slots");
     K = collect_tiles();
