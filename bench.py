@@ -118,6 +118,28 @@ class ClockSampler:
         self.samples = []
         self.proc = None
         self.marks = []
+        # NVML read directly in a tight loop, but only inside the headline
+        # window (first mark() pair): ~1 sample per 0.3 ms where nvidia-smi's
+        # 10 ms period leaves one or two in the driver's 24 ms region
+        self.fast = []
+        self._fast_on = threading.Event()
+        self._fast_quit = False
+        self._nvml = None
+
+    def _fast_loop(self):
+        nv, h = self._nvml
+        names = ((0x8, "hw_slowdown"), (0x40, "hw_thermal_slowdown"), (0x20, "sw_thermal_slowdown"),
+                 (0x4, "sw_power_cap"))
+        while not self._fast_quit:
+            if not self._fast_on.wait(0.05):
+                continue
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                mask = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+            except Exception:
+                return
+            self.fast.append((time.perf_counter(), float(sm), [n for bit, n in names if mask & bit]))
+            time.sleep(0.0002)
 
     def start(self):
         try:
@@ -130,6 +152,19 @@ class ClockSampler:
             return
         self.thread = threading.Thread(target=self._read, daemon=True)
         self.thread.start()
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            try:
+                uuid = "GPU-" + str(torch.cuda.get_device_properties(self.index).uuid)
+                h = nv.nvmlDeviceGetHandleByUUID(uuid.encode() if hasattr(uuid, "encode") else uuid)
+            except Exception:
+                h = nv.nvmlDeviceGetHandleByIndex(self.index)
+            self._fast_max = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+            self._nvml = (nv, h)
+            threading.Thread(target=self._fast_loop, daemon=True).start()
+        except Exception:
+            self._nvml = None
 
     def _read(self):
         for line in self.proc.stdout:
@@ -137,8 +172,13 @@ class ClockSampler:
 
     def mark(self):
         self.marks.append(time.perf_counter())
+        if len(self.marks) == 1:
+            self._fast_on.set()
+        elif len(self.marks) == 2:
+            self._fast_on.clear()
 
     def stop(self):
+        self._fast_quit = True
         if self.proc is not None:
             self.proc.terminate()
             try:
@@ -153,6 +193,15 @@ class ClockSampler:
             t0, t1 = self.marks[2 * window], self.marks[2 * window + 1]
         else:
             t0, t1 = 0, float("inf")
+        fast = [f for f in self.fast if t0 <= f[0] <= t1] if window == 0 else []
+        if len(fast) >= 3:
+            return {
+                "sm_mhz": float(np.median([f[1] for f in fast])),
+                "sm_max_mhz": self._fast_max,
+                "reasons": sorted({r for f in fast for r in f[2]}),
+                "samples": len(fast),
+                "source": "nvml, sampled in a loop inside the timed region",
+            }
         inside = [s for t, s in self.samples if t0 <= t <= t1]
         if not inside:  # region shorter than the sampling period: nearest sample
             inside = [min(self.samples, key=lambda ts: abs(ts[0] - t0))[1]]
