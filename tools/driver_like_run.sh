@@ -1,5 +1,6 @@
+# What the driver runs at round end, in one gpurun call: GPU suite, smoke, both bench arms (plain and under torchrun).
 set -u
-O=gpurun_out/s4
+O=gpurun_out/driver_like
 mkdir -p $O
 ( time timeout 1500 python -m pytest tests -x -q -m gpu ) > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/status
 ( time timeout 300 python -c "import __graft_entry__ as g; g.smoke()" ) > $O/smoke.log 2>&1; echo "smoke rc=$?" >> $O/status
