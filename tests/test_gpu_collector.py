@@ -96,3 +96,19 @@ def test_collector_and_ticket_combines_agree_to_a_rounding():
             a = float.fromhex(res["collector"][str(n)][k])
             b = float.fromhex(res["ticket"][str(n)][k])
             assert abs(a - b) <= 4.5e-16 * abs(b), (n, k, a, b)
+
+
+def test_collector_warp_counts_agree_to_a_rounding():
+    """1 / 2 / 4 / 8 collector warps change the fold order (the product picks
+    1 / 2 / 4 by grid size), never the value beyond a rounding."""
+    sizes = [2048 * 5 + 1, 2048 * 200 + 3, (1 << 23) + 11]
+    res = {}
+    for w in ("1", "2", "4", "8"):
+        env = dict(os.environ, SALT_COLLECT_WARPS=w)
+        r = subprocess.run([sys.executable, "-c", _SCRIPT, str(ROOT), ",".join(map(str, sizes))],
+                           capture_output=True, text=True, env=env, timeout=600, check=True)
+        res[w] = json.loads(r.stdout.strip().splitlines()[-1])
+    for n in sizes:
+        for k in range(2):
+            vals = [float.fromhex(res[w][str(n)][k]) for w in res]
+            assert max(vals) - min(vals) <= 4.5e-16 * abs(vals[0]), (n, k, vals)
