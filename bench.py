@@ -734,7 +734,7 @@ def run_config5(world, rank, dev, iters=100, warmup=3, route="nccl"):
     }
 
 
-PEER_CHILD_TIMEOUT_S = 300
+PEER_CHILD_TIMEOUT_S = 150  # the child takes ~7 s at N = 1; a hung route costs at most this per bench run
 
 
 def _child_env(world, rank, local, port):
