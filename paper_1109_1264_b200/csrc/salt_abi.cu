@@ -454,7 +454,7 @@ struct Plan {
   Sig sa, sr;
   int mode = 0;
   int nl = 0, ns = 0, np = 0;
-  Kernel* cached[2][3] = {};  // [force_jit][vector / V == 1 / small assignment]: lookups done once
+  Kernel* cached[2][4] = {};  // [force_jit][(V == 1) + 2 * (small assignment)]: lookups done once
   salt::Prog prog;            // the same trees as an interpreter program
   bool prog_ok = false;
   std::string prog_err;
@@ -751,8 +751,8 @@ int run_fused(Plan& p, void* const* dsts, int ndst, const void* const* leaves, i
   Kernel* k = nullptr;
   const bool force_interp = g_force_interp.load(std::memory_order_relaxed) != 0;
   // small assignments: the UNR 1 kernel of the same tree (kAssignSmallKind)
-  const bool small = p.mode == salt::MODE_ASSIGN && vec != 1 && a.nvec <= kAssignSmallVectors &&
-                     tuning_unroll() <= 0;
+  const bool small = p.mode == salt::MODE_ASSIGN && tuning_unroll() <= 0 &&
+                     a.nvec <= (vec == 1 ? kAssignSmallElements : kAssignSmallVectors);
   const int kind = small ? kAssignSmallKind : p.mode;
   if (g_trace_buf) {
     // device-observed trace (salt_set_trace): the NVRTC build of this tree
@@ -762,7 +762,7 @@ int run_fused(Plan& p, void* const* dsts, int ndst, const void* const* leaves, i
     a.trace = g_trace_buf;
     a.trace_cap = g_trace_cap;
   } else if (!force_interp) {
-    Kernel*& slot = p.cached[g_force_jit.load(std::memory_order_relaxed)][vec == 1 ? 1 : small ? 2 : 0];
+    Kernel*& slot = p.cached[g_force_jit.load(std::memory_order_relaxed)][(vec == 1 ? 1 : 0) + (small ? 2 : 0)];
     if (!slot) {
       // tiered: trees the interpreter can run do not wait for NVRTC (unless
       // the JIT itself is being tested: salt_set_force_jit)

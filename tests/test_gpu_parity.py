@@ -232,7 +232,7 @@ def test_misaligned_views_and_ragged_lengths(dt):
     kernel's scalar head / V=1 fallback) and lengths around vector and
     block boundaries."""
     g = np.random.default_rng(7)
-    base_n = 70_000
+    base_n = 300_016
     a, b, c = (g.uniform(-1, 1, base_n).astype(NP[dt]) for _ in range(3))
     ta, tb, tc = (torch.from_numpy(v).cuda() for v in (a, b, c))
     td = torch.zeros(base_n, dtype=ta.dtype, device="cuda")
@@ -240,7 +240,9 @@ def test_misaligned_views_and_ragged_lengths(dt):
     for oa, ob, oc, od in [(0, 0, 0, 0), (1, 1, 1, 1), (vec - 1,) * 4, (1, 2, 3, 0), (0, 1, 0, 1)]:
         # 2,048 (f64) / 4,096 (f32) elements: one tile of the V = 1 kernels, which run
         # whole tiles only (the ragged end joins the scalar tail)
-        for n in (0, 1, vec - 1, vec, vec + 1, 2047, 2048, 2049, 4095, 4096, 4097, 8192, 65_537):
+        # (up to 2^17 elements the small V = 1 assignment kernels run: 512-element tiles)
+        for n in (0, 1, vec - 1, vec, vec + 1, 511, 512, 513, 2047, 2048, 2049, 4095, 4096, 4097, 8192, 65_537,
+                  (1 << 17) + 5, 300_001):
             A = lv.DenseVector.from_tensor(ta[oa : oa + n])
             B = lv.DenseVector.from_tensor(tb[ob : ob + n])
             C = lv.DenseVector.from_tensor(tc[oc : oc + n])
