@@ -119,7 +119,7 @@ class ClockSampler:
         self.proc = None
         self.marks = []
         # NVML read directly in a tight loop, but only inside the headline
-        # window (first mark() pair): ~1 sample per 0.3 ms where nvidia-smi's
+        # window (first mark() pair): ~1 sample per ms where nvidia-smi's
         # 10 ms period leaves one or two in the driver's 24 ms region
         self.fast = []
         self._fast_on = threading.Event()
@@ -139,7 +139,7 @@ class ClockSampler:
             except Exception:
                 return
             self.fast.append((time.perf_counter(), float(sm), [n for bit, n in names if mask & bit]))
-            time.sleep(0.0002)
+            time.sleep(0.001)  # ~20 samples in the driver's 24 ms region
 
     def start(self):
         try:
